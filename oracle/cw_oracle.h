@@ -1,0 +1,84 @@
+/* TEST INFRASTRUCTURE ONLY -- the CPU restatement oracle.
+ *
+ * Plain C11 restatement of the reference's hot-path algorithm (cardwave,
+ * /root/reference/proj/core). Used by tests/ (and __graft_entry__.smoke) as
+ * the CHECKER for the CUDA path; never linked into or called by the product.
+ * Pinned against the reference itself (oracle/_ref/libcwref.so) by
+ * tests/test_oracle_pins.py, which requires bit-identical results for every
+ * function below on the reference's own configurations.
+ *
+ * Extensions beyond the reference (3D sheets, zero-conductivity scar, GKr
+ * jitter, the passive model) follow the reference conventions and are marked
+ * "parity unpinned" where they are used.
+ */
+#ifndef CW_ORACLE_H
+#define CW_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* model kinds (same ids as include/cwgpu.h) */
+enum { CWO_AP = 0, CWO_ORD_ENDO = 1, CWO_ORD_EPI = 2, CWO_ORD_MID = 3, CWO_MAC = 4, CWO_PASSIVE = 5 };
+enum { CWO_OST = 0, CWO_OSTAR = 1, CWO_DAETI = 2 };
+
+int cwo_state_count(int kind);
+double cwo_stable_step(int kind);
+/* [V, s...] */
+void cwo_rest_state(int kind, double* out);
+
+/* One rates() evaluation (ionic.hpp:33). gkr_scale multiplies ORd GKr (1.0 = reference). */
+void cwo_rates(int kind, double v, const double* s, double i_stim, double gkr_scale, double* dv,
+               double* ds);
+void cwo_rates_batch(int kind, int64_t n, const double* v, const double* s, const double* i_stim,
+                     double* dv, double* ds);
+
+int cwo_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max);
+int cwo_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad);
+int cwo_k_max_for(double dt, double stable_step);
+
+/* stimulus: flattened per-node entry lists */
+typedef struct {
+  const int32_t* node_ptr; /* n+1 */
+  const int32_t* ids;      /* entry ids */
+  const double* t_start;
+  const double* duration;
+  const double* amplitude;
+  const double* period; /* NaN: single shot */
+} cwo_protocol;
+
+double cwo_stim_current(const cwo_protocol* p, int64_t node, double t);
+
+void cwo_diffusion_substep_csr(int64_t n, const int64_t* row_ptr, const int64_t* col,
+                               const double* val, const double* mass, const double* v,
+                               double dt_sub, double* out);
+
+/* One reaction pass (splitting.cpp:95-155). AoS states s[i*stride+q].
+ * model_kind[m] for model id m, k_max[m]; gkr_scale may be NULL.
+ * khist (len kmax_global+1) accumulated. Returns -1 or the lowest bad node;
+ * *bad_t receives its sub-step time. */
+int64_t cwo_reaction_step(int64_t n, int stride, double* v, double* s, double* last_dvdt,
+                          const uint8_t* model_of_node, const int* model_kind, const int* k_max,
+                          const double* gkr_scale, const cwo_protocol* prot, int scheme, int k0_up,
+                          int k0_down, double dt, double t, int64_t* khist, double* bad_t);
+
+/* Activation detector (postprocess.cpp:18-66), SoA node state. */
+typedef struct {
+  int64_t n;
+  double threshold;
+  double prev_t;
+  int first;
+  double *prev_v, *v_rest, *max_slope, *t_max_slope, *v_peak, *lat, *apd;
+  uint8_t *phase, *has_lat, *has_apd;
+} cwo_detector;
+
+void cwo_detector_init(cwo_detector* d, int64_t n, double threshold);
+void cwo_detector_free(cwo_detector* d);
+void cwo_detector_observe(cwo_detector* d, double t, const double* v);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
