@@ -1,0 +1,220 @@
+/*
+ * cwgpu.h -- C ABI of the B200-native DAETI monodomain hot path.
+ *
+ * This is the drop-in boundary for the reference solver "cardwave"
+ * (/root/reference/proj/core). The reference has no C ABI or plugin registry;
+ * its replaceable seam is the C++ API of proj/core. Every entry point below
+ * states which reference interface it replaces. Plain pointers and sizes only:
+ * no C++ or torch types cross this boundary. The C++ drop-in classes with the
+ * reference's exact signatures (cardwave::gpu::StrangIntegrator,
+ * cardwave::gpu::run_simulation, cardwave::gpu::diffusion_substep) are in
+ * include/cardwave_gpu.hpp, header-only over this ABI.
+ *
+ * Status codes mirror the reference exception taxonomy and the CLI exit codes
+ * (errors.hpp:11-32, tools/main.cpp:322-331):
+ *   CWG_OK 0, CWG_EVALIDATION 2 (ValidationError), CWG_EINSTABILITY 3
+ *   (InstabilityError, node + time in cwg_error), CWG_EIO 4 (IoError),
+ *   CWG_ECUDA 5 (CUDA / NCCL failure; no reference equivalent).
+ *
+ * Threading: one host thread per context; every call is stream-ordered on the
+ * context's stream. Nothing here falls back to the CPU: without a usable
+ * sm_100 device cwg_create fails with CWG_ECUDA.
+ */
+#ifndef CWGPU_H
+#define CWGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CWG_ABI_VERSION 1
+
+enum {
+  CWG_OK = 0,
+  CWG_EVALIDATION = 2,
+  CWG_EINSTABILITY = 3,
+  CWG_EIO = 4,
+  CWG_ECUDA = 5
+};
+
+/* Cell models, by the reference registry names (ionic.cpp:59-70). The passive
+ * model is an extension (non-excitable scar tissue, BASELINE config 3). */
+enum {
+  CWG_MODEL_ALIEV_PANFILOV = 0, /* "aliev-panfilov"   aliev_panfilov.cpp */
+  CWG_MODEL_ORD_ENDO = 1,       /* "ohara2011-endo"   ohara_rudy_2011.cpp */
+  CWG_MODEL_ORD_EPI = 2,        /* "ohara2011-epi" */
+  CWG_MODEL_ORD_MID = 3,        /* "ohara2011-mid" */
+  CWG_MODEL_MACCANNELL = 4,     /* "maccannell2007"   maccannell_2007.cpp */
+  CWG_MODEL_PASSIVE = 5         /* "passive" (extension) */
+};
+
+/* Scheme (splitting.hpp:19) */
+enum { CWG_OST = 0, CWG_OSTAR = 1, CWG_DAETI = 2 };
+
+/* Operator storage chosen on the device. */
+enum {
+  CWG_OP_AUTO = 0,      /* stencil-2D when the CSR is a regular-sheet 9-point operator, else CSR */
+  CWG_OP_CSR = 1,       /* generic CSR row loop, ascending columns (fem.cpp:201-206) */
+  CWG_OP_STENCIL2D = 2, /* per-node 9 coefficients taken verbatim from the CSR */
+  CWG_OP_STRUCT3D = 3   /* extension: structured 3D slab, per-layer tables (see cwg_problem.s3d) */
+};
+
+typedef struct cwg_ctx cwg_ctx;
+
+/* InstabilityError payload (errors.hpp:18-26) */
+typedef struct {
+  int code;       /* CWG_* */
+  int64_t node;   /* lowest offending node (global index), -1 if none */
+  double t_ms;    /* reaction: failing sub-step time t + j*dt/k; diffusion: outer step time */
+  int phase;      /* 1 reaction, 2 diffusion, 0 none */
+  char msg[256];
+} cwg_error;
+
+/* Structured 3D slab operator (EXTENSION): (nx+1) x (ny+1) x
+ * (nz+1) nodes, spacing h, node index = (iy*(nz+1) + iz)*(nx+1) + ix.
+ * Coefficients are the trilinear-hex / 2x2x2-Gauss element integrals computed
+ * on the reference element per z-layer (fibre angle per layer, rotating in
+ * the x-y plane), with row-sum lumped mass. */
+typedef struct {
+  int64_t nx, ny, nz; /* element counts */
+  double h;           /* cm */
+  double d_long, rho; /* D_l, D_t = rho * D_l */
+  const double* fiber_angle_of_layer; /* nz element layers, radians */
+} cwg_struct3d;
+
+/* Everything StrangIntegrator/run_simulation consume (splitting.hpp:83-94,
+ * fem.hpp:23-32, ionic.hpp:39-55, stimulus.hpp:35-50), flattened. */
+typedef struct {
+  /* ---- AssembledOperator (fem.hpp:23-32) */
+  int64_t n;                  /* rows = nodes */
+  const int64_t* row_ptr;     /* n+1 (ignored for CWG_OP_STRUCT3D) */
+  const int64_t* col;         /* nnz, ascending per row */
+  const double* val;          /* nnz */
+  const double* lumped_mass;  /* n */
+  double dt_s;                /* Gershgorin step (fem.cpp:178-192) */
+  int op_kind;                /* CWG_OP_* */
+  int64_t grid_nx1, grid_ny1; /* regular-sheet node counts (x fastest); 0 = unknown */
+  const cwg_struct3d* s3d;    /* for CWG_OP_STRUCT3D */
+
+  /* ---- models (SimulationSetup::models) and NodeStateArray::model_of_node */
+  int n_models;
+  const int* model_kind;        /* [n_models] CWG_MODEL_* */
+  const uint8_t* model_of_node; /* [n] */
+  const double* gkr_scale;      /* [n] optional per-node ORd GKr multiplier (extension); NULL = 1 */
+
+  /* ---- ProtocolIndex (stimulus.hpp:35-50), flattened: entries + per-node id lists */
+  int n_stim;
+  const double* stim_t_start;
+  const double* stim_duration;
+  const double* stim_amplitude;
+  const double* stim_period;      /* NaN = single shot */
+  const int32_t* stim_node_ptr;   /* [n+1] or NULL when n_stim == 0 */
+  const int32_t* stim_ids;        /* entry ids per node, in protocol order */
+
+  /* ---- probes / detector (SimulationSetup) */
+  int n_probes;
+  const int64_t* probes;
+  double lat_threshold_mv;
+  double map_interval_ms;
+
+  /* ---- SchemeConfig (splitting.hpp:24-35) */
+  int scheme;
+  double dt_ms;
+  double t_end_ms;
+  int k0_up, k0_down;
+  int strict_substeps;
+  double record_interval_ms;
+
+  /* ---- placement */
+  int device;     /* CUDA ordinal */
+  int rank, world;                 /* y-slab decomposition; world = 1 for single GPU */
+  const unsigned char* nccl_id;    /* 128-byte ncclUniqueId (world > 1) */
+} cwg_problem;
+
+/* StrangIntegrator ctor (splitting.cpp:74-93): validates, uploads the operator,
+ * stimulus tables and model lists, derives dt_eff, plan and k_max. */
+int cwg_create(const cwg_problem* prob, cwg_ctx** out, cwg_error* err);
+void cwg_destroy(cwg_ctx* ctx);
+
+/* Use an external CUDA stream (e.g. torch's current stream); NULL = own stream. */
+int cwg_set_stream(cwg_ctx* ctx, void* cuda_stream);
+void* cwg_stream(cwg_ctx* ctx);
+
+/* make_initial_state (splitting.cpp:183-217) result upload / final_state
+ * download. AoS host layout s[i*stride+q] (NodeStateArray::s); device is SoA.
+ * For world > 1 the arrays are the GLOBAL arrays; each rank copies its slab. */
+int cwg_upload_state(cwg_ctx* ctx, const double* v, const double* s_aos, int stride,
+                     const double* last_dvdt);
+int cwg_download_state(cwg_ctx* ctx, double* v, double* s_aos, int stride, double* last_dvdt);
+/* Pinned staging for host<->device copies (e2e path); returns host pointers
+ * owned by ctx of the sizes of the local slab. */
+int cwg_pinned_buffers(cwg_ctx* ctx, double** v, double** s_aos, double** last_dvdt);
+
+/* StrangIntegrator::advance (splitting.cpp:171-181): one outer step at t_ms.
+ * Synchronous: returns CWG_EINSTABILITY with the reference's node/time. */
+int cwg_advance(cwg_ctx* ctx, double t_ms, int64_t step_index, int64_t n_steps, cwg_error* err);
+
+/* run_simulation (splitting.cpp:219-294) split into stream-ordered pieces:
+ *   cwg_run_begin   records traces/maps at t = 0 and resets counters;
+ *   cwg_run_steps   enqueues steps [first, first+count) incl. the record /
+ *                   map cadence (CUDA-graph replay; no host sync);
+ *   cwg_run_sync    waits and reports the first InstabilityError, if any.
+ * cwg_run = begin + all steps + sync. */
+int cwg_run_begin(cwg_ctx* ctx);
+int cwg_run_steps(cwg_ctx* ctx, int64_t first, int64_t count);
+int cwg_run_sync(cwg_ctx* ctx, cwg_error* err);
+int cwg_run(cwg_ctx* ctx, cwg_error* err);
+
+/* SimulationResult pieces (splitting.hpp:64-75) */
+typedef struct {
+  double dt_effective, dt_s, dt_ad;
+  int l, k_max_global;
+  int64_t n_steps, steps_per_record, steps_per_map, n_samples;
+  int64_t n_local, node_begin; /* this rank's slab */
+  int op_kind;                 /* resolved CWG_OP_* */
+} cwg_info;
+int cwg_get_info(cwg_ctx* ctx, cwg_info* info);
+int cwg_get_khist(cwg_ctx* ctx, int64_t* out, int len);            /* cumulative, index k */
+int cwg_get_traces(cwg_ctx* ctx, double* t_ms, double* v /* [probe][sample] */);
+int cwg_get_maps(cwg_ctx* ctx, double* lat, uint8_t* lat_valid, double* apd90, uint8_t* apd_valid);
+/* reaction / diffusion / recording device time (ms, CUDA events) of the last
+ * cwg_advance calls (TimingBreakdown, splitting.hpp:57-62) */
+int cwg_get_timing(cwg_ctx* ctx, double* reaction_ms, double* diffusion_ms, double* recording_ms);
+/* Kernel launches issued by this context so far (for the bench's gpu_launches). */
+int64_t cwg_launch_count(cwg_ctx* ctx);
+
+/* diffusion_substep (fem.cpp:194-207): standalone out = v - dt/m * K v on the
+ * device, host in/out, bit-identical to the reference. */
+int cwg_diffusion_substep(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                          const double* lumped_mass, const double* v, double dt_sub, double* out,
+                          int device, cwg_error* err);
+
+/* CellModel::rates (ionic.hpp:33) batched on the device: v[n], s_aos[n*ns],
+ * i_stim[n] -> dv[n], ds_aos[n*ns]. For tests and single-cell tooling. */
+int cwg_rates(int model_kind, int64_t n, const double* v, const double* s_aos, const double* i_stim,
+              double* dv, double* ds_aos, int device, cwg_error* err);
+
+/* Model metadata (CellModel::state_count / stable_step / rest_state) */
+int cwg_model_state_count(int model_kind);
+double cwg_model_stable_step(int model_kind);
+int cwg_model_rest_state(int model_kind, double* out /* state_count+1 */);
+int cwg_model_kind_from_name(const char* name); /* -1 if unknown (make_model, ionic.cpp:59) */
+
+/* Adaptation rules (splitting.cpp:48-72), host-side, exported for parity tests */
+int cwg_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max);
+int cwg_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad);
+int cwg_k_max_for(double dt, int model_kind);
+
+/* y-slab plan for world ranks over ny1 node rows:
+ * [row_begin, row_end) owned rows; balanced by node count. No GPU needed. */
+int cwg_slab_plan(int64_t ny1, int world, int rank, int64_t* row_begin, int64_t* row_end);
+
+const char* cwg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CWGPU_H */

@@ -1,0 +1,67 @@
+/*
+ * cwgpu_setup.h -- host-side problem setup for benches and tests (C ABI).
+ *
+ * Restates the reference's setup path so that the GPU box can build the
+ * operators of BASELINE.json's configurations without the reference tree:
+ *   build_regular_sheet   mesh.cpp:72-98   (node numbering y-outer, x-inner)
+ *   assign_fibrosis       mesh.cpp:100-122 (Fisher-Yates over mt19937_64)
+ *   select_nodes          mesh.cpp:124-180 (1e-9 cm inclusive tolerance)
+ *   nearest_node          mesh.cpp:43-57
+ *   build_diffusion_field fem.cpp:21-51
+ *   assemble              fem.cpp:63-176   (bilinear quad, 2x2 Gauss, row-sum lumping,
+ *                                           triplet std::sort, CSR with ascending columns)
+ *   gershgorin_step       fem.cpp:178-192
+ * The 2D CSR is bit-identical to the reference's (tests/test_setup_parity.py).
+ * Extension (config 3, parity unpinned by the reference): an optional
+ * per-element conductivity scale (0 allowed: scar) with zero rows skipped by
+ * Gershgorin.
+ */
+#ifndef CWGPU_SETUP_H
+#define CWGPU_SETUP_H
+
+#include <stdint.h>
+
+#include "cwgpu.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cwg_sheet cwg_sheet;
+
+/* RegionSelector kinds in reference declaration order (mesh.hpp:50-58) */
+enum {
+  CWG_SEL_X_LE = 0, CWG_SEL_X_GE = 1, CWG_SEL_Y_LE = 2, CWG_SEL_Y_GE = 3,
+  CWG_SEL_RECT = 4, CWG_SEL_NODE_SET = 5, CWG_SEL_DISC = 6
+};
+
+/* build_regular_sheet + assign_fibrosis (fib_fraction > 0) + build_diffusion_field
+ * + assemble. elem_scale: optional [n_elements] multiplier of D (extension). */
+int cwg_sheet_build(double lx_cm, double ly_cm, double h_cm, double fiber_angle_rad,
+                    double d0_myocyte, double d0_fibrotic, double rho, double fib_fraction,
+                    uint64_t seed, const double* elem_scale, cwg_sheet** out, cwg_error* err);
+void cwg_sheet_free(cwg_sheet* s);
+
+int64_t cwg_sheet_nodes(const cwg_sheet* s);
+int64_t cwg_sheet_elements(const cwg_sheet* s);
+int64_t cwg_sheet_nnz(const cwg_sheet* s);
+int64_t cwg_sheet_nx1(const cwg_sheet* s);
+int64_t cwg_sheet_ny1(const cwg_sheet* s);
+double cwg_sheet_dt_s(const cwg_sheet* s);
+/* zero-copy views valid for the sheet's lifetime */
+const int64_t* cwg_sheet_row_ptr(const cwg_sheet* s);
+const int64_t* cwg_sheet_col(const cwg_sheet* s);
+const double* cwg_sheet_val(const cwg_sheet* s);
+const double* cwg_sheet_mass(const cwg_sheet* s);
+const double* cwg_sheet_coords(const cwg_sheet* s); /* [n][2] */
+const int32_t* cwg_sheet_tags(const cwg_sheet* s);  /* per node; 0 myocyte-epi, 1 fibroblast */
+
+/* prm = {value, x0, x1, y0, y1, cx, cy, radius}; returns count (writes <= cap) */
+int64_t cwg_sheet_select(const cwg_sheet* s, int kind, const double* prm, const int64_t* set_nodes,
+                         int64_t n_set, int64_t* out, int64_t cap);
+int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

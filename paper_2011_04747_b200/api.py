@@ -1,0 +1,604 @@
+"""Python mirror of the reference's proj/core interfaces over the cwgpu C ABI.
+
+Names, argument meaning and error behaviour follow cardwave (reference
+/root/reference/proj/core/include/cardwave/*.hpp) so that parity tests read
+like the reference's own usage:
+
+  reference (C++)                               here
+  ---------------------------------------------------------------------------
+  Scheme, SchemeConfig          splitting.hpp:19-35   Scheme, SchemeConfig
+  reaction_substeps             splitting.hpp:42      reaction_substeps
+  DiffusionPlan, diffusion_substeps  :43-51           DiffusionPlan, diffusion_substeps
+  k_max_for                     splitting.hpp:54      k_max_for
+  StrangIntegrator              splitting.hpp:101-127 StrangIntegrator (GPU)
+  run_simulation                splitting.hpp:139     run_simulation (GPU)
+  make_initial_state            splitting.hpp:131     make_initial_state
+  diffusion_substep             fem.hpp:56            diffusion_substep (GPU)
+  CellModel / make_model        ionic.hpp:17-61       CellModel / make_model (rates on GPU)
+  NodeStateArray                ionic.hpp:39-55       NodeStateArray
+  Stimulus/Protocol/ProtocolIndex stimulus.hpp:17-50  same names
+  AssembledOperator             fem.hpp:23-32         AssembledOperator
+  build_regular_sheet+assemble  mesh.cpp/fem.cpp      build_sheet (host setup, cwgpu_setup.h)
+  ValidationError / InstabilityError errors.hpp       same names
+
+Every compute call runs the sm_100a kernels of libcwgpu.so; there is no CPU
+fallback path in this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ----------------------------------------------------------------------------- errors (errors.hpp)
+class ValidationError(RuntimeError):
+    """Invalid configuration or arguments (CLI exit code 2)."""
+
+
+class InstabilityError(RuntimeError):
+    """Non-finite state (CLI exit code 3), with the reference's node and time."""
+
+    def __init__(self, msg, node, t_ms):
+        super().__init__(msg)
+        self.node_index = node
+        self.time_ms = t_ms
+
+
+class IoError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure (no reference equivalent)."""
+
+
+def _raise(code, err: L.cwg_error):
+    msg = err.msg.decode(errors="replace")
+    if code == L.CWG_EVALIDATION:
+        raise ValidationError(msg)
+    if code == L.CWG_EINSTABILITY:
+        raise InstabilityError(msg, int(err.node), float(err.t_ms))
+    if code == L.CWG_EIO:
+        raise IoError(msg)
+    raise DeviceError(msg or f"cwgpu error {code}")
+
+
+def _check(code, err=None):
+    if code != L.CWG_OK:
+        _raise(code, err if err is not None else L.cwg_error(code=code))
+
+
+# ----------------------------------------------------------------------------- scheme (splitting.hpp)
+class Scheme(enum.IntEnum):
+    OST = 0
+    OSTAR = 1
+    DAETI = 2
+
+
+def scheme_from_string(name: str) -> Scheme:
+    try:
+        return Scheme[name]
+    except KeyError:
+        raise ValidationError(f"unknown scheme '{name}' (expected OST, OSTAR or DAETI)") from None
+
+
+@dataclass
+class SchemeConfig:
+    scheme: Scheme = Scheme.DAETI
+    dt_ms: float = 0.1
+    t_end_ms: float = 500.0
+    k0_up: int = 5
+    k0_down: int = 1
+    strict_substeps: bool = False
+    record_interval_ms: float = 1.0
+    workers: int = 0  # accepted for interface parity; the GPU path ignores it
+
+    def validate(self):
+        if not self.dt_ms > 0.0:
+            raise ValidationError("scheme: dt must be positive")
+        if not self.t_end_ms >= self.dt_ms:
+            raise ValidationError("scheme: T must be >= dt")
+        if self.k0_down < 1 or self.k0_up < self.k0_down:
+            raise ValidationError("scheme: need k0_up >= k0_down >= 1")
+        if not self.record_interval_ms > 0.0:
+            raise ValidationError("scheme: record interval must be positive")
+        if self.workers < 0:
+            raise ValidationError("scheme: workers must be >= 0")
+
+
+@dataclass
+class DiffusionPlan:
+    l: int = 1
+    dt_ad: float = 0.0
+
+
+def reaction_substeps(dvdt_prev: float, cfg: SchemeConfig, k_max: int) -> int:
+    return L.lib().cwg_reaction_substeps(float(dvdt_prev), int(cfg.scheme), cfg.k0_up, cfg.k0_down, k_max)
+
+
+def diffusion_substeps(dt_ms: float, dt_s_ms: float, strict: bool, scheme: Scheme) -> DiffusionPlan:
+    l, dt_ad = C.c_int(), C.c_double()
+    if L.lib().cwg_diffusion_substeps(dt_ms, dt_s_ms, int(strict), int(scheme), C.byref(l), C.byref(dt_ad)):
+        raise ValidationError("diffusion sub-steps: dt and dt_s must be positive")
+    return DiffusionPlan(l.value, dt_ad.value)
+
+
+# ----------------------------------------------------------------------------- models (ionic.hpp)
+class CellModel:
+    """Registry model (make_model, ionic.cpp:59-70); rates() evaluates on the GPU."""
+
+    def __init__(self, name: str, kind: int):
+        self._name, self.kind = name, kind
+
+    def name(self):
+        return self._name
+
+    def state_count(self):
+        return L.lib().cwg_model_state_count(self.kind)
+
+    def stable_step(self):
+        return L.lib().cwg_model_stable_step(self.kind)
+
+    def rest_state(self):
+        out = np.zeros(self.state_count() + 1)
+        L.lib().cwg_model_rest_state(self.kind, L.dp(out))
+        return out
+
+    def rates(self, v, s, i_stim, device=0):
+        """Batched rates: v[n], s[n, ns], i_stim[n] -> (dv[n], ds[n, ns])."""
+        v = np.ascontiguousarray(v, np.float64)
+        ns = self.state_count()
+        s = np.ascontiguousarray(s, np.float64).reshape(len(v), ns)
+        i_stim = np.ascontiguousarray(np.broadcast_to(i_stim, v.shape), np.float64)
+        dv = np.zeros_like(v)
+        ds = np.zeros_like(s)
+        err = L.cwg_error()
+        _check(L.lib().cwg_rates(self.kind, len(v), L.dp(v), L.dp(s), L.dp(i_stim), L.dp(dv), L.dp(ds), device,
+                                 C.byref(err)), err)
+        return dv, ds
+
+    def __repr__(self):
+        return f"CellModel({self._name!r})"
+
+
+def registered_model_names():
+    return ["aliev-panfilov", "ohara2011-endo", "ohara2011-epi", "ohara2011-mid", "maccannell2007"]
+
+
+def make_model(name: str) -> CellModel:
+    kind = L.lib().cwg_model_kind_from_name(name.encode())
+    if kind < 0:
+        raise ValidationError(f"unknown cell model: '{name}'")
+    return CellModel(name, kind)
+
+
+def k_max_for(dt_ms: float, model: CellModel) -> int:
+    return L.lib().cwg_k_max_for(dt_ms, model.kind)
+
+
+@dataclass
+class NodeStateArray:
+    n_nodes: int = 0
+    stride: int = 0
+    v: np.ndarray = None
+    s: np.ndarray = None  # n_nodes * stride, node-major (s[i*stride + k])
+    last_dvdt: np.ndarray = None
+    model_of_node: np.ndarray = None
+
+    def states_of(self, node):
+        return self.s[node * self.stride:(node + 1) * self.stride]
+
+    def copy(self):
+        return NodeStateArray(self.n_nodes, self.stride, self.v.copy(), self.s.copy(), self.last_dvdt.copy(),
+                              self.model_of_node.copy())
+
+
+def make_initial_state(n_nodes: int, models: Sequence[CellModel], model_of_node, initial_per_model=None):
+    """make_initial_state (splitting.cpp:183-217) with the tag->model map already applied."""
+    model_of_node = np.ascontiguousarray(model_of_node, np.uint8)
+    if len(model_of_node) != n_nodes:
+        raise ValidationError("initial state: model_of_node must cover every node")
+    stride = max([1] + [m.state_count() for m in models])
+    st = NodeStateArray(n_nodes, stride, np.zeros(n_nodes), np.zeros(n_nodes * stride), np.zeros(n_nodes),
+                        model_of_node)
+    s2 = st.s.reshape(n_nodes, stride)
+    for mid, m in enumerate(models):
+        init = None
+        if initial_per_model is not None and mid < len(initial_per_model) and initial_per_model[mid] is not None:
+            init = np.asarray(initial_per_model[mid], np.float64)
+        if init is None:
+            init = m.rest_state()
+        if len(init) != m.state_count() + 1:
+            raise ValidationError(f"initial state: wrong state vector length for model {m.name()}")
+        sel = model_of_node == mid
+        st.v[sel] = init[0]
+        s2[np.ix_(sel, np.arange(m.state_count()))] = init[1:]
+    if model_of_node.size and model_of_node.max() >= len(models):
+        raise ValidationError("initial state: node has no model")
+    return st
+
+
+# ----------------------------------------------------------------------------- operator + setup
+@dataclass
+class AssembledOperator:
+    row_ptr: np.ndarray
+    col: np.ndarray
+    val: np.ndarray
+    lumped_mass: np.ndarray
+    dt_s: float
+    grid_nx1: int = 0  # regular-sheet node counts (enables the stencil kernel and y-slabs)
+    grid_ny1: int = 0
+
+    def rows(self):
+        return len(self.lumped_mass)
+
+    def entry(self, i, j):
+        for p in range(self.row_ptr[i], self.row_ptr[i + 1]):
+            if self.col[p] == j:
+                return self.val[p]
+        return 0.0
+
+
+class Sheet:
+    """build_regular_sheet (+assign_fibrosis) + build_diffusion_field + assemble, on the host."""
+
+    def __init__(self, lx_cm, ly_cm, h_cm, fiber_angle_rad=0.0, d0_myocyte=0.0017, d0_fibrotic=0.00066, rho=0.25,
+                 fib_fraction=0.0, seed=0, elem_scale=None):
+        lib = L.lib()
+        h = C.c_void_p()
+        err = L.cwg_error()
+        es = None
+        if elem_scale is not None:
+            self._es = np.ascontiguousarray(elem_scale, np.float64)
+            es = L.dp(self._es)
+        rc = lib.cwg_sheet_build(lx_cm, ly_cm, h_cm, fiber_angle_rad, d0_myocyte, d0_fibrotic, rho, fib_fraction, seed,
+                                 es, C.byref(h), C.byref(err))
+        _check(rc, err)
+        self._h = h
+        n = lib.cwg_sheet_nodes(h)
+        nnz = lib.cwg_sheet_nnz(h)
+        self.n = n
+        self.nx1, self.ny1 = lib.cwg_sheet_nx1(h), lib.cwg_sheet_ny1(h)
+        self.n_elements = lib.cwg_sheet_elements(h)
+        as_np = np.ctypeslib.as_array
+        self.op = AssembledOperator(as_np(lib.cwg_sheet_row_ptr(h), (n + 1,)).copy(),
+                                    as_np(lib.cwg_sheet_col(h), (nnz,)).copy(),
+                                    as_np(lib.cwg_sheet_val(h), (nnz,)).copy(),
+                                    as_np(lib.cwg_sheet_mass(h), (n,)).copy(),
+                                    lib.cwg_sheet_dt_s(h), self.nx1, self.ny1)
+        self.coords = as_np(lib.cwg_sheet_coords(h), (n, 2)).copy()
+        self.tags = as_np(lib.cwg_sheet_tags(h), (n,)).copy()
+
+    def __del__(self):
+        if getattr(self, "_h", None) and L._lib is not None:
+            L._lib.cwg_sheet_free(self._h)
+            self._h = None
+
+    _KINDS = {"x_le": 0, "x_ge": 1, "y_le": 2, "y_ge": 3, "rectangle": 4, "node_set": 5, "disc": 6}
+
+    def select(self, kind, value=0.0, x0=0.0, x1=0.0, y0=0.0, y1=0.0, cx=0.0, cy=0.0, radius=0.0, nodes=()):
+        """select_nodes (mesh.cpp:124-180)."""
+        prm = np.array([value, x0, x1, y0, y1, cx, cy, radius], np.float64)
+        sn = np.array(list(nodes) or [0], np.int64)
+        out = np.zeros(self.n, np.int64)
+        m = L.lib().cwg_sheet_select(self._h, self._KINDS[kind], L.dp(prm), L.lp(sn), len(nodes), L.lp(out), self.n)
+        if m < 0:
+            raise ValidationError("selector: invalid selection")
+        return out[:m].copy()
+
+    def nearest(self, x, y):
+        return L.lib().cwg_sheet_nearest(self._h, x, y)
+
+
+def build_sheet(*args, **kw) -> Sheet:
+    return Sheet(*args, **kw)
+
+
+# ----------------------------------------------------------------------------- stimulus (stimulus.hpp)
+@dataclass
+class Stimulus:
+    nodes: np.ndarray
+    t_start_ms: float = 0.0
+    duration_ms: float = 1.0
+    amplitude: float = 0.0
+    period_ms: Optional[float] = None
+    label: str = ""
+
+    def active_at(self, t_ms):
+        if t_ms < self.t_start_ms:
+            return False
+        if self.period_ms is None:
+            return t_ms < self.t_start_ms + self.duration_ms
+        return math.fmod(t_ms - self.t_start_ms, self.period_ms) < self.duration_ms
+
+
+@dataclass
+class Protocol:
+    entries: List[Stimulus] = field(default_factory=list)
+
+
+class ProtocolIndex:
+    """Compiled per-node view (stimulus.cpp:17-31), flattened for the device."""
+
+    def __init__(self, protocol: Protocol, n_nodes: int):
+        lists = [[] for _ in range(n_nodes)]
+        for eid, st in enumerate(protocol.entries):
+            if not st.duration_ms > 0.0:
+                raise ValidationError("stimulus: duration must be positive")
+            if not math.isfinite(st.amplitude):
+                raise ValidationError("stimulus: amplitude must be finite")
+            if len(st.nodes) == 0:
+                raise ValidationError("stimulus: node set is empty")
+            for nd in np.asarray(st.nodes, np.int64):
+                if nd < 0 or nd >= n_nodes:
+                    raise ValidationError(f"stimulus: node {nd} out of range")
+                lists[int(nd)].append(eid)
+        self.n_entries = len(protocol.entries)
+        self.node_ptr = np.zeros(n_nodes + 1, np.int32)
+        self.node_ptr[1:] = np.cumsum([len(x) for x in lists])
+        self.ids = np.array([e for x in lists for e in x] or [0], np.int32)
+        es = protocol.entries
+        self.t_start = np.array([s.t_start_ms for s in es] or [0.0])
+        self.duration = np.array([s.duration_ms for s in es] or [1.0])
+        self.amplitude = np.array([s.amplitude for s in es] or [0.0])
+        self.period = np.array([math.nan if s.period_ms is None else s.period_ms for s in es] or [math.nan])
+
+    def empty(self):
+        return self.n_entries == 0
+
+
+@dataclass
+class Probe:
+    node: int = -1
+    name: str = ""
+
+
+@dataclass
+class Trace:
+    node: int
+    name: str
+    t_ms: np.ndarray
+    v_mv: np.ndarray
+
+
+@dataclass
+class ScalarMap:
+    value: np.ndarray
+    valid: np.ndarray
+
+
+@dataclass
+class TimingBreakdown:
+    total_ms: float = 0.0
+    reaction_ms: float = 0.0
+    diffusion_ms: float = 0.0
+    recording_ms: float = 0.0
+
+
+@dataclass
+class SimulationSetup:
+    op: AssembledOperator = None
+    models: List[CellModel] = field(default_factory=list)
+    protocol: Optional[ProtocolIndex] = None
+    probes: List[Probe] = field(default_factory=list)
+    lat_threshold_mv: float = 0.0
+    map_interval_ms: float = 1.0
+    gkr_scale: Optional[np.ndarray] = None  # extension: per-node ORd GKr multiplier
+
+
+@dataclass
+class SimulationResult:
+    traces: List[Trace]
+    lat_map: ScalarMap
+    apd90_map: ScalarMap
+    timing: TimingBreakdown
+    k_histogram: np.ndarray
+    dt_effective: float
+    dt_s: float
+    plan: DiffusionPlan
+    n_steps: int
+    final_state: NodeStateArray
+
+
+# ----------------------------------------------------------------------------- the GPU integrator
+class StrangIntegrator:
+    """StrangIntegrator (splitting.hpp:101-127) on one B200 (or one y-slab of N).
+
+    The node state lives on the device; advance() mirrors the reference's
+    in-place mutation of the caller's NodeStateArray (upload when the state
+    object changed, download after the step).
+    """
+
+    def __init__(self, setup: SimulationSetup, cfg: SchemeConfig, model_of_node=None, device=0, rank=0, world=1,
+                 nccl_id: bytes = None, op_kind=L.OP_AUTO):
+        cfg.validate()
+        if setup.op is None:
+            raise ValidationError("integrator: missing assembled operator")
+        if not setup.models:
+            raise ValidationError("integrator: no cell models")
+        self.setup, self.cfg = setup, cfg
+        op = setup.op
+        n = op.rows()
+        if model_of_node is None:
+            model_of_node = np.zeros(n, np.uint8)
+        keep = {}
+        p = L.cwg_problem()
+        keep["rp"] = np.ascontiguousarray(op.row_ptr, np.int64)
+        keep["col"] = np.ascontiguousarray(op.col, np.int64)
+        keep["val"] = np.ascontiguousarray(op.val, np.float64)
+        keep["mass"] = np.ascontiguousarray(op.lumped_mass, np.float64)
+        p.n, p.row_ptr, p.col, p.val, p.lumped_mass = n, L.lp(keep["rp"]), L.lp(keep["col"]), L.dp(keep["val"]), L.dp(
+            keep["mass"])
+        p.dt_s = op.dt_s
+        p.op_kind = op_kind
+        p.grid_nx1, p.grid_ny1 = op.grid_nx1, op.grid_ny1
+        keep["kinds"] = np.array([m.kind for m in setup.models], np.int32)
+        p.n_models = len(setup.models)
+        p.model_kind = keep["kinds"].ctypes.data_as(L._ip)
+        keep["mon"] = np.ascontiguousarray(model_of_node, np.uint8)
+        p.model_of_node = keep["mon"].ctypes.data_as(L._u8p)
+        if setup.gkr_scale is not None:
+            keep["gkr"] = np.ascontiguousarray(setup.gkr_scale, np.float64)
+            p.gkr_scale = L.dp(keep["gkr"])
+        pi = setup.protocol
+        if pi is not None and not pi.empty():
+            for k in ("node_ptr", "ids", "t_start", "duration", "amplitude", "period"):
+                keep["st_" + k] = getattr(pi, k)
+            p.n_stim = pi.n_entries
+            p.stim_t_start, p.stim_duration = L.dp(pi.t_start), L.dp(pi.duration)
+            p.stim_amplitude, p.stim_period = L.dp(pi.amplitude), L.dp(pi.period)
+            p.stim_node_ptr = pi.node_ptr.ctypes.data_as(L._i32p)
+            p.stim_ids = pi.ids.ctypes.data_as(L._i32p)
+        keep["probes"] = np.array([pr.node for pr in setup.probes] or [0], np.int64)
+        p.n_probes = len(setup.probes)
+        p.probes = L.lp(keep["probes"])
+        p.lat_threshold_mv = setup.lat_threshold_mv
+        p.map_interval_ms = setup.map_interval_ms
+        p.scheme, p.dt_ms, p.t_end_ms = int(cfg.scheme), cfg.dt_ms, cfg.t_end_ms
+        p.k0_up, p.k0_down, p.strict_substeps = cfg.k0_up, cfg.k0_down, int(cfg.strict_substeps)
+        p.record_interval_ms = cfg.record_interval_ms
+        p.device, p.rank, p.world = device, rank, world
+        if world > 1:
+            if nccl_id is None or len(nccl_id) != 128:
+                raise ValidationError("placement: world > 1 needs a 128-byte NCCL unique id")
+            keep["nid"] = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
+            p.nccl_id = C.cast(keep["nid"], C.POINTER(C.c_ubyte))
+        err = L.cwg_error()
+        h = C.c_void_p()
+        _check(L.lib().cwg_create(C.byref(p), C.byref(h), C.byref(err)), err)
+        self._h = h
+        self._keep = keep
+        self.n = n
+        self.rank, self.world = rank, world
+        info = L.cwg_info()
+        L.lib().cwg_get_info(h, C.byref(info))
+        self.info = info
+        self._state_id = None
+
+    def close(self):
+        if getattr(self, "_h", None) and L._lib is not None:
+            L._lib.cwg_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    # --- reference accessors
+    def dt_effective(self):
+        return self.info.dt_effective
+
+    def plan(self):
+        return DiffusionPlan(self.info.l, self.info.dt_ad)
+
+    def k_max_global(self):
+        return self.info.k_max_global
+
+    def k_histogram(self):
+        h = np.zeros(self.info.k_max_global + 1, np.int64)
+        _check(L.lib().cwg_get_khist(self._h, L.lp(h), len(h)))
+        return h
+
+    def timing(self):
+        r, d, rec = C.c_double(), C.c_double(), C.c_double()
+        L.lib().cwg_get_timing(self._h, C.byref(r), C.byref(d), C.byref(rec))
+        return TimingBreakdown(r.value + d.value + rec.value, r.value, d.value, rec.value)
+
+    def launch_count(self):
+        return L.lib().cwg_launch_count(self._h)
+
+    def stream(self):
+        return L.lib().cwg_stream(self._h)
+
+    def set_stream(self, cuda_stream_handle):
+        _check(L.lib().cwg_set_stream(self._h, cuda_stream_handle))
+
+    # --- state movement
+    def upload(self, state: NodeStateArray):
+        _check(L.lib().cwg_upload_state(self._h, L.dp(state.v), L.dp(state.s), state.stride, L.dp(state.last_dvdt)))
+        self._state_id = id(state)
+
+    def download(self, state: NodeStateArray):
+        _check(L.lib().cwg_download_state(self._h, L.dp(state.v), L.dp(state.s), state.stride, L.dp(state.last_dvdt)))
+
+    def advance(self, state: NodeStateArray, t_ms: float, step_index: int, n_steps: int, sync_state=True):
+        """One outer step; mutates `state` in place like splitting.cpp:171-181."""
+        if self._state_id != id(state):
+            self.upload(state)
+        err = L.cwg_error()
+        rc = L.lib().cwg_advance(self._h, t_ms, step_index, n_steps, C.byref(err))
+        if sync_state or rc == L.CWG_EINSTABILITY:
+            self.download(state)
+        _check(rc, err)
+
+    # --- run_simulation pieces
+    def run_begin(self):
+        _check(L.lib().cwg_run_begin(self._h))
+
+    def run_steps(self, first, count):
+        _check(L.lib().cwg_run_steps(self._h, first, count))
+
+    def run_sync(self):
+        err = L.cwg_error()
+        _check(L.lib().cwg_run_sync(self._h, C.byref(err)), err)
+
+    def traces(self):
+        ns, npb = self.info.n_samples, len(self.setup.probes)
+        t = np.zeros(ns)
+        v = np.zeros(max(npb, 1) * ns)
+        _check(L.lib().cwg_get_traces(self._h, L.dp(t), L.dp(v)))
+        return t, v[: npb * ns].reshape(npb, ns)
+
+    def maps(self):
+        n = self.info.n_local
+        lat, apd = np.zeros(n), np.zeros(n)
+        lv, av = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        _check(L.lib().cwg_get_maps(self._h, L.dp(lat), lv.ctypes.data_as(L._u8p), L.dp(apd),
+                                    av.ctypes.data_as(L._u8p)))
+        return ScalarMap(lat, lv.astype(bool)), ScalarMap(apd, av.astype(bool))
+
+
+def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeConfig, device=0,
+                   integrator: StrangIntegrator = None) -> SimulationResult:
+    """run_simulation (splitting.cpp:219-294) on the GPU; raises InstabilityError like the reference."""
+    import time
+    t0 = time.perf_counter()
+    integ = integrator or StrangIntegrator(setup, cfg, model_of_node=state.model_of_node, device=device)
+    integ.upload(state)
+    integ.run_begin()
+    integ.run_steps(0, integ.info.n_steps)
+    integ.run_sync()
+    final = state.copy()
+    integ.download(final)
+    t, v = integ.traces()
+    lat, apd = integ.maps()
+    traces = [Trace(pr.node, pr.name, t.copy(), v[q].copy()) for q, pr in enumerate(setup.probes)]
+    tb = TimingBreakdown(total_ms=(time.perf_counter() - t0) * 1e3)
+    return SimulationResult(traces, lat, apd, tb, integ.k_histogram(), integ.dt_effective(), setup.op.dt_s,
+                            integ.plan(), integ.info.n_steps, final)
+
+
+def diffusion_substep(op: AssembledOperator, v, dt_sub: float, device=0):
+    """diffusion_substep (fem.cpp:194-207) on the GPU, bit-identical to the reference."""
+    v = np.ascontiguousarray(v, np.float64)
+    out = np.empty_like(v)
+    rp = np.ascontiguousarray(op.row_ptr, np.int64)
+    col = np.ascontiguousarray(op.col, np.int64)
+    val = np.ascontiguousarray(op.val, np.float64)
+    mass = np.ascontiguousarray(op.lumped_mass, np.float64)
+    err = L.cwg_error()
+    _check(L.lib().cwg_diffusion_substep(len(mass), L.lp(rp), L.lp(col), L.dp(val), L.dp(mass), L.dp(v), dt_sub,
+                                         L.dp(out), device, C.byref(err)), err)
+    return out
+
+
+def slab_plan(ny1: int, world: int, rank: int):
+    b, e = C.c_int64(), C.c_int64()
+    if L.lib().cwg_slab_plan(ny1, world, rank, C.byref(b), C.byref(e)):
+        raise ValidationError("placement: fewer rows than ranks")
+    return b.value, e.value

@@ -1,0 +1,1241 @@
+// Host runtime of the cwgpu C ABI (include/cwgpu.h): device-resident solver
+// context, state upload/download, the DAETI step sequence
+// (StrangIntegrator::advance, splitting.cpp:171-181) and run_simulation's
+// outer loop with its record cadence (splitting.cpp:219-294), replayed as
+// CUDA graphs; y-slab halo exchange over NCCL for world > 1.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/cwgpu.h"
+#include "launch.h"
+
+using namespace cwg;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct Fail {
+  int code;
+  std::string msg;
+};
+
+void set_error(cwg_error* e, int code, const std::string& msg) {
+  if (!e) return;
+  e->code = code;
+  e->node = -1;
+  e->t_ms = 0.0;
+  e->phase = 0;
+  std::snprintf(e->msg, sizeof(e->msg), "%s", msg.c_str());
+}
+
+#define CUDA_TRY(x)                                                                              \
+  do {                                                                                           \
+    cudaError_t _e = (x);                                                                        \
+    if (_e != cudaSuccess)                                                                       \
+      throw Fail{CWG_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(_e) + " at " #x};  \
+  } while (0)
+
+void validation(bool ok, const std::string& msg) {
+  if (!ok) throw Fail{CWG_EVALIDATION, msg};
+}
+
+// ------------------------------------------------------------------ models
+int state_count(int kind) {
+  switch (kind) {
+    case CWG_MODEL_ALIEV_PANFILOV: return 1;
+    case CWG_MODEL_ORD_ENDO:
+    case CWG_MODEL_ORD_EPI:
+    case CWG_MODEL_ORD_MID: return 40;
+    case CWG_MODEL_MACCANNELL: return 2;
+    case CWG_MODEL_PASSIVE: return 0;
+    default: return -1;
+  }
+}
+
+double stable_step(int kind) {
+  switch (kind) {
+    case CWG_MODEL_ALIEV_PANFILOV: return 1.0;
+    case CWG_MODEL_MACCANNELL: return 0.1;
+    case CWG_MODEL_PASSIVE: return 1.0;
+    default: return 0.01;
+  }
+}
+
+bool is_ord(int kind) { return kind >= CWG_MODEL_ORD_ENDO && kind <= CWG_MODEL_ORD_MID; }
+
+// k_max_for (splitting.cpp:69-72)
+int kmax_for(double dt, int kind) {
+  const int k = static_cast<int>(std::floor(dt / stable_step(kind)));
+  return k < 1 ? 1 : k;
+}
+
+long long llround_ref(double x) { return std::llround(x); }
+
+// Published quiescent states [V, s...] of the ORd variants (model constants,
+// ohara_rudy_2011.cpp:454-489), state order of StateIndex.
+const double kOrdRest[3][41] = {
+    {-88.069987424096993, 6.7857694543304437, 6.7858240866305497, 145.2270611623554,
+     145.22703970422316, 6.6496500901714538e-05, 6.5363220572944042e-05, 1.1773572696330052,
+     1.1780931136267005, 0.0072940079209426727, 0.7004598461826681, 0.70045979343293074,
+     0.70045953530570237, 0.45778977781006114, 0.70045939195427553, 0.0001858428745214649,
+     0.51535061430259566, 0.31721806727437052, 0.0009965088352518912, 0.99955951365975104,
+     0.99955949399976396, 0.00050774700555622921, 0.99955951368195861, 0.99955949654005649,
+     2.3033854222194026e-09, 0.99999999104293114, 0.99999999105447779, 0.99999999104293658,
+     0.99999999104087156, 0.99999999104142678, 0.0010021110565670483, 0.99999999104268988,
+     0.99999999104270343, 7.9332827982721131e-06, 7.9336066064785696e-06,
+     0.00019132437263296958, 0.00019132414231280508, 0.99674141905341751,
+     5.4200685188624244e-08, 6.7752012471923812e-08, 0.0003810650518518126},
+    {-88.029323128607928, 6.7962192631889486, 6.7962623821225367, 145.20458892004748,
+     145.20456959400204, 5.4852819578522002e-05, 5.4064603199250324e-05, 1.2563944307309074,
+     1.2563851562790889, 0.0073238975664768622, 0.69905606284853461, 0.69905600543119961,
+     0.69905572480467026, 0.45613173681108238, 0.69905556898249277, 0.00018728379656753348,
+     0.51399396544560239, 0.3160425988040147, 0.00099924415555908345, 0.99955636760901723,
+     0.99955636599890663, 0.00050914140569242004, 0.99955636761083866, 0.99955636620603716,
+     2.3256353623298777e-09, 0.99999999094384107, 0.99999999095528003, 0.99999999094384651,
+     0.99999999094178149, 0.99999999094233671, 0.00047971941613231592, 0.9999999909435997,
+     0.99999999094361336, 7.9809446184557774e-06, 7.9812954631181394e-06,
+     0.00019219809297998605, 0.00019219700739629426, 0.99675215233995673,
+     1.0117197919343792e-07, 1.2646498743342686e-07, 0.00025496603469158611},
+    {-87.918787307816828, 6.8844140619690002, 6.8844676613520441, 145.13903811434193,
+     145.13902449899223, 6.3130680404950644e-05, 6.1753113171964479e-05, 1.1286605779696908,
+     1.129987340810549, 0.00740576098250912, 0.69522137580095822, 0.69522116072571494,
+     0.69522011165021347, 0.45162926254354163, 0.69521952838802525, 0.00019125728633946081,
+     0.51029968338090503, 0.31284466603507399, 0.0010067174531280458, 0.99954770073199861,
+     0.99954761833889205, 0.00051295113113861634, 0.99954770082322897, 0.99954762898761162,
+     2.3872087752034307e-09, 0.99999999066891365, 0.99999999064687006, 0.99999999066891909,
+     0.99999999066685408, 0.9999999906674093, 0.00080416517322784442, 0.99999999066867218,
+     0.99999999066868595, 8.1119973876114768e-06, 8.1133560675743664e-06,
+     0.00019463394428381671, 0.00019459031922160661, 0.99678115341920093,
+     1.7708324928868821e-07, 2.2136126205224297e-07, 0.00034040551198936118}};
+
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed)
+struct Nccl {
+  void* h = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) gstart = nullptr;
+  decltype(&ncclGroupEnd) gend = nullptr;
+  decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclGetErrorString) errstr = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names)
+      if ((h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return false;
+    init = reinterpret_cast<decltype(init)>(dlsym(h, "ncclCommInitRank"));
+    destroy = reinterpret_cast<decltype(destroy)>(dlsym(h, "ncclCommDestroy"));
+    send = reinterpret_cast<decltype(send)>(dlsym(h, "ncclSend"));
+    recv = reinterpret_cast<decltype(recv)>(dlsym(h, "ncclRecv"));
+    gstart = reinterpret_cast<decltype(gstart)>(dlsym(h, "ncclGroupStart"));
+    gend = reinterpret_cast<decltype(gend)>(dlsym(h, "ncclGroupEnd"));
+    allreduce = reinterpret_cast<decltype(allreduce)>(dlsym(h, "ncclAllReduce"));
+    errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
+    return init && destroy && send && recv && gstart && gend && allreduce && errstr;
+  }
+};
+Nccl g_nccl;
+
+#define NCCL_TRY(x)                                                                                     \
+  do {                                                                                                  \
+    ncclResult_t _r = (x);                                                                              \
+    if (_r != ncclSuccess) throw Fail{CWG_ECUDA, std::string("NCCL error: ") + g_nccl.errstr(_r)};    \
+  } while (0)
+
+template <class T>
+T* dev_alloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) count = 1;
+  CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+template <class T>
+void dev_free(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+}  // namespace
+
+// ====================================================================== ctx
+struct Bin {
+  int model = 0, kind = 0;
+  int32_t* d_list = nullptr;  // nullptr: dense [first, first+count)
+  long long first = 0, count = 0;
+  int grid = 1;
+  unsigned* d_counter = nullptr;  // [0] counter, [1] done
+};
+
+struct cwg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+
+  // problem geometry
+  long long n_global = 0, w = 0, ny1 = 0;
+  int op_kind = CWG_OP_CSR;
+  int rank = 0, world = 1;
+  long long row_begin = 0, row_end = 0;  // owned rows (stencil / slab)
+  long long n_own = 0, halo = 0, n_alloc = 0;
+  long long node_offset = 0;  // global index of local index 0
+  long long own_global0 = 0;  // global index of the first owned node
+
+  // scheme
+  int scheme = CWG_DAETI;
+  double dt = 0.1, dt_s = 0, t_end = 0, dt_eff = 0, dt_ad = 0;
+  int l = 1, k0_up = 5, k0_down = 1, strict = 0;
+  double record_interval = 1.0, map_interval = 1.0;
+  long long n_steps = 0, spr = 1, spm = 1, evs = 3;
+  int kmax_global = 1, stride = 1;
+  std::vector<int> model_kind, kmax_of_model;
+
+  // device state
+  double* d_v[2] = {nullptr, nullptr};
+  int cur = 0;
+  double* d_S = nullptr;
+  long long pitch = 0;
+  double* d_last = nullptr;
+  double* d_gkr = nullptr;
+
+  // operator
+  double* d_coef = nullptr;  // stencil: [9][n_own]
+  double* d_cm = nullptr;    // dt_ad / m_i
+  long long* d_rp = nullptr;
+  long long* d_col = nullptr;
+  double* d_val = nullptr;
+
+  // stimulus
+  int32_t* d_stim_ptr = nullptr;
+  int32_t* d_stim_ids = nullptr;
+  double *d_st0 = nullptr, *d_sdur = nullptr, *d_samp = nullptr, *d_sper = nullptr;
+
+  std::vector<Bin> bins;
+
+  // bookkeeping
+  ErrRec* d_err = nullptr;
+  long long* d_clock = nullptr;
+  unsigned long long* d_khist = nullptr;
+  int khist_len = 2;
+
+  // recording
+  DetDev det{};
+  double lat_threshold = 0.0;
+  int n_probes = 0;
+  long long* d_probe_loc = nullptr;
+  double* d_traces = nullptr;
+  long long n_samples = 0;
+  bool det_initialised = false;
+
+  // graphs
+  long long G = 0;
+  cudaGraphExec_t graph = nullptr;
+  long long graph_base_mod = 0;
+  long long graph_launches = 0;
+  long long clock_at = -1;  // host knowledge of *d_clock, -1 unknown
+
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+
+  // stats / timing
+  long long launches = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  double t_react = 0, t_diff = 0, t_rec = 0;
+
+  // pinned staging
+  double *h_v = nullptr, *h_s = nullptr, *h_last = nullptr;
+  double* d_stage = nullptr;
+  long long stage_nodes = 0;
+};
+
+namespace {
+
+void ctx_free(cwg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto& b : c->bins) {
+    dev_free(b.d_list);
+    dev_free(b.d_counter);
+  }
+  dev_free(c->d_v[0]);
+  dev_free(c->d_v[1]);
+  dev_free(c->d_S);
+  dev_free(c->d_last);
+  dev_free(c->d_gkr);
+  dev_free(c->d_coef);
+  dev_free(c->d_cm);
+  dev_free(c->d_rp);
+  dev_free(c->d_col);
+  dev_free(c->d_val);
+  dev_free(c->d_stim_ptr);
+  dev_free(c->d_stim_ids);
+  dev_free(c->d_st0);
+  dev_free(c->d_sdur);
+  dev_free(c->d_samp);
+  dev_free(c->d_sper);
+  dev_free(c->d_err);
+  dev_free(c->d_clock);
+  dev_free(c->d_khist);
+  dev_free(c->d_probe_loc);
+  dev_free(c->d_traces);
+  dev_free(c->d_stage);
+  double** dd[] = {&c->det.prev_v, &c->det.v_rest, &c->det.max_slope, &c->det.t_max_slope, &c->det.v_peak,
+                   &c->det.lat, &c->det.apd};
+  for (auto p : dd) dev_free(*p);
+  dev_free(c->det.phase);
+  dev_free(c->det.has_lat);
+  dev_free(c->det.has_apd);
+  if (c->h_v) cudaFreeHost(c->h_v);
+  if (c->h_s) cudaFreeHost(c->h_s);
+  if (c->h_last) cudaFreeHost(c->h_last);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+template <class T>
+T* upload(const T* h, size_t count) {
+  T* d = dev_alloc<T>(count);
+  if (count) CUDA_TRY(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// ---------------------------------------------------------------- step pieces
+void halo_exchange(cwg_ctx* c, double* buf) {
+  if (c->world <= 1) return;
+  const size_t w = static_cast<size_t>(c->w);
+  NCCL_TRY(g_nccl.gstart());
+  if (c->rank > 0) {
+    NCCL_TRY(g_nccl.send(buf + w, w, ncclDouble, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(buf, w, ncclDouble, c->rank - 1, c->comm, c->stream));
+  }
+  if (c->rank + 1 < c->world) {
+    NCCL_TRY(g_nccl.send(buf + c->n_own, w, ncclDouble, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(buf + c->n_own + w, w, ncclDouble, c->rank + 1, c->comm, c->stream));
+  }
+  NCCL_TRY(g_nccl.gend());
+}
+
+void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
+  for (int q = 0; q < count; ++q) {
+    double* vin = c->d_v[c->cur];
+    double* vout = c->d_v[c->cur ^ 1];
+    halo_exchange(c, vin);
+    DiffArgs a{};
+    a.vin = vin;
+    a.vout = vout;
+    a.n = c->n_own;
+    a.halo = c->halo;
+    a.dt_sub = c->dt_ad;
+    a.err = c->d_err;
+    a.clock = c->d_clock;
+    a.step_off = step_off;
+    a.evs = c->evs;
+    a.ev = ev0 + q;
+    a.node_offset = c->own_global0;
+    if (c->op_kind == CWG_OP_STENCIL2D) {
+      Stencil2D s{c->d_coef, c->n_own, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
+      CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
+    } else {
+      CsrDev m{c->d_rp, c->d_col, c->d_val, c->d_cm};
+      CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));
+    }
+    ++c->launches;
+    c->cur ^= 1;
+  }
+}
+
+void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double t_fixed) {
+  for (auto& b : c->bins) {
+    if (b.count == 0) continue;
+    ReactArgs a{};
+    a.v = c->d_v[c->cur];
+    a.S = c->d_S;
+    a.pitch = c->pitch;
+    a.last = c->d_last;
+    a.list = b.d_list;
+    a.first = b.first;
+    a.count = b.count;
+    a.stim = StimDev{c->d_stim_ptr, c->d_stim_ids, c->d_st0, c->d_sdur, c->d_samp, c->d_sper};
+    a.gkr = c->d_gkr;
+    a.dt = c->dt_eff;
+    a.t_fixed = t_fixed;
+    a.use_t_fixed = use_t ? 1 : 0;
+    a.clock = c->d_clock;
+    a.step_off = step_off;
+    a.scheme = c->scheme;
+    a.k0_up = c->k0_up;
+    a.k0_down = c->k0_down;
+    a.kmax = c->kmax_of_model[b.model];
+    a.khist = c->d_khist;
+    a.khist_len = c->khist_len;
+    a.err = c->d_err;
+    a.evs = c->evs;
+    a.ev = ev;
+    a.counter = b.d_counter;
+    a.done = b.d_counter + 1;
+    a.node_offset = c->node_offset;
+    cudaError_t e = is_ord(b.kind) ? launch_react_ord(b.kind, a, b.grid, c->stream)
+                                   : launch_react_exact(b.kind, a, b.grid, c->stream);
+    CUDA_TRY(e);
+    ++c->launches;
+  }
+}
+
+// One outer step (StrangIntegrator::advance, splitting.cpp:171-181) at
+// step = base + off, kernels addressing it as *clock + off. Records (run mode)
+// follow splitting.cpp:274-279: traces when (step+1) % spr == 0, maps when
+// (step+1) % spm == 0.
+void enqueue_step(cwg_ctx* c, long long base, long long off, bool record, bool use_t, double t_fixed) {
+  const long long step = base + off;
+  if (step == 0) enqueue_diffusion(c, c->l, off, 0);  // step I
+  enqueue_reaction(c, off, c->l, use_t, t_fixed);     // step A
+  enqueue_diffusion(c, step == c->n_steps - 1 ? c->l : 2 * c->l, off, c->l + 1);  // step III / merged B
+  if (!record) return;
+  const long long S = step + 1;
+  if (c->n_probes > 0 && S % c->spr == 0) {
+    CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, off + 1,
+                                  c->spr, c->stream));
+    ++c->launches;
+  }
+  if (S % c->spm == 0) {
+    CUDA_TRY(launch_detector_observe(c->d_v[c->cur] + c->halo, c->n_own, 0, c->det, c->d_clock, off + 1, c->spm,
+                                     c->dt_eff, c->stream));
+    ++c->launches;
+  }
+}
+
+void set_clock(cwg_ctx* c, long long value) {
+  if (c->clock_at == value) return;
+  CUDA_TRY(launch_set_clock(c->d_clock, value, c->stream));
+  ++c->launches;
+  c->clock_at = value;
+}
+
+// Graph of G consecutive middle steps (1 <= step, step + G <= n_steps - 1),
+// valid for any base b with b == b0 (mod G) because G is a multiple of both
+// record cadences. Ends with a clock tick so replays chain without host work.
+void build_graph(cwg_ctx* c, long long b0) {
+  cudaGraph_t g = nullptr;
+  const int cur0 = c->cur;
+  CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const long long l0 = c->launches;
+  try {
+    for (long long off = 0; off < c->G; ++off) enqueue_step(c, b0, off, true, false, 0.0);
+    CUDA_TRY(launch_tick_clock(c->d_clock, c->G, c->stream));
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_TRY(cudaStreamEndCapture(c->stream, &g));
+  c->graph_launches = c->launches - l0 + 1;
+  c->launches = l0;
+  CUDA_TRY(cudaGraphInstantiate(&c->graph, g, 0));
+  cudaGraphDestroy(g);
+  if (c->cur != cur0) throw Fail{CWG_ECUDA, "graph block must preserve the V buffer parity"};
+  c->graph_base_mod = ((b0 % c->G) + c->G) % c->G;
+}
+
+long long lcm_ll(long long a, long long b) { return a / std::gcd(a, b) * b; }
+
+}  // namespace
+
+// ====================================================================== C ABI
+namespace {
+
+void build_stencil(cwg_ctx* c, const cwg_problem* p) {
+  // Per-node 9 coefficients taken verbatim from the CSR rows; a row must hold
+  // exactly its in-grid 9-neighbourhood in ascending order.
+  const long long w = c->w;
+  std::vector<double> coef(static_cast<size_t>(9 * c->n_own), 0.0);
+  const long long offs[9] = {-w - 1, -w, -w + 1, -1, 0, 1, w - 1, w, w + 1};
+  for (long long o = 0; o < c->n_own; ++o) {
+    const long long i = c->own_global0 + o;
+    const long long y = i / w, x = i - y * w;
+    int slot = 0;
+    for (long long p_ = p->row_ptr[i]; p_ < p->row_ptr[i + 1]; ++p_) {
+      const long long d = p->col[p_] - i;
+      while (slot < 9 && offs[slot] != d) ++slot;
+      if (slot == 9) throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " is not a 9-point grid row"};
+      const long long gy = y + (slot / 3) - 1, gx = x + (slot % 3) - 1;
+      if (gy < 0 || gy >= c->ny1 || gx < 0 || gx >= w)
+        throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " couples outside the grid"};
+      coef[static_cast<size_t>(slot) * c->n_own + o] = p->val[p_];
+      ++slot;
+    }
+    // every in-grid neighbour must be present (absent ones would be read as 0)
+    int expect = 0;
+    for (int s = 0; s < 9; ++s) {
+      const long long gy = y + (s / 3) - 1, gx = x + (s % 3) - 1;
+      if (gy >= 0 && gy < c->ny1 && gx >= 0 && gx < w) ++expect;
+    }
+    if (p->row_ptr[i + 1] - p->row_ptr[i] != expect)
+      throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " misses grid neighbours"};
+  }
+  c->d_coef = upload(coef.data(), coef.size());
+}
+
+bool stencil_ok(const cwg_problem* p) {
+  if (p->grid_nx1 <= 0 || p->grid_ny1 <= 0 || p->grid_nx1 * p->grid_ny1 != p->n) return false;
+  const long long w = p->grid_nx1;
+  for (long long i = 0; i < p->n; ++i) {
+    const long long y = i / w, x = i - y * w;
+    int expect = 0;
+    for (int s = 0; s < 9; ++s) {
+      const long long gy = y + (s / 3) - 1, gx = x + (s % 3) - 1;
+      if (gy >= 0 && gy < p->grid_ny1 && gx >= 0 && gx < w) ++expect;
+    }
+    if (p->row_ptr[i + 1] - p->row_ptr[i] != expect) return false;
+    long long prev = -1;
+    for (long long q = p->row_ptr[i]; q < p->row_ptr[i + 1]; ++q) {
+      const long long j = p->col[q];
+      const long long jy = j / w, jx = j - jy * w;
+      if (j <= prev || std::llabs(jy - y) > 1 || std::llabs(jx - x) > 1) return false;
+      prev = j;
+    }
+  }
+  return true;
+}
+
+void create_impl(const cwg_problem* p, cwg_ctx* c) {
+  validation(p && p->n > 0, "integrator: empty problem");
+  validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
+  validation(p->n_models > 0 && p->model_kind, "integrator: no cell models");
+  validation(p->dt_ms > 0.0, "scheme: dt must be positive");
+  validation(p->t_end_ms >= p->dt_ms, "scheme: T must be >= dt");
+  validation(p->k0_down >= 1 && p->k0_up >= p->k0_down, "scheme: need k0_up >= k0_down >= 1");
+  validation(p->record_interval_ms > 0.0, "scheme: record interval must be positive");
+  validation(p->scheme >= CWG_OST && p->scheme <= CWG_DAETI, "scheme: unknown scheme");
+  validation(p->dt_s > 0.0, "diffusion sub-steps: dt and dt_s must be positive");
+  validation(p->world >= 1 && p->rank >= 0 && p->rank < p->world, "placement: bad rank/world");
+  validation(p->n < (1ll << 40), "integrator: at most 2^40 nodes");
+
+  c->device = p->device;
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaDeviceProp prop{};
+  CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
+  if (prop.major < 10) throw Fail{CWG_ECUDA, "cwgpu needs an sm_100 (Blackwell) device"};
+  c->num_sms = prop.multiProcessorCount;
+  CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+
+  // ---- scheme (StrangIntegrator ctor, splitting.cpp:74-93)
+  c->scheme = p->scheme;
+  c->dt = p->dt_ms;
+  c->dt_s = p->dt_s;
+  c->t_end = p->t_end_ms;
+  c->k0_up = p->k0_up;
+  c->k0_down = p->k0_down;
+  c->strict = p->strict_substeps;
+  c->record_interval = p->record_interval_ms;
+  c->map_interval = p->map_interval_ms > 0.0 ? p->map_interval_ms : 1.0;
+  c->dt_eff = c->scheme == CWG_OSTAR ? std::min(c->dt, c->dt_s) : c->dt;
+  {
+    int l = 0;
+    double dt_ad = 0;
+    cwg_diffusion_substeps(c->dt_eff, c->dt_s, c->strict, c->scheme, &l, &dt_ad);
+    c->l = l;
+    c->dt_ad = dt_ad;
+  }
+  c->evs = 3ll * c->l + 2;
+  c->model_kind.assign(p->model_kind, p->model_kind + p->n_models);
+  c->stride = 1;
+  for (int m = 0; m < p->n_models; ++m) {
+    validation(state_count(c->model_kind[m]) >= 0, "integrator: unknown model kind " + std::to_string(c->model_kind[m]));
+    c->kmax_of_model.push_back(kmax_for(c->dt_eff, c->model_kind[m]));
+    c->kmax_global = std::max(c->kmax_global, c->kmax_of_model.back());
+    c->stride = std::max(c->stride, state_count(c->model_kind[m]));
+  }
+  validation(c->kmax_global < 2048, "integrator: k_max >= 2048 is not supported");
+  c->khist_len = c->kmax_global + 1;
+  c->n_steps = static_cast<long long>(std::ceil(c->t_end / c->dt_eff - 1e-9));
+  c->spr = std::max<long long>(1, llround_ref(c->record_interval / c->dt_eff));
+  c->spm = std::max<long long>(1, llround_ref(c->map_interval / c->dt_eff));
+
+  // ---- partition and operator layout
+  c->n_global = p->n;
+  int kind = p->op_kind;
+  if (kind == CWG_OP_AUTO) kind = stencil_ok(p) ? CWG_OP_STENCIL2D : CWG_OP_CSR;
+  validation(kind == CWG_OP_CSR || kind == CWG_OP_STENCIL2D, "operator: unsupported op_kind for this build");
+  if (kind == CWG_OP_STENCIL2D) validation(stencil_ok(p), "operator: CSR is not a regular-sheet 9-point operator");
+  c->op_kind = kind;
+  c->rank = p->rank;
+  c->world = p->world;
+  if (kind == CWG_OP_STENCIL2D || p->world > 1) {
+    validation(p->grid_nx1 > 0 && p->grid_ny1 > 0 && p->grid_nx1 * p->grid_ny1 == p->n,
+               "placement: slab decomposition needs the sheet's grid dimensions");
+    c->w = p->grid_nx1;
+    c->ny1 = p->grid_ny1;
+    int64_t rb = 0, re = 0;
+    validation(cwg_slab_plan(c->ny1, c->world, c->rank, &rb, &re) == CWG_OK, "placement: fewer rows than ranks");
+    c->row_begin = rb;
+    c->row_end = re;
+    c->n_own = (re - rb) * c->w;
+    c->halo = c->w;
+    c->own_global0 = rb * c->w;
+    c->node_offset = c->own_global0 - c->halo;
+  } else {
+    c->w = p->grid_nx1;
+    c->ny1 = p->grid_ny1;
+    c->row_begin = 0;
+    c->row_end = p->grid_ny1;
+    c->n_own = p->n;
+    c->halo = 0;
+    c->own_global0 = 0;
+    c->node_offset = 0;
+  }
+  c->n_alloc = c->n_own + 2 * c->halo;
+
+  // ---- device state (SoA, pitch padded to 32 nodes = 256 B)
+  c->pitch = (c->n_alloc + 31) / 32 * 32;
+  c->d_v[0] = dev_alloc<double>(c->n_alloc);
+  c->d_v[1] = dev_alloc<double>(c->n_alloc);
+  CUDA_TRY(cudaMemset(c->d_v[0], 0, c->n_alloc * sizeof(double)));
+  CUDA_TRY(cudaMemset(c->d_v[1], 0, c->n_alloc * sizeof(double)));
+  c->d_S = dev_alloc<double>(static_cast<size_t>(c->pitch) * c->stride);
+  c->d_last = dev_alloc<double>(c->n_alloc);
+  CUDA_TRY(cudaMemset(c->d_S, 0, static_cast<size_t>(c->pitch) * c->stride * sizeof(double)));
+  CUDA_TRY(cudaMemset(c->d_last, 0, c->n_alloc * sizeof(double)));
+
+  // ---- operator upload
+  std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
+  double* d_mass = upload(mass_own.data(), mass_own.size());
+  c->d_cm = dev_alloc<double>(c->n_own);
+  CUDA_TRY(launch_mass_factor(d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  dev_free(d_mass);
+  if (kind == CWG_OP_STENCIL2D) {
+    build_stencil(c, p);
+  } else {
+    validation(p->row_ptr && p->col && p->val, "operator: CSR arrays missing");
+    const long long r0 = c->own_global0, r1 = c->own_global0 + c->n_own;
+    const long long p0 = p->row_ptr[r0], p1 = p->row_ptr[r1];
+    std::vector<long long> rp(static_cast<size_t>(c->n_own + 1));
+    for (long long i = 0; i <= c->n_own; ++i) rp[i] = p->row_ptr[r0 + i] - p0;
+    std::vector<long long> col(static_cast<size_t>(p1 - p0));
+    for (long long q = p0; q < p1; ++q) {
+      const long long lc = p->col[q] - c->node_offset;
+      validation(lc >= 0 && lc < c->n_alloc, "operator: coupling beyond the neighbouring slab rows");
+      col[q - p0] = lc;
+    }
+    c->d_rp = upload(rp.data(), rp.size());
+    c->d_col = upload(col.data(), col.size());
+    c->d_val = upload(p->val + p0, static_cast<size_t>(p1 - p0));
+  }
+
+  // ---- models: per-model node bins over owned nodes (local indices)
+  validation(p->model_of_node != nullptr, "integrator: model_of_node missing");
+  std::vector<std::vector<int32_t>> lists(p->n_models);
+  for (long long o = 0; o < c->n_own; ++o) {
+    const int m = p->model_of_node[c->own_global0 + o];
+    validation(m < p->n_models, "initial state: node " + std::to_string(c->own_global0 + o) + " has no model");
+    lists[m].push_back(static_cast<int32_t>(o + c->halo));
+  }
+  validation(c->n_alloc < (1ll << 31), "integrator: more than 2^31 local nodes per device (use more ranks)");
+  for (int m = 0; m < p->n_models; ++m) {
+    Bin b;
+    b.model = m;
+    b.kind = c->model_kind[m];
+    b.count = static_cast<long long>(lists[m].size());
+    if (b.count == c->n_own) {
+      b.first = c->halo;  // dense
+    } else if (b.count > 0) {
+      b.d_list = upload(lists[m].data(), lists[m].size());
+    }
+    const int threads = is_ord(b.kind) ? react_ord_threads(b.kind) : react_exact_threads(b.kind);
+    const int occ = std::max(1, is_ord(b.kind) ? react_ord_occupancy(b.kind) : react_exact_occupancy(b.kind));
+    const long long need = (b.count + threads - 1) / threads;
+    b.grid = static_cast<int>(std::max<long long>(1, std::min<long long>(need, static_cast<long long>(occ) * c->num_sms)));
+    b.d_counter = dev_alloc<unsigned>(2);
+    CUDA_TRY(cudaMemset(b.d_counter, 0, 2 * sizeof(unsigned)));
+    c->bins.push_back(b);
+  }
+  if (p->gkr_scale) {
+    std::vector<double> g(static_cast<size_t>(c->n_alloc), 1.0);
+    for (long long o = 0; o < c->n_own; ++o) g[o + c->halo] = p->gkr_scale[c->own_global0 + o];
+    c->d_gkr = upload(g.data(), g.size());
+  }
+
+  // ---- stimulus (ProtocolIndex, flattened to the local slab)
+  if (p->n_stim > 0) {
+    validation(p->stim_node_ptr && p->stim_ids && p->stim_t_start && p->stim_duration && p->stim_amplitude &&
+                   p->stim_period, "stimulus: arrays missing");
+    for (int e = 0; e < p->n_stim; ++e) {
+      validation(p->stim_duration[e] > 0.0, "stimulus: duration must be positive");
+      validation(std::isfinite(p->stim_amplitude[e]), "stimulus: amplitude must be finite");
+    }
+    std::vector<int32_t> ptr(static_cast<size_t>(c->n_alloc + 1), 0), ids;
+    for (long long li = 0; li < c->n_alloc; ++li) {
+      const long long g = li + c->node_offset;
+      const bool owned = li >= c->halo && li < c->halo + c->n_own;
+      if (owned && g >= 0 && g < p->n)
+        for (int32_t q = p->stim_node_ptr[g]; q < p->stim_node_ptr[g + 1]; ++q) ids.push_back(p->stim_ids[q]);
+      ptr[static_cast<size_t>(li + 1)] = static_cast<int32_t>(ids.size());
+    }
+    if (!ids.empty()) {
+      c->d_stim_ptr = upload(ptr.data(), ptr.size());
+      c->d_stim_ids = upload(ids.data(), ids.size());
+      c->d_st0 = upload(p->stim_t_start, p->n_stim);
+      c->d_sdur = upload(p->stim_duration, p->n_stim);
+      c->d_samp = upload(p->stim_amplitude, p->n_stim);
+      c->d_sper = upload(p->stim_period, p->n_stim);
+    }
+  }
+
+  // ---- bookkeeping
+  c->d_err = dev_alloc<ErrRec>(1);
+  c->d_clock = dev_alloc<long long>(1);
+  c->d_khist = dev_alloc<unsigned long long>(c->khist_len);
+  ErrRec none{kNoError, -1, 0, 0};
+  CUDA_TRY(cudaMemcpy(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemset(c->d_clock, 0, sizeof(long long)));
+  c->clock_at = 0;
+  CUDA_TRY(cudaMemset(c->d_khist, 0, c->khist_len * sizeof(unsigned long long)));
+
+  // ---- recording
+  c->lat_threshold = p->lat_threshold_mv;
+  c->n_probes = p->n_probes;
+  c->n_samples = c->n_steps / c->spr + 1;
+  if (c->n_probes > 0) {
+    std::vector<long long> loc(static_cast<size_t>(c->n_probes), -1);
+    for (int q = 0; q < c->n_probes; ++q) {
+      const long long g = p->probes[q];
+      validation(g >= 0 && g < p->n, "probe: node out of range");
+      if (g >= c->own_global0 && g < c->own_global0 + c->n_own) loc[q] = g - c->node_offset;
+    }
+    c->d_probe_loc = upload(loc.data(), loc.size());
+    c->d_traces = dev_alloc<double>(static_cast<size_t>(c->n_samples) * c->n_probes);
+    CUDA_TRY(cudaMemset(c->d_traces, 0, static_cast<size_t>(c->n_samples) * c->n_probes * sizeof(double)));
+  }
+  double** dd[] = {&c->det.prev_v, &c->det.v_rest, &c->det.max_slope, &c->det.t_max_slope, &c->det.v_peak,
+                   &c->det.lat, &c->det.apd};
+  for (auto q : dd) *q = dev_alloc<double>(c->n_own);
+  c->det.phase = dev_alloc<unsigned char>(c->n_own);
+  c->det.has_lat = dev_alloc<unsigned char>(c->n_own);
+  c->det.has_apd = dev_alloc<unsigned char>(c->n_own);
+  c->det.threshold = c->lat_threshold;
+
+  // ---- graph block length: a multiple of both record cadences
+  const long long G = lcm_ll(c->spr, c->spm);
+  c->G = G <= 200 ? G : 0;
+
+  // ---- NCCL communicator for the halo exchange
+  if (c->world > 1) {
+    validation(p->nccl_id != nullptr, "placement: world > 1 needs an NCCL unique id");
+    if (!g_nccl.load()) throw Fail{CWG_ECUDA, "NCCL library (libnccl.so.2) not loadable"};
+    ncclUniqueId id;
+    std::memcpy(&id, p->nccl_id, sizeof(id));
+    NCCL_TRY(g_nccl.init(&c->comm, c->world, id, c->rank));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+}
+
+template <class F>
+int guarded(cwg_error* err, F&& f) {
+  try {
+    f();
+    if (err) {
+      err->code = CWG_OK;
+      err->node = -1;
+      err->phase = 0;
+      err->msg[0] = 0;
+    }
+    return CWG_OK;
+  } catch (const Fail& e) {
+    set_error(err, e.code, e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(err, CWG_ECUDA, e.what());
+    return CWG_ECUDA;
+  }
+}
+
+void reset_error(cwg_ctx* c) {
+  ErrRec none{kNoError, -1, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+}
+
+// Read the error record (after a sync) and, for world > 1, agree on the
+// earliest failing event and its lowest node across ranks.
+bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
+  ErrRec r{};
+  CUDA_TRY(cudaMemcpy(&r, c->d_err, sizeof(r), cudaMemcpyDeviceToHost));
+  if (c->world > 1) {
+    long long* tmp = dev_alloc<long long>(2);
+    long long h[2] = {r.key == kNoError ? (1ll << 62) : r.seq, 0};
+    CUDA_TRY(cudaMemcpy(tmp, h, sizeof(long long), cudaMemcpyHostToDevice));
+    NCCL_TRY(g_nccl.allreduce(tmp, tmp, 1, ncclInt64, ncclMin, c->comm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(h, tmp, sizeof(long long), cudaMemcpyDeviceToHost));
+    unsigned long long key = (r.key != kNoError && r.seq == h[0]) ? r.key : kNoError;
+    CUDA_TRY(cudaMemcpy(tmp, &key, sizeof(key), cudaMemcpyHostToDevice));
+    NCCL_TRY(g_nccl.allreduce(tmp, tmp, 1, ncclUint64, ncclMin, c->comm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemcpy(&key, tmp, sizeof(key), cudaMemcpyDeviceToHost));
+    dev_free(tmp);
+    r.key = key;
+    r.seq = h[0];
+  }
+  if (r.key == kNoError) return false;
+  const long long node = static_cast<long long>(r.key >> 22);
+  const long long step = r.seq / c->evs;
+  const long long ev = r.seq % c->evs;
+  const double t = use_t ? t_fixed : static_cast<double>(step) * c->dt_eff;
+  char buf[256];
+  if (ev == c->l) {  // reaction event
+    const int k = static_cast<int>((r.key >> 11) & 2047u);
+    const int j = static_cast<int>(r.key & 2047u);
+    const double dt_ar = c->dt_eff / static_cast<double>(k);
+    const double ts = t + static_cast<double>(j) * dt_ar;
+    std::snprintf(buf, sizeof(buf), "reaction step produced non-finite V (node %lld, t = %f ms)", node, ts);
+    if (out) {
+      out->code = CWG_EINSTABILITY;
+      out->node = node;
+      out->t_ms = ts;
+      out->phase = 1;
+    }
+  } else {
+    std::snprintf(buf, sizeof(buf), "diffusion sub-step produced non-finite V (node %lld, t = %f ms)", node, t);
+    if (out) {
+      out->code = CWG_EINSTABILITY;
+      out->node = node;
+      out->t_ms = t;
+      out->phase = 2;
+    }
+  }
+  if (out) std::snprintf(out->msg, sizeof(out->msg), "%s", buf);
+  return true;
+}
+
+void normalise_parity(cwg_ctx* c) {
+  if (c->cur == 0) return;
+  CUDA_TRY(cudaMemcpyAsync(c->d_v[0], c->d_v[1], c->n_alloc * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  c->cur = 0;
+}
+
+void ensure_stage(cwg_ctx* c) {
+  if (c->d_stage) return;
+  c->stage_nodes = std::min<long long>(c->n_own, 1ll << 20);
+  c->d_stage = dev_alloc<double>(static_cast<size_t>(std::max<long long>(c->stage_nodes, 1)) * c->stride);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cwg_version(void) { return "cwgpu 1 (sm_100a)"; }
+
+int cwg_model_state_count(int kind) { return state_count(kind); }
+
+int cwg_model_rest_state(int kind, double* out) {
+  const int ns = state_count(kind);
+  if (ns < 0) return CWG_EVALIDATION;
+  if (is_ord(kind)) {
+    std::memcpy(out, kOrdRest[kind - CWG_MODEL_ORD_ENDO], 41 * sizeof(double));
+  } else if (kind == CWG_MODEL_ALIEV_PANFILOV) {
+    out[0] = -80.0;
+    out[1] = 0.0;
+  } else if (kind == CWG_MODEL_MACCANNELL) {
+    out[0] = -48.865796143695611;
+    out[1] = 0.067599408770662575;
+    out[2] = 0.97575886906521692;
+  } else {
+    out[0] = -85.0;  // passive: its reversal potential
+  }
+  return CWG_OK;
+}
+double cwg_model_stable_step(int kind) { return stable_step(kind); }
+
+int cwg_model_kind_from_name(const char* name) {
+  if (!name) return -1;
+  const std::string n(name);
+  if (n == "aliev-panfilov") return CWG_MODEL_ALIEV_PANFILOV;
+  if (n == "ohara2011-endo") return CWG_MODEL_ORD_ENDO;
+  if (n == "ohara2011-epi") return CWG_MODEL_ORD_EPI;
+  if (n == "ohara2011-mid") return CWG_MODEL_ORD_MID;
+  if (n == "maccannell2007") return CWG_MODEL_MACCANNELL;
+  if (n == "passive") return CWG_MODEL_PASSIVE;
+  return -1;
+}
+
+int cwg_reaction_substeps(double dvdt, int scheme, int k0_up, int k0_down, int k_max) {
+  if (scheme == CWG_OST) return 1;
+  const int k0 = dvdt > 0.0 ? k0_up : k0_down;
+  const double raw = static_cast<double>(k0) + std::floor(std::fabs(dvdt));
+  const int k = raw > static_cast<double>(k_max) ? k_max : static_cast<int>(raw);
+  return k < 1 ? 1 : k;
+}
+
+int cwg_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad) {
+  if (!(dt > 0.0) || !(dt_s > 0.0)) return CWG_EVALIDATION;
+  int ll = 1;
+  if (scheme == CWG_DAETI && dt / 2.0 > dt_s) {
+    const double q = dt / (2.0 * dt_s);
+    ll = static_cast<int>(strict ? std::ceil(q) : std::floor(q));
+    if (ll < 1) ll = 1;
+  }
+  *l = ll;
+  *dt_ad = dt / (2.0 * ll);
+  return CWG_OK;
+}
+
+int cwg_k_max_for(double dt, int kind) { return kmax_for(dt, kind); }
+
+int cwg_slab_plan(int64_t ny1, int world, int rank, int64_t* row_begin, int64_t* row_end) {
+  if (world < 1 || rank < 0 || rank >= world || ny1 < world) return CWG_EVALIDATION;
+  const int64_t base = ny1 / world, extra = ny1 % world;
+  *row_begin = rank * base + std::min<int64_t>(rank, extra);
+  *row_end = *row_begin + base + (rank < extra ? 1 : 0);
+  return CWG_OK;
+}
+
+int cwg_create(const cwg_problem* prob, cwg_ctx** out, cwg_error* err) {
+  cwg_ctx* c = new cwg_ctx();
+  const int rc = guarded(err, [&] { create_impl(prob, c); });
+  if (rc != CWG_OK) {
+    ctx_free(c);
+    *out = nullptr;
+    return rc;
+  }
+  *out = c;
+  return CWG_OK;
+}
+
+void cwg_destroy(cwg_ctx* c) { ctx_free(c); }
+
+int cwg_set_stream(cwg_ctx* c, void* s) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) CUDA_TRY(cudaStreamDestroy(c->stream));
+    if (s) {
+      c->stream = static_cast<cudaStream_t>(s);
+      c->own_stream = false;
+    } else {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+  });
+}
+
+void* cwg_stream(cwg_ctx* c) { return c->stream; }
+
+int cwg_upload_state(cwg_ctx* c, const double* v, const double* s_aos, int stride, const double* last) {
+  return guarded(nullptr, [&] {
+    validation(stride >= c->stride, "state: stride smaller than the largest model state count");
+    CUDA_TRY(cudaSetDevice(c->device));
+    c->cur = 0;
+    const long long g0 = c->own_global0;
+    CUDA_TRY(cudaMemcpyAsync(c->d_v[0] + c->halo, v + g0, c->n_own * sizeof(double), cudaMemcpyHostToDevice,
+                             c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_last + c->halo, last + g0, c->n_own * sizeof(double), cudaMemcpyHostToDevice,
+                             c->stream));
+    ensure_stage(c);
+    for (long long o = 0; o < c->n_own; o += c->stage_nodes) {
+      const long long cnt = std::min(c->stage_nodes, c->n_own - o);
+      CUDA_TRY(cudaMemcpyAsync(c->d_stage, s_aos + (g0 + o) * stride, cnt * stride * sizeof(double),
+                               cudaMemcpyHostToDevice, c->stream));
+      CUDA_TRY(launch_aos_to_soa(c->d_stage, stride, c->stride, cnt, c->d_S, c->pitch, c->halo + o, c->stream));
+      ++c->launches;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int cwg_download_state(cwg_ctx* c, double* v, double* s_aos, int stride, double* last) {
+  return guarded(nullptr, [&] {
+    validation(stride >= c->stride, "state: stride smaller than the largest model state count");
+    CUDA_TRY(cudaSetDevice(c->device));
+    const long long g0 = c->own_global0;
+    if (v)
+      CUDA_TRY(cudaMemcpyAsync(v + g0, c->d_v[c->cur] + c->halo, c->n_own * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+    if (last)
+      CUDA_TRY(cudaMemcpyAsync(last + g0, c->d_last + c->halo, c->n_own * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+    if (s_aos) {
+      ensure_stage(c);
+      for (long long o = 0; o < c->n_own; o += c->stage_nodes) {
+        const long long cnt = std::min(c->stage_nodes, c->n_own - o);
+        CUDA_TRY(launch_soa_to_aos(c->d_S, c->pitch, c->halo + o, c->stride, cnt, c->d_stage, stride, c->stream));
+        ++c->launches;
+        CUDA_TRY(cudaMemcpyAsync(s_aos + (g0 + o) * stride, c->d_stage, cnt * stride * sizeof(double),
+                                 cudaMemcpyDeviceToHost, c->stream));
+      }
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int cwg_pinned_buffers(cwg_ctx* c, double** v, double** s_aos, double** last) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->h_v) {
+      CUDA_TRY(cudaMallocHost(&c->h_v, std::max<long long>(c->n_global, 1) * sizeof(double)));
+      CUDA_TRY(cudaMallocHost(&c->h_s, std::max<long long>(c->n_global, 1) * c->stride * sizeof(double)));
+      CUDA_TRY(cudaMallocHost(&c->h_last, std::max<long long>(c->n_global, 1) * sizeof(double)));
+    }
+    *v = c->h_v;
+    *s_aos = c->h_s;
+    *last = c->h_last;
+  });
+}
+
+int cwg_advance(cwg_ctx* c, double t_ms, int64_t step, int64_t n_steps, cwg_error* err) {
+  cwg_error e{};
+  bool inst = false;
+  const int rc = guarded(err, [&] {
+    validation(step < n_steps, "integrator: step index past the end of the run");
+    CUDA_TRY(cudaSetDevice(c->device));
+    reset_error(c);
+    set_clock(c, step);
+    const long long saved = c->n_steps;
+    c->n_steps = n_steps;
+    CUDA_TRY(cudaEventRecord(c->ev[0], c->stream));
+    if (step == 0) enqueue_diffusion(c, c->l, 0, 0);                       // step I
+    CUDA_TRY(cudaEventRecord(c->ev[1], c->stream));
+    enqueue_reaction(c, 0, c->l, true, t_ms);                               // step A
+    CUDA_TRY(cudaEventRecord(c->ev[2], c->stream));
+    enqueue_diffusion(c, step == n_steps - 1 ? c->l : 2 * c->l, 0, c->l + 1);  // step III / B
+    CUDA_TRY(cudaEventRecord(c->ev[3], c->stream));
+    c->n_steps = saved;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    float a = 0, b = 0, d = 0;
+    cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&b, c->ev[1], c->ev[2]);
+    cudaEventElapsedTime(&d, c->ev[2], c->ev[3]);
+    c->t_react += b;
+    c->t_diff += a + d;
+    inst = fetch_error(c, true, t_ms, &e);
+  });
+  if (rc != CWG_OK) return rc;
+  if (inst) {
+    if (err) *err = e;
+    return CWG_EINSTABILITY;
+  }
+  return CWG_OK;
+}
+
+int cwg_run_begin(cwg_ctx* c) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    normalise_parity(c);
+    reset_error(c);
+    CUDA_TRY(cudaMemsetAsync(c->d_khist, 0, c->khist_len * sizeof(unsigned long long), c->stream));
+    set_clock(c, 0);
+    if (c->n_probes > 0) {
+      CUDA_TRY(cudaMemsetAsync(c->d_traces, 0, static_cast<size_t>(c->n_samples) * c->n_probes * sizeof(double),
+                               c->stream));
+      CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, 0, c->spr,
+                                    c->stream));
+      ++c->launches;
+    }
+    CUDA_TRY(launch_detector_init(c->d_v[c->cur] + c->halo, c->n_own, 0, c->det, c->stream));
+    ++c->launches;
+    c->det_initialised = true;
+  });
+}
+
+int cwg_run_steps(cwg_ctx* c, int64_t first, int64_t count) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    validation(first >= 0 && first + count <= c->n_steps, "run: step range outside [0, n_steps)");
+    long long s = first;
+    const long long end = first + count;
+    while (s < end) {
+      const bool block_ok = c->G > 0 && s >= 1 && s + c->G <= c->n_steps - 1 && s + c->G <= end &&
+                            (c->graph == nullptr ? (s % c->G == 1 % c->G) : (s % c->G == c->graph_base_mod));
+      if (block_ok) {
+        set_clock(c, s);
+        if (!c->graph) build_graph(c, s);
+        CUDA_TRY(cudaGraphLaunch(c->graph, c->stream));
+        c->launches += c->graph_launches;
+        c->clock_at = s + c->G;
+        s += c->G;
+      } else {
+        set_clock(c, s);
+        enqueue_step(c, s, 0, true, false, 0.0);
+        ++s;
+      }
+    }
+  });
+}
+
+int cwg_run_sync(cwg_ctx* c, cwg_error* err) {
+  cwg_error e{};
+  bool inst = false;
+  const int rc = guarded(err, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    inst = fetch_error(c, false, 0.0, &e);
+  });
+  if (rc != CWG_OK) return rc;
+  if (inst) {
+    if (err) *err = e;
+    return CWG_EINSTABILITY;
+  }
+  return CWG_OK;
+}
+
+int cwg_run(cwg_ctx* c, cwg_error* err) {
+  int rc = cwg_run_begin(c);
+  if (rc) return rc;
+  rc = cwg_run_steps(c, 0, c->n_steps);
+  if (rc) return rc;
+  return cwg_run_sync(c, err);
+}
+
+int cwg_get_info(cwg_ctx* c, cwg_info* i) {
+  i->dt_effective = c->dt_eff;
+  i->dt_s = c->dt_s;
+  i->dt_ad = c->dt_ad;
+  i->l = c->l;
+  i->k_max_global = c->kmax_global;
+  i->n_steps = c->n_steps;
+  i->steps_per_record = c->spr;
+  i->steps_per_map = c->spm;
+  i->n_samples = c->n_samples;
+  i->n_local = c->n_own;
+  i->node_begin = c->own_global0;
+  i->op_kind = c->op_kind;
+  return CWG_OK;
+}
+
+int cwg_get_khist(cwg_ctx* c, int64_t* out, int len) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (c->world > 1) {
+      unsigned long long* tmp = dev_alloc<unsigned long long>(c->khist_len);
+      NCCL_TRY(g_nccl.allreduce(c->d_khist, tmp, c->khist_len, ncclUint64, ncclSum, c->comm, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      std::vector<unsigned long long> h(c->khist_len);
+      CUDA_TRY(cudaMemcpy(h.data(), tmp, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
+      dev_free(tmp);
+      for (int k = 0; k < len; ++k) out[k] = k < c->khist_len ? static_cast<int64_t>(h[k]) : 0;
+    } else {
+      std::vector<unsigned long long> h(c->khist_len);
+      CUDA_TRY(cudaMemcpy(h.data(), c->d_khist, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
+      for (int k = 0; k < len; ++k) out[k] = k < c->khist_len ? static_cast<int64_t>(h[k]) : 0;
+    }
+  });
+}
+
+int cwg_get_traces(cwg_ctx* c, double* t_ms, double* v) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    for (long long q = 0; q < c->n_samples; ++q) t_ms[q] = static_cast<double>(q * c->spr) * c->dt_eff;
+    if (c->n_probes == 0) return;
+    const size_t cnt = static_cast<size_t>(c->n_samples) * c->n_probes;
+    double* src = c->d_traces;
+    double* tmp = nullptr;
+    if (c->world > 1) {  // non-owned probes are 0 on each rank
+      tmp = dev_alloc<double>(cnt);
+      NCCL_TRY(g_nccl.allreduce(c->d_traces, tmp, cnt, ncclDouble, ncclSum, c->comm, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      src = tmp;
+    }
+    std::vector<double> h(cnt);
+    CUDA_TRY(cudaMemcpy(h.data(), src, cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    if (tmp) dev_free(tmp);
+    for (int p = 0; p < c->n_probes; ++p)
+      for (long long q = 0; q < c->n_samples; ++q) v[p * c->n_samples + q] = h[q * c->n_probes + p];
+  });
+}
+
+int cwg_get_maps(cwg_ctx* c, double* lat, uint8_t* lat_valid, double* apd, uint8_t* apd_valid) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const size_t n = static_cast<size_t>(c->n_own);
+    std::vector<double> L(n), A(n);
+    std::vector<unsigned char> lv(n), av(n);
+    CUDA_TRY(cudaMemcpy(L.data(), c->det.lat, n * sizeof(double), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(A.data(), c->det.apd, n * sizeof(double), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(lv.data(), c->det.has_lat, n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(av.data(), c->det.has_apd, n, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) {
+      if (lat) lat[i] = lv[i] ? L[i] : std::nan("");
+      if (lat_valid) lat_valid[i] = lv[i];
+      if (apd) apd[i] = av[i] ? A[i] : std::nan("");
+      if (apd_valid) apd_valid[i] = av[i];
+    }
+  });
+}
+
+int cwg_get_timing(cwg_ctx* c, double* r, double* d, double* rec) {
+  *r = c->t_react;
+  *d = c->t_diff;
+  *rec = c->t_rec;
+  return CWG_OK;
+}
+
+int64_t cwg_launch_count(cwg_ctx* c) { return c->launches; }
+
+int cwg_diffusion_substep(int64_t n, const int64_t* rp, const int64_t* col, const double* val, const double* mass,
+                          const double* v, double dt_sub, double* out, int device, cwg_error* err) {
+  return guarded(err, [&] {
+    CUDA_TRY(cudaSetDevice(device));
+    const long long nnz = rp[n];
+    long long* d_rp = upload(reinterpret_cast<const long long*>(rp), n + 1);
+    long long* d_col = upload(reinterpret_cast<const long long*>(col), nnz);
+    double* d_val = upload(val, nnz);
+    double* d_m = upload(mass, n);
+    double* d_v = upload(v, n);
+    double* d_o = dev_alloc<double>(n);
+    CUDA_TRY(launch_diffuse_csr_plain(n, d_rp, d_col, d_val, d_m, d_v, dt_sub, d_o, nullptr));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(out, d_o, n * sizeof(double), cudaMemcpyDeviceToHost));
+    dev_free(d_rp);
+    dev_free(d_col);
+    dev_free(d_val);
+    dev_free(d_m);
+    dev_free(d_v);
+    dev_free(d_o);
+  });
+}
+
+int cwg_rates(int kind, int64_t n, const double* v, const double* s, const double* ist, double* dv, double* ds,
+              int device, cwg_error* err) {
+  return guarded(err, [&] {
+    validation(state_count(kind) >= 0, "unknown cell model kind");
+    CUDA_TRY(cudaSetDevice(device));
+    const int ns = state_count(kind);
+    double* d_v = upload(v, n);
+    double* d_s = upload(s, static_cast<size_t>(n) * ns);
+    double* d_i = upload(ist, n);
+    double* d_dv = dev_alloc<double>(n);
+    double* d_ds = dev_alloc<double>(static_cast<size_t>(n) * ns);
+    CUDA_TRY(is_ord(kind) ? launch_rates_ord(kind, n, d_v, d_s, d_i, d_dv, d_ds, nullptr)
+                          : launch_rates_exact(kind, n, d_v, d_s, d_i, d_dv, d_ds, nullptr));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(dv, d_dv, n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (ns) CUDA_TRY(cudaMemcpy(ds, d_ds, static_cast<size_t>(n) * ns * sizeof(double), cudaMemcpyDeviceToHost));
+    dev_free(d_v);
+    dev_free(d_s);
+    dev_free(d_i);
+    dev_free(d_dv);
+    dev_free(d_ds);
+  });
+}
+
+}  // extern "C"

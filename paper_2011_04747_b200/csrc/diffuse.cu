@@ -1,0 +1,269 @@
+// Diffusion sub-step, activation detector, probe recording and layout
+// kernels. Compiled with --fmad=false: every product and sum rounds exactly
+// like the reference's x86-64 build, so diffusion is bit-identical to
+// diffusion_substep (fem.cpp:194-207) and the detector to
+// ActivationDetector::observe (postprocess.cpp:18-66).
+#include "launch.h"
+
+namespace cwg {
+
+// ---------------------------------------------------------------------------
+// Stencil-2D: a regular sheet's 9-point rows with per-node coefficients taken
+// verbatim from the CSR (absent boundary entries stored as 0 and skipped
+// without reading V, so 0*Inf never appears). Row sums run in ascending
+// column order starting from 0.0 like fem.cpp:202-205.
+//   coef[c*cpitch + i], c = 0..8 for offsets {-w-1,-w,-w+1,-1,0,1,w-1,w,w+1}
+//   cm[i] = dt_sub / m_i (the reference's own division)
+// Local layout per rank: one halo row (w nodes) below and above the owned
+// rows; the owned row r (0-based) starts at (r+1)*w.
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s) {
+  const long long nown = s.rows * s.w;
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = o + s.w;  // local index
+    const double vi = a.vin[i];
+    if (skip) {
+      a.vout[i] = vi;
+      continue;
+    }
+    const long long r = o / s.w, x = o - r * s.w;
+    const long long gy = s.row_begin + r;
+    const bool has_s = gy > 0, has_n = gy + 1 < s.ny1, has_w = x > 0, has_e = x + 1 < s.w;
+    const double* c = s.coef + o;
+    const long long P = s.cpitch;
+    double acc = 0.0;
+    if (has_s) {
+      if (has_w) acc += c[0 * P] * a.vin[i - s.w - 1];
+      acc += c[1 * P] * a.vin[i - s.w];
+      if (has_e) acc += c[2 * P] * a.vin[i - s.w + 1];
+    }
+    if (has_w) acc += c[3 * P] * a.vin[i - 1];
+    acc += c[4 * P] * vi;
+    if (has_e) acc += c[5 * P] * a.vin[i + 1];
+    if (has_n) {
+      if (has_w) acc += c[6 * P] * a.vin[i + s.w - 1];
+      acc += c[7 * P] * a.vin[i + s.w];
+      if (has_e) acc += c[8 * P] * a.vin[i + s.w + 1];
+    }
+    const double out = vi - s.cm[o] * acc;
+    a.vout[i] = out;
+    if (!isfinite(out))
+      record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.w) << 22, seq, 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generic CSR (fem.cpp:201-206), one thread per row, ascending columns.
+// cols are local indices into vin; row i (owned) lives at vin[halo + i].
+// ---------------------------------------------------------------------------
+
+__global__ void __launch_bounds__(256) diffuse_csr(DiffArgs a, CsrDev m) {
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < a.n;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = o + a.halo;
+    if (skip) {
+      a.vout[i] = a.vin[i];
+      continue;
+    }
+    double acc = 0.0;
+    const long long p1 = m.row_ptr[o + 1];
+    for (long long p = m.row_ptr[o]; p < p1; ++p) acc += m.val[p] * a.vin[m.col[p]];
+    const double out = a.vin[i] - m.cm[o] * acc;
+    a.vout[i] = out;
+    if (!isfinite(out)) record_failure(a.err, static_cast<unsigned long long>(o + a.node_offset) << 22, seq, 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ActivationDetector::observe (postprocess.cpp:18-66), SoA node state.
+// t = S*dt, previous sample time = (S - every)*dt, both computed exactly as
+// the reference computed the times it stored (splitting.cpp:272).
+// ---------------------------------------------------------------------------
+
+__global__ void detector_init(const double* v, long long n, long long halo, DetDev d) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double x = v[i + halo];
+  d.prev_v[i] = x;
+  d.v_rest[i] = x;
+  d.max_slope[i] = -INFINITY;
+  d.t_max_slope[i] = 0.0;
+  d.v_peak[i] = 0.0;
+  d.lat[i] = 0.0;
+  d.apd[i] = 0.0;
+  d.phase[i] = 0;
+  d.has_lat[i] = 0;
+  d.has_apd[i] = 0;
+}
+
+__global__ void detector_observe(const double* v, long long n, long long halo, DetDev d, const long long* clock,
+                                 long long s_off, long long every, double dt) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const long long S = *clock + s_off;
+  const double t = static_cast<double>(S) * dt;
+  const double pt = static_cast<double>(S - every) * dt;
+  const double h = t - pt;
+  if (d.phase[i] == 2) return;
+  const double x = v[i + halo], px = d.prev_v[i];
+  const double slope = (x - px) / h;
+  if (slope > d.max_slope[i]) {
+    d.max_slope[i] = slope;
+    d.t_max_slope[i] = pt + 0.5 * h;
+  }
+  const double thr = d.threshold;
+  if (d.phase[i] == 0) {
+    if (px < thr && x >= thr) {
+      d.lat[i] = pt + (thr - px) / (x - px) * h;
+      d.has_lat[i] = 1;
+      d.phase[i] = 1;
+      d.v_peak[i] = x;
+    } else {
+      const double r = d.v_rest[i];
+      d.v_rest[i] = x < r ? x : r;  // std::min(r, x)
+    }
+  } else {
+    double pk = d.v_peak[i];
+    pk = pk < x ? x : pk;  // std::max(pk, x)
+    d.v_peak[i] = pk;
+    const double rest = d.v_rest[i];
+    const double v90 = pk - 0.9 * (pk - rest);
+    if (px >= v90 && x < v90 && pk - rest >= 20.0) {
+      const double tc = pt + (px - v90) / (px - x) * h;
+      d.apd[i] = tc - d.t_max_slope[i];
+      d.has_apd[i] = 1;
+      d.phase[i] = 2;
+    }
+  }
+  d.prev_v[i] = x;
+}
+
+// probe samples: out[sample * np + p] = v[loc[p]] for owned probes (loc >= 0)
+__global__ void record_probes(const double* v, const long long* loc, int np, double* out, const long long* clock,
+                              long long s_off, long long every) {
+  const int p = threadIdx.x + blockIdx.x * blockDim.x;
+  if (p >= np) return;
+  const long long S = *clock + s_off;
+  const long long sample = S / every;
+  const long long l = loc[p];
+  out[sample * np + p] = l >= 0 ? v[l] : 0.0;
+}
+
+__global__ void set_clock(long long* clock, long long value) { *clock = value; }
+__global__ void tick_clock(long long* clock, long long by) { *clock += by; }
+
+// AoS (NodeStateArray::s, ionic.hpp:44) <-> SoA chunk transposes
+__global__ void aos_to_soa(const double* aos, int stride, int ns, long long count, double* soa, long long pitch,
+                           long long dst0) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= count) return;
+  for (int q = 0; q < ns; ++q) soa[q * pitch + dst0 + i] = aos[i * stride + q];
+}
+
+__global__ void soa_to_aos(const double* soa, long long pitch, long long src0, int ns, long long count, double* aos,
+                           int stride) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= count) return;
+  for (int q = 0; q < ns; ++q) aos[i * stride + q] = soa[q * pitch + src0 + i];
+  for (int q = ns; q < stride; ++q) aos[i * stride + q] = 0.0;
+}
+
+// standalone diffusion_substep for cwg_diffusion_substep (no halo, no error record)
+__global__ void diffuse_csr_plain(long long n, const long long* rp, const long long* col, const double* val,
+                                  const double* mass, const double* v, double dt_sub, double* out) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+  for (long long p = rp[i]; p < rp[i + 1]; ++p) acc += val[p] * v[col[p]];
+  out[i] = v[i] - dt_sub / mass[i] * acc;
+}
+
+// cm[i] = dt_sub / m_i
+__global__ void mass_factor(const double* mass, long long n, double dt_sub, double* cm) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n) cm[i] = dt_sub / mass[i];
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static inline int blocks_for(long long n, int t, int cap) {
+  long long b = (n + t - 1) / t;
+  if (b > cap) b = cap;
+  return static_cast<int>(b < 1 ? 1 : b);
+}
+
+cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st) {
+  diffuse_stencil2d<<<blocks_for(s.rows * s.w, 256, max_blocks), 256, 0, st>>>(a, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st) {
+  diffuse_csr<<<blocks_for(a.n, 256, max_blocks), 256, 0, st>>>(a, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st) {
+  detector_init<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(v, n, halo, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,
+                                    const long long* clock, long long s_off, long long every, double dt,
+                                    cudaStream_t st) {
+  detector_observe<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(v, n, halo, d, clock, s_off, every, dt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_record_probes(const double* v, const long long* loc, int np, double* out, const long long* clock,
+                                 long long s_off, long long every, cudaStream_t st) {
+  if (np == 0) return cudaSuccess;
+  record_probes<<<(np + 127) / 128, 128, 0, st>>>(v, loc, np, out, clock, s_off, every);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_clock(long long* clock, long long value, cudaStream_t st) {
+  set_clock<<<1, 1, 0, st>>>(clock, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tick_clock(long long* clock, long long by, cudaStream_t st) {
+  tick_clock<<<1, 1, 0, st>>>(clock, by);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_aos_to_soa(const double* aos, int stride, int ns, long long count, double* soa, long long pitch,
+                              long long dst0, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  aos_to_soa<<<blocks_for(count, 256, 1 << 30), 256, 0, st>>>(aos, stride, ns, count, soa, pitch, dst0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_soa_to_aos(const double* soa, long long pitch, long long src0, int ns, long long count,
+                              double* aos, int stride, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  soa_to_aos<<<blocks_for(count, 256, 1 << 30), 256, 0, st>>>(soa, pitch, src0, ns, count, aos, stride);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const long long* col, const double* val,
+                                     const double* mass, const double* v, double dt_sub, double* out,
+                                     cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  diffuse_csr_plain<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(n, rp, col, val, mass, v, dt_sub, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  mass_factor<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(mass, n, dt_sub, cm);
+  return cudaGetLastError();
+}
+
+}  // namespace cwg

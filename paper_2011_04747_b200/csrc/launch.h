@@ -1,0 +1,39 @@
+// Host-side declarations of the kernel launchers (defined in the .cu files).
+#pragma once
+
+#include "common.cuh"
+
+namespace cwg {
+
+cudaError_t launch_react_exact(int kind, const ReactArgs& a, int grid, cudaStream_t st);
+int react_exact_threads(int kind);
+int react_exact_occupancy(int kind);
+cudaError_t launch_rates_exact(int kind, long long n, const double* v, const double* s, const double* ist,
+                               double* dv, double* ds, cudaStream_t st);
+
+cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_t st);
+int react_ord_threads(int kind);
+int react_ord_occupancy(int kind);
+cudaError_t launch_rates_ord(int kind, long long n, const double* v, const double* s, const double* ist, double* dv,
+                             double* ds, cudaStream_t st);
+
+cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st);
+cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st);
+cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st);
+cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,
+                                    const long long* clock, long long s_off, long long every, double dt,
+                                    cudaStream_t st);
+cudaError_t launch_record_probes(const double* v, const long long* loc, int np, double* out, const long long* clock,
+                                 long long s_off, long long every, cudaStream_t st);
+cudaError_t launch_set_clock(long long* clock, long long value, cudaStream_t st);
+cudaError_t launch_tick_clock(long long* clock, long long by, cudaStream_t st);
+cudaError_t launch_aos_to_soa(const double* aos, int stride, int ns, long long count, double* soa, long long pitch,
+                              long long dst0, cudaStream_t st);
+cudaError_t launch_soa_to_aos(const double* soa, long long pitch, long long src0, int ns, long long count,
+                              double* aos, int stride, cudaStream_t st);
+cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const long long* col, const double* val,
+                                     const double* mass, const double* v, double dt_sub, double* out,
+                                     cudaStream_t st);
+cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st);
+
+}  // namespace cwg

@@ -1,0 +1,115 @@
+// The reaction pass (StrangIntegrator::reaction_step, splitting.cpp:95-155) as
+// one sm_100a kernel template per cell model.
+//
+// Work distribution ("lane refill"): each lane owns one node at a time and
+// runs that node's k forward-Euler sub-steps; every loop trip is ONE rates()
+// evaluation for every busy lane, so the expensive model code always runs
+// warp-converged. A lane whose node finished its k sub-steps (or went
+// non-finite) writes the node back and takes the next node position from a
+// global counter with one warp-aggregated atomicAdd. Adaptive k therefore
+// costs no divergence: a warp never waits for its slowest node (the
+// reference's per-node k, splitting.cpp:116, makes the order of nodes
+// irrelevant to the results, so the dynamic schedule stays bit-deterministic).
+//
+// State is SoA (S[q*pitch + i]); the needy lanes of one refill get
+// consecutive node positions, so their 41 state loads coalesce.
+#pragma once
+
+#include "common.cuh"
+
+namespace cwg {
+
+template <class M>
+__device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const long long step = *a.clock + a.step_off;
+  const double t = a.use_t_fixed ? a.t_fixed : static_cast<double>(step) * a.dt;  // splitting.cpp:270
+  const long long seq = step * a.evs + a.ev;
+
+  long long node = -1;
+  bool open = true;  // may still receive work
+  int k = 0, j = 0, p0 = 0, p1 = 0;
+  double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
+  double s[M::NS > 0 ? M::NS : 1];
+
+  while (true) {
+    const bool need = node < 0 && open;
+    const unsigned m = __ballot_sync(kFull, need);
+    if (m) {
+      const int leader = __ffs(m) - 1;
+      unsigned base = 0;
+      if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(m)));
+      base = __shfl_sync(kFull, base, leader);
+      if (need) {
+        const long long pos = static_cast<long long>(base) + __popc(m & lt);
+        if (pos < a.count) {
+          node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
+          v = a.v[node];
+          const double last = a.last[node];
+          k = substeps(last, a.scheme, a.k0_up, a.k0_down, a.kmax);
+          h = a.dt / static_cast<double>(k);  // dt_ar (splitting.cpp:117)
+          j = 0;
+          dv = 0.0;
+#pragma unroll
+          for (int q = 0; q < M::NS; ++q) s[q] = a.S[q * a.pitch + node];
+          if (a.stim.node_ptr) {
+            p0 = __ldg(a.stim.node_ptr + node);
+            p1 = __ldg(a.stim.node_ptr + node + 1);
+          }
+          if (M::kUsesGkr) g = a.gkr ? __ldg(a.gkr + node) : 1.0;
+          atomicAdd(shist + k, 1u);
+        } else {
+          open = false;
+        }
+      }
+    }
+    if (!__any_sync(kFull, node >= 0)) break;
+    if (node >= 0) {
+      const double ts = __dadd_rn(t, __dmul_rn(static_cast<double>(j), h));  // t + j*dt_ar, never contracted
+      const double ist = p1 > p0 ? stim_current(a.stim, p0, p1, ts) : 0.0;
+      M::advance(v, s, ist, g, h, dv);
+      ++j;
+      const bool bad = !isfinite(v);
+      if (bad) {
+        const unsigned long long key = (static_cast<unsigned long long>(node + a.node_offset) << 22) |
+                                       (static_cast<unsigned long long>(k) << 11) |
+                                       static_cast<unsigned long long>(j - 1);
+        record_failure(a.err, key, seq, 1);
+      }
+      if (bad || j == k) {
+        a.v[node] = v;
+        a.last[node] = dv;  // dv at the start of the last sub-step (splitting.cpp:143)
+#pragma unroll
+        for (int q = 0; q < M::NS; ++q) a.S[q * a.pitch + node] = s[q];
+        node = -1;
+      }
+    }
+  }
+}
+
+template <class M>
+__global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(ReactArgs a) {
+  extern __shared__ unsigned shist[];
+  {
+    const long long seq = (*a.clock + a.step_off) * a.evs + a.ev;
+    if (earlier_failure(a.err, seq)) return;  // uniform across the grid
+  }
+  for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x) shist[i] = 0u;
+  __syncthreads();
+  react_body<M>(a, shist);
+  __syncthreads();
+  for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x)
+    if (shist[i]) atomicAdd(a.khist + i, static_cast<unsigned long long>(shist[i]));
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(a.done, 1u);
+    if (prev == gridDim.x - 1) {  // last block out resets the work counter for the next launch
+      *a.counter = 0u;
+      *a.done = 0u;
+      __threadfence();
+    }
+  }
+}
+
+}  // namespace cwg

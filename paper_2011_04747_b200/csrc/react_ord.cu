@@ -1,0 +1,457 @@
+// O'Hara-Rudy 2011 reaction kernels (ohara_rudy_2011.cpp:85-444) for sm_100a.
+//
+// The model is FP64-pipe bound (libdevice exp/log/expm1 are DFMA polynomials,
+// IEEE reciprocals are MUFU.RCP64H + DFMA Newton steps). This formulation is
+// mathematically identical to the reference but spends fewer FP64
+// instructions per evaluation:
+//   * division by a constant  -> multiplication by its (compile-time) reciprocal;
+//   * gates integrate (x_inf - x) * rate with rate = 1/tau taken directly
+//     where tau is written as 1/(a e^u + b e^w) (no division at all);
+//   * 1/(1 + a/x) style terms are rewritten as x/(x + a) (one reciprocal);
+//   * e^x, e^2x, expm1(2x) for the GHK terms derive from one expm1(x); the
+//     reciprocal-pair exponentials (tff, tfcaf) share one exp;
+//   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one exp(log).
+// It therefore agrees with the reference to rounding, not bitwise; the parity
+// contract for ORd is max|dV| <= 1e-6 mV (tests/test_gpu_parity.py), which
+// the survey's +-1-ulp experiment shows is met with ~8 orders of margin.
+//
+// Register pressure: every gate is forward-Euler-updated in place right after
+// the last current that reads its old value (exact FE semantics: each gate's
+// derivative depends only on V and itself), so old and new gate values are
+// never live together; concentrations, which every current reads, are updated
+// last. The FE update itself (x + h*dx) is never contracted.
+#include "react.cuh"
+
+namespace cwg {
+namespace ord {
+
+constexpr double F = 96485.0;
+constexpr double RT = 8314.0 * 310.0;
+constexpr double RTF = RT / F;
+constexpr double FRT = F / RT;
+constexpr double NAO = 140.0, CAO = 1.8, KO = 5.4;
+constexpr double VCELL = 1000.0 * 3.14 * 0.0011 * 0.0011 * 0.01;
+constexpr double AGEO = 2.0 * 3.14 * 0.0011 * 0.0011 + 2.0 * 3.14 * 0.0011 * 0.01;
+constexpr double ACAP = 2.0 * AGEO;
+constexpr double VMYO = 0.68 * VCELL, VNSR = 0.0552 * VCELL, VJSR = 0.0048 * VCELL, VSS = 0.02 * VCELL;
+
+__device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ double sigm(double u) { return __drcp_rn(1.0 + exp(u)); }  // 1/(1+e^u)
+
+template <int CT>  // 0 endo, 1 epi, 2 mid (ohara_rudy_2011.cpp:86-87 celltype_)
+struct Var {
+  static constexpr bool epi = CT == 1, mid = CT == 2;
+  static constexpr double gnal = 0.0075 * (epi ? 0.6 : 1.0);
+  static constexpr double gto = 0.02 * ((epi || mid) ? 4.0 : 1.0);
+  static constexpr double pca = 0.0001 * (epi ? 1.2 : (mid ? 2.5 : 1.0));
+  static constexpr double gkr = 0.046 * (epi ? 1.3 : (mid ? 0.8 : 1.0));
+  static constexpr double gks = 0.0034 * (epi ? 1.4 : 1.0);
+  static constexpr double gk1 = 0.1908 * (epi ? 1.2 : (mid ? 1.3 : 1.0));
+  static constexpr double gncx = 0.0008 * (epi ? 1.1 : (mid ? 1.4 : 1.0));
+  static constexpr double pnak = 30.0 * (epi ? 0.9 : (mid ? 0.7 : 1.0));
+  static constexpr double gkb = 0.003 * (epi ? 0.6 : 1.0);
+  static constexpr double jrel = mid ? 1.7 : 1.0;
+  static constexpr double jup = epi ? 1.3 : 1.0;
+  static constexpr double cmdn = 0.05 * (epi ? 1.3 : 1.0);
+};
+
+// x / expm1(x) given em = expm1(x) (ohara_rudy_2011.cpp:67-70)
+__device__ __forceinline__ double xem1(double x, double em) {
+  return fabs(x) < 1e-8 ? rcp(1.0 + 0.5 * x) : x * rcp(em);
+}
+
+struct NcxShared {
+  double hna, hca_r, h8, h9;
+};
+
+// Na/Ca exchanger flux for one compartment (ohara_rudy_2011.cpp:264-300)
+__device__ __forceinline__ double ncx(double na, double ca, const NcxShared& c) {
+  constexpr double h10 = 12.5 + 1.0 + NAO / 15.0 * (1.0 + NAO / 5.0);
+  constexpr double h11 = NAO * NAO / (h10 * 15.0 * 5.0);
+  constexpr double k1 = 1.0 / h10 * CAO * 1.5e6;
+  constexpr double k2 = 5.0e3, k5 = 5.0e3;
+  const double r1 = rcp(1.0 + na * (1.0 / 88.12) * (1.0 + c.hna));
+  const double h2 = na * c.hna * (1.0 / 88.12) * r1;
+  const double r4 = rcp(1.0 + na * (1.0 / 15.0) * (1.0 + na * (1.0 / 5.0)));
+  const double h5 = na * na * (1.0 / 75.0) * r4;
+  const double k3pp = c.h8 * 5.0e3;
+  const double k3 = c.h9 * 6.0e4 + k3pp;
+  const double k4pp = h2 * 5.0e3;
+  const double k4 = r1 * 6.0e4 * c.hca_r + k4pp;
+  const double k6 = r4 * ca * 1.5e6;
+  const double k7 = h5 * h2 * 6.0e4;
+  const double k8 = c.h8 * h11 * 6.0e4;
+  const double x1 = k2 * k4 * (k7 + k6) + k5 * k7 * (k2 + k3);
+  const double x2 = k1 * k7 * (k4 + k5) + k4 * k6 * (k1 + k8);
+  const double x3 = k1 * k3 * (k7 + k6) + k8 * k6 * (k2 + k3);
+  const double x4 = k2 * k8 * (k4 + k5) + k3 * k5 * (k1 + k8);
+  const double rt = rcp(x1 + x2 + x3 + x4);
+  const double ca2 = ca * ca;
+  const double allo = ca2 * rcp(ca2 + 150.0e-6 * 150.0e-6);
+  const double j_na = 3.0 * (x4 * k7 - x1 * k8) + x3 * k4pp - x2 * k3pp;
+  const double j_ca = x2 * k2 - x1 * k1;
+  return allo * rt * (j_na + 2.0 * j_ca);
+}
+
+// State indices (StateIndex, ohara_rudy_2011.cpp:18-26)
+enum {
+  NAI, NASS, KI, KSS, CAI, CASS, CANSR, CAJSR, M, HF, HS, J, HSP, JP, ML, HL, HLP, A, IF, IS, AP, IFP, ISP,
+  D, FF, FS, FCAF, FCAS, JCA, NCA, FFP, FCAFP, XRF, XRS, XS1, XS2, XK1, JRELNP, JRELP, CAMKT, NSTATE
+};
+
+// gate FE update: x += h * (x_inf - x) * rate
+// Output policy: R = false integrates in place (x += h*dx, never contracted);
+// R = true only reports dx (CellModel::rates semantics, for cwg_rates).
+template <bool R>
+__device__ __forceinline__ void put(double* s, double* ds, int i, double h, double d) {
+  if (R) ds[i] = d;
+  else s[i] = fe(s[i], h, d);
+}
+template <bool R>
+__device__ __forceinline__ void gate(double* s, double* ds, int i, double h, double xinf, double rate) {
+  put<R>(s, ds, i, h, (xinf - s[i]) * rate);
+}
+
+template <int CT, bool R>
+__device__ __forceinline__ void step(double& v, double* s, double* ds, double ist, double gkr_scale, double h,
+                                     double& dv) {
+  using P = Var<CT>;
+  const double nai = s[NAI], nass = s[NASS], ki = s[KI], kss = s[KSS];
+  const double cai = s[CAI], cass = s[CASS], cansr = s[CANSR], cajsr = s[CAJSR];
+
+  const double ena = RTF * log(NAO * rcp(nai));
+  const double ek = RTF * log(KO * rcp(ki));
+  const double eks = RTF * log((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
+  const double camkt = s[CAMKT];
+  const double camk_b = 0.05 * (1.0 - camkt) * cass * rcp(cass + 0.0015);
+  const double camk_a = camk_b + camkt;
+  const double fk = camk_a * rcp(camk_a + 0.15);
+  const double nfk = 1.0 - fk;
+  const double vfrt = v * FRT;
+
+  // ---------------- INa
+  double i_na;
+  {
+    const double m_inf = sigm(-(v + 39.57) * (1.0 / 9.871));
+    const double r_m = 6.765 * exp((v + 11.64) * (1.0 / 34.77)) + 8.552 * exp(-(v + 77.42) * (1.0 / 5.955));
+    const double h_inf = sigm((v + 82.90) * (1.0 / 6.086));
+    const double r_hf = 1.432e-5 * exp(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * exp((v + 0.5096) * (1.0 / 20.27));
+    const double r_hs = 0.009794 * exp(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * exp((v + 5.730) * (1.0 / 56.66));
+    const double r_j = rcp(2.038 + rcp(0.02136 * exp(-(v + 100.6) * (1.0 / 8.281)) +
+                                       0.3052 * exp((v + 0.9941) * (1.0 / 38.45))));
+    const double hp_inf = sigm((v + 89.1) * (1.0 / 6.086));
+    const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
+    const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
+    const double m = s[M];
+    i_na = 75.0 * (v - ena) * (m * m * m) * (nfk * hmix * s[J] + fk * hpmix * s[JP]);
+    gate<R>(s, ds, M, h, m_inf, r_m);
+    gate<R>(s, ds, HF, h, h_inf, r_hf);
+    gate<R>(s, ds, HS, h, h_inf, r_hs);
+    gate<R>(s, ds, J, h, h_inf, r_j);
+    gate<R>(s, ds, HSP, h, hp_inf, r_hs * (1.0 / 3.0));
+    gate<R>(s, ds, JP, h, h_inf, r_j * (1.0 / 1.46));
+    // ---------------- INaL (tmL = tm)
+    const double ml_inf = sigm(-(v + 42.85) * (1.0 / 5.264));
+    const double hl_inf = sigm((v + 87.61) * (1.0 / 7.488));
+    const double hlp_inf = sigm((v + 93.81) * (1.0 / 7.488));
+    const double i_nal = P::gnal * (v - ena) * s[ML] * (nfk * s[HL] + fk * s[HLP]);
+    i_na += i_nal;  // INa + INaL travel together into dv and d[nai]
+    gate<R>(s, ds, ML, h, ml_inf, r_m);
+    gate<R>(s, ds, HL, h, hl_inf, 1.0 / 200.0);
+    gate<R>(s, ds, HLP, h, hlp_inf, 1.0 / 600.0);
+  }
+
+  // ---------------- Ito
+  double i_to;
+  {
+    const double a_inf = sigm(-(v - 14.34) * (1.0 / 14.82));
+    const double r_a = (1.0 / 1.0515) * (rcp(1.2089 * (1.0 + exp(-(v - 18.4099) * (1.0 / 29.3814)))) +
+                                         3.5 * sigm((v + 100.0) * (1.0 / 29.3814)));
+    const double i_inf = sigm((v + 43.94) * (1.0 / 5.711));
+    double t_if = 4.562 + rcp(0.3933 * exp(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * exp((v + 50.0) * (1.0 / 16.59)));
+    double t_is = 23.62 + rcp(0.001416 * exp(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * exp((v + 114.1) * (1.0 / 8.079)));
+    if (P::epi) {
+      const double d_epi = 1.0 - 0.95 * sigm((v + 70.0) * (1.0 / 5.0));
+      t_if *= d_epi;
+      t_is *= d_epi;
+    }
+    const double r_if = rcp(t_if), r_is = rcp(t_is);
+    const double a_if = sigm((v - 213.6) * (1.0 / 151.2));
+    const double a_is = 1.0 - a_if;
+    const double ap_inf = sigm(-(v - 24.34) * (1.0 / 14.82));
+    const double dev = 1.354 + 1.0e-4 * rcp(exp((v - 167.4) * (1.0 / 15.89)) + exp(-(v - 12.23) * (1.0 / 0.2154)));
+    const double rec = 1.0 - 0.5 * sigm((v + 70.0) * (1.0 / 20.0));
+    const double r_dr = rcp(dev * rec);
+    const double imix = a_if * s[IF] + a_is * s[IS];
+    const double ipmix = a_if * s[IFP] + a_is * s[ISP];
+    i_to = P::gto * (v - ek) * (nfk * s[A] * imix + fk * s[AP] * ipmix);
+    gate<R>(s, ds, A, h, a_inf, r_a);
+    gate<R>(s, ds, IF, h, i_inf, r_if);
+    gate<R>(s, ds, IS, h, i_inf, r_is);
+    gate<R>(s, ds, AP, h, ap_inf, r_a);
+    gate<R>(s, ds, IFP, h, i_inf, r_if * r_dr);
+    gate<R>(s, ds, ISP, h, i_inf, r_is * r_dr);
+  }
+
+  // ---------------- GHK driving terms (one expm1 for e^x, e^2x, expm1(2x))
+  const double em1 = expm1(vfrt);
+  const double e1 = em1 + 1.0;
+  const double e2 = e1 * e1;
+  const double em2 = em1 * (em1 + 2.0);
+  const double xq1 = xem1(vfrt, em1);
+  const double xq2 = xem1(2.0 * vfrt, em2);
+
+  // ---------------- ICaL, ICaNa, ICaK
+  double i_cal, i_cana, i_cak;
+  {
+    const double d_inf = sigm(-(v + 3.940) * (1.0 / 4.230));
+    const double r_d = rcp(0.6 + rcp(exp(-0.05 * (v + 6.0)) + exp(0.09 * (v + 14.0))));
+    const double f_inf = sigm((v + 19.58) * (1.0 / 3.696));
+    const double eff = exp((v + 20.0) * (1.0 / 10.0));
+    const double r_ff = rcp(7.0 + rcp(0.0045 * (rcp(eff) + eff)));
+    const double r_fs = rcp(1000.0 + rcp(0.000035 * exp(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * exp((v + 5.0) * (1.0 / 6.0))));
+    const double efc = exp((v - 4.0) * (1.0 / 7.0));
+    const double r_fcaf = rcp(7.0 + rcp(0.04 * (rcp(efc) + efc)));
+    const double r_fcas = rcp(100.0 + rcp(0.00012 * exp(-v * (1.0 / 3.0)) + 0.00012 * exp(v * (1.0 / 7.0))));
+    const double a_fcaf = 0.3 + 0.6 * sigm((v - 10.0) * (1.0 / 10.0));
+    const double a_fcas = 1.0 - a_fcaf;
+    const double fmix = 0.6 * s[FF] + (1.0 - 0.6) * s[FS];
+    const double fcamix = a_fcaf * s[FCAF] + a_fcas * s[FCAS];
+    const double fpmix = 0.6 * s[FFP] + (1.0 - 0.6) * s[FS];
+    const double fcapmix = a_fcaf * s[FCAFP] + a_fcas * s[FCAS];
+    const double jca = s[JCA], nca = s[NCA];
+    const double cn = (cass + 0.002) * rcp(cass);
+    const double cn2 = cn * cn;
+    const double anca = jca * rcp(1000.0 + jca * (cn2 * cn2));
+    const double phi_cal = 2.0 * F * (cass * e2 - 0.341 * CAO) * xq2;
+    const double phi_cana = F * (0.75 * nass * e1 - 0.75 * NAO) * xq1;
+    const double phi_cak = F * (0.75 * kss * e1 - 0.75 * KO) * xq1;
+    const double g_np = s[D] * (fmix * (1.0 - nca) + jca * fcamix * nca);
+    const double g_p = s[D] * (fpmix * (1.0 - nca) + jca * fcapmix * nca);
+    const double mixed = nfk * g_np + fk * 1.1 * g_p;  // PCap = 1.1 PCa
+    i_cal = P::pca * phi_cal * mixed;
+    i_cana = (0.00125 * P::pca) * phi_cana * mixed;
+    i_cak = (3.574e-4 * P::pca) * phi_cak * mixed;
+    gate<R>(s, ds, D, h, d_inf, r_d);
+    gate<R>(s, ds, FF, h, f_inf, r_ff);
+    gate<R>(s, ds, FS, h, f_inf, r_fs);
+    gate<R>(s, ds, FCAF, h, f_inf, r_fcaf);
+    gate<R>(s, ds, FCAS, h, f_inf, r_fcas);
+    gate<R>(s, ds, JCA, h, f_inf, 1.0 / 75.0);
+    put<R>(s, ds, NCA, h, anca * 1000.0 - jca * nca);
+    gate<R>(s, ds, FFP, h, f_inf, r_ff * (1.0 / 2.5));
+    gate<R>(s, ds, FCAFP, h, f_inf, r_fcaf * (1.0 / 2.5));
+  }
+
+  // ---------------- IKr, IKs, IK1
+  double i_k;  // IKr + IKs + IK1
+  {
+    const double xr_inf = sigm(-(v + 8.337) * (1.0 / 6.789));
+    const double r_xrf = rcp(12.98 + rcp(0.3652 * exp((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * exp(-(v - 47.78) * (1.0 / 20.38))));
+    const double r_xrs = rcp(1.865 + rcp(0.06629 * exp((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * exp(-(v - 29.74) * (1.0 / 25.94))));
+    const double a_xrf = sigm((v + 54.81) * (1.0 / 38.21));
+    const double xrmix = a_xrf * s[XRF] + (1.0 - a_xrf) * s[XRS];
+    const double rkr = rcp((1.0 + exp((v + 55.0) * (1.0 / 75.0))) * (1.0 + exp((v - 10.0) * (1.0 / 30.0))));
+    const double i_kr = (P::gkr * gkr_scale) * xrmix * rkr * (v - ek);  // sqrt(ko/5.4) == 1
+    gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
+    gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
+
+    const double xs_inf = sigm(-(v + 11.60) * (1.0 / 8.932));
+    const double r_xs1 = rcp(817.3 + rcp(2.326e-4 * exp((v + 48.28) * (1.0 / 17.80)) + 0.001292 * exp(-(v + 210.0) * (1.0 / 230.0))));
+    const double r_xs2 = 0.01 * exp((v - 50.0) * (1.0 / 20.0)) + 0.0193 * exp(-(v + 66.54) * (1.0 / 31.0));
+    const double ksca = 1.0 + 0.6 * rcp(1.0 + exp(1.4 * (-10.177924398237888 - log(cai)))  /* log(3.8e-5) */);
+    const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
+    gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
+    gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
+
+    const double xk1_inf = sigm(-(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)));
+    const double r_xk1 = (exp(-(v + 127.2) * (1.0 / 20.36)) + exp((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
+    const double rk1 = sigm((v + 105.8 - 2.6 * KO) * (1.0 / 9.493));
+    const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
+    gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
+    i_k = i_kr + i_ks + i_k1;
+  }
+
+  // ---------------- INaCa (bulk + subspace)
+  double inaca_i, inaca_ss;
+  {
+    NcxShared c;
+    c.hna = exp(0.5224 * vfrt);
+    c.hca_r = exp(-0.1670 * vfrt);  // 1/hca
+    const double hna_r = rcp(c.hna);
+    const double r7 = rcp(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
+    c.h9 = r7;
+    c.h8 = NAO * (1.0 / 88.12) * hna_r * r7;
+    inaca_i = (0.8 * P::gncx) * ncx(nai, cai, c);
+    inaca_ss = (0.2 * P::gncx) * ncx(nass, cass, c);
+  }
+
+  // ---------------- INaK
+  double i_nak;
+  {
+    constexpr double rko = KO / 0.3582;
+    constexpr double qo = (1.0 + rko) * (1.0 + rko);
+    constexpr double b1 = 182.4 * 0.05, a2 = 687.2;
+    constexpr double a4 = 639.0 * 9.8 / 1.698e-7 / (1.0 + 9.8 / 1.698e-7);
+    constexpr double b3c = 79300.0 * 1.0e-7 / (1.0 + 9.8 / 1.698e-7);
+    const double p_hp = 4.2 * rcp(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
+    const double ri = nai * (1.0 / 9.073) * exp((0.1550 / 3.0) * vfrt);     // nai / Knai
+    const double ro = NAO * (1.0 / 27.78) * exp(-(1.1550 / 3.0) * vfrt);   // nao / Knao
+    const double rk = ki * 2.0;                                            // ki / 0.5
+    const double ci = (1.0 + ri) * (1.0 + ri) * (1.0 + ri), qi = (1.0 + rk) * (1.0 + rk);
+    const double co = (1.0 + ro) * (1.0 + ro) * (1.0 + ro);
+    const double di = rcp(ci + qi - 1.0), dco = rcp(co + qo - 1.0);
+    const double a1 = 949.5 * (ri * ri * ri) * di;
+    const double b2 = 39.4 * (ro * ro * ro) * dco;
+    const double a3 = 1899.0 * (rko * rko) * dco;
+    const double b3 = b3c * p_hp;
+    const double b4 = 40.0 * (rk * rk) * di;
+    const double y1 = a4 * a1 * a2 + b2 * b4 * b3 + a2 * b4 * b3 + b3 * a1 * a2;
+    const double y2 = b2 * b1 * b4 + a1 * a2 * a3 + a3 * b1 * b4 + a2 * a3 * b4;
+    const double y3 = a2 * a3 * a4 + b3 * b2 * b1 + b2 * b1 * a4 + a3 * a4 * b1;
+    const double y4 = b4 * b3 * b2 + a3 * a4 * a1 + b2 * a4 * a1 + b3 * b2 * a1;
+    const double ry = rcp(y1 + y2 + y3 + y4);
+    i_nak = P::pnak * ry * (3.0 * (y1 * a3 - y2 * b3) + 2.0 * (y4 * b1 - y3 * a1));
+  }
+
+  // ---------------- background currents
+  const double i_kb = P::gkb * sigm(-(v - 14.48) * (1.0 / 18.34)) * (v - ek);
+  const double i_nab = (3.75e-10 * F) * (nai * e1 - NAO) * xq1;
+  const double i_cab = (2.5e-8 * 2.0 * F) * (cai * e2 - 0.341 * CAO) * xq2;
+  const double i_pca = 0.0005 * cai * rcp(0.0005 + cai);
+
+  // ---------------- SR release / uptake, buffers
+  const double jrel = nfk * s[JRELNP] + fk * s[JRELP];
+  {
+    const double rr = 1.5 * rcp(cajsr);
+    const double rr2 = rr * rr, rr4 = rr2 * rr2;
+    const double gate_rel = rcp(1.0 + rr4 * rr4);
+    const double jrel_inf = (0.5 * 4.75 * P::jrel) * (-i_cal) * gate_rel;
+    double r_rel = (cajsr + 0.0123) * rcp(4.75 * cajsr);  // 1/tau_rel
+    double r_relp = r_rel * (1.0 / 1.25);
+    r_rel = r_rel > 200.0 ? 200.0 : r_rel;  // tau_rel >= 0.005 (NaN passes through, like the reference)
+    r_relp = r_relp > 200.0 ? 200.0 : r_relp;
+    gate<R>(s, ds, JRELNP, h, jrel_inf, r_rel);
+    gate<R>(s, ds, JRELP, h, jrel_inf * 1.25, r_relp);
+    put<R>(s, ds, CAMKT, h, 0.05 * camk_b * (camk_b + camkt) - 0.00068 * camkt);
+  }
+  const double jup_np = (0.004375 * P::jup) * cai * rcp(cai + 0.00092);
+  const double jup_p = (2.75 * 0.004375 * P::jup) * cai * rcp(cai + 0.00092 - 0.00017);
+  const double j_up = nfk * jup_np + fk * jup_p - (0.0039375 / 15.0) * cansr;
+  const double j_tr = (cansr - cajsr) * (1.0 / 100.0);
+  const double jd_na = (nass - nai) * 0.5;
+  const double jd_k = (kss - ki) * 0.5;
+  const double jd_ca = (cass - cai) * 5.0;
+  double b_cai, b_cass, b_cajsr;
+  {
+    const double kc = 0.00238 + cai, kt = 0.0005 + cai;
+    const double kc2 = kc * kc, kt2 = kt * kt;
+    const double pc = kc2 * kt2;
+    b_cai = pc * rcp(pc + (P::cmdn * 0.00238) * kt2 + (0.07 * 0.0005) * kc2);
+    const double kb = 0.00087 + cass, kl = 0.0087 + cass;
+    const double kb2 = kb * kb, kl2 = kl * kl;
+    const double pb = kb2 * kl2;
+    b_cass = pb * rcp(pb + (0.047 * 0.00087) * kl2 + (1.124 * 0.0087) * kb2);
+    const double kq = 0.8 + cajsr;
+    const double kq2 = kq * kq;
+    b_cajsr = kq2 * rcp(kq2 + 10.0 * 0.8);
+  }
+
+  // ---------------- concentrations (last: every current above read the old values)
+  constexpr double cm_myo = ACAP / (F * VMYO), cm_ss = ACAP / (F * VSS);
+  put<R>(s, ds, NAI, h, -(i_na + 3.0 * inaca_i + 3.0 * i_nak + i_nab) * cm_myo + jd_na * (VSS / VMYO));
+  put<R>(s, ds, NASS, h, -(i_cana + 3.0 * inaca_ss) * cm_ss - jd_na);
+  put<R>(s, ds, KI, h, -(i_to + i_k + i_kb - 2.0 * i_nak) * cm_myo + jd_k * (VSS / VMYO));
+  put<R>(s, ds, KSS, h, -i_cak * cm_ss - jd_k);
+  put<R>(s, ds, CAI, h, b_cai * (-(i_pca + i_cab - 2.0 * inaca_i) * (0.5 * cm_myo) - j_up * (VNSR / VMYO) + jd_ca * (VSS / VMYO)));
+  put<R>(s, ds, CASS, h, b_cass * (-(i_cal - 2.0 * inaca_ss) * (0.5 * cm_ss) + jrel * (VJSR / VSS) - jd_ca));
+  put<R>(s, ds, CANSR, h, j_up - j_tr * (VJSR / VNSR));
+  put<R>(s, ds, CAJSR, h, b_cajsr * (j_tr - jrel));
+
+  dv = -(i_na + i_to + i_cal + i_cana + i_cak + i_k + inaca_i + inaca_ss + i_nak + i_kb + i_nab + i_pca + i_cab) + ist;
+  if (!R) v = fe(v, h, dv);
+}
+
+// CellModel::rates (no update), for the batched rates entry point / tests
+template <int CT>
+__device__ void rates(double v, const double* s, double ist, double& dv, double* ds) {
+  double tmp[NSTATE];
+#pragma unroll
+  for (int q = 0; q < NSTATE; ++q) tmp[q] = s[q];
+  step<CT, true>(v, tmp, ds, ist, 1.0, 0.0, dv);
+}
+
+}  // namespace ord
+
+template <int CT>
+struct ModelOrd {
+  static constexpr int NS = ord::NSTATE;
+  static constexpr int kThreads = 128;
+  static constexpr int kMinBlocks = 2;
+  static constexpr bool kUsesGkr = true;
+  __device__ __forceinline__ static void advance(double& v, double* s, double ist, double g, double h, double& dv) {
+    ord::step<CT, false>(v, s, nullptr, ist, g, h, dv);
+  }
+};
+
+template <int CT>
+__global__ void ord_rates_kernel(long long n, const double* v, const double* s, const double* ist, double* dv,
+                                 double* ds) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  double sl[ord::NSTATE], dl[ord::NSTATE];
+  for (int q = 0; q < ord::NSTATE; ++q) sl[q] = s[i * ord::NSTATE + q];
+  double d;
+  ord::rates<CT>(v[i], sl, ist[i], d, dl);
+  dv[i] = d;
+  for (int q = 0; q < ord::NSTATE; ++q) ds[i * ord::NSTATE + q] = dl[q];
+}
+
+template <class M>
+static cudaError_t launch_react_t(const ReactArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(a.khist_len) * sizeof(unsigned);
+  react_kernel<M><<<grid, M::kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <class M>
+static int occupancy_t() {
+  int b = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, react_kernel<M>, M::kThreads, 2048 * sizeof(unsigned));
+  return b;
+}
+
+cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_t st) {
+  switch (kind) {
+    case 1: return launch_react_t<ModelOrd<0>>(a, grid, st);
+    case 2: return launch_react_t<ModelOrd<1>>(a, grid, st);
+    case 3: return launch_react_t<ModelOrd<2>>(a, grid, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int react_ord_threads(int) { return 128; }
+
+int react_ord_occupancy(int kind) {
+  switch (kind) {
+    case 1: return occupancy_t<ModelOrd<0>>();
+    case 2: return occupancy_t<ModelOrd<1>>();
+    case 3: return occupancy_t<ModelOrd<2>>();
+    default: return 0;
+  }
+}
+
+cudaError_t launch_rates_ord(int kind, long long n, const double* v, const double* s, const double* ist, double* dv,
+                             double* ds, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  const int grid = static_cast<int>((n + 127) / 128);
+  switch (kind) {
+    case 1: ord_rates_kernel<0><<<grid, 128, 0, st>>>(n, v, s, ist, dv, ds); break;
+    case 2: ord_rates_kernel<1><<<grid, 128, 0, st>>>(n, v, s, ist, dv, ds); break;
+    case 3: ord_rates_kernel<2><<<grid, 128, 0, st>>>(n, v, s, ist, dv, ds); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace cwg

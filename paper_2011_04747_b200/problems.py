@@ -1,0 +1,109 @@
+"""BASELINE.json configurations as synthetic problems.
+
+There is no public dataset: each config is a seeded synthetic tissue with the
+BASELINE shapes. C1/C2 are expressible in the reference as-is (parity pinned
+against the reference); C3 needs the extensions (scar with zero
+conductivity, passive non-excitable nodes, per-node GKr jitter) and its
+parity is pinned only against our CPU restatement oracle.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import api
+
+
+@dataclass
+class Problem:
+    name: str
+    sheet: api.Sheet
+    models: List[str]
+    model_of_node: np.ndarray
+    stimuli: List[tuple]  # (nodes, t_start, duration, amplitude, period|None)
+    cfg: api.SchemeConfig
+    probes: List[int] = field(default_factory=list)
+    gkr_scale: Optional[np.ndarray] = None
+    notes: str = ""
+
+    @property
+    def n(self):
+        return self.sheet.n
+
+    def setup(self) -> api.SimulationSetup:
+        prot = api.Protocol([api.Stimulus(np.asarray(s[0], np.int64), s[1], s[2], s[3], s[4]) for s in self.stimuli])
+        return api.SimulationSetup(op=self.sheet.op, models=[api.make_model(m) for m in self.models],
+                                   protocol=api.ProtocolIndex(prot, self.n),
+                                   probes=[api.Probe(int(p), f"p{q}") for q, p in enumerate(self.probes)],
+                                   gkr_scale=self.gkr_scale)
+
+    def initial_state(self) -> api.NodeStateArray:
+        return api.make_initial_state(self.n, [api.make_model(m) for m in self.models], self.model_of_node)
+
+
+# C1: 1x1 cm, h = 0.01, D = 0.001 isotropic; ORd-epi; left-edge line x <= 0 for
+# t in [0, 1) at 2 x the reference's diastolic threshold (296 mV/ms, measured
+# in the survey with cardwave::diastolic_threshold) = 592 mV/ms; DAETI dt 0.1,
+# k0_down = 3 (the paper's k0_down = 1 aborts in the reference).
+C1_AMPLITUDE = 592.0
+# C2: 5x5 cm, h = 0.025, fibres 45 deg, D_l = 0.0012, D_t = 0.0003; corner disc
+# (radius 2h) stimulus. Amplitude chosen stable + propagating in the reference
+# (SURVEY.md 8(d) caution 2; probe recorded in DESIGN.md).
+C2_AMPLITUDE = 100.0
+C2_RADIUS = 0.05
+
+
+def c1(model="ohara2011-epi", t_end=400.0, k0_down=3, amplitude=None, strip=None, scheme=api.Scheme.DAETI,
+       dt=0.1) -> Problem:
+    sh = api.Sheet(1.0, 1.0, 0.01, 0.0, d0_myocyte=0.001, rho=1.0)
+    if model == "aliev-panfilov":
+        strip = 0.05 if strip is None else strip
+        amplitude = 100.0 if amplitude is None else amplitude
+    amp = C1_AMPLITUDE if amplitude is None else amplitude
+    nodes = sh.select("x_le", value=0.0 if strip is None else strip)
+    cfg = api.SchemeConfig(scheme=scheme, dt_ms=dt, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
+    probes = [sh.nearest(0.0, 0.5), sh.nearest(0.5, 0.5), sh.nearest(1.0, 0.5)]
+    return Problem("C1", sh, [model], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, amp, None)], cfg, probes)
+
+
+def c2(model="ohara2011-epi", t_end=500.0, k0_down=3, amplitude=C2_AMPLITUDE, radius=C2_RADIUS,
+       scheme=api.Scheme.DAETI) -> Problem:
+    sh = api.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0_myocyte=0.0012, rho=0.25)
+    nodes = sh.select("disc", cx=0.0, cy=0.0, radius=radius)
+    cfg = api.SchemeConfig(scheme=scheme, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
+    probes = [sh.nearest(0.0, 0.0), sh.nearest(2.5, 2.5), sh.nearest(5.0, 5.0)]
+    return Problem("C2", sh, [model], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, amplitude, None)], cfg, probes)
+
+
+def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size=5.0) -> Problem:
+    """Pathological sheet (EXTENSION; parity pinned to the C oracle only).
+
+    Central scar (r = 1 cm): elements with D = 0 and passive nodes; border
+    zone (1-1.5 cm): D x 0.5 and per-node GKr x U(0.8, 1.2) drawn with
+    numpy's PCG64(seed). S1: left edge x <= 0 at t = 0; S2: quadrant
+    [0, size/2]^2 at t = 300 ms.
+    """
+    nx = int(round(size / h))
+    c = size / 2.0
+    # element centroids
+    ex = (np.arange(nx) + 0.5) * h
+    X, Y = np.meshgrid(ex, ex)
+    r = np.hypot(X - c, Y - c).ravel()
+    scale = np.where(r <= 1.0, 0.0, np.where(r <= 1.5, 0.5, 1.0))
+    sh = api.Sheet(size, size, h, 0.0, d0_myocyte=0.001, rho=1.0, elem_scale=scale)
+    rn = np.hypot(sh.coords[:, 0] - c, sh.coords[:, 1] - c)
+    model_of_node = np.where(rn < 1.0 - 1e-9, 1, 0).astype(np.uint8)  # strictly inside the scar: passive
+    rng = np.random.Generator(np.random.PCG64(seed))
+    gkr = np.ones(sh.n)
+    bz = (rn >= 1.0) & (rn <= 1.5)
+    gkr[bz] = rng.uniform(0.8, 1.2, int(bz.sum()))
+    s1 = sh.select("x_le", value=0.0)
+    s2 = sh.select("rectangle", x0=0.0, x1=c, y0=0.0, y1=c)
+    cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
+    probes = [sh.nearest(0.5, c), sh.nearest(c, 0.5), sh.nearest(size - 0.5, c)]
+    return Problem("C3", sh, ["ohara2011-epi", "passive"], model_of_node,
+                   [(s1, 0.0, 1.0, amplitude, None), (s2, 300.0, 1.0, amplitude, None)], cfg, probes, gkr,
+                   notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)")

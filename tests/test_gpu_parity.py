@@ -1,0 +1,221 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle.
+
+Bit-exact where the reference arithmetic allows it (integer rules,
+diffusion, Aliev-Panfilov, the detector); ORd/MacCannell go through libdevice
+exp/log instead of glibc's, so they are held to the fp64 tolerance of
+north_star: max|dV| <= 1e-6 mV on traces and the final field, identical
+k-histogram, identical LAT rank order on the sampled node set.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import gpu_run, lat_order_equal, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+V_TOL_MV = 1e-6  # north_star: max|dV| <= 1e-6 mV
+
+
+@pytest.fixture(scope="module")
+def cw():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2011_04747_b200 as cw
+    return cw
+
+
+@pytest.fixture(scope="module")
+def problems(cw):
+    from paper_2011_04747_b200 import problems
+    return problems
+
+
+def _states(rest, n, rng, spread):
+    ns = len(rest) - 1
+    s = np.tile(rest[1:], (n, 1)) * rng.uniform(1 - spread, 1 + spread, (n, ns))
+    return s
+
+
+@pytest.mark.parametrize("model", ["aliev-panfilov", "maccannell2007", "ohara2011-endo", "ohara2011-epi",
+                                   "ohara2011-mid"])
+def test_rates_against_oracle(cw, ora, model):
+    rng = np.random.default_rng(1)
+    m = cw.make_model(model)
+    rest = m.rest_state()
+    assert np.array_equal(rest, ora.rest_state(model))
+    n = 4096
+    v = rng.uniform(-95.0, 45.0, n) if model != "aliev-panfilov" else rng.uniform(-85.0, 25.0, n)
+    s = _states(rest, n, rng, 0.3) if model != "aliev-panfilov" else rng.uniform(0.0, 2.0, (n, 1))
+    ist = rng.choice([0.0, 80.0], n)
+    dv_g, ds_g = m.rates(v, s, ist)
+    dv_o, ds_o = ora.rates(model, v, s, ist)
+    if model == "aliev-panfilov":
+        assert np.array_equal(dv_g, dv_o) and np.array_equal(ds_g, ds_o)
+    else:
+        scale_v = np.maximum(1.0, np.abs(dv_o))
+        assert np.max(np.abs(dv_g - dv_o) / scale_v) < 1e-11
+        scale_s = np.maximum(np.abs(ds_o), 1e-300) + 1e-9 * np.max(np.abs(ds_o), axis=0)
+        assert np.max(np.abs(ds_g - ds_o) / scale_s) < 1e-9
+
+
+@pytest.mark.parametrize("which", ["c1", "c2", "fib"])
+def test_diffusion_substep_bitwise(cw, ora, which):
+    rng = np.random.default_rng(2)
+    if which == "c1":
+        sh = cw.Sheet(1.0, 1.0, 0.01, 0.0, d0_myocyte=0.001, rho=1.0)
+    elif which == "c2":
+        sh = cw.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0_myocyte=0.0012, rho=0.25)
+    else:
+        sh = cw.Sheet(2.0, 1.0, 0.02, 0.7, fib_fraction=0.3, seed=11)
+    op = sh.op
+    v = rng.uniform(-90.0, 40.0, sh.n)
+    out_g = cw.diffusion_substep(op, v, 0.01)
+    out_o = ora.diffusion_substep((op.row_ptr, op.col, op.val, op.lumped_mass), v, 0.01)
+    assert np.array_equal(out_g, out_o)
+
+
+def _compare_exact(res, o):
+    assert np.array_equal(res.final_state.v, o["v"])
+    assert np.array_equal(res.final_state.s.reshape(o["s"].shape), o["s"])
+    assert np.array_equal(res.final_state.last_dvdt, o["last_dvdt"])
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    for q, tr in enumerate(res.traces):
+        assert np.array_equal(tr.v_mv, o["traces"][q])
+        assert np.array_equal(tr.t_ms, o["trace_t"])
+    assert np.array_equal(res.lat_map.valid, o["lat_valid"])
+    assert np.array_equal(res.lat_map.value[o["lat_valid"]], o["lat"][o["lat_valid"]])
+    assert np.array_equal(res.apd90_map.valid, o["apd_valid"])
+    assert np.array_equal(res.apd90_map.value[o["apd_valid"]], o["apd90"][o["apd_valid"]])
+
+
+def _compare_tol(res, o, nx1):
+    dv = np.max(np.abs(res.final_state.v - o["v"]))
+    assert dv <= V_TOL_MV, f"final V differs by {dv} mV"
+    for q, tr in enumerate(res.traces):
+        d = np.max(np.abs(tr.v_mv - o["traces"][q]))
+        assert d <= V_TOL_MV, f"trace {q} differs by {d} mV"
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    assert np.array_equal(res.lat_map.valid, o["lat_valid"])
+    assert lat_order_equal(res.lat_map.value, res.lat_map.valid, o["lat"], o["lat_valid"], nx1)
+    lv = o["lat_valid"]
+    if lv.any():
+        assert np.max(np.abs(res.lat_map.value[lv] - o["lat"][lv])) < 1e-6
+
+
+def test_c1_aliev_panfilov_bitwise(cw, ora, problems):
+    p = problems.c1(model="aliev-panfilov", t_end=120.0, k0_down=1)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_exact(res, o)
+    assert res.lat_map.valid.sum() > 0.9 * p.n  # the wave crossed the sheet
+
+
+def test_c1_ord_epi_tolerance(cw, ora, problems):
+    p = problems.c1(t_end=30.0)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_tol(res, o, p.sheet.nx1)
+    assert res.lat_map.valid.sum() > 100
+
+
+def test_c1_ord_abort_fixture(cw, ora, problems):
+    """Paper k0 (k0_down = 1) aborts in the reference at node 16, t = 2.04 ms."""
+    p = problems.c1(t_end=10.0, k0_down=1)
+    with pytest.raises(ora.OracleInstability) as eo:
+        oracle_run(p)
+    with pytest.raises(cw.InstabilityError) as eg:
+        gpu_run(p)
+    assert eg.value.node_index == eo.value.node == 16
+    assert eg.value.time_ms == eo.value.t
+    assert abs(eg.value.time_ms - 2.04) < 1e-9
+
+
+@pytest.mark.parametrize("scheme,dt", [("OST", 0.01), ("OSTAR", 0.1)])
+def test_schemes_ap_bitwise(cw, ora, problems, scheme, dt):
+    p = problems.c1(model="aliev-panfilov", t_end=15.0, scheme=cw.Scheme[scheme], dt=dt)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_exact(res, o)
+
+
+def test_daeti_reduces_to_ostar_bitwise(cw, problems):
+    """with dt/2 <= dt_s and k_max = 1, DAETI == OSTAR bit for bit."""
+    from paper_2011_04747_b200 import api
+    sh = cw.Sheet(2.0, 2.0, 0.02, math.pi / 4, d0_myocyte=0.0012, rho=0.25)
+    nodes = sh.select("x_le", value=0.05)
+    out = []
+    for scheme in (api.Scheme.DAETI, api.Scheme.OSTAR):
+        prob = problems.Problem("red", sh, ["aliev-panfilov"], np.zeros(sh.n, np.uint8),
+                                [(nodes, 0.0, 1.0, 100.0, None)],
+                                api.SchemeConfig(scheme=scheme, dt_ms=0.05, t_end_ms=30.0), [0, sh.n // 2])
+        assert 0.05 / 2 <= sh.op.dt_s
+        out.append(gpu_run(prob))
+    a, b = out
+    assert np.array_equal(a.final_state.v, b.final_state.v)
+    assert np.array_equal(a.traces[1].v_mv, b.traces[1].v_mv)
+    assert np.array_equal(a.lat_map.value[a.lat_map.valid], b.lat_map.value[b.lat_map.valid])
+
+
+def test_advance_matches_graph_run(cw, problems):
+    """StrangIntegrator::advance step by step == the graph-replayed run_simulation."""
+    p = problems.c1(model="ohara2011-epi", t_end=6.0)
+    setup = p.setup()
+    st = p.initial_state()
+    integ = cw.StrangIntegrator(setup, p.cfg, model_of_node=p.model_of_node)
+    n_steps = integ.info.n_steps
+    for step in range(n_steps):
+        integ.advance(st, step * integ.dt_effective(), step, n_steps, sync_state=(step == n_steps - 1))
+    res = gpu_run(p)
+    assert np.array_equal(st.v, res.final_state.v)
+    assert np.array_equal(st.s, res.final_state.s)
+    assert np.array_equal(integ.k_histogram(), res.k_histogram)
+
+
+def test_periodic_stimulus_ap_bitwise(cw, ora, problems):
+    p = problems.c1(model="aliev-panfilov", t_end=40.0)
+    nodes = p.stimuli[0][0]
+    p.stimuli = [(nodes, 2.0, 1.5, 90.0, 17.0), (nodes[:5], 0.0, 1.0, 50.0, None)]
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_exact(res, o)
+
+
+def test_fibrosis_two_models(cw, ora, problems):
+    """Fibroblast-tagged nodes run MacCannell, myocytes ORd-epi (model bins)."""
+    from paper_2011_04747_b200 import api
+    sh = cw.Sheet(1.0, 0.5, 0.02, 0.3, d0_myocyte=0.0017, d0_fibrotic=0.00066, rho=0.25, fib_fraction=0.2, seed=5)
+    nodes = sh.select("x_le", value=0.05)
+    prob = problems.Problem("fib", sh, ["ohara2011-epi", "maccannell2007"], sh.tags.astype(np.uint8),
+                            [(nodes, 0.0, 1.0, 150.0, None)], api.SchemeConfig(dt_ms=0.1, t_end_ms=12.0, k0_down=3),
+                            [0, sh.n - 1])
+    res = gpu_run(prob)
+    o = oracle_run(prob)
+    _compare_tol(res, o, sh.nx1)
+
+
+def test_c2_short(cw, ora, problems):
+    p = problems.c2(t_end=8.0)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_tol(res, o, p.sheet.nx1)
+
+
+def test_c3_extension_small(cw, ora, problems):
+    """Scar / border zone / passive nodes / GKr jitter (extension; oracle-pinned only)."""
+    p = problems.c3(t_end=12.0, h=0.05, size=5.0)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_tol(res, o, p.sheet.nx1)
+
+
+def test_launches_counted(cw, problems):
+    p = problems.c1(model="aliev-panfilov", t_end=3.0)
+    integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=p.model_of_node)
+    integ.upload(p.initial_state())
+    integ.run_begin()
+    integ.run_steps(0, integ.info.n_steps)
+    integ.run_sync()
+    assert integ.launch_count() > integ.info.n_steps
