@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the DAETI hot path on B200 (one JSON line on rank 0).
+
+Workload (N = 1): BASELINE.json configs[1] ("C2"): 5x5 cm anisotropic sheet,
+201x201 nodes, fibres 45 deg, D_l 0.0012 / D_t 0.0003, ORd-epi from rest,
+corner-disc stimulus (r 0.15 cm, 100 mV/ms, 1 ms), DAETI dt 0.1 ms
+(k0_up 5, k0_down 3), fp64. A "step" is one outer Strang step (the
+adaptive reaction pass + 2l diffusion sub-steps + the record cadence).
+The default run is the whole 500 ms simulation: W warm-up steps, then
+K = 5000 - W timed steps. N > 1 (torchrun): weak scaling, rank r owns a
+201-row y-slab of a 5 x 5N cm sheet, halo exchange per diffusion sub-step.
+
+metric: node-updates/s = (reaction rates evaluations + diffusion node
+sub-steps) per second, whole job. Timing: CUDA events per step on the
+solver's stream, with a 256 MiB L2-evicting write before every timed step
+(untimed); max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "node-updates/sec (reaction+diffusion) and simulated ms per wall-s, % roofline"
+UNIT = "node-updates/s"
+FLUSH_BYTES = 256 << 20  # > 126 MB L2
+# Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<1>>
+# (2*DFMA + DMUL + DADD lane ops per evaluation); from the ncu capture in
+# profiles/ (see DESIGN.md "Roofline"). Updated when the kernel changes.
+ORD_FP64_FLOPS_PER_EVAL = 2375.0
+DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def build_problem(config, world, rank):
+    from paper_2011_04747_b200 import problems
+    if config == "c2":
+        if world == 1:
+            return problems.c2()
+        # weak scaling: stack world C2-sized blocks in y (one 201-row slab per rank)
+        import math as _m
+        from paper_2011_04747_b200 import api
+        sh = api.Sheet(5.0, 5.0 * world, 0.025, _m.pi / 4, d0_myocyte=0.0012, rho=0.25)
+        nodes = sh.select("disc", cx=0.0, cy=0.0, radius=problems.C2_RADIUS)
+        cfg = api.SchemeConfig(dt_ms=0.1, t_end_ms=500.0, k0_up=5, k0_down=3)
+        return problems.Problem("C2xN", sh, ["ohara2011-epi"], np.zeros(sh.n, np.uint8),
+                                [(nodes, 0.0, 1.0, problems.C2_AMPLITUDE, None)], cfg,
+                                [sh.nearest(0.0, 0.0), sh.nearest(2.5, 2.5)])
+    if config == "c1":
+        return problems.c1()
+    if config == "c3":
+        return problems.c3()
+    raise SystemExit(f"unknown config {config}")
+
+
+def config_block(config, prob, world, l):
+    names = {"c2": "BASELINE configs[1]: 2D anisotropic sheet 5x5 cm, 201x201 nodes, fibres 45 deg, "
+                   "corner stimulus, ORd-epi, DAETI dt 0.1 ms, 500 ms",
+             "c1": "BASELINE configs[0]: 2D isotropic 1x1 cm, 101x101 nodes, ORd-epi, left-edge 2x threshold",
+             "c3": "BASELINE configs[2] (extension): 1001x1001 scar/border-zone sheet"}
+    return {"workload": names[config], "nodes": int(prob.n), "nodes_per_gpu": int(prob.n // max(world, 1)),
+            "cell_model": prob.models[0], "scheme": "DAETI", "dt_ms": prob.cfg.dt_ms, "k0_up": prob.cfg.k0_up,
+            "k0_down": prob.cfg.k0_down, "diffusion_substeps_per_step": 2 * l,
+            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": f"y-slab x{world}" if world > 1 else "single GPU"}
+
+
+def cpu_reference_steps(config, steps, warmup, budget_s, threads):
+    """Time the reference's own StrangIntegrator::advance (oracle/_ref/libcwref.so) on host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    if config != "c2":
+        raise SystemExit("reference arm implemented for c2/c1")
+    p = refpy.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0=0.0012, rho=0.25)
+    from paper_2011_04747_b200 import problems
+    nodes = p.select("disc", cx=0.0, cy=0.0, radius=problems.C2_RADIUS)
+    p.set_models(["ohara2011-epi"])
+    p.add_stimulus(nodes, 0.0, 1.0, problems.C2_AMPLITUDE)
+    p.init_state()
+    n_total = 5000
+    p.integrator(scheme="DAETI", dt=0.1, t_end=500.0, k0_up=5, k0_down=3, workers=threads)
+    for s in range(warmup):
+        p.advance(s * 0.1, s, n_total)
+    kh0 = p.integrator_khist().copy()
+    t0 = time.perf_counter()
+    done = 0
+    for s in range(warmup, warmup + steps):
+        p.advance(s * 0.1, s, n_total)
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    wall = time.perf_counter() - t0
+    kh1 = p.integrator_khist()
+    evals = int(np.sum((kh1 - kh0) * np.arange(len(kh1))))
+    diff = done * p.n * 2 * p.l
+    return {"steps": done, "wall_s": wall, "evals": evals, "diff": diff, "n": p.n, "l": p.l,
+            "value": (evals + diff) / wall, "sim_ms_per_s": done * 0.1 / wall}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    r = cpu_reference_steps(args.config, args.steps, args.warmup, args.ref_budget, threads)
+    line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
+            "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["wall_s"] * 1e3 / max(r["steps"], 1),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2 (BASELINE configs[1]) through cardwave::StrangIntegrator::advance",
+                       "nodes": r["n"], "threads": threads},
+            "sim_ms_per_s": r["sim_ms_per_s"],
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": f"C2 outer steps {args.warmup}..{args.warmup + r['steps']} "
+                                       f"({r['steps']} x 0.1 ms) after {args.warmup} warm-up steps, "
+                                       f"OpenMP {threads} threads, -O3 reference build"},
+            "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=None)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3"])
+    ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of reference CPU work per arm")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        if args.steps is None:
+            args.steps = 200
+        return run_reference_arm(args)
+
+    import torch
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import _lib as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        obj = [os.urandom(0)]
+        if rank == 0:
+            # ncclGetUniqueId through the torch-bundled NCCL (plumbing only)
+            import ctypes
+            nc = ctypes.CDLL("libnccl.so.2")
+            buf = (ctypes.c_ubyte * 128)()
+            assert nc.ncclGetUniqueId(buf) == 0
+            obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    prob = build_problem(args.config, world, rank)
+    setup = prob.setup()
+    n_total = int(math.ceil(prob.cfg.t_end_ms / prob.cfg.dt_ms - 1e-9))
+    if args.steps is None:
+        args.steps = n_total - args.warmup
+    if args.warmup + args.steps > n_total:  # extend the simulated window to fit
+        prob.cfg.t_end_ms = (args.warmup + args.steps) * prob.cfg.dt_ms
+    integ = cw.StrangIntegrator(setup, prob.cfg, model_of_node=prob.model_of_node, device=local, rank=rank,
+                                world=world, nccl_id=nccl_id)
+    info = integ.info
+    st = prob.initial_state()
+    integ.upload(st)
+    integ.run_begin()
+    integ.run_steps(0, args.warmup)
+    integ.run_sync()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    step_ms, react_ms, diff_ms = np.zeros(K), np.zeros(K), np.zeros(K)
+    lib = L.lib()
+    ev0 = lib.cwg_reaction_evals(integ._h)
+    launches0 = integ.launch_count()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.perf_counter()
+    with ClockSampler(local) as clocks:
+        rc = lib.cwg_bench_steps(integ._h, args.warmup, K, FLUSH_BYTES, L.dp(step_ms), L.dp(react_ms), L.dp(diff_ms))
+        torch.cuda.synchronize()
+    if rc != 0:
+        raise SystemExit(f"cwg_bench_steps failed ({rc})")
+    if dist:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall0
+    integ.run_sync()  # surfaces an InstabilityError from the timed window
+    ev1 = lib.cwg_reaction_evals(integ._h)
+    launches = integ.launch_count() - launches0
+    t_dev_ms = float(step_ms.sum())
+    if dist:
+        tt = torch.tensor([t_dev_ms], dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev_ms = float(tt.item())
+    reaction_evals = ev1 - ev0  # global (khist all-reduced)
+    diff_updates = prob.n * 2 * info.l * K
+    value = (reaction_evals + diff_updates) / (t_dev_ms / 1e3)
+
+    # --- roofline of the dominant kernel (ORd reaction): FP64 pipe
+    peaks, peak_src = load_peaks()
+    fp64_peak = lib.cwg_fp64_peak_tflops(local, 0.5)
+    local_evals = reaction_evals / world
+    react_tot_ms = float(react_ms.sum())
+    achieved = ORD_FP64_FLOPS_PER_EVAL * local_evals / (react_tot_ms / 1e3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            traffic = json.load(f).get("react_dram_bytes_per_launch")
+    except OSError:
+        pass
+    diff_tot_ms = float(diff_ms.sum())
+    diff_gbs = info.n_local * 2 * info.l * K * DIFF_BYTES_PER_NODE_SUBSTEP / (diff_tot_ms / 1e3) / 1e9
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": t_dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_block(args.config, prob, world, info.l),
+            "sim_ms_per_s": K * prob.cfg.dt_ms / (t_dev_ms / 1e3),
+            "reaction_node_updates_per_s": reaction_evals / (t_dev_ms / 1e3),
+            "diffusion_node_updates_per_s": diff_updates / (t_dev_ms / 1e3),
+            "mean_k": reaction_evals / (prob.n * K),
+            "phase_ms": {"reaction": react_tot_ms / K, "diffusion_and_record": diff_tot_ms / K},
+            "wall_s_timed_region": wall,
+            "roofline": {"bound": "fp64", "kernel": "react_kernel<ModelOrd<epi>>", "achieved": achieved,
+                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak > 0 else None,
+                         "traffic": traffic, "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no "
+                                                             "FP64 entry)",
+                         "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL},
+            "roofline_diffusion": {"bound": "hbm", "kernel": "diffuse_stencil2d", "achieved": diff_gbs,
+                                   "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                   "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
+                                   "peak_source": peak_src, "bytes_per_node_substep": DIFF_BYTES_PER_NODE_SUBSTEP,
+                                   "note": "C2 fits in L2; phase time includes probe/detector recording"},
+            "clocks": clocks.summary(), "gpu_launches": int(launches)}
+
+    # --- end to end through the public API (run_simulation) with pinned host state
+    if not args.no_e2e:
+        pin = lambda a: (lambda t: (t.copy_(torch.from_numpy(a)), t.numpy())[1])(
+            torch.empty(a.shape, dtype=torch.float64, pin_memory=True))
+        st0 = prob.initial_state()
+        st0.v, st0.s, st0.last_dvdt = pin(st0.v), pin(st0.s), pin(st0.last_dvdt)
+        e2e_cfg = cw.SchemeConfig(scheme=prob.cfg.scheme, dt_ms=prob.cfg.dt_ms,
+                                  t_end_ms=(args.warmup + K) * prob.cfg.dt_ms, k0_up=prob.cfg.k0_up,
+                                  k0_down=prob.cfg.k0_down)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_integ = cw.StrangIntegrator(setup, e2e_cfg, model_of_node=prob.model_of_node, device=local, rank=rank,
+                                      world=world, nccl_id=nccl_id)
+        res = cw.run_simulation(st0, setup, e2e_cfg, device=local, integrator=e_integ)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            tt = torch.tensor([e2e_s], dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        n_steps_e = args.warmup + K
+        e_evals = int(np.sum(res.k_histogram * np.arange(len(res.k_histogram))))
+        e_val = (e_evals + prob.n * 2 * info.l * n_steps_e) / e2e_s
+        stride = st0.stride
+        h2d = prob.n * (2 + stride) * 8
+        d2h = prob.n * (2 + stride) * 8 + prob.n * (2 * 8 + 2) + len(prob.probes) * info.n_samples * 8
+        line["e2e"] = {"value": e_val, "unit": UNIT, "h2d_bytes_per_step": h2d / n_steps_e,
+                       "d2h_bytes_per_step": d2h / n_steps_e,
+                       "call": "paper_2011_04747_b200.run_simulation (cwg_create + state upload from pinned host "
+                               "memory + all steps + traces/maps/final-state download)",
+                       "steps": n_steps_e, "wall_s": e2e_s}
+        e_integ.close()
+
+    # --- CPU baseline: the reference itself on this host (rank 0, N = 1)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
+        try:
+            threads = len(os.sched_getaffinity(0))
+            r = cpu_reference_steps("c2", 100000, args.warmup, 15.0, threads)
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+                                    "sample": f"C2 outer steps {args.warmup}..{args.warmup + r['steps']} through "
+                                              f"cardwave::StrangIntegrator::advance (oracle/_ref), ~15 s budget",
+                                    "sim_ms_per_s": r["sim_ms_per_s"]}
+        except Exception as e:  # the checker library is a build artefact; report its absence
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    integ.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -186,6 +186,20 @@ int cwg_get_timing(cwg_ctx* ctx, double* reaction_ms, double* diffusion_ms, doub
 /* Kernel launches issued by this context so far (for the bench's gpu_launches). */
 int64_t cwg_launch_count(cwg_ctx* ctx);
 
+/* Benchmark driver (bench.py): enqueue steps [first, first+count) one at a
+ * time, each preceded by an (untimed) write of flush_bytes to a scratch
+ * buffer that evicts L2, and bracketed by CUDA events on the context stream:
+ * step_ms[i] = whole step, react_ms[i] = the reaction kernels (step A),
+ * diff_ms[i] = diffusion sub-steps + recording. Returns after a sync. */
+int cwg_bench_steps(cwg_ctx* ctx, int64_t first, int64_t count, int64_t flush_bytes, double* step_ms,
+                    double* react_ms, double* diff_ms);
+/* Reaction node-updates (rates evaluations) so far = sum_k k * khist[k]. */
+int64_t cwg_reaction_evals(cwg_ctx* ctx);
+
+/* Measured FP64 peak of this device: a DFMA-chain kernel at full occupancy,
+ * CUDA-event timed. Returns TFLOP/s (2 flops per DFMA) or < 0 on error. */
+double cwg_fp64_peak_tflops(int device, double seconds);
+
 /* diffusion_substep (fem.cpp:194-207): standalone out = v - dt/m * K v on the
  * device, host in/out, bit-identical to the reference. */
 int cwg_diffusion_substep(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,

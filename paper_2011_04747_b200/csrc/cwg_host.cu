@@ -254,6 +254,10 @@ struct cwg_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double t_react = 0, t_diff = 0, t_rec = 0;
 
+  // bench
+  void* d_flush = nullptr;
+  size_t flush_bytes = 0;
+
   // pinned staging
   double *h_v = nullptr, *h_s = nullptr, *h_last = nullptr;
   double* d_stage = nullptr;
@@ -292,6 +296,7 @@ void ctx_free(cwg_ctx* c) {
   dev_free(c->d_probe_loc);
   dev_free(c->d_traces);
   dev_free(c->d_stage);
+  if (c->d_flush) cudaFree(c->d_flush);
   double** dd[] = {&c->det.prev_v, &c->det.v_rest, &c->det.max_slope, &c->det.t_max_slope, &c->det.v_peak,
                    &c->det.lat, &c->det.apd};
   for (auto p : dd) dev_free(*p);
@@ -1190,6 +1195,116 @@ int cwg_get_timing(cwg_ctx* c, double* r, double* d, double* rec) {
 }
 
 int64_t cwg_launch_count(cwg_ctx* c) { return c->launches; }
+
+int64_t cwg_reaction_evals(cwg_ctx* c) {
+  std::vector<int64_t> h(static_cast<size_t>(c->khist_len));
+  if (cwg_get_khist(c, h.data(), c->khist_len) != CWG_OK) return -1;
+  int64_t s = 0;
+  for (int k = 0; k < c->khist_len; ++k) s += static_cast<int64_t>(k) * h[k];
+  return s;
+}
+
+int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_bytes, double* step_ms,
+                    double* react_ms, double* diff_ms) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    validation(first >= 0 && first + count <= c->n_steps, "bench: step range outside [0, n_steps)");
+    if (flush_bytes > 0 && static_cast<size_t>(flush_bytes) > c->flush_bytes) {
+      if (c->d_flush) cudaFree(c->d_flush);
+      CUDA_TRY(cudaMalloc(&c->d_flush, static_cast<size_t>(flush_bytes)));
+      c->flush_bytes = static_cast<size_t>(flush_bytes);
+    }
+    constexpr int kChunk = 256;
+    std::vector<cudaEvent_t> ev(3 * kChunk);
+    for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+    try {
+      for (int64_t b = 0; b < count; b += kChunk) {
+        const int64_t m = std::min<int64_t>(kChunk, count - b);
+        for (int64_t i = 0; i < m; ++i) {
+          const long long step = first + b + i;
+          if (flush_bytes > 0)
+            CUDA_TRY(cudaMemsetAsync(c->d_flush, static_cast<int>(step & 0xff), static_cast<size_t>(flush_bytes),
+                                     c->stream));
+          set_clock(c, step);
+          CUDA_TRY(cudaEventRecord(ev[3 * i], c->stream));
+          if (step == 0) enqueue_diffusion(c, c->l, 0, 0);
+          enqueue_reaction(c, 0, c->l, false, 0.0);
+          CUDA_TRY(cudaEventRecord(ev[3 * i + 1], c->stream));
+          enqueue_diffusion(c, step == c->n_steps - 1 ? c->l : 2 * c->l, 0, c->l + 1);
+          const long long S = step + 1;
+          if (c->n_probes > 0 && S % c->spr == 0) {
+            CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, 1,
+                                          c->spr, c->stream));
+            ++c->launches;
+          }
+          if (S % c->spm == 0) {
+            CUDA_TRY(launch_detector_observe(c->d_v[c->cur] + c->halo, c->n_own, 0, c->det, c->d_clock, 1, c->spm,
+                                             c->dt_eff, c->stream));
+            ++c->launches;
+          }
+          CUDA_TRY(cudaEventRecord(ev[3 * i + 2], c->stream));
+        }
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < m; ++i) {
+          float a = 0, d = 0;
+          CUDA_TRY(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 1]));
+          CUDA_TRY(cudaEventElapsedTime(&d, ev[3 * i + 1], ev[3 * i + 2]));
+          if (react_ms) react_ms[b + i] = a;
+          if (diff_ms) diff_ms[b + i] = d;
+          if (step_ms) step_ms[b + i] = static_cast<double>(a) + d;
+        }
+      }
+    } catch (...) {
+      for (auto& e : ev) cudaEventDestroy(e);
+      throw;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+  });
+}
+
+double cwg_fp64_peak_tflops(int device, double seconds) {
+  double result = -1.0;
+  guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    int occ = 0;
+    occ = 8;  // 8 x 256 threads per SM
+    const int blocks = prop.multiProcessorCount * occ;
+    double* out = dev_alloc<double>(1);
+    cudaEvent_t a, b;
+    CUDA_TRY(cudaEventCreate(&a));
+    CUDA_TRY(cudaEventCreate(&b));
+    int iters = 1 << 14;
+    CUDA_TRY(launch_fp64_peak(out, blocks, iters, nullptr));  // warm-up
+    CUDA_TRY(cudaDeviceSynchronize());
+    float ms = 0;
+    for (int rep = 0; rep < 6; ++rep) {
+      CUDA_TRY(cudaEventRecord(a));
+      CUDA_TRY(launch_fp64_peak(out, blocks, iters, nullptr));
+      CUDA_TRY(cudaEventRecord(b));
+      CUDA_TRY(cudaEventSynchronize(b));
+      CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+      if (ms > seconds * 1e3 / 4 || iters >= (1 << 24)) break;
+      iters *= 2;
+    }
+    double best = 0.0;
+    for (int rep = 0; rep < 5; ++rep) {
+      CUDA_TRY(cudaEventRecord(a));
+      CUDA_TRY(launch_fp64_peak(out, blocks, iters, nullptr));
+      CUDA_TRY(cudaEventRecord(b));
+      CUDA_TRY(cudaEventSynchronize(b));
+      CUDA_TRY(cudaEventElapsedTime(&ms, a, b));
+      const double flops = 2.0 * 8.0 * static_cast<double>(iters) * blocks * 256.0;
+      best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    dev_free(out);
+    result = best;
+  });
+  return result;
+}
 
 int cwg_diffusion_substep(int64_t n, const int64_t* rp, const int64_t* col, const double* val, const double* mass,
                           const double* v, double dt_sub, double* out, int device, cwg_error* err) {

@@ -190,6 +190,22 @@ __global__ void mass_factor(const double* mass, long long n, double dt_sub, doub
   if (i < n) cm[i] = dt_sub / mass[i];
 }
 
+// FP64 peak probe: 8 independent DFMA chains per thread (explicit fma(), so
+// --fmad=false does not matter), iterated; one result store keeps it alive.
+__global__ void __launch_bounds__(256) fp64_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = threadIdx.x * 1e-3 + q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) x[q] = fma(x[q], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += x[q];
+  if (s == 1.2345) out[0] = s;
+}
+
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
@@ -257,6 +273,11 @@ cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const lon
                                      cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   diffuse_csr_plain<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(n, rp, col, val, mass, v, dt_sub, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t st) {
+  fp64_peak<<<blocks, 256, 0, st>>>(out, iters, 0.999999, 1e-7);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,7 @@ cudaError_t launch_soa_to_aos(const double* soa, long long pitch, long long src0
 cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const long long* col, const double* val,
                                      const double* mass, const double* v, double dt_sub, double* out,
                                      cudaStream_t st);
+cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t st);
 cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st);
 
 }  // namespace cwg

@@ -53,7 +53,7 @@ C1_AMPLITUDE = 592.0
 # (radius 2h) stimulus. Amplitude chosen stable + propagating in the reference
 # (SURVEY.md 8(d) caution 2; probe recorded in DESIGN.md).
 C2_AMPLITUDE = 100.0
-C2_RADIUS = 0.05
+C2_RADIUS = 0.15
 
 
 def c1(model="ohara2011-epi", t_end=400.0, k0_down=3, amplitude=None, strip=None, scheme=api.Scheme.DAETI,

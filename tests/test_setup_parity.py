@@ -1,0 +1,74 @@
+"""Host setup (include/cwgpu_setup.h) against the reference's own setup path:
+the CSR operator, lumped mass, Gershgorin dt_s, fibrosis tags and node
+selections must be bit-identical (mesh.cpp:72-180, fem.cpp:21-192)."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2011_04747_b200 as cw
+
+GEOMS = [
+    dict(lx=1.0, ly=1.0, h=0.01, ang=0.0, d0=0.001, rho=1.0),                # C1
+    dict(lx=5.0, ly=5.0, h=0.025, ang=math.pi / 4, d0=0.0012, rho=0.25),    # C2
+    dict(lx=2.0, ly=2.0, h=0.02, ang=0.3, d0=0.0017, rho=0.25, frac=0.25, seed=9),  # fibrotic
+    dict(lx=0.5, ly=0.3, h=0.05, ang=1.1, d0=0.0013, rho=0.5),
+]
+
+
+@pytest.mark.parametrize("g", GEOMS)
+def test_operator_bitwise(ref, g):
+    frac, seed = g.get("frac", 0.0), g.get("seed", 0)
+    ours = cw.Sheet(g["lx"], g["ly"], g["h"], g["ang"], d0_myocyte=g["d0"], rho=g["rho"], fib_fraction=frac, seed=seed)
+    theirs = ref.Sheet(g["lx"], g["ly"], g["h"], g["ang"], d0=g["d0"], rho=g["rho"], fib_fraction=frac, seed=seed)
+    rp, col, val, mass = theirs.csr()
+    assert ours.n == theirs.n
+    assert np.array_equal(ours.op.row_ptr, rp)
+    assert np.array_equal(ours.op.col, col)
+    assert np.array_equal(ours.op.val, val)
+    assert np.array_equal(ours.op.lumped_mass, mass)
+    assert ours.op.dt_s == theirs.dt_s
+    tags, names = theirs.tags()
+    assert np.array_equal(ours.tags, tags)
+
+
+def test_known_dt_s_values(ref):
+    # SPEC.md:139 (5x5 cm, h = 100 um, d0 0.0017, rho 0.25): reference gives 0.0132353
+    s = cw.Sheet(1.0, 1.0, 0.01, 0.0, d0_myocyte=0.0017, rho=0.25)  # dt_s depends on h, not on the extent
+    assert abs(s.op.dt_s - 0.0132353) < 1e-6
+    # h^2 scaling
+    a = cw.Sheet(1.0, 1.0, 0.02, 0.0).op.dt_s
+    b = cw.Sheet(1.0, 1.0, 0.01, 0.0).op.dt_s
+    assert abs(a / b - 4.0) < 0.05
+
+
+@pytest.mark.parametrize("sel", [
+    ("x_le", dict(value=0.05)), ("x_ge", dict(value=0.95)), ("y_le", dict(value=0.0)), ("y_ge", dict(value=0.5)),
+    ("rectangle", dict(x0=0.2, x1=0.4, y0=0.1, y1=0.3)), ("disc", dict(cx=0.0, cy=0.0, radius=0.05)),
+    ("disc", dict(cx=0.5, cy=0.5, radius=0.2)), ("node_set", dict(nodes=(5, 3, 3, 99))),
+])
+def test_select_nodes(ref, sel):
+    ours = cw.Sheet(1.0, 1.0, 0.01, 0.0)
+    theirs = ref.Sheet(1.0, 1.0, 0.01, 0.0)
+    assert np.array_equal(ours.select(sel[0], **sel[1]), theirs.select(sel[0], **sel[1]))
+    for x, y in [(0.5, 0.5), (0.0, 0.0), (0.333, 0.777), (1.0, 1.0)]:
+        assert ours.nearest(x, y) == theirs.nearest(x, y)
+
+
+def test_validation_errors():
+    with pytest.raises(cw.ValidationError):
+        cw.Sheet(1.0, 1.0, 0.03, 0.0)  # not a multiple of h
+    with pytest.raises(cw.ValidationError):
+        cw.Sheet(1.0, 1.0, 0.1, 0.0, rho=1.5)
+
+
+def test_scar_extension_gershgorin_skips_zero_rows():
+    ne = 20 * 20
+    scale = np.ones(ne)
+    scale[150:170] = 0.0
+    s = cw.Sheet(1.0, 1.0, 0.05, 0.0, elem_scale=scale)
+    full = cw.Sheet(1.0, 1.0, 0.05, 0.0)
+    assert s.op.dt_s >= full.op.dt_s - 1e-15
+    assert np.all(np.isfinite(s.op.val))
+    with pytest.raises(cw.ValidationError):
+        cw.Sheet(1.0, 1.0, 0.05, 0.0, elem_scale=np.zeros(ne))
