@@ -1,0 +1,95 @@
+// TEST INFRASTRUCTURE: the C++ drop-in (include/cardwave_gpu.hpp) side by side
+// with the unmodified reference, on the same reference-built problem.
+//   shim_parity ap|ord|abort|diffusion   -> one JSON line; exit 0 on parity
+// Built by oracle/Makefile (target `shim`) into oracle/_ref/shim_parity,
+// linked against the reference objects and ../paper_2011_04747_b200/libcwgpu.so.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "cardwave/errors.hpp"
+#include "cardwave/fem.hpp"
+#include "cardwave/mesh.hpp"
+#include "cardwave/splitting.hpp"
+#include "cardwave/stimulus.hpp"
+#include "cardwave_gpu.hpp"
+
+using namespace cardwave;
+
+int main(int argc, char** argv) {
+  const std::string mode = argc > 1 ? argv[1] : "ap";
+  Mesh mesh = build_regular_sheet(1.0, 1.0, 0.01, 0.0);
+  AssembledOperator op = assemble(mesh, build_diffusion_field(mesh, 0.001, 0.00066, 1.0));
+  if (mode == "diffusion") {
+    std::vector<double> v(op.rows()), a, b;
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = -80.0 + 100.0 * std::sin(0.37 * static_cast<double>(i));
+    diffusion_substep(op, v, 0.0123, a);
+    gpu::diffusion_substep(op, v, 0.0123, b);
+    const bool same = a == b;
+    std::printf("{\"mode\":\"diffusion\",\"bitwise\":%s}\n", same ? "true" : "false");
+    return same ? 0 : 1;
+  }
+  const bool ap = mode == "ap";
+  std::vector<std::shared_ptr<const CellModel>> models = {make_model(ap ? "aliev-panfilov" : "ohara2011-epi")};
+  RegionSelector sel;
+  sel.kind = RegionSelector::Kind::half_plane_x_le;
+  sel.value = ap ? 0.05 : 0.0;
+  Protocol prot;
+  Stimulus st;
+  st.nodes = select_nodes(mesh, sel);
+  st.amplitude = ap ? 100.0 : 592.0;
+  prot.entries.push_back(st);
+  ProtocolIndex index(prot, mesh.node_count());
+  SimulationSetup setup;
+  setup.op = &op;
+  setup.models = models;
+  setup.protocol = &index;
+  setup.probes = {Probe{5050, "mid"}, Probe{10200, "far"}};
+  SchemeConfig cfg;
+  cfg.scheme = Scheme::DAETI;
+  cfg.dt_ms = 0.1;
+  cfg.t_end_ms = ap ? 100.0 : 20.0;
+  cfg.k0_down = mode == "abort" ? 1 : (ap ? 1 : 3);
+  NodeStateArray s0 = make_initial_state(mesh, models, {0});
+
+  long ref_node = -1, gpu_node = -1;
+  double ref_t = 0, gpu_t = 0;
+  SimulationResult a, b;
+  bool ref_ok = true, gpu_ok = true;
+  try {
+    a = run_simulation(s0, setup, cfg);
+  } catch (const InstabilityError& e) {
+    ref_ok = false;
+    ref_node = e.node_index;
+    ref_t = e.time_ms;
+  }
+  try {
+    b = gpu::run_simulation(s0, setup, cfg);
+  } catch (const InstabilityError& e) {
+    gpu_ok = false;
+    gpu_node = e.node_index;
+    gpu_t = e.time_ms;
+  }
+  if (!ref_ok || !gpu_ok) {
+    const bool same = !ref_ok && !gpu_ok && ref_node == gpu_node && ref_t == gpu_t;
+    std::printf("{\"mode\":\"%s\",\"ref_abort\":[%ld,%.17g],\"gpu_abort\":[%ld,%.17g],\"match\":%s}\n", mode.c_str(),
+                ref_node, ref_t, gpu_node, gpu_t, same ? "true" : "false");
+    return same ? 0 : 1;
+  }
+  double dv = 0, dl = 0;
+  for (std::size_t i = 0; i < a.final_state.v.size(); ++i) dv = std::max(dv, std::abs(a.final_state.v[i] - b.final_state.v[i]));
+  for (std::size_t p = 0; p < a.traces.size(); ++p)
+    for (std::size_t q = 0; q < a.traces[p].v_mv.size(); ++q)
+      dv = std::max(dv, std::abs(a.traces[p].v_mv[q] - b.traces[p].v_mv[q]));
+  bool valid_same = a.lat_map.valid == b.lat_map.valid;
+  for (std::size_t i = 0; i < a.lat_map.value.size(); ++i)
+    if (a.lat_map.valid[i]) dl = std::max(dl, std::abs(a.lat_map.value[i] - b.lat_map.value[i]));
+  const bool kh = a.k_histogram == b.k_histogram;
+  const bool pass = ap ? (dv == 0.0 && dl == 0.0 && kh && valid_same) : (dv <= 1e-6 && dl < 1e-6 && kh && valid_same);
+  std::printf("{\"mode\":\"%s\",\"max_dV_mV\":%.3e,\"max_dLAT_ms\":%.3e,\"khist_equal\":%s,\"lat_valid_equal\":%s,"
+              "\"pass\":%s,\"ref_ms\":%.1f,\"gpu_ms\":%.1f}\n",
+              mode.c_str(), dv, dl, kh ? "true" : "false", valid_same ? "true" : "false", pass ? "true" : "false",
+              a.timing.total_ms, b.timing.total_ms);
+  return pass ? 0 : 1;
+}

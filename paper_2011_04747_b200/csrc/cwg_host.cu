@@ -518,8 +518,23 @@ bool stencil_ok(const cwg_problem* p) {
   return true;
 }
 
-void create_impl(const cwg_problem* p, cwg_ctx* c) {
-  validation(p && p->n > 0, "integrator: empty problem");
+// A regular sheet's row 0 couples {0, 1, w, w+1} (mesh.hpp:23-24 numbering):
+// infer the grid when the caller (e.g. the C++ drop-in) has only the CSR.
+void infer_grid(cwg_problem* q) {
+  if (q->grid_nx1 > 0 || !q->row_ptr || q->n < 4) return;
+  if (q->row_ptr[1] - q->row_ptr[0] != 4) return;
+  const long long w = q->col[2];
+  if (q->col[0] != 0 || q->col[1] != 1 || w < 2 || q->col[3] != w + 1 || q->n % w != 0) return;
+  q->grid_nx1 = w;
+  q->grid_ny1 = q->n / w;
+}
+
+void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
+  validation(p_in != nullptr, "integrator: empty problem");
+  cwg_problem pc = *p_in;
+  if (pc.op_kind == CWG_OP_AUTO) infer_grid(&pc);
+  const cwg_problem* p = &pc;
+  validation(p->n > 0, "integrator: empty problem");
   validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
   validation(p->n_models > 0 && p->model_kind, "integrator: no cell models");
   validation(p->dt_ms > 0.0, "scheme: dt must be positive");
