@@ -1,0 +1,23 @@
+"""The C++ drop-in (include/cardwave_gpu.hpp) side by side with the unmodified
+reference in one process: oracle/_ref/shim_parity runs cardwave::run_simulation
+and cardwave::gpu::run_simulation on the same reference-built problem."""
+import json
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+EXE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "shim_parity")
+
+
+@pytest.mark.parametrize("mode", ["diffusion", "ap", "ord", "abort"])
+def test_cpp_dropin_matches_reference(mode):
+    if not os.path.exists(EXE):
+        pytest.skip("shim_parity not built (needs /root/reference at build time)")
+    r = subprocess.run([EXE, mode], capture_output=True, text=True, timeout=900)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    if mode == "abort":
+        assert line["ref_abort"][0] == 16 and line["match"]
