@@ -250,7 +250,8 @@ def main():
     torch.cuda.synchronize()
     t_wall0 = time.perf_counter()
     with ClockSampler(local) as clocks:
-        rc = lib.cwg_bench_steps(integ._h, args.warmup, K, FLUSH_BYTES, L.dp(step_ms), L.dp(react_ms), L.dp(diff_ms))
+        rc = lib.cwg_bench_steps(integ._h, args.warmup, K, FLUSH_BYTES, 0, L.dp(step_ms), L.dp(react_ms),
+                                 L.dp(diff_ms))
         torch.cuda.synchronize()
     if rc != 0:
         raise SystemExit(f"cwg_bench_steps failed ({rc})")
@@ -303,7 +304,9 @@ def main():
                                    "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                    "peak_source": peak_src, "bytes_per_node_substep": DIFF_BYTES_PER_NODE_SUBSTEP,
                                    "note": "C2 fits in L2; phase time includes probe/detector recording"},
-            "clocks": clocks.summary(), "gpu_launches": int(launches)}
+            "clocks": clocks.summary(), "gpu_launches": int(launches),
+            "launch_mode": "one CUDA graph per step (event-record nodes at step start / after reaction / end)",
+            "ord_min_blocks": int(os.environ.get("CWG_ORD_MINB", "2"))}
 
     # --- end to end through the public API (run_simulation) with pinned host state
     if not args.no_e2e:

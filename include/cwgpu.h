@@ -188,11 +188,13 @@ int64_t cwg_launch_count(cwg_ctx* ctx);
 
 /* Benchmark driver (bench.py): enqueue steps [first, first+count) one at a
  * time, each preceded by an (untimed) write of flush_bytes to a scratch
- * buffer that evicts L2, and bracketed by CUDA events on the context stream:
- * step_ms[i] = whole step, react_ms[i] = the reaction kernels (step A),
- * diff_ms[i] = diffusion sub-steps + recording. Returns after a sync. */
-int cwg_bench_steps(cwg_ctx* ctx, int64_t first, int64_t count, int64_t flush_bytes, double* step_ms,
-                    double* react_ms, double* diff_ms);
+ * buffer that evicts L2, and bracketed by CUDA events on the context stream.
+ * split_phases = 0: each middle step is one single-step CUDA graph (the
+ * production launch path), step_ms[i] = the step; split_phases = 1: direct
+ * launches with an extra event between the reaction kernels (step A) and
+ * the diffusion sub-steps + recording: react_ms[i], diff_ms[i]. */
+int cwg_bench_steps(cwg_ctx* ctx, int64_t first, int64_t count, int64_t flush_bytes, int split_phases,
+                    double* step_ms, double* react_ms, double* diff_ms);
 /* Reaction node-updates (rates evaluations) so far = sum_k k * khist[k]. */
 int64_t cwg_reaction_evals(cwg_ctx* ctx);
 

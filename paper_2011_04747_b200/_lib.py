@@ -73,7 +73,7 @@ _SIGS = {
     "cwg_get_maps": (C.c_int, [C.c_void_p, _dp, _u8p, _dp, _u8p]),
     "cwg_get_timing": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "cwg_launch_count": (C.c_int64, [C.c_void_p]),
-    "cwg_bench_steps": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _dp]),
+    "cwg_bench_steps": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, _dp, _dp, _dp]),
     "cwg_reaction_evals": (C.c_int64, [C.c_void_p]),
     "cwg_fp64_peak_tflops": (C.c_double, [C.c_int, C.c_double]),
     "cwg_diffusion_substep": (C.c_int, [C.c_int64, _lp, _lp, _dp, _dp, _dp, C.c_double, _dp, C.c_int,

@@ -457,6 +457,80 @@ void build_graph(cwg_ctx* c, long long b0) {
   c->graph_base_mod = ((b0 % c->G) + c->G) % c->G;
 }
 
+// One middle step as a graph (bench timing: the production launch path,
+// kernels back to back) with three external event-record nodes -- step start,
+// end of the reaction pass, step end -- whose events are swapped per launch
+// (cudaGraphExecEventRecordNodeSetEvent) so every timed step has its own.
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphNode_t ev_nodes[3] = {nullptr, nullptr, nullptr};
+  long long launches = 0;
+};
+
+StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
+  const long long S = step + 1;
+  const int flags = ((c->n_probes > 0 && S % c->spr == 0) ? 1 : 0) | (S % c->spm == 0 ? 2 : 0);
+  StepGraph& sg = cache[flags];
+  if (sg.exec) return sg;
+  cudaGraph_t g = nullptr;
+  const int cur0 = c->cur;
+  const long long l0 = c->launches;
+  cudaEvent_t tmp[3];
+  for (auto& e : tmp) CUDA_TRY(cudaEventCreate(&e));
+  CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    CUDA_TRY(cudaEventRecordWithFlags(tmp[0], c->stream, cudaEventRecordExternal));
+    enqueue_reaction(c, 0, c->l, false, 0.0);
+    CUDA_TRY(cudaEventRecordWithFlags(tmp[1], c->stream, cudaEventRecordExternal));
+    const long long base = step;
+    enqueue_diffusion(c, 2 * c->l, 0, c->l + 1);
+    if (flags & 1) {
+      CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, 1, c->spr,
+                                    c->stream));
+      ++c->launches;
+    }
+    if (flags & 2) {
+      CUDA_TRY(launch_detector_observe(c->d_v[c->cur] + c->halo, c->n_own, 0, c->det, c->d_clock, 1, c->spm,
+                                       c->dt_eff, c->stream));
+      ++c->launches;
+    }
+    (void)base;
+    CUDA_TRY(cudaEventRecordWithFlags(tmp[2], c->stream, cudaEventRecordExternal));
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    for (auto& e : tmp) cudaEventDestroy(e);
+    throw;
+  }
+  CUDA_TRY(cudaStreamEndCapture(c->stream, &g));
+  sg.launches = c->launches - l0;
+  c->launches = l0;
+  // locate the event-record nodes in capture order (they form a chain with the kernels)
+  size_t nn = 0;
+  CUDA_TRY(cudaGraphGetNodes(g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  CUDA_TRY(cudaGraphGetNodes(g, nodes.data(), &nn));
+  int found = 0;
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e;
+    CUDA_TRY(cudaGraphEventRecordNodeGetEvent(nd, &e));
+    for (int q = 0; q < 3; ++q)
+      if (e == tmp[q]) {
+        sg.ev_nodes[q] = nd;
+        ++found;
+      }
+  }
+  if (found != 3) throw Fail{CWG_ECUDA, "step graph: event nodes not found"};
+  CUDA_TRY(cudaGraphInstantiate(&sg.exec, g, 0));
+  cudaGraphDestroy(g);
+  for (auto& e : tmp) cudaEventDestroy(e);
+  if (c->cur != cur0) throw Fail{CWG_ECUDA, "step graph must preserve the V buffer parity"};
+  return sg;
+}
+
 long long lcm_ll(long long a, long long b) { return a / std::gcd(a, b) * b; }
 
 }  // namespace
@@ -1219,8 +1293,8 @@ int64_t cwg_reaction_evals(cwg_ctx* c) {
   return s;
 }
 
-int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_bytes, double* step_ms,
-                    double* react_ms, double* diff_ms) {
+int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_bytes, int split_phases,
+                    double* step_ms, double* react_ms, double* diff_ms) {
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     validation(first >= 0 && first + count <= c->n_steps, "bench: step range outside [0, n_steps)");
@@ -1230,6 +1304,7 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
       c->flush_bytes = static_cast<size_t>(flush_bytes);
     }
     constexpr int kChunk = 256;
+    StepGraph graphs[4];
     std::vector<cudaEvent_t> ev(3 * kChunk);
     for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
     try {
@@ -1241,6 +1316,15 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
             CUDA_TRY(cudaMemsetAsync(c->d_flush, static_cast<int>(step & 0xff), static_cast<size_t>(flush_bytes),
                                      c->stream));
           set_clock(c, step);
+          const bool middle = step >= 1 && step < c->n_steps - 1;
+          if (middle && split_phases == 0) {
+            StepGraph& sg = step_graph(c, step, graphs);
+            for (int q = 0; q < 3; ++q)
+              CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(sg.exec, sg.ev_nodes[q], ev[3 * i + q]));
+            CUDA_TRY(cudaGraphLaunch(sg.exec, c->stream));
+            c->launches += sg.launches;
+            continue;
+          }
           CUDA_TRY(cudaEventRecord(ev[3 * i], c->stream));
           if (step == 0) enqueue_diffusion(c, c->l, 0, 0);
           enqueue_reaction(c, 0, c->l, false, 0.0);
@@ -1271,9 +1355,13 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
       }
     } catch (...) {
       for (auto& e : ev) cudaEventDestroy(e);
+      for (auto& sg : graphs)
+        if (sg.exec) cudaGraphExecDestroy(sg.exec);
       throw;
     }
     for (auto& e : ev) cudaEventDestroy(e);
+    for (auto& sg : graphs)
+      if (sg.exec) cudaGraphExecDestroy(sg.exec);
   });
 }
 

@@ -10,7 +10,7 @@
 //   * 1/(1 + a/x) style terms are rewritten as x/(x + a) (one reciprocal);
 //   * e^x, e^2x, expm1(2x) for the GHK terms derive from one expm1(x); the
 //     reciprocal-pair exponentials (tff, tfcaf) share one exp;
-//   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one exp(log).
+//   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one fexp(log).
 // It therefore agrees with the reference to rounding, not bitwise; the parity
 // contract for ORd is max|dV| <= 1e-6 mV (tests/test_gpu_parity.py), which
 // the survey's +-1-ulp experiment shows is met with ~8 orders of margin.
@@ -20,6 +20,9 @@
 // derivative depends only on V and itself), so old and new gate values are
 // never live together; concentrations, which every current reads, are updated
 // last. The FE update itself (x + h*dx) is never contracted.
+#include <cstdlib>
+
+#include "fastmath.cuh"
 #include "react.cuh"
 
 namespace cwg {
@@ -36,7 +39,7 @@ constexpr double ACAP = 2.0 * AGEO;
 constexpr double VMYO = 0.68 * VCELL, VNSR = 0.0552 * VCELL, VJSR = 0.0048 * VCELL, VSS = 0.02 * VCELL;
 
 __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
-__device__ __forceinline__ double sigm(double u) { return __drcp_rn(1.0 + exp(u)); }  // 1/(1+e^u)
+__device__ __forceinline__ double sigm(double u) { return __drcp_rn(1.0 + fexp(u)); }  // 1/(1+e^u)
 
 template <int CT>  // 0 endo, 1 epi, 2 mid (ohara_rudy_2011.cpp:86-87 celltype_)
 struct Var {
@@ -133,12 +136,12 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double i_na;
   {
     const double m_inf = sigm(-(v + 39.57) * (1.0 / 9.871));
-    const double r_m = 6.765 * exp((v + 11.64) * (1.0 / 34.77)) + 8.552 * exp(-(v + 77.42) * (1.0 / 5.955));
+    const double r_m = 6.765 * fexp((v + 11.64) * (1.0 / 34.77)) + 8.552 * fexp(-(v + 77.42) * (1.0 / 5.955));
     const double h_inf = sigm((v + 82.90) * (1.0 / 6.086));
-    const double r_hf = 1.432e-5 * exp(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * exp((v + 0.5096) * (1.0 / 20.27));
-    const double r_hs = 0.009794 * exp(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * exp((v + 5.730) * (1.0 / 56.66));
-    const double r_j = rcp(2.038 + rcp(0.02136 * exp(-(v + 100.6) * (1.0 / 8.281)) +
-                                       0.3052 * exp((v + 0.9941) * (1.0 / 38.45))));
+    const double r_hf = 1.432e-5 * fexp(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * fexp((v + 0.5096) * (1.0 / 20.27));
+    const double r_hs = 0.009794 * fexp(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * fexp((v + 5.730) * (1.0 / 56.66));
+    const double r_j = rcp(2.038 + rcp(0.02136 * fexp(-(v + 100.6) * (1.0 / 8.281)) +
+                                       0.3052 * fexp((v + 0.9941) * (1.0 / 38.45))));
     const double hp_inf = sigm((v + 89.1) * (1.0 / 6.086));
     const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
     const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
@@ -165,11 +168,11 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double i_to;
   {
     const double a_inf = sigm(-(v - 14.34) * (1.0 / 14.82));
-    const double r_a = (1.0 / 1.0515) * (rcp(1.2089 * (1.0 + exp(-(v - 18.4099) * (1.0 / 29.3814)))) +
+    const double r_a = (1.0 / 1.0515) * (rcp(1.2089 * (1.0 + fexp(-(v - 18.4099) * (1.0 / 29.3814)))) +
                                          3.5 * sigm((v + 100.0) * (1.0 / 29.3814)));
     const double i_inf = sigm((v + 43.94) * (1.0 / 5.711));
-    double t_if = 4.562 + rcp(0.3933 * exp(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * exp((v + 50.0) * (1.0 / 16.59)));
-    double t_is = 23.62 + rcp(0.001416 * exp(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * exp((v + 114.1) * (1.0 / 8.079)));
+    double t_if = 4.562 + rcp(0.3933 * fexp(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * fexp((v + 50.0) * (1.0 / 16.59)));
+    double t_is = 23.62 + rcp(0.001416 * fexp(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * fexp((v + 114.1) * (1.0 / 8.079)));
     if (P::epi) {
       const double d_epi = 1.0 - 0.95 * sigm((v + 70.0) * (1.0 / 5.0));
       t_if *= d_epi;
@@ -179,7 +182,7 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
     const double a_if = sigm((v - 213.6) * (1.0 / 151.2));
     const double a_is = 1.0 - a_if;
     const double ap_inf = sigm(-(v - 24.34) * (1.0 / 14.82));
-    const double dev = 1.354 + 1.0e-4 * rcp(exp((v - 167.4) * (1.0 / 15.89)) + exp(-(v - 12.23) * (1.0 / 0.2154)));
+    const double dev = 1.354 + 1.0e-4 * rcp(fexp((v - 167.4) * (1.0 / 15.89)) + fexp(-(v - 12.23) * (1.0 / 0.2154)));
     const double rec = 1.0 - 0.5 * sigm((v + 70.0) * (1.0 / 20.0));
     const double r_dr = rcp(dev * rec);
     const double imix = a_if * s[IF] + a_is * s[IS];
@@ -205,14 +208,14 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double i_cal, i_cana, i_cak;
   {
     const double d_inf = sigm(-(v + 3.940) * (1.0 / 4.230));
-    const double r_d = rcp(0.6 + rcp(exp(-0.05 * (v + 6.0)) + exp(0.09 * (v + 14.0))));
+    const double r_d = rcp(0.6 + rcp(fexp(-0.05 * (v + 6.0)) + fexp(0.09 * (v + 14.0))));
     const double f_inf = sigm((v + 19.58) * (1.0 / 3.696));
-    const double eff = exp((v + 20.0) * (1.0 / 10.0));
+    const double eff = fexp((v + 20.0) * (1.0 / 10.0));
     const double r_ff = rcp(7.0 + rcp(0.0045 * (rcp(eff) + eff)));
-    const double r_fs = rcp(1000.0 + rcp(0.000035 * exp(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * exp((v + 5.0) * (1.0 / 6.0))));
-    const double efc = exp((v - 4.0) * (1.0 / 7.0));
+    const double r_fs = rcp(1000.0 + rcp(0.000035 * fexp(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * fexp((v + 5.0) * (1.0 / 6.0))));
+    const double efc = fexp((v - 4.0) * (1.0 / 7.0));
     const double r_fcaf = rcp(7.0 + rcp(0.04 * (rcp(efc) + efc)));
-    const double r_fcas = rcp(100.0 + rcp(0.00012 * exp(-v * (1.0 / 3.0)) + 0.00012 * exp(v * (1.0 / 7.0))));
+    const double r_fcas = rcp(100.0 + rcp(0.00012 * fexp(-v * (1.0 / 3.0)) + 0.00012 * fexp(v * (1.0 / 7.0))));
     const double a_fcaf = 0.3 + 0.6 * sigm((v - 10.0) * (1.0 / 10.0));
     const double a_fcas = 1.0 - a_fcaf;
     const double fmix = 0.6 * s[FF] + (1.0 - 0.6) * s[FS];
@@ -247,25 +250,25 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double i_k;  // IKr + IKs + IK1
   {
     const double xr_inf = sigm(-(v + 8.337) * (1.0 / 6.789));
-    const double r_xrf = rcp(12.98 + rcp(0.3652 * exp((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * exp(-(v - 47.78) * (1.0 / 20.38))));
-    const double r_xrs = rcp(1.865 + rcp(0.06629 * exp((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * exp(-(v - 29.74) * (1.0 / 25.94))));
+    const double r_xrf = rcp(12.98 + rcp(0.3652 * fexp((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * fexp(-(v - 47.78) * (1.0 / 20.38))));
+    const double r_xrs = rcp(1.865 + rcp(0.06629 * fexp((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * fexp(-(v - 29.74) * (1.0 / 25.94))));
     const double a_xrf = sigm((v + 54.81) * (1.0 / 38.21));
     const double xrmix = a_xrf * s[XRF] + (1.0 - a_xrf) * s[XRS];
-    const double rkr = rcp((1.0 + exp((v + 55.0) * (1.0 / 75.0))) * (1.0 + exp((v - 10.0) * (1.0 / 30.0))));
+    const double rkr = rcp((1.0 + fexp((v + 55.0) * (1.0 / 75.0))) * (1.0 + fexp((v - 10.0) * (1.0 / 30.0))));
     const double i_kr = (P::gkr * gkr_scale) * xrmix * rkr * (v - ek);  // sqrt(ko/5.4) == 1
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
     const double xs_inf = sigm(-(v + 11.60) * (1.0 / 8.932));
-    const double r_xs1 = rcp(817.3 + rcp(2.326e-4 * exp((v + 48.28) * (1.0 / 17.80)) + 0.001292 * exp(-(v + 210.0) * (1.0 / 230.0))));
-    const double r_xs2 = 0.01 * exp((v - 50.0) * (1.0 / 20.0)) + 0.0193 * exp(-(v + 66.54) * (1.0 / 31.0));
-    const double ksca = 1.0 + 0.6 * rcp(1.0 + exp(1.4 * (-10.177924398237888 - log(cai)))  /* log(3.8e-5) */);
+    const double r_xs1 = rcp(817.3 + rcp(2.326e-4 * fexp((v + 48.28) * (1.0 / 17.80)) + 0.001292 * fexp(-(v + 210.0) * (1.0 / 230.0))));
+    const double r_xs2 = 0.01 * fexp((v - 50.0) * (1.0 / 20.0)) + 0.0193 * fexp(-(v + 66.54) * (1.0 / 31.0));
+    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - log(cai)))  /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
 
     const double xk1_inf = sigm(-(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)));
-    const double r_xk1 = (exp(-(v + 127.2) * (1.0 / 20.36)) + exp((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
+    const double r_xk1 = (fexp(-(v + 127.2) * (1.0 / 20.36)) + fexp((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
     const double rk1 = sigm((v + 105.8 - 2.6 * KO) * (1.0 / 9.493));
     const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
     gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
@@ -276,8 +279,8 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double inaca_i, inaca_ss;
   {
     NcxShared c;
-    c.hna = exp(0.5224 * vfrt);
-    c.hca_r = exp(-0.1670 * vfrt);  // 1/hca
+    c.hna = fexp(0.5224 * vfrt);
+    c.hca_r = fexp(-0.1670 * vfrt);  // 1/hca
     const double hna_r = rcp(c.hna);
     const double r7 = rcp(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
     c.h9 = r7;
@@ -295,8 +298,8 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
     constexpr double a4 = 639.0 * 9.8 / 1.698e-7 / (1.0 + 9.8 / 1.698e-7);
     constexpr double b3c = 79300.0 * 1.0e-7 / (1.0 + 9.8 / 1.698e-7);
     const double p_hp = 4.2 * rcp(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
-    const double ri = nai * (1.0 / 9.073) * exp((0.1550 / 3.0) * vfrt);     // nai / Knai
-    const double ro = NAO * (1.0 / 27.78) * exp(-(1.1550 / 3.0) * vfrt);   // nao / Knao
+    const double ri = nai * (1.0 / 9.073) * fexp((0.1550 / 3.0) * vfrt);     // nai / Knai
+    const double ro = NAO * (1.0 / 27.78) * fexp(-(1.1550 / 3.0) * vfrt);   // nao / Knao
     const double rk = ki * 2.0;                                            // ki / 0.5
     const double ci = (1.0 + ri) * (1.0 + ri) * (1.0 + ri), qi = (1.0 + rk) * (1.0 + rk);
     const double co = (1.0 + ro) * (1.0 + ro) * (1.0 + ro);
@@ -383,11 +386,11 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 
 }  // namespace ord
 
-template <int CT>
+template <int CT, int MINB = 2>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
   static constexpr int kThreads = 128;
-  static constexpr int kMinBlocks = 2;
+  static constexpr int kMinBlocks = MINB;  // 2: <= 255 regs; 3: <= 168 regs (more warps, possible spills)
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void advance(double& v, double* s, double ist, double g, double h, double& dv) {
     ord::step<CT, false>(v, s, nullptr, ist, g, h, dv);
@@ -421,11 +424,22 @@ static int occupancy_t() {
   return b;
 }
 
+// Occupancy variant: 2 or 3 resident 128-thread blocks per SM (register
+// budget 255 / 168). Selected once per process (CWG_ORD_MINB, default 2).
+static int ord_minb() {
+  static int v = [] {
+    const char* e = getenv("CWG_ORD_MINB");
+    return (e && atoi(e) == 3) ? 3 : 2;
+  }();
+  return v;
+}
+
 cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_t st) {
+  const bool m3 = ord_minb() == 3;
   switch (kind) {
-    case 1: return launch_react_t<ModelOrd<0>>(a, grid, st);
-    case 2: return launch_react_t<ModelOrd<1>>(a, grid, st);
-    case 3: return launch_react_t<ModelOrd<2>>(a, grid, st);
+    case 1: return m3 ? launch_react_t<ModelOrd<0, 3>>(a, grid, st) : launch_react_t<ModelOrd<0>>(a, grid, st);
+    case 2: return m3 ? launch_react_t<ModelOrd<1, 3>>(a, grid, st) : launch_react_t<ModelOrd<1>>(a, grid, st);
+    case 3: return m3 ? launch_react_t<ModelOrd<2, 3>>(a, grid, st) : launch_react_t<ModelOrd<2>>(a, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -433,10 +447,11 @@ cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_
 int react_ord_threads(int) { return 128; }
 
 int react_ord_occupancy(int kind) {
+  const bool m3 = ord_minb() == 3;
   switch (kind) {
-    case 1: return occupancy_t<ModelOrd<0>>();
-    case 2: return occupancy_t<ModelOrd<1>>();
-    case 3: return occupancy_t<ModelOrd<2>>();
+    case 1: return m3 ? occupancy_t<ModelOrd<0, 3>>() : occupancy_t<ModelOrd<0>>();
+    case 2: return m3 ? occupancy_t<ModelOrd<1, 3>>() : occupancy_t<ModelOrd<1>>();
+    case 3: return m3 ? occupancy_t<ModelOrd<2, 3>>() : occupancy_t<ModelOrd<2>>();
     default: return 0;
   }
 }
