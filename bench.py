@@ -254,7 +254,7 @@ def main():
                                  L.dp(diff_ms))
         torch.cuda.synchronize()
     if rc != 0:
-        raise SystemExit(f"cwg_bench_steps failed ({rc})")
+        raise SystemExit(f"cwg_bench_steps failed ({rc}): {lib.cwg_last_error().decode()}")
     if dist:
         dist.barrier()
     wall = time.perf_counter() - t_wall0

@@ -229,6 +229,8 @@ int cwg_k_max_for(double dt, int model_kind);
 int cwg_slab_plan(int64_t ny1, int world, int rank, int64_t* row_begin, int64_t* row_end);
 
 const char* cwg_version(void);
+/* Message of the last failed call on this host thread ("" if none). */
+const char* cwg_last_error(void);
 
 #ifdef __cplusplus
 }

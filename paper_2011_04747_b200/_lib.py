@@ -55,6 +55,7 @@ class cwg_info(C.Structure):
 
 _SIGS = {
     "cwg_version": (C.c_char_p, []),
+    "cwg_last_error": (C.c_char_p, []),
     "cwg_create": (C.c_int, [C.POINTER(cwg_problem), C.POINTER(C.c_void_p), C.POINTER(cwg_error)]),
     "cwg_destroy": (None, [C.c_void_p]),
     "cwg_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),

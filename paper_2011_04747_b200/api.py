@@ -72,7 +72,10 @@ def _raise(code, err: L.cwg_error):
 
 def _check(code, err=None):
     if code != L.CWG_OK:
-        _raise(code, err if err is not None else L.cwg_error(code=code))
+        if err is None:
+            err = L.cwg_error(code=code)
+            err.msg = L.lib().cwg_last_error()[:255]
+        _raise(code, err)
 
 
 # ----------------------------------------------------------------------------- scheme (splitting.hpp)

@@ -462,10 +462,20 @@ void build_graph(cwg_ctx* c, long long b0) {
 // end of the reaction pass, step end -- whose events are swapped per launch
 // (cudaGraphExecEventRecordNodeSetEvent) so every timed step has its own.
 struct StepGraph {
+  cudaGraph_t graph = nullptr;  // kept: node handles are only valid while their graph lives
+  cudaEvent_t tmp[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t exec = nullptr;
   cudaGraphNode_t ev_nodes[3] = {nullptr, nullptr, nullptr};
   long long launches = 0;
 };
+
+void free_step_graph(StepGraph& sg) {
+  if (sg.exec) cudaGraphExecDestroy(sg.exec);
+  if (sg.graph) cudaGraphDestroy(sg.graph);
+  for (auto& e : sg.tmp)
+    if (e) cudaEventDestroy(e);
+  sg = StepGraph{};
+}
 
 StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   const long long S = step + 1;
@@ -475,8 +485,8 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   cudaGraph_t g = nullptr;
   const int cur0 = c->cur;
   const long long l0 = c->launches;
-  cudaEvent_t tmp[3];
-  for (auto& e : tmp) CUDA_TRY(cudaEventCreate(&e));
+  cudaEvent_t* tmp = sg.tmp;
+  for (int q = 0; q < 3; ++q) CUDA_TRY(cudaEventCreate(&tmp[q]));
   CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
     CUDA_TRY(cudaEventRecordWithFlags(tmp[0], c->stream, cudaEventRecordExternal));
@@ -499,10 +509,10 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   } catch (...) {
     cudaStreamEndCapture(c->stream, &g);
     if (g) cudaGraphDestroy(g);
-    for (auto& e : tmp) cudaEventDestroy(e);
     throw;
   }
   CUDA_TRY(cudaStreamEndCapture(c->stream, &g));
+  sg.graph = g;
   sg.launches = c->launches - l0;
   c->launches = l0;
   // locate the event-record nodes in capture order (they form a chain with the kernels)
@@ -525,8 +535,6 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   }
   if (found != 3) throw Fail{CWG_ECUDA, "step graph: event nodes not found"};
   CUDA_TRY(cudaGraphInstantiate(&sg.exec, g, 0));
-  cudaGraphDestroy(g);
-  for (auto& e : tmp) cudaEventDestroy(e);
   if (c->cur != cur0) throw Fail{CWG_ECUDA, "step graph must preserve the V buffer parity"};
   return sg;
 }
@@ -841,8 +849,11 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 }
 
+thread_local std::string g_last_error;
+
 template <class F>
 int guarded(cwg_error* err, F&& f) {
+  g_last_error.clear();
   try {
     f();
     if (err) {
@@ -853,9 +864,11 @@ int guarded(cwg_error* err, F&& f) {
     }
     return CWG_OK;
   } catch (const Fail& e) {
+    g_last_error = e.msg;
     set_error(err, e.code, e.msg);
     return e.code;
   } catch (const std::exception& e) {
+    g_last_error = e.what();
     set_error(err, CWG_ECUDA, e.what());
     return CWG_ECUDA;
   }
@@ -936,6 +949,8 @@ void ensure_stage(cwg_ctx* c) {
 extern "C" {
 
 const char* cwg_version(void) { return "cwgpu 1 (sm_100a)"; }
+
+const char* cwg_last_error(void) { return g_last_error.c_str(); }
 
 int cwg_model_state_count(int kind) { return state_count(kind); }
 
@@ -1355,13 +1370,11 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
       }
     } catch (...) {
       for (auto& e : ev) cudaEventDestroy(e);
-      for (auto& sg : graphs)
-        if (sg.exec) cudaGraphExecDestroy(sg.exec);
+      for (auto& sg : graphs) free_step_graph(sg);
       throw;
     }
     for (auto& e : ev) cudaEventDestroy(e);
-    for (auto& sg : graphs)
-      if (sg.exec) cudaGraphExecDestroy(sg.exec);
+    for (auto& sg : graphs) free_step_graph(sg);
   });
 }
 

@@ -19,6 +19,12 @@
 
 namespace cwg {
 
+// kSync (M::kBlockSync): the warps of the (single, persistent) block on an SM
+// advance one rates() evaluation per loop trip in lockstep (one
+// __syncthreads_or per trip). The ORd body is ~40 KB of SASS, larger than the
+// 32 KB L1.5 instruction cache; warps that drift to different PCs thrash it
+// (ncu: ~35% of stall cycles were instruction fetch). In lockstep every
+// fetched line serves all warps.
 template <class M>
 __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
   const int lane = threadIdx.x & 31;
@@ -64,7 +70,11 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         }
       }
     }
-    if (!__any_sync(kFull, node >= 0)) break;
+    if (M::kBlockSync) {
+      if (!__syncthreads_or(node >= 0)) break;
+    } else if (!__any_sync(kFull, node >= 0)) {
+      break;
+    }
     if (node >= 0) {
       const double ts = __dadd_rn(t, __dmul_rn(static_cast<double>(j), h));  // t + j*dt_ar, never contracted
       const double ist = p1 > p0 ? stim_current(a.stim, p0, p1, ts) : 0.0;

@@ -12,6 +12,7 @@ struct ModelAP {
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
+  static constexpr bool kBlockSync = false;
   __device__ __forceinline__ static void rates(double v, const double* s, double ist, double& dv, double* ds) {
     const double u = (v - (-80.0)) / 100.0;
     const double w = s[0];
@@ -35,6 +36,7 @@ struct ModelMac {
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
+  static constexpr bool kBlockSync = false;
   __device__ __forceinline__ static void rates(double v, const double* s, double ist, double& dv, double* ds) {
     const double rtf = 8314.0 * 306.15 / 96485.0;
     const double e_k = rtf * log(5.4 / 129.4349);
@@ -74,6 +76,7 @@ struct ModelPassive {
   static constexpr int kThreads = 256;
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
+  static constexpr bool kBlockSync = false;
   __device__ __forceinline__ static void rates(double v, const double*, double ist, double& dv, double*) {
     dv = -0.01 * (v - (-85.0)) + ist;
   }

@@ -386,11 +386,15 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 
 }  // namespace ord
 
-template <int CT, int MINB = 2>
+// Launch shapes: V = 0: 128-thread blocks, 2 per SM (<= 255 regs), warps free-running;
+// V = 1: one persistent 384-thread block per SM (<= 168 regs, 12 warps), lockstep;
+// V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep.
+template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = 128;
-  static constexpr int kMinBlocks = MINB;  // 2: <= 255 regs; 3: <= 168 regs (more warps, possible spills)
+  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : 128);
+  static constexpr int kMinBlocks = V == 0 ? 2 : 1;
+  static constexpr bool kBlockSync = V != 0;
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void advance(double& v, double* s, double ist, double g, double h, double& dv) {
     ord::step<CT, false>(v, s, nullptr, ist, g, h, dv);
@@ -424,34 +428,56 @@ static int occupancy_t() {
   return b;
 }
 
-// Occupancy variant: 2 or 3 resident 128-thread blocks per SM (register
-// budget 255 / 168). Selected once per process (CWG_ORD_MINB, default 2).
-static int ord_minb() {
+// Launch-shape variant, once per process (CWG_ORD_VARIANT = 0 | 1 | 2, default 1).
+static int ord_variant() {
   static int v = [] {
-    const char* e = getenv("CWG_ORD_MINB");
-    return (e && atoi(e) == 3) ? 3 : 2;
+    const char* e = getenv("CWG_ORD_VARIANT");
+    const int x = e ? atoi(e) : 1;
+    return (x >= 0 && x <= 2) ? x : 1;
   }();
   return v;
 }
 
+template <int CT>
+static cudaError_t launch_ct(const ReactArgs& a, int grid, cudaStream_t st) {
+  switch (ord_variant()) {
+    case 0: return launch_react_t<ModelOrd<CT, 0>>(a, grid, st);
+    case 2: return launch_react_t<ModelOrd<CT, 2>>(a, grid, st);
+    default: return launch_react_t<ModelOrd<CT, 1>>(a, grid, st);
+  }
+}
+
 cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_t st) {
-  const bool m3 = ord_minb() == 3;
   switch (kind) {
-    case 1: return m3 ? launch_react_t<ModelOrd<0, 3>>(a, grid, st) : launch_react_t<ModelOrd<0>>(a, grid, st);
-    case 2: return m3 ? launch_react_t<ModelOrd<1, 3>>(a, grid, st) : launch_react_t<ModelOrd<1>>(a, grid, st);
-    case 3: return m3 ? launch_react_t<ModelOrd<2, 3>>(a, grid, st) : launch_react_t<ModelOrd<2>>(a, grid, st);
+    case 1: return launch_ct<0>(a, grid, st);
+    case 2: return launch_ct<1>(a, grid, st);
+    case 3: return launch_ct<2>(a, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-int react_ord_threads(int) { return 128; }
+int react_ord_threads(int) {
+  switch (ord_variant()) {
+    case 0: return ModelOrd<0, 0>::kThreads;
+    case 2: return ModelOrd<0, 2>::kThreads;
+    default: return ModelOrd<0, 1>::kThreads;
+  }
+}
+
+template <int CT>
+static int occ_ct() {
+  switch (ord_variant()) {
+    case 0: return occupancy_t<ModelOrd<CT, 0>>();
+    case 2: return occupancy_t<ModelOrd<CT, 2>>();
+    default: return occupancy_t<ModelOrd<CT, 1>>();
+  }
+}
 
 int react_ord_occupancy(int kind) {
-  const bool m3 = ord_minb() == 3;
   switch (kind) {
-    case 1: return m3 ? occupancy_t<ModelOrd<0, 3>>() : occupancy_t<ModelOrd<0>>();
-    case 2: return m3 ? occupancy_t<ModelOrd<1, 3>>() : occupancy_t<ModelOrd<1>>();
-    case 3: return m3 ? occupancy_t<ModelOrd<2, 3>>() : occupancy_t<ModelOrd<2>>();
+    case 1: return occ_ct<0>();
+    case 2: return occ_ct<1>();
+    case 3: return occ_ct<2>();
     default: return 0;
   }
 }
