@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -172,6 +173,7 @@ void dev_free(T*& p) {
 // ====================================================================== ctx
 struct Bin {
   int model = 0, kind = 0;
+  int variant = 0;  // ORd launch shape (react_ord.cu ModelOrd)
   int32_t* d_list = nullptr;  // nullptr: dense [first, first+count)
   long long first = 0, count = 0;
   int grid = 1;
@@ -395,7 +397,7 @@ void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double
     a.counter = b.d_counter;
     a.done = b.d_counter + 1;
     a.node_offset = c->node_offset;
-    cudaError_t e = is_ord(b.kind) ? launch_react_ord(b.kind, a, b.grid, c->stream)
+    cudaError_t e = is_ord(b.kind) ? launch_react_ord(b.kind, b.variant, a, b.grid, c->stream)
                                    : launch_react_exact(b.kind, a, b.grid, c->stream);
     CUDA_TRY(e);
     ++c->launches;
@@ -576,6 +578,19 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
       throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " misses grid neighbours"};
   }
   c->d_coef = upload(coef.data(), coef.size());
+}
+
+// ORd launch shape. Latency regime (the bin fits in about one wave of
+// 256-thread blocks, e.g. C2's 40k nodes): 256 threads x 252 registers --
+// fewer, wider warps shorten the per-evaluation latency that bounds the
+// k = 10 wavefront nodes. Throughput regime: 384 threads x 168 registers
+// (12 warps per SM). Both run one persistent lockstep block per SM.
+int choose_ord_variant(long long count, int num_sms) {
+  if (const char* e = getenv("CWG_ORD_VARIANT")) {
+    const int v = atoi(e);
+    if (v >= 0 && v <= 3) return v;
+  }
+  return count <= static_cast<long long>(num_sms) * 256 * 5 / 4 ? 2 : 1;
 }
 
 bool stencil_ok(const cwg_problem* p) {
@@ -761,8 +776,10 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     } else if (b.count > 0) {
       b.d_list = upload(lists[m].data(), lists[m].size());
     }
-    const int threads = is_ord(b.kind) ? react_ord_threads(b.kind) : react_exact_threads(b.kind);
-    const int occ = std::max(1, is_ord(b.kind) ? react_ord_occupancy(b.kind) : react_exact_occupancy(b.kind));
+    b.variant = choose_ord_variant(b.count, c->num_sms);
+    const int threads = is_ord(b.kind) ? react_ord_threads(b.variant) : react_exact_threads(b.kind);
+    const int occ =
+        std::max(1, is_ord(b.kind) ? react_ord_occupancy(b.kind, b.variant) : react_exact_occupancy(b.kind));
     const long long need = (b.count + threads - 1) / threads;
     b.grid = static_cast<int>(std::max<long long>(1, std::min<long long>(need, static_cast<long long>(occ) * c->num_sms)));
     b.d_counter = dev_alloc<unsigned>(2);

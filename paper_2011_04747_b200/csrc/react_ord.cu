@@ -39,7 +39,19 @@ constexpr double ACAP = 2.0 * AGEO;
 constexpr double VMYO = 0.68 * VCELL, VNSR = 0.0552 * VCELL, VJSR = 0.0048 * VCELL, VSS = 0.02 * VCELL;
 
 __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
-__device__ __forceinline__ double sigm(double u) { return __drcp_rn(1.0 + fexp(u)); }  // 1/(1+e^u)
+
+// FP = true ("fast" evaluation, taken when |V| <= 130 mV): every exponent
+// argument that depends on V alone is then provably < 708 in magnitude and
+// every V-dependent denominator is a normal positive number, so those calls
+// use the branch-free fexp_nc / rcp_nc. Concentration-dependent reciprocals
+// and exponentials always use the checked forms (they can reach 0 / Inf /
+// NaN while a node blows up, where IEEE semantics decide the abort step).
+template <bool FP>
+__device__ __forceinline__ double vexp(double x) { return FP ? fexp_nc(x) : fexp(x); }
+template <bool FP>
+__device__ __forceinline__ double vrcp(double x) { return FP ? rcp_nc(x) : __drcp_rn(x); }
+template <bool FP>
+__device__ __forceinline__ double sigm(double u) { return vrcp<FP>(1.0 + vexp<FP>(u)); }  // 1/(1+e^u)
 
 template <int CT>  // 0 endo, 1 epi, 2 mid (ohara_rudy_2011.cpp:86-87 celltype_)
 struct Var {
@@ -59,8 +71,9 @@ struct Var {
 };
 
 // x / expm1(x) given em = expm1(x) (ohara_rudy_2011.cpp:67-70)
+template <bool FP>
 __device__ __forceinline__ double xem1(double x, double em) {
-  return fabs(x) < 1e-8 ? rcp(1.0 + 0.5 * x) : x * rcp(em);
+  return fabs(x) < 1e-8 ? vrcp<FP>(1.0 + 0.5 * x) : x * vrcp<FP>(em);
 }
 
 struct NcxShared {
@@ -115,7 +128,7 @@ __device__ __forceinline__ void gate(double* s, double* ds, int i, double h, dou
   put<R>(s, ds, i, h, (xinf - s[i]) * rate);
 }
 
-template <int CT, bool R>
+template <int CT, bool R, bool FP>
 __device__ __forceinline__ void step(double& v, double* s, double* ds, double ist, double gkr_scale, double h,
                                      double& dv) {
   using P = Var<CT>;
@@ -135,14 +148,14 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   // ---------------- INa
   double i_na;
   {
-    const double m_inf = sigm(-(v + 39.57) * (1.0 / 9.871));
-    const double r_m = 6.765 * fexp((v + 11.64) * (1.0 / 34.77)) + 8.552 * fexp(-(v + 77.42) * (1.0 / 5.955));
-    const double h_inf = sigm((v + 82.90) * (1.0 / 6.086));
-    const double r_hf = 1.432e-5 * fexp(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * fexp((v + 0.5096) * (1.0 / 20.27));
-    const double r_hs = 0.009794 * fexp(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * fexp((v + 5.730) * (1.0 / 56.66));
-    const double r_j = rcp(2.038 + rcp(0.02136 * fexp(-(v + 100.6) * (1.0 / 8.281)) +
-                                       0.3052 * fexp((v + 0.9941) * (1.0 / 38.45))));
-    const double hp_inf = sigm((v + 89.1) * (1.0 / 6.086));
+    const double m_inf = sigm<FP>(-(v + 39.57) * (1.0 / 9.871));
+    const double r_m = 6.765 * vexp<FP>((v + 11.64) * (1.0 / 34.77)) + 8.552 * vexp<FP>(-(v + 77.42) * (1.0 / 5.955));
+    const double h_inf = sigm<FP>((v + 82.90) * (1.0 / 6.086));
+    const double r_hf = 1.432e-5 * vexp<FP>(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * vexp<FP>((v + 0.5096) * (1.0 / 20.27));
+    const double r_hs = 0.009794 * vexp<FP>(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * vexp<FP>((v + 5.730) * (1.0 / 56.66));
+    const double r_j = vrcp<FP>(2.038 + vrcp<FP>(0.02136 * vexp<FP>(-(v + 100.6) * (1.0 / 8.281)) +
+                                       0.3052 * vexp<FP>((v + 0.9941) * (1.0 / 38.45))));
+    const double hp_inf = sigm<FP>((v + 89.1) * (1.0 / 6.086));
     const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
     const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
     const double m = s[M];
@@ -154,9 +167,9 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
     gate<R>(s, ds, HSP, h, hp_inf, r_hs * (1.0 / 3.0));
     gate<R>(s, ds, JP, h, h_inf, r_j * (1.0 / 1.46));
     // ---------------- INaL (tmL = tm)
-    const double ml_inf = sigm(-(v + 42.85) * (1.0 / 5.264));
-    const double hl_inf = sigm((v + 87.61) * (1.0 / 7.488));
-    const double hlp_inf = sigm((v + 93.81) * (1.0 / 7.488));
+    const double ml_inf = sigm<FP>(-(v + 42.85) * (1.0 / 5.264));
+    const double hl_inf = sigm<FP>((v + 87.61) * (1.0 / 7.488));
+    const double hlp_inf = sigm<FP>((v + 93.81) * (1.0 / 7.488));
     const double i_nal = P::gnal * (v - ena) * s[ML] * (nfk * s[HL] + fk * s[HLP]);
     i_na += i_nal;  // INa + INaL travel together into dv and d[nai]
     gate<R>(s, ds, ML, h, ml_inf, r_m);
@@ -167,24 +180,24 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   // ---------------- Ito
   double i_to;
   {
-    const double a_inf = sigm(-(v - 14.34) * (1.0 / 14.82));
-    const double r_a = (1.0 / 1.0515) * (rcp(1.2089 * (1.0 + fexp(-(v - 18.4099) * (1.0 / 29.3814)))) +
-                                         3.5 * sigm((v + 100.0) * (1.0 / 29.3814)));
-    const double i_inf = sigm((v + 43.94) * (1.0 / 5.711));
-    double t_if = 4.562 + rcp(0.3933 * fexp(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * fexp((v + 50.0) * (1.0 / 16.59)));
-    double t_is = 23.62 + rcp(0.001416 * fexp(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * fexp((v + 114.1) * (1.0 / 8.079)));
+    const double a_inf = sigm<FP>(-(v - 14.34) * (1.0 / 14.82));
+    const double r_a = (1.0 / 1.0515) * (vrcp<FP>(1.2089 * (1.0 + vexp<FP>(-(v - 18.4099) * (1.0 / 29.3814)))) +
+                                         3.5 * sigm<FP>((v + 100.0) * (1.0 / 29.3814)));
+    const double i_inf = sigm<FP>((v + 43.94) * (1.0 / 5.711));
+    double t_if = 4.562 + vrcp<FP>(0.3933 * vexp<FP>(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * vexp<FP>((v + 50.0) * (1.0 / 16.59)));
+    double t_is = 23.62 + vrcp<FP>(0.001416 * vexp<FP>(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * vexp<FP>((v + 114.1) * (1.0 / 8.079)));
     if (P::epi) {
-      const double d_epi = 1.0 - 0.95 * sigm((v + 70.0) * (1.0 / 5.0));
+      const double d_epi = 1.0 - 0.95 * sigm<FP>((v + 70.0) * (1.0 / 5.0));
       t_if *= d_epi;
       t_is *= d_epi;
     }
-    const double r_if = rcp(t_if), r_is = rcp(t_is);
-    const double a_if = sigm((v - 213.6) * (1.0 / 151.2));
+    const double r_if = vrcp<FP>(t_if), r_is = vrcp<FP>(t_is);
+    const double a_if = sigm<FP>((v - 213.6) * (1.0 / 151.2));
     const double a_is = 1.0 - a_if;
-    const double ap_inf = sigm(-(v - 24.34) * (1.0 / 14.82));
-    const double dev = 1.354 + 1.0e-4 * rcp(fexp((v - 167.4) * (1.0 / 15.89)) + fexp(-(v - 12.23) * (1.0 / 0.2154)));
-    const double rec = 1.0 - 0.5 * sigm((v + 70.0) * (1.0 / 20.0));
-    const double r_dr = rcp(dev * rec);
+    const double ap_inf = sigm<FP>(-(v - 24.34) * (1.0 / 14.82));
+    const double dev = 1.354 + 1.0e-4 * vrcp<FP>(vexp<FP>((v - 167.4) * (1.0 / 15.89)) + vexp<FP>(-(v - 12.23) * (1.0 / 0.2154)));
+    const double rec = 1.0 - 0.5 * sigm<FP>((v + 70.0) * (1.0 / 20.0));
+    const double r_dr = vrcp<FP>(dev * rec);
     const double imix = a_if * s[IF] + a_is * s[IS];
     const double ipmix = a_if * s[IFP] + a_is * s[ISP];
     i_to = P::gto * (v - ek) * (nfk * s[A] * imix + fk * s[AP] * ipmix);
@@ -201,22 +214,22 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   const double e1 = em1 + 1.0;
   const double e2 = e1 * e1;
   const double em2 = em1 * (em1 + 2.0);
-  const double xq1 = xem1(vfrt, em1);
-  const double xq2 = xem1(2.0 * vfrt, em2);
+  const double xq1 = xem1<FP>(vfrt, em1);
+  const double xq2 = xem1<FP>(2.0 * vfrt, em2);
 
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
-    const double d_inf = sigm(-(v + 3.940) * (1.0 / 4.230));
-    const double r_d = rcp(0.6 + rcp(fexp(-0.05 * (v + 6.0)) + fexp(0.09 * (v + 14.0))));
-    const double f_inf = sigm((v + 19.58) * (1.0 / 3.696));
-    const double eff = fexp((v + 20.0) * (1.0 / 10.0));
-    const double r_ff = rcp(7.0 + rcp(0.0045 * (rcp(eff) + eff)));
-    const double r_fs = rcp(1000.0 + rcp(0.000035 * fexp(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * fexp((v + 5.0) * (1.0 / 6.0))));
-    const double efc = fexp((v - 4.0) * (1.0 / 7.0));
-    const double r_fcaf = rcp(7.0 + rcp(0.04 * (rcp(efc) + efc)));
-    const double r_fcas = rcp(100.0 + rcp(0.00012 * fexp(-v * (1.0 / 3.0)) + 0.00012 * fexp(v * (1.0 / 7.0))));
-    const double a_fcaf = 0.3 + 0.6 * sigm((v - 10.0) * (1.0 / 10.0));
+    const double d_inf = sigm<FP>(-(v + 3.940) * (1.0 / 4.230));
+    const double r_d = vrcp<FP>(0.6 + vrcp<FP>(vexp<FP>(-0.05 * (v + 6.0)) + vexp<FP>(0.09 * (v + 14.0))));
+    const double f_inf = sigm<FP>((v + 19.58) * (1.0 / 3.696));
+    const double eff = vexp<FP>((v + 20.0) * (1.0 / 10.0));
+    const double r_ff = vrcp<FP>(7.0 + vrcp<FP>(0.0045 * (vrcp<FP>(eff) + eff)));
+    const double r_fs = vrcp<FP>(1000.0 + vrcp<FP>(0.000035 * vexp<FP>(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * vexp<FP>((v + 5.0) * (1.0 / 6.0))));
+    const double efc = vexp<FP>((v - 4.0) * (1.0 / 7.0));
+    const double r_fcaf = vrcp<FP>(7.0 + vrcp<FP>(0.04 * (vrcp<FP>(efc) + efc)));
+    const double r_fcas = vrcp<FP>(100.0 + vrcp<FP>(0.00012 * vexp<FP>(-v * (1.0 / 3.0)) + 0.00012 * vexp<FP>(v * (1.0 / 7.0))));
+    const double a_fcaf = 0.3 + 0.6 * sigm<FP>((v - 10.0) * (1.0 / 10.0));
     const double a_fcas = 1.0 - a_fcaf;
     const double fmix = 0.6 * s[FF] + (1.0 - 0.6) * s[FS];
     const double fcamix = a_fcaf * s[FCAF] + a_fcas * s[FCAS];
@@ -249,27 +262,27 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   // ---------------- IKr, IKs, IK1
   double i_k;  // IKr + IKs + IK1
   {
-    const double xr_inf = sigm(-(v + 8.337) * (1.0 / 6.789));
-    const double r_xrf = rcp(12.98 + rcp(0.3652 * fexp((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * fexp(-(v - 47.78) * (1.0 / 20.38))));
-    const double r_xrs = rcp(1.865 + rcp(0.06629 * fexp((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * fexp(-(v - 29.74) * (1.0 / 25.94))));
-    const double a_xrf = sigm((v + 54.81) * (1.0 / 38.21));
+    const double xr_inf = sigm<FP>(-(v + 8.337) * (1.0 / 6.789));
+    const double r_xrf = vrcp<FP>(12.98 + vrcp<FP>(0.3652 * vexp<FP>((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * vexp<FP>(-(v - 47.78) * (1.0 / 20.38))));
+    const double r_xrs = vrcp<FP>(1.865 + vrcp<FP>(0.06629 * vexp<FP>((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * vexp<FP>(-(v - 29.74) * (1.0 / 25.94))));
+    const double a_xrf = sigm<FP>((v + 54.81) * (1.0 / 38.21));
     const double xrmix = a_xrf * s[XRF] + (1.0 - a_xrf) * s[XRS];
-    const double rkr = rcp((1.0 + fexp((v + 55.0) * (1.0 / 75.0))) * (1.0 + fexp((v - 10.0) * (1.0 / 30.0))));
+    const double rkr = vrcp<FP>((1.0 + vexp<FP>((v + 55.0) * (1.0 / 75.0))) * (1.0 + vexp<FP>((v - 10.0) * (1.0 / 30.0))));
     const double i_kr = (P::gkr * gkr_scale) * xrmix * rkr * (v - ek);  // sqrt(ko/5.4) == 1
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
-    const double xs_inf = sigm(-(v + 11.60) * (1.0 / 8.932));
-    const double r_xs1 = rcp(817.3 + rcp(2.326e-4 * fexp((v + 48.28) * (1.0 / 17.80)) + 0.001292 * fexp(-(v + 210.0) * (1.0 / 230.0))));
-    const double r_xs2 = 0.01 * fexp((v - 50.0) * (1.0 / 20.0)) + 0.0193 * fexp(-(v + 66.54) * (1.0 / 31.0));
+    const double xs_inf = sigm<FP>(-(v + 11.60) * (1.0 / 8.932));
+    const double r_xs1 = vrcp<FP>(817.3 + vrcp<FP>(2.326e-4 * vexp<FP>((v + 48.28) * (1.0 / 17.80)) + 0.001292 * vexp<FP>(-(v + 210.0) * (1.0 / 230.0))));
+    const double r_xs2 = 0.01 * vexp<FP>((v - 50.0) * (1.0 / 20.0)) + 0.0193 * vexp<FP>(-(v + 66.54) * (1.0 / 31.0));
     const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - log(cai)))  /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
 
-    const double xk1_inf = sigm(-(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)));
-    const double r_xk1 = (fexp(-(v + 127.2) * (1.0 / 20.36)) + fexp((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
-    const double rk1 = sigm((v + 105.8 - 2.6 * KO) * (1.0 / 9.493));
+    const double xk1_inf = sigm<FP>(-(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)));
+    const double r_xk1 = (vexp<FP>(-(v + 127.2) * (1.0 / 20.36)) + vexp<FP>((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
+    const double rk1 = sigm<FP>((v + 105.8 - 2.6 * KO) * (1.0 / 9.493));
     const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
     gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
     i_k = i_kr + i_ks + i_k1;
@@ -279,10 +292,10 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   double inaca_i, inaca_ss;
   {
     NcxShared c;
-    c.hna = fexp(0.5224 * vfrt);
-    c.hca_r = fexp(-0.1670 * vfrt);  // 1/hca
-    const double hna_r = rcp(c.hna);
-    const double r7 = rcp(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
+    c.hna = vexp<FP>(0.5224 * vfrt);
+    c.hca_r = vexp<FP>(-0.1670 * vfrt);  // 1/hca
+    const double hna_r = vrcp<FP>(c.hna);
+    const double r7 = vrcp<FP>(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
     c.h9 = r7;
     c.h8 = NAO * (1.0 / 88.12) * hna_r * r7;
     inaca_i = (0.8 * P::gncx) * ncx(nai, cai, c);
@@ -298,8 +311,8 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
     constexpr double a4 = 639.0 * 9.8 / 1.698e-7 / (1.0 + 9.8 / 1.698e-7);
     constexpr double b3c = 79300.0 * 1.0e-7 / (1.0 + 9.8 / 1.698e-7);
     const double p_hp = 4.2 * rcp(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
-    const double ri = nai * (1.0 / 9.073) * fexp((0.1550 / 3.0) * vfrt);     // nai / Knai
-    const double ro = NAO * (1.0 / 27.78) * fexp(-(1.1550 / 3.0) * vfrt);   // nao / Knao
+    const double ri = nai * (1.0 / 9.073) * vexp<FP>((0.1550 / 3.0) * vfrt);     // nai / Knai
+    const double ro = NAO * (1.0 / 27.78) * vexp<FP>(-(1.1550 / 3.0) * vfrt);   // nao / Knao
     const double rk = ki * 2.0;                                            // ki / 0.5
     const double ci = (1.0 + ri) * (1.0 + ri) * (1.0 + ri), qi = (1.0 + rk) * (1.0 + rk);
     const double co = (1.0 + ro) * (1.0 + ro) * (1.0 + ro);
@@ -318,7 +331,7 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   }
 
   // ---------------- background currents
-  const double i_kb = P::gkb * sigm(-(v - 14.48) * (1.0 / 18.34)) * (v - ek);
+  const double i_kb = P::gkb * sigm<FP>(-(v - 14.48) * (1.0 / 18.34)) * (v - ek);
   const double i_nab = (3.75e-10 * F) * (nai * e1 - NAO) * xq1;
   const double i_cab = (2.5e-8 * 2.0 * F) * (cai * e2 - 0.341 * CAO) * xq2;
   const double i_pca = 0.0005 * cai * rcp(0.0005 + cai);
@@ -381,23 +394,27 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
   double tmp[NSTATE];
 #pragma unroll
   for (int q = 0; q < NSTATE; ++q) tmp[q] = s[q];
-  step<CT, true>(v, tmp, ds, ist, 1.0, 0.0, dv);
+  step<CT, true, false>(v, tmp, ds, ist, 1.0, 0.0, dv);
 }
 
 }  // namespace ord
 
 // Launch shapes: V = 0: 128-thread blocks, 2 per SM (<= 255 regs), warps free-running;
 // V = 1: one persistent 384-thread block per SM (<= 168 regs, 12 warps), lockstep;
-// V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep.
+// V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep;
+// V = 3: one persistent 512-thread block per SM (<= 128 regs, 16 warps), lockstep.
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : 128);
+  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 3 ? 512 : 128));
   static constexpr int kMinBlocks = V == 0 ? 2 : 1;
   static constexpr bool kBlockSync = V != 0;
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void advance(double& v, double* s, double ist, double g, double h, double& dv) {
-    ord::step<CT, false>(v, s, nullptr, ist, g, h, dv);
+    if (fabs(v) <= 130.0)
+      ord::step<CT, false, true>(v, s, nullptr, ist, g, h, dv);
+    else
+      ord::step<CT, false, false>(v, s, nullptr, ist, g, h, dv);
   }
 };
 
@@ -428,56 +445,51 @@ static int occupancy_t() {
   return b;
 }
 
-// Launch-shape variant, once per process (CWG_ORD_VARIANT = 0 | 1 | 2, default 1).
-static int ord_variant() {
-  static int v = [] {
-    const char* e = getenv("CWG_ORD_VARIANT");
-    const int x = e ? atoi(e) : 1;
-    return (x >= 0 && x <= 2) ? x : 1;
-  }();
-  return v;
-}
-
+// Launch-shape variants (see ModelOrd). The host picks one per model bin
+// (cwg_host.cu: choose_ord_variant); CWG_ORD_VARIANT overrides for experiments.
 template <int CT>
-static cudaError_t launch_ct(const ReactArgs& a, int grid, cudaStream_t st) {
-  switch (ord_variant()) {
+static cudaError_t launch_ct(int variant, const ReactArgs& a, int grid, cudaStream_t st) {
+  switch (variant) {
     case 0: return launch_react_t<ModelOrd<CT, 0>>(a, grid, st);
     case 2: return launch_react_t<ModelOrd<CT, 2>>(a, grid, st);
+    case 3: return launch_react_t<ModelOrd<CT, 3>>(a, grid, st);
     default: return launch_react_t<ModelOrd<CT, 1>>(a, grid, st);
   }
 }
 
-cudaError_t launch_react_ord(int kind, const ReactArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_react_ord(int kind, int variant, const ReactArgs& a, int grid, cudaStream_t st) {
   switch (kind) {
-    case 1: return launch_ct<0>(a, grid, st);
-    case 2: return launch_ct<1>(a, grid, st);
-    case 3: return launch_ct<2>(a, grid, st);
+    case 1: return launch_ct<0>(variant, a, grid, st);
+    case 2: return launch_ct<1>(variant, a, grid, st);
+    case 3: return launch_ct<2>(variant, a, grid, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-int react_ord_threads(int) {
-  switch (ord_variant()) {
+int react_ord_threads(int variant) {
+  switch (variant) {
     case 0: return ModelOrd<0, 0>::kThreads;
     case 2: return ModelOrd<0, 2>::kThreads;
+    case 3: return ModelOrd<0, 3>::kThreads;
     default: return ModelOrd<0, 1>::kThreads;
   }
 }
 
 template <int CT>
-static int occ_ct() {
-  switch (ord_variant()) {
+static int occ_ct(int variant) {
+  switch (variant) {
     case 0: return occupancy_t<ModelOrd<CT, 0>>();
     case 2: return occupancy_t<ModelOrd<CT, 2>>();
+    case 3: return occupancy_t<ModelOrd<CT, 3>>();
     default: return occupancy_t<ModelOrd<CT, 1>>();
   }
 }
 
-int react_ord_occupancy(int kind) {
+int react_ord_occupancy(int kind, int variant) {
   switch (kind) {
-    case 1: return occ_ct<0>();
-    case 2: return occ_ct<1>();
-    case 3: return occ_ct<2>();
+    case 1: return occ_ct<0>(variant);
+    case 2: return occ_ct<1>(variant);
+    case 3: return occ_ct<2>(variant);
     default: return 0;
   }
 }
