@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcwgpu.so")
+LIB_PATH = os.environ.get("CWG_LIB_PATH") or os.path.join(HERE, "libcwgpu.so")  # override: experiments only
 
 CWG_OK, CWG_EVALIDATION, CWG_EINSTABILITY, CWG_EIO, CWG_ECUDA = 0, 2, 3, 4, 5
 OP_AUTO, OP_CSR, OP_STENCIL2D, OP_STRUCT3D = 0, 1, 2, 3

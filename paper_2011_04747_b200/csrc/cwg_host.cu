@@ -588,7 +588,7 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
 int choose_ord_variant(long long count, int num_sms) {
   if (const char* e = getenv("CWG_ORD_VARIANT")) {
     const int v = atoi(e);
-    if (v >= 0 && v <= 3) return v;
+    if (v >= 0 && v <= 5) return v;
   }
   return count <= static_cast<long long>(num_sms) * 256 * 5 / 4 ? 2 : 1;
 }

@@ -25,6 +25,36 @@ namespace cwg {
 // 32 KB L1.5 instruction cache; warps that drift to different PCs thrash it
 // (ncu: ~35% of stall cycles were instruction fetch). In lockstep every
 // fetched line serves all warps.
+// Per-thread state column in shared memory (M::kSmemStates): s[q] is
+// sst[q * kThreads + tid]. Frees the ~80 registers the 40 ORd states would
+// pin, so more exponentials can be in flight (the kernel is FP64-latency
+// bound). The stride is a compile-time constant, so the compiler knows the
+// columns never alias.
+template <int STRIDE>
+struct SmemCol {
+  double* p;
+  __device__ __forceinline__ double& operator[](int q) const { return p[q * STRIDE]; }
+};
+
+template <class M, bool SM = M::kSmemStates>
+struct StateStore;
+
+template <class M>
+struct StateStore<M, false> {
+  double s[M::NS > 0 ? M::NS : 1];
+  __device__ __forceinline__ StateStore(unsigned*, int) {}
+  __device__ __forceinline__ double* acc() { return s; }
+};
+
+template <class M>
+struct StateStore<M, true> {
+  SmemCol<M::kThreads> col;
+  __device__ __forceinline__ StateStore(unsigned* smem_after_hist, int) {
+    col.p = reinterpret_cast<double*>(smem_after_hist) + threadIdx.x;
+  }
+  __device__ __forceinline__ SmemCol<M::kThreads> acc() { return col; }
+};
+
 template <class M>
 __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
   const int lane = threadIdx.x & 31;
@@ -37,7 +67,8 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   bool open = true;  // may still receive work
   int k = 0, j = 0, p0 = 0, p1 = 0;
   double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
-  double s[M::NS > 0 ? M::NS : 1];
+  StateStore<M> store(shist + ((a.khist_len + 1) & ~1), 0);
+  auto s = store.acc();
 
   while (true) {
     const bool need = node < 0 && open;
@@ -100,7 +131,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
 
 template <class M>
 __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(ReactArgs a) {
-  extern __shared__ unsigned shist[];
+  extern __shared__ __align__(16) unsigned shist[];
   {
     const long long seq = (*a.clock + a.step_off) * a.evs + a.ev;
     if (earlier_failure(a.err, seq)) return;  // uniform across the grid

@@ -52,6 +52,24 @@ template <bool FP>
 __device__ __forceinline__ double vrcp(double x) { return FP ? rcp_nc(x) : __drcp_rn(x); }
 template <bool FP>
 __device__ __forceinline__ double sigm(double u) { return vrcp<FP>(1.0 + vexp<FP>(u)); }  // 1/(1+e^u)
+template <bool FP, int N>
+__device__ __forceinline__ void vexp_n(double (&x)[N]) {
+  if (FP) {
+    fexp_nc_n(x);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = fexp(x[i]);
+  }
+}
+template <bool FP, int N>
+__device__ __forceinline__ void vrcp_n(double (&x)[N]) {
+  if (FP) {
+    rcp_nc_n(x);
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = __drcp_rn(x[i]);
+  }
+}
 
 template <int CT>  // 0 endo, 1 epi, 2 mid (ohara_rudy_2011.cpp:86-87 celltype_)
 struct Var {
@@ -115,21 +133,21 @@ enum {
   D, FF, FS, FCAF, FCAS, JCA, NCA, FFP, FCAFP, XRF, XRS, XS1, XS2, XK1, JRELNP, JRELP, CAMKT, NSTATE
 };
 
-// gate FE update: x += h * (x_inf - x) * rate
+// gate FE update: x += h * (x_inf - x) * rate (SA: register array or shared-memory column)
 // Output policy: R = false integrates in place (x += h*dx, never contracted);
 // R = true only reports dx (CellModel::rates semantics, for cwg_rates).
-template <bool R>
-__device__ __forceinline__ void put(double* s, double* ds, int i, double h, double d) {
+template <bool R, class SA>
+__device__ __forceinline__ void put(SA s, double* ds, int i, double h, double d) {
   if (R) ds[i] = d;
   else s[i] = fe(s[i], h, d);
 }
-template <bool R>
-__device__ __forceinline__ void gate(double* s, double* ds, int i, double h, double xinf, double rate) {
+template <bool R, class SA>
+__device__ __forceinline__ void gate(SA s, double* ds, int i, double h, double xinf, double rate) {
   put<R>(s, ds, i, h, (xinf - s[i]) * rate);
 }
 
-template <int CT, bool R, bool FP>
-__device__ __forceinline__ void step(double& v, double* s, double* ds, double ist, double gkr_scale, double h,
+template <int CT, bool R, bool FP, class SA>
+__device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, double gkr_scale, double h,
                                      double& dv) {
   using P = Var<CT>;
   const double nai = s[NAI], nass = s[NASS], ki = s[KI], kss = s[KSS];
@@ -145,17 +163,23 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   const double nfk = 1.0 - fk;
   const double vfrt = v * FRT;
 
-  // ---------------- INa
+  // ---------------- INa + INaL: the 14 V-dependent exponentials in one batch
   double i_na;
   {
-    const double m_inf = sigm<FP>(-(v + 39.57) * (1.0 / 9.871));
-    const double r_m = 6.765 * vexp<FP>((v + 11.64) * (1.0 / 34.77)) + 8.552 * vexp<FP>(-(v + 77.42) * (1.0 / 5.955));
-    const double h_inf = sigm<FP>((v + 82.90) * (1.0 / 6.086));
-    const double r_hf = 1.432e-5 * vexp<FP>(-(v + 1.196) * (1.0 / 6.285)) + 6.149 * vexp<FP>((v + 0.5096) * (1.0 / 20.27));
-    const double r_hs = 0.009794 * vexp<FP>(-(v + 17.95) * (1.0 / 28.05)) + 0.3343 * vexp<FP>((v + 5.730) * (1.0 / 56.66));
-    const double r_j = vrcp<FP>(2.038 + vrcp<FP>(0.02136 * vexp<FP>(-(v + 100.6) * (1.0 / 8.281)) +
-                                       0.3052 * vexp<FP>((v + 0.9941) * (1.0 / 38.45))));
-    const double hp_inf = sigm<FP>((v + 89.1) * (1.0 / 6.086));
+    double e[14] = {-(v + 39.57) * (1.0 / 9.871),   (v + 11.64) * (1.0 / 34.77),  -(v + 77.42) * (1.0 / 5.955),
+                    (v + 82.90) * (1.0 / 6.086),    -(v + 1.196) * (1.0 / 6.285), (v + 0.5096) * (1.0 / 20.27),
+                    -(v + 17.95) * (1.0 / 28.05),   (v + 5.730) * (1.0 / 56.66),  -(v + 100.6) * (1.0 / 8.281),
+                    (v + 0.9941) * (1.0 / 38.45),   (v + 89.1) * (1.0 / 6.086),   -(v + 42.85) * (1.0 / 5.264),
+                    (v + 87.61) * (1.0 / 7.488),    (v + 93.81) * (1.0 / 7.488)};
+    vexp_n<FP>(e);
+    double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e[10], 1.0 + e[11], 1.0 + e[12], 1.0 + e[13],
+                   0.02136 * e[8] + 0.3052 * e[9]};
+    vrcp_n<FP>(q);
+    const double m_inf = q[0], h_inf = q[1], hp_inf = q[2];
+    const double r_m = 6.765 * e[1] + 8.552 * e[2];
+    const double r_hf = 1.432e-5 * e[4] + 6.149 * e[5];
+    const double r_hs = 0.009794 * e[6] + 0.3343 * e[7];
+    const double r_j = vrcp<FP>(2.038 + q[6]);
     const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
     const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
     const double m = s[M];
@@ -166,38 +190,45 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
     gate<R>(s, ds, J, h, h_inf, r_j);
     gate<R>(s, ds, HSP, h, hp_inf, r_hs * (1.0 / 3.0));
     gate<R>(s, ds, JP, h, h_inf, r_j * (1.0 / 1.46));
-    // ---------------- INaL (tmL = tm)
-    const double ml_inf = sigm<FP>(-(v + 42.85) * (1.0 / 5.264));
-    const double hl_inf = sigm<FP>((v + 87.61) * (1.0 / 7.488));
-    const double hlp_inf = sigm<FP>((v + 93.81) * (1.0 / 7.488));
+    // INaL (tmL = tm)
     const double i_nal = P::gnal * (v - ena) * s[ML] * (nfk * s[HL] + fk * s[HLP]);
     i_na += i_nal;  // INa + INaL travel together into dv and d[nai]
-    gate<R>(s, ds, ML, h, ml_inf, r_m);
-    gate<R>(s, ds, HL, h, hl_inf, 1.0 / 200.0);
-    gate<R>(s, ds, HLP, h, hlp_inf, 1.0 / 600.0);
+    gate<R>(s, ds, ML, h, q[3], r_m);
+    gate<R>(s, ds, HL, h, q[4], 1.0 / 200.0);
+    gate<R>(s, ds, HLP, h, q[5], 1.0 / 600.0);
   }
 
   // ---------------- Ito
   double i_to;
   {
-    const double a_inf = sigm<FP>(-(v - 14.34) * (1.0 / 14.82));
-    const double r_a = (1.0 / 1.0515) * (vrcp<FP>(1.2089 * (1.0 + vexp<FP>(-(v - 18.4099) * (1.0 / 29.3814)))) +
-                                         3.5 * sigm<FP>((v + 100.0) * (1.0 / 29.3814)));
-    const double i_inf = sigm<FP>((v + 43.94) * (1.0 / 5.711));
-    double t_if = 4.562 + vrcp<FP>(0.3933 * vexp<FP>(-(v + 100.0) * (1.0 / 100.0)) + 0.08004 * vexp<FP>((v + 50.0) * (1.0 / 16.59)));
-    double t_is = 23.62 + vrcp<FP>(0.001416 * vexp<FP>(-(v + 96.52) * (1.0 / 59.05)) + 1.780e-8 * vexp<FP>((v + 114.1) * (1.0 / 8.079)));
+    double e[14] = {-(v - 14.34) * (1.0 / 14.82),     -(v - 18.4099) * (1.0 / 29.3814), (v + 100.0) * (1.0 / 29.3814),
+                    (v + 43.94) * (1.0 / 5.711),      -(v + 100.0) * (1.0 / 100.0),     (v + 50.0) * (1.0 / 16.59),
+                    -(v + 96.52) * (1.0 / 59.05),     (v + 114.1) * (1.0 / 8.079),      (v + 70.0) * (1.0 / 5.0),
+                    (v - 213.6) * (1.0 / 151.2),      -(v - 24.34) * (1.0 / 14.82),     (v - 167.4) * (1.0 / 15.89),
+                    -(v - 12.23) * (1.0 / 0.2154),    (v + 70.0) * (1.0 / 20.0)};
+    vexp_n<FP>(e);
+    double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), 1.0 + e[2], 1.0 + e[3],
+                    0.3933 * e[4] + 0.08004 * e[5], 0.001416 * e[6] + 1.780e-8 * e[7], 1.0 + e[8],
+                    1.0 + e[9], 1.0 + e[10], e[11] + e[12], 1.0 + e[13]};
+    vrcp_n<FP>(q);
+    const double a_inf = q[0];
+    const double r_a = (1.0 / 1.0515) * (q[1] + 3.5 * q[2]);
+    const double i_inf = q[3];
+    double t_if = 4.562 + q[4];
+    double t_is = 23.62 + q[5];
     if (P::epi) {
-      const double d_epi = 1.0 - 0.95 * sigm<FP>((v + 70.0) * (1.0 / 5.0));
+      const double d_epi = 1.0 - 0.95 * q[6];
       t_if *= d_epi;
       t_is *= d_epi;
     }
-    const double r_if = vrcp<FP>(t_if), r_is = vrcp<FP>(t_is);
-    const double a_if = sigm<FP>((v - 213.6) * (1.0 / 151.2));
+    const double a_if = q[7];
     const double a_is = 1.0 - a_if;
-    const double ap_inf = sigm<FP>(-(v - 24.34) * (1.0 / 14.82));
-    const double dev = 1.354 + 1.0e-4 * vrcp<FP>(vexp<FP>((v - 167.4) * (1.0 / 15.89)) + vexp<FP>(-(v - 12.23) * (1.0 / 0.2154)));
-    const double rec = 1.0 - 0.5 * sigm<FP>((v + 70.0) * (1.0 / 20.0));
-    const double r_dr = vrcp<FP>(dev * rec);
+    const double ap_inf = q[8];
+    const double dev = 1.354 + 1.0e-4 * q[9];
+    const double rec = 1.0 - 0.5 * q[10];
+    double r3[3] = {t_if, t_is, dev * rec};
+    vrcp_n<FP>(r3);
+    const double r_if = r3[0], r_is = r3[1], r_dr = r3[2];
     const double imix = a_if * s[IF] + a_is * s[IS];
     const double ipmix = a_if * s[IFP] + a_is * s[ISP];
     i_to = P::gto * (v - ek) * (nfk * s[A] * imix + fk * s[AP] * ipmix);
@@ -220,16 +251,22 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
-    const double d_inf = sigm<FP>(-(v + 3.940) * (1.0 / 4.230));
-    const double r_d = vrcp<FP>(0.6 + vrcp<FP>(vexp<FP>(-0.05 * (v + 6.0)) + vexp<FP>(0.09 * (v + 14.0))));
-    const double f_inf = sigm<FP>((v + 19.58) * (1.0 / 3.696));
-    const double eff = vexp<FP>((v + 20.0) * (1.0 / 10.0));
-    const double r_ff = vrcp<FP>(7.0 + vrcp<FP>(0.0045 * (vrcp<FP>(eff) + eff)));
-    const double r_fs = vrcp<FP>(1000.0 + vrcp<FP>(0.000035 * vexp<FP>(-(v + 5.0) * (1.0 / 4.0)) + 0.000035 * vexp<FP>((v + 5.0) * (1.0 / 6.0))));
-    const double efc = vexp<FP>((v - 4.0) * (1.0 / 7.0));
-    const double r_fcaf = vrcp<FP>(7.0 + vrcp<FP>(0.04 * (vrcp<FP>(efc) + efc)));
-    const double r_fcas = vrcp<FP>(100.0 + vrcp<FP>(0.00012 * vexp<FP>(-v * (1.0 / 3.0)) + 0.00012 * vexp<FP>(v * (1.0 / 7.0))));
-    const double a_fcaf = 0.3 + 0.6 * sigm<FP>((v - 10.0) * (1.0 / 10.0));
+    double e[11] = {-(v + 3.940) * (1.0 / 4.230), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
+                    (v + 19.58) * (1.0 / 3.696),  (v + 20.0) * (1.0 / 10.0),  -(v + 5.0) * (1.0 / 4.0),
+                    (v + 5.0) * (1.0 / 6.0),      (v - 4.0) * (1.0 / 7.0),    -v * (1.0 / 3.0),
+                    v * (1.0 / 7.0),              (v - 10.0) * (1.0 / 10.0)};
+    vexp_n<FP>(e);
+    const double eff = e[4], efc = e[7];
+    double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, 0.000035 * e[5] + 0.000035 * e[6], efc,
+                   0.00012 * e[8] + 0.00012 * e[9], 1.0 + e[10]};
+    vrcp_n<FP>(q);
+    double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
+    vrcp_n<FP>(q2);
+    double q3[2] = {7.0 + q2[1], 7.0 + q2[3]};
+    vrcp_n<FP>(q3);
+    const double d_inf = q[0], f_inf = q[2];
+    const double r_d = q2[0], r_fs = q2[2], r_fcas = q2[4], r_ff = q3[0], r_fcaf = q3[1];
+    const double a_fcaf = 0.3 + 0.6 * q[7];
     const double a_fcas = 1.0 - a_fcaf;
     const double fmix = 0.6 * s[FF] + (1.0 - 0.6) * s[FS];
     const double fcamix = a_fcaf * s[FCAF] + a_fcas * s[FCAS];
@@ -262,27 +299,39 @@ __device__ __forceinline__ void step(double& v, double* s, double* ds, double is
   // ---------------- IKr, IKs, IK1
   double i_k;  // IKr + IKs + IK1
   {
-    const double xr_inf = sigm<FP>(-(v + 8.337) * (1.0 / 6.789));
-    const double r_xrf = vrcp<FP>(12.98 + vrcp<FP>(0.3652 * vexp<FP>((v - 31.66) * (1.0 / 3.869)) + 4.123e-5 * vexp<FP>(-(v - 47.78) * (1.0 / 20.38))));
-    const double r_xrs = vrcp<FP>(1.865 + vrcp<FP>(0.06629 * vexp<FP>((v - 34.70) * (1.0 / 7.355)) + 1.128e-5 * vexp<FP>(-(v - 29.74) * (1.0 / 25.94))));
-    const double a_xrf = sigm<FP>((v + 54.81) * (1.0 / 38.21));
+    double e[8] = {-(v + 8.337) * (1.0 / 6.789), (v - 31.66) * (1.0 / 3.869), -(v - 47.78) * (1.0 / 20.38),
+                   (v - 34.70) * (1.0 / 7.355),  -(v - 29.74) * (1.0 / 25.94), (v + 54.81) * (1.0 / 38.21),
+                   (v + 55.0) * (1.0 / 75.0),    (v - 10.0) * (1.0 / 30.0)};
+    vexp_n<FP>(e);
+    double q[5] = {1.0 + e[0], 0.3652 * e[1] + 4.123e-5 * e[2], 0.06629 * e[3] + 1.128e-5 * e[4], 1.0 + e[5],
+                   (1.0 + e[6]) * (1.0 + e[7])};
+    vrcp_n<FP>(q);
+    double q2[2] = {12.98 + q[1], 1.865 + q[2]};
+    vrcp_n<FP>(q2);
+    const double xr_inf = q[0], r_xrf = q2[0], r_xrs = q2[1], a_xrf = q[3], rkr = q[4];
     const double xrmix = a_xrf * s[XRF] + (1.0 - a_xrf) * s[XRS];
-    const double rkr = vrcp<FP>((1.0 + vexp<FP>((v + 55.0) * (1.0 / 75.0))) * (1.0 + vexp<FP>((v - 10.0) * (1.0 / 30.0))));
     const double i_kr = (P::gkr * gkr_scale) * xrmix * rkr * (v - ek);  // sqrt(ko/5.4) == 1
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
-    const double xs_inf = sigm<FP>(-(v + 11.60) * (1.0 / 8.932));
-    const double r_xs1 = vrcp<FP>(817.3 + vrcp<FP>(2.326e-4 * vexp<FP>((v + 48.28) * (1.0 / 17.80)) + 0.001292 * vexp<FP>(-(v + 210.0) * (1.0 / 230.0))));
-    const double r_xs2 = 0.01 * vexp<FP>((v - 50.0) * (1.0 / 20.0)) + 0.0193 * vexp<FP>(-(v + 66.54) * (1.0 / 31.0));
-    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - log(cai)))  /* log(3.8e-5) */);
+    double f[9] = {-(v + 11.60) * (1.0 / 8.932),  (v + 48.28) * (1.0 / 17.80), -(v + 210.0) * (1.0 / 230.0),
+                   (v - 50.0) * (1.0 / 20.0),     -(v + 66.54) * (1.0 / 31.0),
+                   -(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)),
+                   -(v + 127.2) * (1.0 / 20.36),  (v + 236.8) * (1.0 / 69.33),  (v + 105.8 - 2.6 * KO) * (1.0 / 9.493)};
+    vexp_n<FP>(f);
+    double p[4] = {1.0 + f[0], 2.326e-4 * f[1] + 0.001292 * f[2], 1.0 + f[5], 1.0 + f[8]};
+    vrcp_n<FP>(p);
+    const double xs_inf = p[0];
+    const double r_xs1 = vrcp<FP>(817.3 + p[1]);
+    const double r_xs2 = 0.01 * f[3] + 0.0193 * f[4];
+    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - log(cai))) /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
 
-    const double xk1_inf = sigm<FP>(-(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)));
-    const double r_xk1 = (vexp<FP>(-(v + 127.2) * (1.0 / 20.36)) + vexp<FP>((v + 236.8) * (1.0 / 69.33))) * (1.0 / 122.2);
-    const double rk1 = sigm<FP>((v + 105.8 - 2.6 * KO) * (1.0 / 9.493));
+    const double xk1_inf = p[2];
+    const double r_xk1 = (f[6] + f[7]) * (1.0 / 122.2);
+    const double rk1 = p[3];
     const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
     gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
     i_k = i_kr + i_ks + i_k1;
@@ -394,7 +443,7 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
   double tmp[NSTATE];
 #pragma unroll
   for (int q = 0; q < NSTATE; ++q) tmp[q] = s[q];
-  step<CT, true, false>(v, tmp, ds, ist, 1.0, 0.0, dv);
+  step<CT, true, false, double*>(v, tmp, ds, ist, 1.0, 0.0, dv);
 }
 
 }  // namespace ord
@@ -402,15 +451,19 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 // Launch shapes: V = 0: 128-thread blocks, 2 per SM (<= 255 regs), warps free-running;
 // V = 1: one persistent 384-thread block per SM (<= 168 regs, 12 warps), lockstep;
 // V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep;
-// V = 3: one persistent 512-thread block per SM (<= 128 regs, 16 warps), lockstep.
+// V = 3: one persistent 512-thread block per SM (<= 128 regs, 16 warps), lockstep;
+// V = 4: like 3 with the node states in shared memory (160 KB);
+// V = 5: like 1 (384 threads) with the node states in shared memory (120 KB).
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 3 ? 512 : 128));
+  static constexpr int kThreads = V == 1 || V == 5 ? 384 : (V == 2 ? 256 : (V == 3 || V == 4 ? 512 : 128));
   static constexpr int kMinBlocks = V == 0 ? 2 : 1;
   static constexpr bool kBlockSync = V != 0;
+  static constexpr bool kSmemStates = V >= 4;
   static constexpr bool kUsesGkr = true;
-  __device__ __forceinline__ static void advance(double& v, double* s, double ist, double g, double h, double& dv) {
+  template <class SA>
+  __device__ __forceinline__ static void advance(double& v, SA s, double ist, double g, double h, double& dv) {
     if (fabs(v) <= 130.0)
       ord::step<CT, false, true>(v, s, nullptr, ist, g, h, dv);
     else
@@ -432,8 +485,21 @@ __global__ void ord_rates_kernel(long long n, const double* v, const double* s, 
 }
 
 template <class M>
+static size_t smem_bytes(int khist_len) {
+  const size_t hist = static_cast<size_t>((khist_len + 1) & ~1) * sizeof(unsigned);
+  return hist + (M::kSmemStates ? static_cast<size_t>(M::NS) * M::kThreads * sizeof(double) : 0);
+}
+
+template <class M>
 static cudaError_t launch_react_t(const ReactArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>(a.khist_len) * sizeof(unsigned);
+  const size_t smem = smem_bytes<M>(a.khist_len);
+  if (smem > 48 * 1024) {
+    static bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(react_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      set = true;
+    }
+  }
   react_kernel<M><<<grid, M::kThreads, smem, st>>>(a);
   return cudaGetLastError();
 }
@@ -441,7 +507,9 @@ static cudaError_t launch_react_t(const ReactArgs& a, int grid, cudaStream_t st)
 template <class M>
 static int occupancy_t() {
   int b = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, react_kernel<M>, M::kThreads, 2048 * sizeof(unsigned));
+  const size_t smem = smem_bytes<M>(2048);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(react_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, react_kernel<M>, M::kThreads, smem);
   return b;
 }
 
@@ -453,6 +521,8 @@ static cudaError_t launch_ct(int variant, const ReactArgs& a, int grid, cudaStre
     case 0: return launch_react_t<ModelOrd<CT, 0>>(a, grid, st);
     case 2: return launch_react_t<ModelOrd<CT, 2>>(a, grid, st);
     case 3: return launch_react_t<ModelOrd<CT, 3>>(a, grid, st);
+    case 4: return launch_react_t<ModelOrd<CT, 4>>(a, grid, st);
+    case 5: return launch_react_t<ModelOrd<CT, 5>>(a, grid, st);
     default: return launch_react_t<ModelOrd<CT, 1>>(a, grid, st);
   }
 }
@@ -471,6 +541,8 @@ int react_ord_threads(int variant) {
     case 0: return ModelOrd<0, 0>::kThreads;
     case 2: return ModelOrd<0, 2>::kThreads;
     case 3: return ModelOrd<0, 3>::kThreads;
+    case 4: return ModelOrd<0, 4>::kThreads;
+    case 5: return ModelOrd<0, 5>::kThreads;
     default: return ModelOrd<0, 1>::kThreads;
   }
 }
@@ -481,6 +553,8 @@ static int occ_ct(int variant) {
     case 0: return occupancy_t<ModelOrd<CT, 0>>();
     case 2: return occupancy_t<ModelOrd<CT, 2>>();
     case 3: return occupancy_t<ModelOrd<CT, 3>>();
+    case 4: return occupancy_t<ModelOrd<CT, 4>>();
+    case 5: return occupancy_t<ModelOrd<CT, 5>>();
     default: return occupancy_t<ModelOrd<CT, 1>>();
   }
 }
