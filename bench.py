@@ -113,6 +113,12 @@ def build_problem(config, world, rank):
         return problems.c1()
     if config == "c3":
         return problems.c3()
+    if config in ("c4", "c5"):
+        # weak scaling: the slab grows in y with the number of ranks (same y extent per GPU)
+        if config == "c4":
+            return problems.slab(5.0, 5.0 * world, 1.0, 0.02, t_end=500.0)
+        return problems.slab(10.0, 10.0 * world, 2.0, 0.01, t_end=5.0 if world == 1 else 5.0, stim="sites",
+                             n_sites=16 * world)
     raise SystemExit(f"unknown config {config}")
 
 
@@ -120,7 +126,11 @@ def config_block(config, prob, world, l):
     names = {"c2": "BASELINE configs[1]: 2D anisotropic sheet 5x5 cm, 201x201 nodes, fibres 45 deg, "
                    "corner stimulus, ORd-epi, DAETI dt 0.1 ms, 500 ms",
              "c1": "BASELINE configs[0]: 2D isotropic 1x1 cm, 101x101 nodes, ORd-epi, left-edge 2x threshold",
-             "c3": "BASELINE configs[2] (extension): 1001x1001 scar/border-zone sheet"}
+             "c3": "BASELINE configs[2] (extension): 1001x1001 scar/border-zone sheet",
+             "c4": "BASELINE configs[3] (extension): 3D slab 5x5x1 cm, 251x251x51 nodes per GPU, fibres +60..-60 deg, "
+                   "endocardial face stimulus, ORd-epi",
+             "c5": "BASELINE configs[4] (extension): 3D slab 10x10x2 cm, 1001x1001x201 nodes per GPU, 16 random "
+                   "endocardial sites, ORd-epi"}
     return {"workload": names[config], "nodes": int(prob.n), "nodes_per_gpu": int(prob.n // max(world, 1)),
             "cell_model": prob.models[0], "scheme": "DAETI", "dt_ms": prob.cfg.dt_ms, "k0_up": prob.cfg.k0_up,
             "k0_down": prob.cfg.k0_down, "diffusion_substeps_per_step": 2 * l,
@@ -187,7 +197,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3"])
+    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5"])
     ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of reference CPU work per arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -233,8 +243,11 @@ def main():
     integ = cw.StrangIntegrator(setup, prob.cfg, model_of_node=prob.model_of_node, device=local, rank=rank,
                                 world=world, nccl_id=nccl_id)
     info = integ.info
-    st = prob.initial_state()
-    integ.upload(st)
+    big = prob.n > 20_000_000
+    if big:  # 10^8 nodes: make_initial_state on the device (the AoS host copy would be ~64 GB)
+        integ.init_rest()
+    else:
+        integ.upload(prob.initial_state())
     integ.run_begin()
     integ.run_steps(0, args.warmup)
     integ.run_sync()
@@ -309,7 +322,10 @@ def main():
             "ord_min_blocks": int(os.environ.get("CWG_ORD_MINB", "2"))}
 
     # --- end to end through the public API (run_simulation) with pinned host state
-    if not args.no_e2e:
+    if big:
+        line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                       "note": "skipped: host AoS state of a 10^8-node slab is ~64 GB"}
+    if not args.no_e2e and not big:
         pin = lambda a: (lambda t: (t.copy_(torch.from_numpy(a)), t.numpy())[1])(
             torch.empty(a.shape, dtype=torch.float64, pin_memory=True))
         st0 = prob.initial_state()

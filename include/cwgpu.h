@@ -149,6 +149,9 @@ void* cwg_stream(cwg_ctx* ctx);
 int cwg_upload_state(cwg_ctx* ctx, const double* v, const double* s_aos, int stride,
                      const double* last_dvdt);
 int cwg_download_state(cwg_ctx* ctx, double* v, double* s_aos, int stride, double* last_dvdt);
+/* make_initial_state from the models' rest states directly on the device
+ * (no host arrays; for 10^8-node slabs). last_dvdt = 0, V = rest V. */
+int cwg_init_rest_state(cwg_ctx* ctx);
 /* Pinned staging for host<->device copies (e2e path); returns host pointers
  * owned by ctx of the sizes of the local slab. */
 int cwg_pinned_buffers(cwg_ctx* ctx, double** v, double** s_aos, double** last_dvdt);

@@ -61,6 +61,21 @@ int64_t cwg_sheet_select(const cwg_sheet* s, int kind, const double* prm, const 
                          int64_t n_set, int64_t* out, int64_t cap);
 int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y);
 
+/* ---- 3D slab (EXTENSION for BASELINE configs 4-5; parity pinned to the C
+ * oracle's independent CSR assembly, oracle/cw_oracle.c cwo_assemble_slab3d).
+ * Structured operator of cwg_struct3d (cwgpu.h): node (ix, iy, iz) has index
+ * (iy*(nz+1) + iz)*(nx+1) + ix; hex element (ex, ey, ez) has index
+ * (ey*nz + ez)*nx + ex and layer ez's fibre angle. Element integrals on the
+ * cube [0,h]^3: trilinear shape functions, 2x2x2 Gauss, row-sum lumped mass
+ * (the 3D analogue of fem.cpp:63-108). A row's coefficients depend only on the
+ * node class c = (by*3 + bx)*(nz+1) + iz with bx/by = 0 (low face), 1
+ * (interior), 2 (high face); each coefficient sums its element contributions
+ * in ascending element index, exactly as a CSR assembly would.
+ *   coef[c*27 + (dy+1)*9 + (dz+1)*3 + (dx+1)]  (0 where the neighbour is absent)
+ *   mass[c]
+ * n_classes = 9*(nz+1). Returns dt_s (Gershgorin, fem.cpp:178-192) or < 0. */
+double cwg_struct3d_tables(const cwg_struct3d* s, double* coef, double* mass);
+
 #ifdef __cplusplus
 }
 #endif

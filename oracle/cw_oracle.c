@@ -632,3 +632,108 @@ void cwo_detector_observe(cwo_detector* d, double t, const double* v) {
   }
   d->prev_t = t;
 }
+
+/* ------------------------------------------------------------------ *
+ * 3D slab assembly (EXTENSION; the 3D analogue of fem.cpp:63-176)     *
+ * ------------------------------------------------------------------ */
+static void hex_integrals(double h, const double D[3][3], double k[8][8], double m[8]) {
+  const double g = 0.57735026918962576;
+  const double gp[2] = {-g, g};
+  for (int a = 0; a < 8; ++a) {
+    m[a] = 0.0;
+    for (int b = 0; b < 8; ++b) k[a][b] = 0.0;
+  }
+  const double det = h * h * h / 8.0;
+  const double sc = 2.0 / h;
+  for (int q = 0; q < 8; ++q) {
+    const double xi = gp[q & 1], eta = gp[(q >> 1) & 1], zeta = gp[q >> 2];
+    double n[8], gx[8], gy[8], gz[8];
+    for (int a = 0; a < 8; ++a) {
+      const double sx = (a & 1) ? 1.0 : -1.0, sy = (a & 2) ? 1.0 : -1.0, sz = (a & 4) ? 1.0 : -1.0;
+      const double fx = 1.0 + sx * xi, fy = 1.0 + sy * eta, fz = 1.0 + sz * zeta;
+      n[a] = 0.125 * fx * fy * fz;
+      gx[a] = sc * (0.125 * sx * fy * fz);
+      gy[a] = sc * (0.125 * fx * sy * fz);
+      gz[a] = sc * (0.125 * fx * fy * sz);
+    }
+    for (int a = 0; a < 8; ++a) {
+      const double dgx = D[0][0] * gx[a] + D[0][1] * gy[a] + D[0][2] * gz[a];
+      const double dgy = D[1][0] * gx[a] + D[1][1] * gy[a] + D[1][2] * gz[a];
+      const double dgz = D[2][0] * gx[a] + D[2][1] * gy[a] + D[2][2] * gz[a];
+      for (int b = 0; b < 8; ++b) k[a][b] += det * (dgx * gx[b] + dgy * gy[b] + dgz * gz[b]);
+      m[a] += det * n[a];
+    }
+  }
+}
+
+double cwo_assemble_slab3d(int64_t nx, int64_t ny, int64_t nz, double h, double d_long, double rho,
+                           const double* angle_of_layer, int64_t** row_ptr_out, int64_t** col_out,
+                           double** val_out, double** mass_out) {
+  const int64_t nx1 = nx + 1, ny1 = ny + 1, nz1 = nz + 1, n = nx1 * ny1 * nz1;
+  double* acc = (double*)calloc((size_t)n * 27, sizeof(double));
+  unsigned char* has = (unsigned char*)calloc((size_t)n * 27, 1);
+  double* mass = (double*)calloc((size_t)n, sizeof(double));
+  double(*K)[8][8] = (double(*)[8][8])malloc((size_t)nz * sizeof(double[8][8]));
+  double(*M)[8] = (double(*)[8])malloc((size_t)nz * sizeof(double[8]));
+  for (int64_t ez = 0; ez < nz; ++ez) {
+    const double th = angle_of_layer[ez];
+    const double f[3] = {cos(th), sin(th), 0.0};
+    const double dt = rho * d_long;
+    double D[3][3];
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        const double ff = f[i] * f[j];
+        D[i][j] = d_long * ff + dt * ((i == j ? 1.0 : 0.0) - ff);
+      }
+    hex_integrals(h, D, K[ez], M[ez]);
+  }
+  /* element loop in ascending element index e = (ey*nz + ez)*nx + ex */
+  for (int64_t ey = 0; ey < ny; ++ey)
+    for (int64_t ez = 0; ez < nz; ++ez)
+      for (int64_t ex = 0; ex < nx; ++ex)
+        for (int a = 0; a < 8; ++a) {
+          const int64_t ix = ex + (a & 1), iy = ey + ((a >> 1) & 1), iz = ez + ((a >> 2) & 1);
+          const int64_t i = (iy * nz1 + iz) * nx1 + ix;
+          mass[i] += M[ez][a];
+          for (int b = 0; b < 8; ++b) {
+            const int64_t dx = ex + (b & 1) - ix, dy = ey + ((b >> 1) & 1) - iy, dz = ez + ((b >> 2) & 1) - iz;
+            const int64_t slot = i * 27 + (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1);
+            acc[slot] += K[ez][a][b];
+            has[slot] = 1;
+          }
+        }
+  int64_t nnz = 0;
+  for (int64_t s = 0; s < n * 27; ++s) nnz += has[s];
+  int64_t* rp = (int64_t*)malloc((size_t)(n + 1) * sizeof(int64_t));
+  int64_t* col = (int64_t*)malloc((size_t)nnz * sizeof(int64_t));
+  double* val = (double*)malloc((size_t)nnz * sizeof(double));
+  const int64_t plane = nz1 * nx1;
+  int64_t p = 0;
+  double min_ratio = INFINITY;
+  for (int64_t i = 0; i < n; ++i) {
+    rp[i] = p;
+    double den = 0.0;
+    /* slots in (dy, dz, dx) lexicographic order == ascending column index */
+    for (int q = 0; q < 27; ++q) {
+      if (!has[i * 27 + q]) continue;
+      const int64_t dy = q / 9 - 1, dz = (q / 3) % 3 - 1, dx = q % 3 - 1;
+      col[p] = i + dy * plane + dz * nx1 + dx;
+      val[p] = acc[i * 27 + q];
+      den += q == 13 ? val[p] : fabs(val[p]);
+      ++p;
+    }
+    if (den > 0.0 && mass[i] / den < min_ratio) min_ratio = mass[i] / den;
+  }
+  rp[n] = p;
+  free(acc);
+  free(has);
+  free(K);
+  free(M);
+  *row_ptr_out = rp;
+  *col_out = col;
+  *val_out = val;
+  *mass_out = mass;
+  return 0.9 * min_ratio;
+}
+
+void cwo_free(void* p) { free(p); }

@@ -78,6 +78,17 @@ void cwo_detector_init(cwo_detector* d, int64_t n, double threshold);
 void cwo_detector_free(cwo_detector* d);
 void cwo_detector_observe(cwo_detector* d, double t, const double* v);
 
+/* 3D slab operator (EXTENSION, BASELINE configs 4-5): CSR assembly of the
+ * trilinear-hex / 2x2x2-Gauss / row-sum-lumped operator on an (nx, ny, nz)
+ * element grid of spacing h, node index (iy*(nz+1)+iz)*(nx+1)+ix, element
+ * index (ey*nz+ez)*nx+ex, fibre angle per element layer. Contributions are
+ * accumulated per (row, column) in ascending element index; columns ascend.
+ * Caller frees the arrays with free(). Returns dt_s (Gershgorin) or < 0. */
+double cwo_assemble_slab3d(int64_t nx, int64_t ny, int64_t nz, double h, double d_long, double rho,
+                           const double* angle_of_layer, int64_t** row_ptr, int64_t** col, double** val,
+                           double** mass);
+void cwo_free(void* p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,9 @@ def lib():
             "cwo_detector_init": (None, [C.c_void_p, I64, D]),
             "cwo_detector_free": (None, [C.c_void_p]),
             "cwo_detector_observe": (None, [C.c_void_p, D, dp]),
+            "cwo_assemble_slab3d": (D, [I64, I64, I64, D, D, D, dp, C.POINTER(lp), C.POINTER(lp), C.POINTER(dp),
+                                        C.POINTER(dp)]),
+            "cwo_free": (None, [C.c_void_p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -108,6 +111,23 @@ def diffusion_substeps(dt, dt_s, strict, scheme):
 
 def k_max_for(dt, model):
     return lib().cwo_k_max_for(dt, stable_step(model))
+
+
+def assemble_slab3d(nx, ny, nz, h, d_long, rho, angles):
+    """CSR (row_ptr, col, val, mass) and dt_s of the 3D slab operator (extension)."""
+    L = lib()
+    ang = np.ascontiguousarray(angles, np.float64)
+    rp, col, val, mass = C.POINTER(C.c_int64)(), C.POINTER(C.c_int64)(), C.POINTER(C.c_double)(), C.POINTER(C.c_double)()
+    dt_s = L.cwo_assemble_slab3d(nx, ny, nz, h, d_long, rho, _dp(ang), C.byref(rp), C.byref(col), C.byref(val),
+                                 C.byref(mass))
+    n = (nx + 1) * (ny + 1) * (nz + 1)
+    rpa = np.ctypeslib.as_array(rp, (n + 1,)).copy()
+    nnz = int(rpa[-1])
+    out = (rpa, np.ctypeslib.as_array(col, (nnz,)).copy(), np.ctypeslib.as_array(val, (nnz,)).copy(),
+           np.ctypeslib.as_array(mass, (n,)).copy())
+    for ptr in (rp, col, val, mass):
+        L.cwo_free(C.cast(ptr, C.c_void_p))
+    return out, dt_s
 
 
 def diffusion_substep(csr, v, dt_sub):

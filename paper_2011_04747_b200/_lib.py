@@ -62,6 +62,8 @@ _SIGS = {
     "cwg_stream": (C.c_void_p, [C.c_void_p]),
     "cwg_upload_state": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int, _dp]),
     "cwg_download_state": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int, _dp]),
+    "cwg_init_rest_state": (C.c_int, [C.c_void_p]),
+    "cwg_struct3d_tables": (C.c_double, [C.POINTER(cwg_struct3d), _dp, _dp]),
     "cwg_pinned_buffers": (C.c_int, [C.c_void_p, C.POINTER(_dp), C.POINTER(_dp), C.POINTER(_dp)]),
     "cwg_advance": (C.c_int, [C.c_void_p, C.c_double, C.c_int64, C.c_int64, C.POINTER(cwg_error)]),
     "cwg_run_begin": (C.c_int, [C.c_void_p]),

@@ -304,6 +304,69 @@ def build_sheet(*args, **kw) -> Sheet:
     return Sheet(*args, **kw)
 
 
+def _cells(length, h, axis):
+    q = length / h
+    r = round(q)
+    if r < 1 or abs(q - r) > 1e-9 * max(1.0, q):
+        raise ValidationError(f"mesh: {axis} extent {length} cm is not a positive multiple of h = {h} cm")
+    return int(r)
+
+
+class Slab3D:
+    """3D slab (EXTENSION for BASELINE configs 4-5; the reference is 2D only).
+
+    (nx+1) x (ny+1) x (nz+1) nodes at spacing h, node index
+    (iy*(nz+1) + iz)*(nx+1) + ix (y outermost: y-slabs are contiguous),
+    trilinear hexahedra with 2x2x2 Gauss and row-sum lumped mass, transmural
+    fibre rotation linear in z from angle_endo (z = 0) to angle_epi (z = lz)
+    evaluated at each element layer's mid-plane, D_t = rho * D_l. The device
+    keeps 27 coefficients per node class (cwgpu_setup.h) instead of a CSR.
+    Acts as the operator object of SimulationSetup.op.
+    """
+
+    def __init__(self, lx, ly, lz, h, d_long=0.0012, rho=0.25, angle_endo_deg=60.0, angle_epi_deg=-60.0):
+        self.nx, self.ny, self.nz = _cells(lx, h, "x"), _cells(ly, h, "y"), _cells(lz, h, "z")
+        self.h, self.d_long, self.rho = h, d_long, rho
+        self.nx1, self.ny1, self.nz1 = self.nx + 1, self.ny + 1, self.nz + 1
+        self.n = self.nx1 * self.ny1 * self.nz1
+        self.plane = self.nx1 * self.nz1
+        self.angles = np.deg2rad(angle_endo_deg + (angle_epi_deg - angle_endo_deg) * (np.arange(self.nz) + 0.5) / self.nz)
+        self.s3d = L.cwg_struct3d(self.nx, self.ny, self.nz, h, d_long, rho, L.dp(self.angles))
+        ncls = 9 * self.nz1
+        self.coef = np.zeros(ncls * 27)
+        self.mass = np.zeros(ncls)
+        self.dt_s = L.lib().cwg_struct3d_tables(C.byref(self.s3d), L.dp(self.coef), L.dp(self.mass))
+        if not self.dt_s > 0:
+            raise ValidationError("slab: invalid parameters")
+        self.op = self
+
+    def rows(self):
+        return self.n
+
+    def index(self, ix, iy, iz):
+        return (np.asarray(iy) * self.nz1 + np.asarray(iz)) * self.nx1 + np.asarray(ix)
+
+    def face_z0(self):
+        """Endocardial face (z = 0) node indices, ascending."""
+        iy, ix = np.meshgrid(np.arange(self.ny1), np.arange(self.nx1), indexing="ij")
+        return np.sort(self.index(ix, iy, 0).ravel())
+
+    def discs_z0(self, centers, radius):
+        """z = 0 nodes within `radius` of any (cx, cy) (1e-9 cm inclusive, like select_nodes)."""
+        iy, ix = np.meshgrid(np.arange(self.ny1), np.arange(self.nx1), indexing="ij")
+        x, y = ix * self.h, iy * self.h
+        sel = np.zeros(ix.shape, bool)
+        for cx, cy in centers:
+            sel |= np.sqrt((x - cx) ** 2 + (y - cy) ** 2) <= radius + 1e-9
+        return np.sort(self.index(ix[sel], iy[sel], 0))
+
+    def nearest(self, x, y, z):
+        ix = min(max(int(round(x / self.h)), 0), self.nx)
+        iy = min(max(int(round(y / self.h)), 0), self.ny)
+        iz = min(max(int(round(z / self.h)), 0), self.nz)
+        return int(self.index(ix, iy, iz))
+
+
 # ----------------------------------------------------------------------------- stimulus (stimulus.hpp)
 @dataclass
 class Stimulus:
@@ -331,23 +394,31 @@ class ProtocolIndex:
     """Compiled per-node view (stimulus.cpp:17-31), flattened for the device."""
 
     def __init__(self, protocol: Protocol, n_nodes: int):
-        lists = [[] for _ in range(n_nodes)]
-        for eid, st in enumerate(protocol.entries):
+        es = protocol.entries
+        for st in es:
             if not st.duration_ms > 0.0:
                 raise ValidationError("stimulus: duration must be positive")
             if not math.isfinite(st.amplitude):
                 raise ValidationError("stimulus: amplitude must be finite")
             if len(st.nodes) == 0:
                 raise ValidationError("stimulus: node set is empty")
-            for nd in np.asarray(st.nodes, np.int64):
-                if nd < 0 or nd >= n_nodes:
-                    raise ValidationError(f"stimulus: node {nd} out of range")
-                lists[int(nd)].append(eid)
-        self.n_entries = len(protocol.entries)
+            nd = np.asarray(st.nodes, np.int64)
+            if nd.min() < 0 or nd.max() >= n_nodes:
+                bad = nd[(nd < 0) | (nd >= n_nodes)][0]
+                raise ValidationError(f"stimulus: node {bad} out of range")
+        self.n_entries = len(es)
+        # per-node entry lists in protocol order (stimulus.cpp:17-31), vectorised
+        if es:
+            nodes = np.concatenate([np.asarray(st.nodes, np.int64) for st in es])
+            eids = np.concatenate([np.full(len(st.nodes), e, np.int32) for e, st in enumerate(es)])
+            order = np.lexsort((eids, nodes))
+            counts = np.bincount(nodes, minlength=n_nodes)
+            self.ids = np.ascontiguousarray(eids[order])
+        else:
+            counts = np.zeros(n_nodes, np.int64)
+            self.ids = np.zeros(1, np.int32)
         self.node_ptr = np.zeros(n_nodes + 1, np.int32)
-        self.node_ptr[1:] = np.cumsum([len(x) for x in lists])
-        self.ids = np.array([e for x in lists for e in x] or [0], np.int32)
-        es = protocol.entries
+        np.cumsum(counts, out=self.node_ptr[1:])
         self.t_start = np.array([s.t_start_ms for s in es] or [0.0])
         self.duration = np.array([s.duration_ms for s in es] or [1.0])
         self.amplitude = np.array([s.amplitude for s in es] or [0.0])
@@ -433,15 +504,21 @@ class StrangIntegrator:
             model_of_node = np.zeros(n, np.uint8)
         keep = {}
         p = L.cwg_problem()
-        keep["rp"] = np.ascontiguousarray(op.row_ptr, np.int64)
-        keep["col"] = np.ascontiguousarray(op.col, np.int64)
-        keep["val"] = np.ascontiguousarray(op.val, np.float64)
-        keep["mass"] = np.ascontiguousarray(op.lumped_mass, np.float64)
-        p.n, p.row_ptr, p.col, p.val, p.lumped_mass = n, L.lp(keep["rp"]), L.lp(keep["col"]), L.dp(keep["val"]), L.dp(
-            keep["mass"])
+        p.n = n
         p.dt_s = op.dt_s
-        p.op_kind = op_kind
-        p.grid_nx1, p.grid_ny1 = op.grid_nx1, op.grid_ny1
+        if isinstance(op, Slab3D):
+            keep["s3d"] = op.s3d
+            p.op_kind = L.OP_STRUCT3D
+            p.s3d = C.pointer(op.s3d)
+        else:
+            keep["rp"] = np.ascontiguousarray(op.row_ptr, np.int64)
+            keep["col"] = np.ascontiguousarray(op.col, np.int64)
+            keep["val"] = np.ascontiguousarray(op.val, np.float64)
+            keep["mass"] = np.ascontiguousarray(op.lumped_mass, np.float64)
+            p.row_ptr, p.col, p.val, p.lumped_mass = L.lp(keep["rp"]), L.lp(keep["col"]), L.dp(keep["val"]), L.dp(
+                keep["mass"])
+            p.op_kind = op_kind
+            p.grid_nx1, p.grid_ny1 = op.grid_nx1, op.grid_ny1
         keep["kinds"] = np.array([m.kind for m in setup.models], np.int32)
         p.n_models = len(setup.models)
         p.model_kind = keep["kinds"].ctypes.data_as(L._ip)
@@ -522,6 +599,11 @@ class StrangIntegrator:
         _check(L.lib().cwg_set_stream(self._h, cuda_stream_handle))
 
     # --- state movement
+    def init_rest(self):
+        """make_initial_state from rest states directly on the device (no host arrays)."""
+        _check(L.lib().cwg_init_rest_state(self._h))
+        self._state_id = None
+
     def upload(self, state: NodeStateArray):
         _check(L.lib().cwg_upload_state(self._h, L.dp(state.v), L.dp(state.s), state.stride, L.dp(state.last_dvdt)))
         self._state_id = id(state)

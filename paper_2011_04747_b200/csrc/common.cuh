@@ -129,6 +129,16 @@ struct Stencil2D {
   long long ny1;        // global rows
 };
 
+// Structured 3D slab (EXTENSION): per-class 27-point coefficients
+struct Struct3D {
+  const double* coef;  // [n_classes][27]
+  const double* cm;    // [n_classes] dt_sub / m
+  long long nx1, nz1, plane;  // plane = nx1 * nz1 nodes per y-plane
+  long long planes;           // owned y-planes
+  long long row_begin;        // global y of owned plane 0
+  long long ny1;
+};
+
 struct CsrDev {
   const long long* row_ptr;
   const long long* col;

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "../../include/cwgpu.h"
+#include "../../include/cwgpu_setup.h"
 #include "launch.h"
 
 using namespace cwg;
@@ -213,7 +214,8 @@ struct cwg_ctx {
   double* d_gkr = nullptr;
 
   // operator
-  double* d_coef = nullptr;  // stencil: [9][n_own]
+  long long s3_nx1 = 0, s3_nz1 = 0;  // struct3d
+  double* d_coef = nullptr;  // stencil: [9][n_own]; struct3d: [classes][27]
   double* d_cm = nullptr;    // dt_ad / m_i
   long long* d_rp = nullptr;
   long long* d_col = nullptr;
@@ -358,6 +360,9 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     if (c->op_kind == CWG_OP_STENCIL2D) {
       Stencil2D s{c->d_coef, c->n_own, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
       CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
+    } else if (c->op_kind == CWG_OP_STRUCT3D) {
+      Struct3D s{c->d_coef, c->d_cm, c->s3_nx1, c->s3_nz1, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
+      CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms * 16, c->stream));
     } else {
       CsrDev m{c->d_rp, c->d_col, c->d_val, c->d_cm};
       CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));
@@ -632,7 +637,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   if (pc.op_kind == CWG_OP_AUTO) infer_grid(&pc);
   const cwg_problem* p = &pc;
   validation(p->n > 0, "integrator: empty problem");
-  validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
+  validation(p->lumped_mass != nullptr || p->op_kind == CWG_OP_STRUCT3D, "integrator: missing assembled operator");
   validation(p->n_models > 0 && p->model_kind, "integrator: no cell models");
   validation(p->dt_ms > 0.0, "scheme: dt must be positive");
   validation(p->t_end_ms >= p->dt_ms, "scheme: T must be >= dt");
@@ -687,15 +692,40 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->spm = std::max<long long>(1, llround_ref(c->map_interval / c->dt_eff));
 
   // ---- partition and operator layout
+  std::vector<double> s3_coef, s3_mass;
+  if (p->op_kind == CWG_OP_STRUCT3D) {
+    validation(p->s3d != nullptr, "operator: CWG_OP_STRUCT3D needs cwg_problem.s3d");
+    const cwg_struct3d& s3 = *p->s3d;
+    validation(s3.nx >= 1 && s3.ny >= 1 && s3.nz >= 1, "operator: 3D slab needs >= 1 element per axis");
+    const long long n3 = (s3.nx + 1) * (s3.ny + 1) * (s3.nz + 1);
+    validation(p->n == n3, "operator: n does not match the 3D slab");
+    s3_coef.resize(static_cast<size_t>(9 * (s3.nz + 1) * 27));
+    s3_mass.resize(static_cast<size_t>(9 * (s3.nz + 1)));
+    const double dts = cwg_struct3d_tables(p->s3d, s3_coef.data(), s3_mass.data());
+    validation(dts > 0.0, "operator: invalid 3D slab parameters");
+    c->s3_nx1 = s3.nx + 1;
+    c->s3_nz1 = s3.nz + 1;
+  }
   c->n_global = p->n;
   int kind = p->op_kind;
   if (kind == CWG_OP_AUTO) kind = stencil_ok(p) ? CWG_OP_STENCIL2D : CWG_OP_CSR;
-  validation(kind == CWG_OP_CSR || kind == CWG_OP_STENCIL2D, "operator: unsupported op_kind for this build");
+  validation(kind == CWG_OP_CSR || kind == CWG_OP_STENCIL2D || kind == CWG_OP_STRUCT3D, "operator: unknown op_kind");
   if (kind == CWG_OP_STENCIL2D) validation(stencil_ok(p), "operator: CSR is not a regular-sheet 9-point operator");
   c->op_kind = kind;
   c->rank = p->rank;
   c->world = p->world;
-  if (kind == CWG_OP_STENCIL2D || p->world > 1) {
+  if (kind == CWG_OP_STRUCT3D) {  // y-slabs of (nx+1)*(nz+1)-node planes
+    c->w = c->s3_nx1 * c->s3_nz1;
+    c->ny1 = p->s3d->ny + 1;
+    int64_t rb = 0, re = 0;
+    validation(cwg_slab_plan(c->ny1, c->world, c->rank, &rb, &re) == CWG_OK, "placement: fewer planes than ranks");
+    c->row_begin = rb;
+    c->row_end = re;
+    c->n_own = (re - rb) * c->w;
+    c->halo = c->w;
+    c->own_global0 = rb * c->w;
+    c->node_offset = c->own_global0 - c->halo;
+  } else if (kind == CWG_OP_STENCIL2D || p->world > 1) {
     validation(p->grid_nx1 > 0 && p->grid_ny1 > 0 && p->grid_nx1 * p->grid_ny1 == p->n,
                "placement: slab decomposition needs the sheet's grid dimensions");
     c->w = p->grid_nx1;
@@ -732,13 +762,25 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   CUDA_TRY(cudaMemset(c->d_last, 0, c->n_alloc * sizeof(double)));
 
   // ---- operator upload
-  std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
-  double* d_mass = upload(mass_own.data(), mass_own.size());
-  c->d_cm = dev_alloc<double>(c->n_own);
-  CUDA_TRY(launch_mass_factor(d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
-  CUDA_TRY(cudaStreamSynchronize(c->stream));
-  dev_free(d_mass);
-  if (kind == CWG_OP_STENCIL2D) {
+  if (kind == CWG_OP_STRUCT3D) {
+    double* d_mass = upload(s3_mass.data(), s3_mass.size());
+    c->d_cm = dev_alloc<double>(s3_mass.size());
+    CUDA_TRY(launch_mass_factor(d_mass, static_cast<long long>(s3_mass.size()), c->dt_ad, c->d_cm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    dev_free(d_mass);
+    c->d_coef = upload(s3_coef.data(), s3_coef.size());
+  } else {
+    validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
+    std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
+    double* d_mass = upload(mass_own.data(), mass_own.size());
+    c->d_cm = dev_alloc<double>(c->n_own);
+    CUDA_TRY(launch_mass_factor(d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    dev_free(d_mass);
+  }
+  if (kind == CWG_OP_STRUCT3D) {
+    // tables uploaded above
+  } else if (kind == CWG_OP_STENCIL2D) {
     build_stencil(c, p);
   } else {
     validation(p->row_ptr && p->col && p->val, "operator: CSR arrays missing");
@@ -759,22 +801,26 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
 
   // ---- models: per-model node bins over owned nodes (local indices)
   validation(p->model_of_node != nullptr, "integrator: model_of_node missing");
-  std::vector<std::vector<int32_t>> lists(p->n_models);
+  validation(c->n_alloc < (1ll << 31), "integrator: more than 2^31 local nodes per device (use more ranks)");
+  std::vector<long long> per_model(static_cast<size_t>(p->n_models), 0);
   for (long long o = 0; o < c->n_own; ++o) {
     const int m = p->model_of_node[c->own_global0 + o];
     validation(m < p->n_models, "initial state: node " + std::to_string(c->own_global0 + o) + " has no model");
-    lists[m].push_back(static_cast<int32_t>(o + c->halo));
+    ++per_model[static_cast<size_t>(m)];
   }
-  validation(c->n_alloc < (1ll << 31), "integrator: more than 2^31 local nodes per device (use more ranks)");
   for (int m = 0; m < p->n_models; ++m) {
     Bin b;
     b.model = m;
     b.kind = c->model_kind[m];
-    b.count = static_cast<long long>(lists[m].size());
+    b.count = per_model[static_cast<size_t>(m)];
     if (b.count == c->n_own) {
       b.first = c->halo;  // dense
     } else if (b.count > 0) {
-      b.d_list = upload(lists[m].data(), lists[m].size());
+      std::vector<int32_t> list;
+      list.reserve(static_cast<size_t>(b.count));
+      for (long long o = 0; o < c->n_own; ++o)
+        if (p->model_of_node[c->own_global0 + o] == m) list.push_back(static_cast<int32_t>(o + c->halo));
+      b.d_list = upload(list.data(), list.size());
     }
     b.variant = choose_ord_variant(b.count, c->num_sms);
     const int threads = is_ord(b.kind) ? react_ord_threads(b.variant) : react_exact_threads(b.kind);
@@ -1083,6 +1129,23 @@ int cwg_upload_state(cwg_ctx* c, const double* v, const double* s_aos, int strid
       ++c->launches;
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int cwg_init_rest_state(cwg_ctx* c) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    c->cur = 0;
+    for (const auto& b : c->bins) {
+      double rest[64] = {0};
+      cwg_model_rest_state(b.kind, rest);
+      double* d_rest = upload(rest, 64);
+      CUDA_TRY(launch_init_rest(c->d_v[0], c->d_S, c->pitch, c->d_last, b.d_list, b.first, b.count, d_rest,
+                                state_count(b.kind), c->stride, c->stream));
+      ++c->launches;
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      dev_free(d_rest);
+    }
   });
 }
 

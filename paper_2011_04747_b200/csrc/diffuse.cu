@@ -57,6 +57,54 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
 }
 
 // ---------------------------------------------------------------------------
+// Structured 3D slab (EXTENSION): 27-point rows whose coefficients depend only
+// on the node class (x face, y face, z layer); ascending-column order is
+// (dy, dz, dx) lexicographic for the y-outer numbering. 16 B of node traffic
+// per sub-step (V in/out) plus cached neighbour reads; bit-identical to the
+// oracle's CSR assembly of the same operator.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) diffuse_struct3d(DiffArgs a, Struct3D s) {
+  const long long nown = s.planes * s.plane;
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  const long long nx = s.nx1 - 1, nz = s.nz1 - 1;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long i = o + s.plane;  // one halo plane below
+    const double vi = a.vin[i];
+    if (skip) {
+      a.vout[i] = vi;
+      continue;
+    }
+    const long long yl = o / s.plane, rem = o - yl * s.plane;
+    const long long iz = rem / s.nx1, ix = rem - iz * s.nx1;
+    const long long gy = s.row_begin + yl;
+    const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
+    const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
+    const long long cls = (by * 3 + bx) * s.nz1 + iz;
+    const double* cf = s.coef + cls * 27;
+    double acc = 0.0;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+#pragma unroll
+      for (int dz = -1; dz <= 1; ++dz) {
+        if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+          if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
+          acc += __ldg(cf + (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)) * a.vin[i + dy * s.plane + dz * s.nx1 + dx];
+        }
+      }
+    }
+    const double out = vi - __ldg(s.cm + cls) * acc;
+    a.vout[i] = out;
+    if (!isfinite(out))
+      record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.plane) << 22, seq, 2);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Generic CSR (fem.cpp:201-206), one thread per row, ascending columns.
 // cols are local indices into vin; row i (owned) lives at vin[halo + i].
 // ---------------------------------------------------------------------------
@@ -174,6 +222,18 @@ __global__ void soa_to_aos(const double* soa, long long pitch, long long src0, i
   for (int q = ns; q < stride; ++q) aos[i * stride + q] = 0.0;
 }
 
+// make_initial_state on the device (splitting.cpp:183-217 with rest states):
+// V, all stride state slots (0 beyond the model's count) and last_dvdt = 0.
+__global__ void init_rest(double* v, double* S, long long pitch, double* last, const int32_t* list, long long first,
+                          long long count, const double* rest, int ns, int stride) {
+  const long long p = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (p >= count) return;
+  const long long i = list ? static_cast<long long>(list[p]) : first + p;
+  v[i] = rest[0];
+  last[i] = 0.0;
+  for (int q = 0; q < stride; ++q) S[q * pitch + i] = q < ns ? rest[q + 1] : 0.0;
+}
+
 // standalone diffusion_substep for cwg_diffusion_substep (no halo, no error record)
 __global__ void diffuse_csr_plain(long long n, const long long* rp, const long long* col, const double* val,
                                   const double* mass, const double* v, double dt_sub, double* out) {
@@ -217,6 +277,11 @@ static inline int blocks_for(long long n, int t, int cap) {
 
 cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st) {
   diffuse_stencil2d<<<blocks_for(s.rows * s.w, 256, max_blocks), 256, 0, st>>>(a, s);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int max_blocks, cudaStream_t st) {
+  diffuse_struct3d<<<blocks_for(s.planes * s.plane, 256, max_blocks), 256, 0, st>>>(a, s);
   return cudaGetLastError();
 }
 
@@ -278,6 +343,14 @@ cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const lon
 
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t st) {
   fp64_peak<<<blocks, 256, 0, st>>>(out, iters, 0.999999, 1e-7);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_rest(double* v, double* S, long long pitch, double* last, const int32_t* list,
+                              long long first, long long count, const double* rest, int ns, int stride,
+                              cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  init_rest<<<blocks_for(count, 256, 1 << 30), 256, 0, st>>>(v, S, pitch, last, list, first, count, rest, ns, stride);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,7 @@ cudaError_t launch_rates_ord(int kind, long long n, const double* v, const doubl
                              double* ds, cudaStream_t st);
 
 cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st);
+cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int max_blocks, cudaStream_t st);
 cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st);
 cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st);
 cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,
@@ -35,6 +36,9 @@ cudaError_t launch_diffuse_csr_plain(long long n, const long long* rp, const lon
                                      const double* mass, const double* v, double dt_sub, double* out,
                                      cudaStream_t st);
 cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t st);
+cudaError_t launch_init_rest(double* v, double* S, long long pitch, double* last, const int32_t* list,
+                              long long first, long long count, const double* rest, int ns, int stride,
+                              cudaStream_t st);
 cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st);
 
 }  // namespace cwg

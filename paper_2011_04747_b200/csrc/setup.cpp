@@ -7,6 +7,7 @@
 // order and the triplets go through the same std::sort, so the CSR is
 // bit-identical to cardwave::assemble (tests/test_setup_parity.py).
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -321,3 +322,103 @@ int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y) {
 }
 
 }  // extern "C"
+
+// ===================================================================== 3D slab
+namespace {
+
+// Trilinear hexahedron on the cube [0,h]^3 with a constant 3x3 tensor D:
+// 2x2x2 Gauss, local node a = dx + 2*dy + 4*dz (dx, dy, dz in {0, 1}).
+// Same evaluation order as oracle/cw_oracle.c:hex_integrals (bit-identical).
+void hex_integrals(double h, const double D[3][3], double k[8][8], double m[8]) {
+  constexpr double g = 0.57735026918962576;
+  const double gp[2] = {-g, g};
+  for (int a = 0; a < 8; ++a) {
+    m[a] = 0.0;
+    for (int b = 0; b < 8; ++b) k[a][b] = 0.0;
+  }
+  const double det = h * h * h / 8.0;
+  const double sc = 2.0 / h;
+  for (int q = 0; q < 8; ++q) {
+    const double xi = gp[q & 1], eta = gp[(q >> 1) & 1], zeta = gp[q >> 2];
+    double n[8], gx[8], gy[8], gz[8];
+    for (int a = 0; a < 8; ++a) {
+      const double sx = (a & 1) ? 1.0 : -1.0, sy = (a & 2) ? 1.0 : -1.0, sz = (a & 4) ? 1.0 : -1.0;
+      const double fx = 1.0 + sx * xi, fy = 1.0 + sy * eta, fz = 1.0 + sz * zeta;
+      n[a] = 0.125 * fx * fy * fz;
+      gx[a] = sc * (0.125 * sx * fy * fz);
+      gy[a] = sc * (0.125 * fx * sy * fz);
+      gz[a] = sc * (0.125 * fx * fy * sz);
+    }
+    for (int a = 0; a < 8; ++a) {
+      const double dgx = D[0][0] * gx[a] + D[0][1] * gy[a] + D[0][2] * gz[a];
+      const double dgy = D[1][0] * gx[a] + D[1][1] * gy[a] + D[1][2] * gz[a];
+      const double dgz = D[2][0] * gx[a] + D[2][1] * gy[a] + D[2][2] * gz[a];
+      for (int b = 0; b < 8; ++b) k[a][b] += det * (dgx * gx[b] + dgy * gy[b] + dgz * gz[b]);
+      m[a] += det * n[a];
+    }
+  }
+}
+
+// D = d_l f f^T + d_t (I - f f^T), f = (cos th, sin th, 0)
+void layer_tensor(double dl, double rho, double th, double D[3][3]) {
+  const double f[3] = {std::cos(th), std::sin(th), 0.0};
+  const double dt = rho * dl;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const double ff = f[i] * f[j];
+      D[i][j] = dl * ff + dt * ((i == j ? 1.0 : 0.0) - ff);
+    }
+}
+
+}  // namespace
+
+extern "C" double cwg_struct3d_tables(const cwg_struct3d* s, double* coef, double* mass) {
+  if (!s || s->nx < 1 || s->ny < 1 || s->nz < 1 || !(s->h > 0.0) || !(s->d_long > 0.0) || !(s->rho > 0.0) ||
+      !s->fiber_angle_of_layer)
+    return -1.0;
+  const int64_t nz = s->nz, nz1 = nz + 1;
+  std::vector<std::array<std::array<double, 8>, 8>> K(static_cast<size_t>(nz));
+  std::vector<std::array<double, 8>> M(static_cast<size_t>(nz));
+  for (int64_t ez = 0; ez < nz; ++ez) {
+    double D[3][3], k[8][8], m[8];
+    layer_tensor(s->d_long, s->rho, s->fiber_angle_of_layer[ez], D);
+    hex_integrals(s->h, D, k, m);
+    for (int a = 0; a < 8; ++a) {
+      M[ez][a] = m[a];
+      for (int b = 0; b < 8; ++b) K[ez][a][b] = k[a][b];
+    }
+  }
+  double min_ratio = std::numeric_limits<double>::infinity();
+  for (int by = 0; by < 3; ++by)
+    for (int bx = 0; bx < 3; ++bx)
+      for (int64_t iz = 0; iz < nz1; ++iz) {
+        const int64_t c = (by * 3 + bx) * nz1 + iz;
+        double* cf = coef + c * 27;
+        for (int q = 0; q < 27; ++q) cf[q] = 0.0;
+        double ms = 0.0;
+        // representative node of the class: ix/iy = 0 (low), 1 (interior), n (high)
+        const int64_t ix = bx == 0 ? 0 : (bx == 1 ? 1 : s->nx), iy = by == 0 ? 0 : (by == 1 ? 1 : s->ny);
+        if ((bx == 1 && s->nx < 2) || (by == 1 && s->ny < 2)) continue;  // class does not occur
+        // adjacent elements in ascending element index (ey, ez, ex)
+        for (int64_t ey = iy - 1; ey <= iy; ++ey) {
+          if (ey < 0 || ey >= s->ny) continue;
+          for (int64_t ez = iz - 1; ez <= iz; ++ez) {
+            if (ez < 0 || ez >= nz) continue;
+            for (int64_t ex = ix - 1; ex <= ix; ++ex) {
+              if (ex < 0 || ex >= s->nx) continue;
+              const int a = static_cast<int>((ix - ex) + 2 * (iy - ey) + 4 * (iz - ez));
+              ms += M[ez][a];
+              for (int b = 0; b < 8; ++b) {
+                const int64_t dx = ex + (b & 1) - ix, dy = ey + ((b >> 1) & 1) - iy, dz = ez + ((b >> 2) & 1) - iz;
+                cf[(dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)] += K[ez][a][b];
+              }
+            }
+          }
+        }
+        mass[c] = ms;
+        double den = 0.0;
+        for (int q = 0; q < 27; ++q) den += q == 13 ? cf[q] : std::abs(cf[q]);
+        if (den > 0.0) min_ratio = std::min(min_ratio, ms / den);
+      }
+  return std::isfinite(min_ratio) ? 0.9 * min_ratio : -1.0;
+}

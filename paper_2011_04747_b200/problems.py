@@ -107,3 +107,31 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
     return Problem("C3", sh, ["ohara2011-epi", "passive"], model_of_node,
                    [(s1, 0.0, 1.0, amplitude, None), (s2, 300.0, 1.0, amplitude, None)], cfg, probes, gkr,
                    notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)")
+
+
+def slab(lx, ly, lz, h, model="ohara2011-epi", t_end=10.0, k0_down=3, amplitude=150.0, stim="face", seed=2011,
+         n_sites=16, site_radius=0.1, d_long=0.0012, rho=0.25) -> Problem:
+    """3D slab (EXTENSION; oracle-pinned). Fibres rotate +60 -> -60 deg from endocardium (z = 0) to
+    epicardium, D_l:D_t = 4:1 (rho 0.25), D_l = 0.0012 cm^2/ms (as C2). Stimulus on z = 0: the whole
+    face ("face", config 4) or n_sites seeded random discs ("sites", config 5; numpy PCG64(seed))."""
+    sl = api.Slab3D(lx, ly, lz, h, d_long=d_long, rho=rho)
+    if stim == "face":
+        nodes = sl.face_z0()
+    else:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        centers = list(zip(rng.uniform(0.0, lx, n_sites), rng.uniform(0.0, ly, n_sites)))
+        nodes = sl.discs_z0(centers, site_radius)
+    cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
+    probes = [sl.nearest(lx / 2, ly / 2, 0.0), sl.nearest(lx / 2, ly / 2, lz), sl.nearest(lx, ly, lz / 2)]
+    return Problem(f"slab{sl.nx1}x{sl.ny1}x{sl.nz1}", sl, [model], np.zeros(sl.n, np.uint8),
+                   [(nodes, 0.0, 1.0, amplitude, None)], cfg, probes, notes="extension: 3D slab")
+
+
+def c4(t_end=500.0, **kw) -> Problem:
+    """BASELINE configs[3]: 5x5x1 cm, h = 0.02 (251x251x51 = 3.2M nodes), endocardial face stimulus."""
+    return slab(5.0, 5.0, 1.0, 0.02, t_end=t_end, **kw)
+
+
+def c5(t_end=5.0, **kw) -> Problem:
+    """BASELINE configs[4]: 10x10x2 cm, h = 0.01 (1001x1001x201 = 201M nodes), 16 random endocardial sites."""
+    return slab(10.0, 10.0, 2.0, 0.01, t_end=t_end, stim="sites", **kw)

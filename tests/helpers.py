@@ -4,6 +4,10 @@ import numpy as np
 
 def csr_of(problem):
     op = problem.sheet.op
+    if hasattr(op, "s3d"):  # 3D slab: the oracle's own CSR assembly of the same operator
+        import orapy
+        csr, _ = orapy.assemble_slab3d(op.nx, op.ny, op.nz, op.h, op.d_long, op.rho, op.angles)
+        return csr
     return (op.row_ptr, op.col, op.val, op.lumped_mass)
 
 

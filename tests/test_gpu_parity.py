@@ -240,3 +240,18 @@ def test_launches_counted(cw, problems):
     integ.run_steps(0, integ.info.n_steps)
     integ.run_sync()
     assert integ.launch_count() > integ.info.n_steps
+
+
+# ----------------------------------------------------------------------------- 3D slabs (extension)
+def test_slab3d_aliev_panfilov_bitwise(cw, ora, problems):
+    """Structured 27-point operator + reaction vs the oracle's independent CSR assembly: bit-exact."""
+    p = problems.slab(0.4, 0.3, 0.2, 0.02, model="aliev-panfilov", t_end=20.0, amplitude=100.0)
+    res = gpu_run(p)
+    o = oracle_run(p)
+    _compare_exact(res, o)
+
+
+def test_slab3d_ord_sites_tolerance(cw, ora, problems):
+    p = problems.slab(0.6, 0.4, 0.2, 0.02, t_end=8.0, stim="sites", n_sites=3, site_radius=0.1, amplitude=150.0)
+    res, o = run_both(p)
+    _compare_tol(res, o, p.sheet.nx1, p.probes)

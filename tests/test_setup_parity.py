@@ -72,3 +72,34 @@ def test_scar_extension_gershgorin_skips_zero_rows():
     assert np.all(np.isfinite(s.op.val))
     with pytest.raises(cw.ValidationError):
         cw.Sheet(1.0, 1.0, 0.05, 0.0, elem_scale=np.zeros(ne))
+
+
+def test_slab3d_tables_match_oracle_csr(ora):
+    """3D extension: per-class device tables == the oracle's CSR assembly, bit for bit (incl. dt_s)."""
+    import numpy as np
+    sl = cw.Slab3D(0.14, 0.1, 0.08, 0.02)
+    (rp, col, val, mass), dts = ora.assemble_slab3d(sl.nx, sl.ny, sl.nz, sl.h, sl.d_long, sl.rho, sl.angles)
+    assert dts == sl.dt_s
+    for iy in range(sl.ny1):
+        for iz in range(sl.nz1):
+            for ix in range(sl.nx1):
+                i = int(sl.index(ix, iy, iz))
+                bx = 0 if ix == 0 else (2 if ix == sl.nx else 1)
+                by = 0 if iy == 0 else (2 if iy == sl.ny else 1)
+                c = (by * 3 + bx) * sl.nz1 + iz
+                assert mass[i] == sl.mass[c]
+                present = np.zeros(27, bool)
+                for p in range(rp[i], rp[i + 1]):
+                    d = int(col[p] - i)
+                    dy = int(round(d / sl.plane))
+                    r = d - dy * sl.plane
+                    dz = int(round(r / sl.nx1))
+                    dx = r - dz * sl.nx1
+                    q = (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)
+                    present[q] = True
+                    assert val[p] == sl.coef[c * 27 + q]
+                assert np.all(sl.coef[c * 27:(c + 1) * 27][~present] == 0.0)
+    # operator sanity: symmetric, zero row sums, lumped mass = volume
+    assert abs(mass.sum() - 0.14 * 0.1 * 0.08) < 1e-15
+    rs = np.add.reduceat(val, rp[:-1])
+    assert np.abs(rs).max() < 1e-18
