@@ -205,6 +205,27 @@ int64_t cwg_reaction_evals(cwg_ctx* ctx);
  * CUDA-event timed. Returns TFLOP/s (2 flops per DFMA) or < 0 on error. */
 double cwg_fp64_peak_tflops(int device, double seconds);
 
+/* ThresholdOptions (stimulus.hpp:60-67) */
+typedef struct {
+  double duration_ms;    /* 1.0 */
+  double upper_factor;   /* 1000.0 */
+  double initial_guess;  /* 1.0 mV/ms */
+  double rel_tol;        /* 0.05 */
+  double window_ms;      /* 50.0 */
+  double dt_ms;          /* 0.05 */
+} cwg_threshold_options;
+
+/* diastolic_threshold (stimulus.cpp:115-157) on the device: bisection over
+ * the amplitude of a single-shot stimulus on stim_nodes, each probe a fixed-
+ * step monodomain run from rest (reaction with k = 1 at dt = min(opt.dt,
+ * dt0/2, dt_s), then one diffusion sub-step of dt) that propagates when V at
+ * the node farthest from the stimulus (>= 1 cm) exceeds 0 mV within the
+ * window. prob supplies the 2D operator, ONE model and the device; its scheme
+ * and stimulus fields are ignored. coords_xy: [n][2] node coordinates. */
+int cwg_diastolic_threshold(const cwg_problem* prob, const double* coords_xy, const int64_t* stim_nodes,
+                            int64_t n_stim, const cwg_threshold_options* opt, double* threshold,
+                            int64_t* probe_node, cwg_error* err);
+
 /* diffusion_substep (fem.cpp:194-207): standalone out = v - dt/m * K v on the
  * device, host in/out, bit-identical to the reference. */
 int cwg_diffusion_substep(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,

@@ -46,6 +46,11 @@ class cwg_problem(C.Structure):
     ]
 
 
+class cwg_threshold_options(C.Structure):
+    _fields_ = [("duration_ms", C.c_double), ("upper_factor", C.c_double), ("initial_guess", C.c_double),
+                ("rel_tol", C.c_double), ("window_ms", C.c_double), ("dt_ms", C.c_double)]
+
+
 class cwg_info(C.Structure):
     _fields_ = [("dt_effective", C.c_double), ("dt_s", C.c_double), ("dt_ad", C.c_double), ("l", C.c_int),
                 ("k_max_global", C.c_int), ("n_steps", C.c_int64), ("steps_per_record", C.c_int64),
@@ -79,6 +84,8 @@ _SIGS = {
     "cwg_bench_steps": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, _dp, _dp, _dp]),
     "cwg_reaction_evals": (C.c_int64, [C.c_void_p]),
     "cwg_fp64_peak_tflops": (C.c_double, [C.c_int, C.c_double]),
+    "cwg_diastolic_threshold": (C.c_int, [C.POINTER(cwg_problem), _dp, _lp, C.c_int64,
+                                          C.POINTER(cwg_threshold_options), _dp, _lp, C.POINTER(cwg_error)]),
     "cwg_diffusion_substep": (C.c_int, [C.c_int64, _lp, _lp, _dp, _dp, _dp, C.c_double, _dp, C.c_int,
                                         C.POINTER(cwg_error)]),
     "cwg_rates": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(cwg_error)]),

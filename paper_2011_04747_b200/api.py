@@ -687,3 +687,41 @@ def slab_plan(ny1: int, world: int, rank: int):
     if L.lib().cwg_slab_plan(ny1, world, rank, C.byref(b), C.byref(e)):
         raise ValidationError("placement: fewer rows than ranks")
     return b.value, e.value
+
+
+@dataclass
+class ThresholdOptions:
+    """stimulus.hpp:60-67"""
+    duration_ms: float = 1.0
+    upper_factor: float = 1000.0
+    initial_guess: float = 1.0
+    rel_tol: float = 0.05
+    window_ms: float = 50.0
+    dt_ms: float = 0.05
+
+
+def diastolic_threshold(sheet: Sheet, model: CellModel, stim_nodes, options: ThresholdOptions = None, device=0,
+                        return_probe=False):
+    """diastolic_threshold (stimulus.cpp:115-157) with every probe run on the GPU."""
+    o = options or ThresholdOptions()
+    op = sheet.op
+    p = L.cwg_problem()
+    keep = [np.ascontiguousarray(op.row_ptr, np.int64), np.ascontiguousarray(op.col, np.int64),
+            np.ascontiguousarray(op.val, np.float64), np.ascontiguousarray(op.lumped_mass, np.float64)]
+    p.n = op.rows()
+    p.row_ptr, p.col, p.val, p.lumped_mass = L.lp(keep[0]), L.lp(keep[1]), L.dp(keep[2]), L.dp(keep[3])
+    p.dt_s = op.dt_s
+    p.op_kind = L.OP_AUTO
+    p.grid_nx1, p.grid_ny1 = op.grid_nx1, op.grid_ny1
+    kinds = np.array([model.kind], np.int32)
+    mon = np.zeros(p.n, np.uint8)
+    p.n_models, p.model_kind, p.model_of_node = 1, kinds.ctypes.data_as(L._ip), mon.ctypes.data_as(L._u8p)
+    p.scheme, p.dt_ms, p.t_end_ms, p.k0_up, p.k0_down, p.record_interval_ms = 0, 0.1, 0.1, 1, 1, 1.0
+    p.device, p.world = device, 1
+    xy = np.ascontiguousarray(sheet.coords, np.float64)
+    sn = np.ascontiguousarray(stim_nodes, np.int64)
+    opt = L.cwg_threshold_options(o.duration_ms, o.upper_factor, o.initial_guess, o.rel_tol, o.window_ms, o.dt_ms)
+    thr, probe, err = C.c_double(), C.c_int64(-1), L.cwg_error()
+    _check(L.lib().cwg_diastolic_threshold(C.byref(p), L.dp(xy), L.lp(sn), len(sn), C.byref(opt), C.byref(thr),
+                                            C.byref(probe), C.byref(err)), err)
+    return (thr.value, probe.value) if return_probe else thr.value

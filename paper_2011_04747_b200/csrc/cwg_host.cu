@@ -217,6 +217,7 @@ struct cwg_ctx {
   long long s3_nx1 = 0, s3_nz1 = 0;  // struct3d
   double* d_coef = nullptr;  // stencil: [9][n_own]; struct3d: [classes][27]
   double* d_cm = nullptr;    // dt_ad / m_i
+  double* d_mass = nullptr;  // lumped mass of the owned rows (2D)
   long long* d_rp = nullptr;
   long long* d_col = nullptr;
   double* d_val = nullptr;
@@ -258,6 +259,13 @@ struct cwg_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   double t_react = 0, t_diff = 0, t_rec = 0;
 
+  // fixed-step mode (diastolic_threshold probe runs, stimulus.cpp:76-111):
+  // reaction (k = 1) then ONE diffusion sub-step of dt, no NaN check after diffusion
+  bool fixed_step = false;
+  ErrRec* d_err_dummy = nullptr;
+  long long* d_cross = nullptr;
+  long long probe_local = -1;
+
   // bench
   void* d_flush = nullptr;
   size_t flush_bytes = 0;
@@ -285,6 +293,7 @@ void ctx_free(cwg_ctx* c) {
   dev_free(c->d_gkr);
   dev_free(c->d_coef);
   dev_free(c->d_cm);
+  dev_free(c->d_mass);
   dev_free(c->d_rp);
   dev_free(c->d_col);
   dev_free(c->d_val);
@@ -300,6 +309,8 @@ void ctx_free(cwg_ctx* c) {
   dev_free(c->d_probe_loc);
   dev_free(c->d_traces);
   dev_free(c->d_stage);
+  dev_free(c->d_err_dummy);
+  dev_free(c->d_cross);
   if (c->d_flush) cudaFree(c->d_flush);
   double** dd[] = {&c->det.prev_v, &c->det.v_rest, &c->det.max_slope, &c->det.t_max_slope, &c->det.v_peak,
                    &c->det.lat, &c->det.apd};
@@ -351,7 +362,7 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     a.n = c->n_own;
     a.halo = c->halo;
     a.dt_sub = c->dt_ad;
-    a.err = c->d_err;
+    a.err = c->fixed_step ? c->d_err_dummy : c->d_err;
     a.clock = c->d_clock;
     a.step_off = step_off;
     a.evs = c->evs;
@@ -772,11 +783,10 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   } else {
     validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
     std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
-    double* d_mass = upload(mass_own.data(), mass_own.size());
+    c->d_mass = upload(mass_own.data(), mass_own.size());
     c->d_cm = dev_alloc<double>(c->n_own);
-    CUDA_TRY(launch_mass_factor(d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
+    CUDA_TRY(launch_mass_factor(c->d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    dev_free(d_mass);
   }
   if (kind == CWG_OP_STRUCT3D) {
     // tables uploaded above
@@ -993,6 +1003,14 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
   }
   if (out) std::snprintf(out->msg, sizeof(out->msg), "%s", buf);
   return true;
+}
+
+// recompute cm = dt_ad / m after dt_ad changed (fixed-step mode)
+cudaError_t launch_mass_factor_fix(cwg_ctx* c) {
+  if (!c->d_mass) return cudaErrorNotSupported;
+  const cudaError_t e = launch_mass_factor(c->d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(c->stream);
 }
 
 void normalise_parity(cwg_ctx* c) {
@@ -1500,6 +1518,178 @@ double cwg_fp64_peak_tflops(int device, double seconds) {
     result = best;
   });
   return result;
+}
+
+// ---------------------------------------------------------------- diastolic_threshold
+namespace {
+
+// One fixed-step probe run (stimulus.cpp:76-111) at `amp`; true when V[probe] > 0
+// within the window. Chunks of G steps are replayed as a CUDA graph; the host
+// checks the device crossing flag and the error record between chunks.
+bool propagates(cwg_ctx* c, double amp, long long steps, cudaGraphExec_t& graph, long long G) {
+  CUDA_TRY(cudaMemcpyAsync(c->d_samp, &amp, sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  c->cur = 0;
+  for (const auto& b : c->bins) {
+    double rest[64] = {0};
+    cwg_model_rest_state(b.kind, rest);
+    double* d_rest = upload(rest, 64);
+    CUDA_TRY(launch_init_rest(c->d_v[0], c->d_S, c->pitch, c->d_last, b.d_list, b.first, b.count, d_rest,
+                              state_count(b.kind), c->stride, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    dev_free(d_rest);
+  }
+  ErrRec none{kNoError, -1, 0, 0};
+  CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
+  const long long never = 0x7fffffffffffffffll;
+  CUDA_TRY(cudaMemcpyAsync(c->d_cross, &never, sizeof(never), cudaMemcpyHostToDevice, c->stream));
+  auto enqueue = [&](long long off) {
+    enqueue_reaction(c, off, 0, false, 0.0);
+    enqueue_diffusion(c, 1, off, 1);
+    CUDA_TRY(launch_probe_cross(c->d_v[c->cur], c->probe_local, c->d_cross, c->d_clock, off, c->stream));
+  };
+  if (!graph) {  // capture G steps + clock tick (parity of V buffers: G even)
+    cudaGraph_t g = nullptr;
+    const int cur0 = c->cur;
+    CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (long long off = 0; off < G; ++off) enqueue(off);
+    CUDA_TRY(launch_tick_clock(c->d_clock, G, c->stream));
+    CUDA_TRY(cudaStreamEndCapture(c->stream, &g));
+    CUDA_TRY(cudaGraphInstantiate(&graph, g, 0));
+    cudaGraphDestroy(g);
+    if (c->cur != cur0) throw Fail{CWG_ECUDA, "threshold graph must preserve the V buffer parity"};
+  }
+  CUDA_TRY(launch_set_clock(c->d_clock, 0, c->stream));
+  for (long long s = 0; s < steps;) {
+    if (s + G <= steps) {
+      CUDA_TRY(cudaGraphLaunch(graph, c->stream));
+      c->launches += G * (static_cast<long long>(c->bins.size()) + 2) + 1;
+      s += G;
+    } else {  // tail steps, launched directly on a correctly set clock
+      CUDA_TRY(launch_set_clock(c->d_clock, s, c->stream));
+      enqueue(0);
+      s += 1;
+    }
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    long long cross = never;
+    CUDA_TRY(cudaMemcpy(&cross, c->d_cross, sizeof(cross), cudaMemcpyDeviceToHost));
+    ErrRec r{};
+    CUDA_TRY(cudaMemcpy(&r, c->d_err, sizeof(r), cudaMemcpyDeviceToHost));
+    const long long err_step = r.key == kNoError ? never : r.seq / c->evs;
+    if (err_step != never && err_step <= cross) {  // the reaction of that step throws first
+      const long long node = static_cast<long long>(r.key >> 22);
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "threshold probe run diverged (node %lld, t = %f ms)", node,
+                    static_cast<double>(err_step) * c->dt);
+      throw Fail{CWG_EINSTABILITY, buf};
+    }
+    if (cross != never && cross < steps) return true;
+  }
+  return false;
+}
+
+}  // namespace
+
+extern "C" int cwg_diastolic_threshold(const cwg_problem* prob, const double* coords_xy, const int64_t* stim_nodes,
+                                       int64_t n_stim, const cwg_threshold_options* opt, double* threshold,
+                                       int64_t* probe_out, cwg_error* err) {
+  cwg_ctx* c = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  long long fail_node = -1;
+  double fail_t = 0.0;
+  const int rc = guarded(err, [&] {
+    validation(prob && coords_xy && stim_nodes && opt, "threshold: missing arguments");
+    validation(n_stim > 0, "threshold: stimulus node set is empty");
+    validation(prob->world <= 1, "threshold: single device only");
+    validation(prob->n_models == 1, "threshold: one cell model");
+    const long long n = prob->n;
+    std::vector<long long> sn(stim_nodes, stim_nodes + n_stim);
+    std::sort(sn.begin(), sn.end());
+    sn.erase(std::unique(sn.begin(), sn.end()), sn.end());
+    for (long long i : sn) validation(i >= 0 && i < n, "threshold: stimulus node out of range");
+    // probe: the node farthest from the stimulus region, required >= 1 cm away (stimulus.cpp:120-134)
+    long long probe = -1;
+    double best = -1.0;
+    for (long long i = 0; i < n; ++i) {
+      double dmin = std::numeric_limits<double>::infinity();
+      for (long long q : sn) {
+        const double dx = coords_xy[2 * i] - coords_xy[2 * q];
+        const double dy = coords_xy[2 * i + 1] - coords_xy[2 * q + 1];
+        dmin = std::min(dmin, std::hypot(dx, dy));
+      }
+      if (dmin > best) {
+        best = dmin;
+        probe = i;
+      }
+    }
+    if (best < 1.0) throw Fail{CWG_EVALIDATION, "threshold: no probe node >= 1 cm from the stimulus region"};
+    if (probe_out) *probe_out = probe;
+    // fixed-step problem: dt = min(opt.dt, dt0/2, dt_s) (stimulus.cpp:90)
+    const double dt = std::min({opt->dt_ms, stable_step(prob->model_kind[0]) / 2.0, prob->dt_s});
+    const long long steps = static_cast<long long>(std::ceil(opt->window_ms / dt));
+    cwg_problem p = *prob;
+    std::vector<int32_t> ptr(static_cast<size_t>(n + 1), 0), ids(sn.size(), 0);
+    for (long long i : sn) ptr[static_cast<size_t>(i + 1)] = 1;
+    for (long long i = 0; i < n; ++i) ptr[static_cast<size_t>(i + 1)] += ptr[static_cast<size_t>(i)];
+    const double t0 = 0.0, dur = opt->duration_ms, amp0 = 0.0, per = std::nan("");
+    p.n_stim = 1;
+    p.stim_t_start = &t0;
+    p.stim_duration = &dur;
+    p.stim_amplitude = &amp0;
+    p.stim_period = &per;
+    p.stim_node_ptr = ptr.data();
+    p.stim_ids = ids.data();
+    p.n_probes = 0;
+    p.scheme = CWG_OST;
+    p.dt_ms = dt;
+    p.t_end_ms = static_cast<double>(steps) * dt;
+    p.k0_up = 1;
+    p.k0_down = 1;
+    p.strict_substeps = 0;
+    p.record_interval_ms = p.t_end_ms;
+    p.map_interval_ms = p.t_end_ms;
+    p.gkr_scale = nullptr;
+    c = new cwg_ctx();
+    create_impl(&p, c);
+    c->fixed_step = true;
+    c->dt_ad = dt;  // one diffusion sub-step of the full dt (stimulus.cpp:106)
+    c->evs = 2;     // ev 0 reaction, ev 1 diffusion
+    CUDA_TRY(launch_mass_factor_fix(c));
+    c->d_err_dummy = dev_alloc<ErrRec>(1);
+    c->d_cross = dev_alloc<long long>(1);
+    c->probe_local = probe - c->node_offset;
+    // bisection (stimulus.cpp:136-156)
+    const long long G = 64;
+    const double cap = opt->upper_factor * opt->initial_guess;
+    double lo = 0.0, hi = opt->initial_guess;
+    while (!propagates(c, hi, steps, graph, G)) {
+      lo = hi;
+      hi *= 2.0;
+      if (hi > cap) throw Fail{CWG_EVALIDATION, "threshold: no propagation at upper bracket " + std::to_string(cap)};
+    }
+    while ((hi - lo) / hi > opt->rel_tol) {
+      const double mid = 0.5 * (lo + hi);
+      if (propagates(c, mid, steps, graph, G))
+        hi = mid;
+      else
+        lo = mid;
+    }
+    *threshold = hi;
+  });
+  if (rc == CWG_EINSTABILITY && err) {
+    // message carries node and time; parse them back for the structured fields
+    long long node = -1;
+    double t = 0.0;
+    if (std::sscanf(err->msg, "threshold probe run diverged (node %lld, t = %lf", &node, &t) == 2) {
+      fail_node = node;
+      fail_t = t;
+    }
+    err->node = fail_node;
+    err->t_ms = fail_t;
+    err->phase = 1;
+  }
+  if (graph) cudaGraphExecDestroy(graph);
+  ctx_free(c);
+  return rc;
 }
 
 int cwg_diffusion_substep(int64_t n, const int64_t* rp, const int64_t* col, const double* val, const double* mass,

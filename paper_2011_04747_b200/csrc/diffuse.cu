@@ -63,44 +63,84 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
 // per sub-step (V in/out) plus cached neighbour reads; bit-identical to the
 // oracle's CSR assembly of the same operator.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) diffuse_struct3d(DiffArgs a, Struct3D s) {
-  const long long nown = s.planes * s.plane;
+// 2.5D blocking: a block owns a TX x TZ tile of the (x, z) plane and marches
+// over a chunk of y-planes, keeping planes y-1, y, y+1 (tile + 1-node halo) in
+// a shared-memory ring, so each V value is fetched from global memory ~1.3x
+// per sub-step instead of up to 27x. No 64-bit division: (x, z, y) come from
+// the launch geometry.
+constexpr int S3_TX = 32, S3_TZ = 8, S3_YCHUNK = 16;
+
+__global__ void __launch_bounds__(S3_TX * S3_TZ) diffuse_struct3d(DiffArgs a, Struct3D s) {
+  constexpr int PX = S3_TX + 2, PZ = S3_TZ + 2, PL = PX * PZ;
+  __shared__ double ring[3][PL];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
+  const int tx = threadIdx.x % S3_TX, tz = threadIdx.x / S3_TX;
+  const long long x0 = static_cast<long long>(blockIdx.x) * S3_TX, z0 = static_cast<long long>(blockIdx.y) * S3_TZ;
+  const long long ix = x0 + tx, iz = z0 + tz;
   const long long nx = s.nx1 - 1, nz = s.nz1 - 1;
-  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown;
-       o += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = o + s.plane;  // one halo plane below
-    const double vi = a.vin[i];
-    if (skip) {
-      a.vout[i] = vi;
-      continue;
+  const long long yb = static_cast<long long>(blockIdx.z) * S3_YCHUNK;
+  const long long ye = yb + S3_YCHUNK < s.planes ? yb + S3_YCHUNK : s.planes;
+  const bool inside = ix < s.nx1 && iz < s.nz1;
+  // load local plane yl (-1..planes) into ring slot (halo planes are valid memory)
+  auto load = [&](long long yl, int slot) {
+    const long long base = (yl + 1) * s.plane;  // local index of (0, yl, 0)
+    for (int t = threadIdx.x; t < PL; t += S3_TX * S3_TZ) {
+      const long long lx = x0 - 1 + t % PX, lz = z0 - 1 + t / PX;
+      double val = 0.0;
+      if (lx >= 0 && lx < s.nx1 && lz >= 0 && lz < s.nz1) val = a.vin[base + lz * s.nx1 + lx];
+      ring[slot][t] = val;
     }
-    const long long yl = o / s.plane, rem = o - yl * s.plane;
-    const long long iz = rem / s.nx1, ix = rem - iz * s.nx1;
-    const long long gy = s.row_begin + yl;
-    const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
-    const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
-    const long long cls = (by * 3 + bx) * s.nz1 + iz;
-    const double* cf = s.coef + cls * 27;
-    double acc = 0.0;
+  };
+  const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
+  double creg[27];
+  double cm_in = 0.0;
+  if (inside) {  // class of this (x, z) column on interior y-planes (by = 1)
+    const long long cin = (3 + bx) * s.nz1 + iz;
 #pragma unroll
-    for (int dy = -1; dy <= 1; ++dy) {
-      if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+    for (int q = 0; q < 27; ++q) creg[q] = __ldg(s.coef + cin * 27 + q);
+    cm_in = __ldg(s.cm + cin);
+  }
+  load(yb - 1, (yb + 2) % 3);
+  load(yb, yb % 3);
+  for (long long yl = yb; yl < ye; ++yl) {
+    load(yl + 1, (yl + 1) % 3);
+    __syncthreads();
+    if (inside) {
+      const long long i = (yl + 1) * s.plane + iz * s.nx1 + ix;
+      const double* pc = ring[yl % 3];
+      const int c0 = (tz + 1) * PX + (tx + 1);
+      const double vi = pc[c0];
+      if (skip) {
+        a.vout[i] = vi;
+      } else {
+        const long long gy = s.row_begin + yl;
+        const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
+        // interior planes use the register copy of this thread's 27 coefficients
+        const double* cf = s.coef + ((by * 3 + bx) * s.nz1 + iz) * 27;
+        double acc = 0.0;
 #pragma unroll
-      for (int dz = -1; dz <= 1; ++dz) {
-        if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+          const double* pl = ring[(yl + 3 + dy) % 3];
 #pragma unroll
-        for (int dx = -1; dx <= 1; ++dx) {
-          if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
-          acc += __ldg(cf + (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)) * a.vin[i + dy * s.plane + dz * s.nx1 + dx];
+          for (int dz = -1; dz <= 1; ++dz) {
+            if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+#pragma unroll
+            for (int dx = -1; dx <= 1; ++dx) {
+              if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
+              const int q = (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1);
+              acc += (by == 1 ? creg[q] : __ldg(cf + q)) * pl[c0 + dz * PX + dx];
+            }
+          }
         }
+        const double out = vi - (by == 1 ? cm_in : __ldg(s.cm + (by * 3 + bx) * s.nz1 + iz)) * acc;
+        a.vout[i] = out;
+        if (!isfinite(out))
+          record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2);
       }
     }
-    const double out = vi - __ldg(s.cm + cls) * acc;
-    a.vout[i] = out;
-    if (!isfinite(out))
-      record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.plane) << 22, seq, 2);
+    __syncthreads();  // slot (yl+2)%3 is overwritten next trip
   }
 }
 
@@ -204,6 +244,11 @@ __global__ void record_probes(const double* v, const long long* loc, int np, dou
 }
 
 __global__ void set_clock(long long* clock, long long value) { *clock = value; }
+
+// diastolic_threshold probe (stimulus.cpp:107): first step whose V[probe] > 0
+__global__ void probe_cross(const double* v, long long probe, long long* cross, const long long* clock, long long off) {
+  if (v[probe] > 0.0) atomicMin(reinterpret_cast<unsigned long long*>(cross), static_cast<unsigned long long>(*clock + off));
+}
 __global__ void tick_clock(long long* clock, long long by) { *clock += by; }
 
 // AoS (NodeStateArray::s, ionic.hpp:44) <-> SoA chunk transposes
@@ -280,8 +325,10 @@ cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int 
   return cudaGetLastError();
 }
 
-cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int max_blocks, cudaStream_t st) {
-  diffuse_struct3d<<<blocks_for(s.planes * s.plane, 256, max_blocks), 256, 0, st>>>(a, s);
+cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int, cudaStream_t st) {
+  const dim3 grid(static_cast<unsigned>((s.nx1 + S3_TX - 1) / S3_TX), static_cast<unsigned>((s.nz1 + S3_TZ - 1) / S3_TZ),
+                  static_cast<unsigned>((s.planes + S3_YCHUNK - 1) / S3_YCHUNK));
+  diffuse_struct3d<<<grid, S3_TX * S3_TZ, 0, st>>>(a, s);
   return cudaGetLastError();
 }
 
@@ -306,6 +353,12 @@ cudaError_t launch_record_probes(const double* v, const long long* loc, int np, 
                                  long long s_off, long long every, cudaStream_t st) {
   if (np == 0) return cudaSuccess;
   record_probes<<<(np + 127) / 128, 128, 0, st>>>(v, loc, np, out, clock, s_off, every);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_cross(const double* v, long long probe, long long* cross, const long long* clock,
+                               long long off, cudaStream_t st) {
+  probe_cross<<<1, 1, 0, st>>>(v, probe, cross, clock, off);
   return cudaGetLastError();
 }
 

@@ -26,6 +26,8 @@ cudaError_t launch_detector_observe(const double* v, long long n, long long halo
                                     cudaStream_t st);
 cudaError_t launch_record_probes(const double* v, const long long* loc, int np, double* out, const long long* clock,
                                  long long s_off, long long every, cudaStream_t st);
+cudaError_t launch_probe_cross(const double* v, long long probe, long long* cross, const long long* clock,
+                               long long off, cudaStream_t st);
 cudaError_t launch_set_clock(long long* clock, long long value, cudaStream_t st);
 cudaError_t launch_tick_clock(long long* clock, long long by, cudaStream_t st);
 cudaError_t launch_aos_to_soa(const double* aos, int stride, int ns, long long count, double* soa, long long pitch,
