@@ -1540,6 +1540,7 @@ bool propagates(cwg_ctx* c, double amp, long long steps, cudaGraphExec_t& graph,
   }
   ErrRec none{kNoError, -1, 0, 0};
   CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->d_err_dummy, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
   const long long never = 0x7fffffffffffffffll;
   CUDA_TRY(cudaMemcpyAsync(c->d_cross, &never, sizeof(never), cudaMemcpyHostToDevice, c->stream));
   auto enqueue = [&](long long off) {
@@ -1655,6 +1656,10 @@ extern "C" int cwg_diastolic_threshold(const cwg_problem* prob, const double* co
     c->evs = 2;     // ev 0 reaction, ev 1 diffusion
     CUDA_TRY(launch_mass_factor_fix(c));
     c->d_err_dummy = dev_alloc<ErrRec>(1);
+    {
+      const ErrRec none{kNoError, -1, 0, 0};
+      CUDA_TRY(cudaMemcpy(c->d_err_dummy, &none, sizeof(none), cudaMemcpyHostToDevice));
+    }
     c->d_cross = dev_alloc<long long>(1);
     c->probe_local = probe - c->node_offset;
     // bisection (stimulus.cpp:136-156)

@@ -93,14 +93,6 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ) diffuse_struct3d(DiffArgs a, St
     }
   };
   const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
-  double creg[27];
-  double cm_in = 0.0;
-  if (inside) {  // class of this (x, z) column on interior y-planes (by = 1)
-    const long long cin = (3 + bx) * s.nz1 + iz;
-#pragma unroll
-    for (int q = 0; q < 27; ++q) creg[q] = __ldg(s.coef + cin * 27 + q);
-    cm_in = __ldg(s.cm + cin);
-  }
   load(yb - 1, (yb + 2) % 3);
   load(yb, yb % 3);
   for (long long yl = yb; yl < ye; ++yl) {
@@ -116,8 +108,8 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ) diffuse_struct3d(DiffArgs a, St
       } else {
         const long long gy = s.row_begin + yl;
         const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
-        // interior planes use the register copy of this thread's 27 coefficients
-        const double* cf = s.coef + ((by * 3 + bx) * s.nz1 + iz) * 27;
+        const long long cls = (by * 3 + bx) * s.nz1 + iz;
+        const double* cf = s.coef + cls * 27;
         double acc = 0.0;
 #pragma unroll
         for (int dy = -1; dy <= 1; ++dy) {
@@ -130,11 +122,11 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ) diffuse_struct3d(DiffArgs a, St
             for (int dx = -1; dx <= 1; ++dx) {
               if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
               const int q = (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1);
-              acc += (by == 1 ? creg[q] : __ldg(cf + q)) * pl[c0 + dz * PX + dx];
+              acc += __ldg(cf + q) * pl[c0 + dz * PX + dx];
             }
           }
         }
-        const double out = vi - (by == 1 ? cm_in : __ldg(s.cm + (by * 3 + bx) * s.nz1 + iz)) * acc;
+        const double out = vi - __ldg(s.cm + cls) * acc;
         a.vout[i] = out;
         if (!isfinite(out))
           record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2);
