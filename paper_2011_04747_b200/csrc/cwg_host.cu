@@ -351,8 +351,22 @@ void halo_exchange(cwg_ctx* c, double* buf) {
   NCCL_TRY(g_nccl.gend());
 }
 
+// sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides)
+int diffusion_fuse(const cwg_ctx* c) {
+  if (c->op_kind != CWG_OP_STENCIL2D || c->world > 1) return 1;  // T-row halos are not exchanged
+  if (const char* e = getenv("CWG_DIFF_TB")) return std::max(1, std::min(4, atoi(e)));
+  return 4;
+}
+
 void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
-  for (int q = 0; q < count; ++q) {
+  // Launches m >= ceil(count / fuse) with m = count (mod 2): every launch flips
+  // the V double buffer, and captured step graphs must keep its parity.
+  const int fuse = diffusion_fuse(c);
+  int m = (count + fuse - 1) / fuse;
+  if ((m - count) & 1) ++m;
+  for (int q = 0, launch = 0; q < count; ++launch) {
+    const int left = m - launch;
+    const int T = (count - q + left - 1) / left;  // balanced group sizes
     double* vin = c->d_v[c->cur];
     double* vout = c->d_v[c->cur ^ 1];
     halo_exchange(c, vin);
@@ -370,7 +384,10 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     a.node_offset = c->own_global0;
     if (c->op_kind == CWG_OP_STENCIL2D) {
       Stencil2D s{c->d_coef, c->n_own, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
-      CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
+      if (T > 1)
+        CUDA_TRY(launch_diffuse_stencil2d_tb(T, a, s, c->num_sms, c->stream));
+      else
+        CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
     } else if (c->op_kind == CWG_OP_STRUCT3D) {
       Struct3D s{c->d_coef, c->d_cm, c->s3_nx1, c->s3_nz1, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
       CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms * 16, c->stream));
@@ -380,6 +397,7 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     }
     ++c->launches;
     c->cur ^= 1;
+    q += T;
   }
 }
 
@@ -596,17 +614,21 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
   c->d_coef = upload(coef.data(), coef.size());
 }
 
-// ORd launch shape. Latency regime (the bin fits in about one wave of
-// 256-thread blocks, e.g. C2's 40k nodes): 256 threads x 252 registers --
-// fewer, wider warps shorten the per-evaluation latency that bounds the
-// k = 10 wavefront nodes. Throughput regime: 384 threads x 168 registers
-// (12 warps per SM). Both run one persistent lockstep block per SM.
+// ORd launch shape: one persistent lockstep block per SM. Latency regime
+// (the bin fits into <= 10 warps per SM, e.g. C2's 40k nodes): the smallest
+// block that holds EVERY node in one round (256 / 288 / 320 threads with
+// 252 / 224 / 204 registers) -- a second round of nodes per lane would double
+// the step's makespan. Throughput regime: 384 threads x 168 registers.
 int choose_ord_variant(long long count, int num_sms) {
   if (const char* e = getenv("CWG_ORD_VARIANT")) {
     const int v = atoi(e);
-    if (v >= 0 && v <= 5) return v;
+    if (v >= 0 && v <= 8) return v;
   }
-  return count <= static_cast<long long>(num_sms) * 256 * 5 / 4 ? 2 : 1;
+  const long long warps_per_sm = (count + 32ll * num_sms - 1) / (32ll * num_sms);
+  if (warps_per_sm <= 8) return 2;
+  if (warps_per_sm == 9) return 7;
+  if (warps_per_sm == 10) return 8;
+  return 1;
 }
 
 bool stencil_ok(const cwg_problem* p) {
@@ -953,6 +975,8 @@ void reset_error(cwg_ctx* c) {
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 }
 
+bool ev_is_reaction(const cwg_ctx* c, long long seq) { return seq % c->evs == c->l; }
+
 // Read the error record (after a sync) and, for world > 1, agree on the
 // earliest failing event and its lowest node across ranks.
 bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
@@ -975,7 +999,8 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
     r.seq = h[0];
   }
   if (r.key == kNoError) return false;
-  const long long node = static_cast<long long>(r.key >> 22);
+  // diffusion keys carry the fused sub-step index in bits 58..63 (temporal blocking)
+  const long long node = static_cast<long long>(r.key >> 22) & (ev_is_reaction(c, r.seq) ? -1ll : (1ll << 36) - 1);
   const long long step = r.seq / c->evs;
   const long long ev = r.seq % c->evs;
   const double t = use_t ? t_fixed : static_cast<double>(step) * c->dt_eff;

@@ -57,6 +57,154 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
 }
 
 // ---------------------------------------------------------------------------
+// Temporal blocking: T consecutive sub-steps in one kernel. A block owns a
+// TBX x TBY output tile. Sub-step q (0-based) is computed on the tile plus a
+// (T-1-q)-node halo, so the block needs V on the tile + T halo (shared memory,
+// double-buffered) and the 9+1 coefficients of the tile + (T-1) halo: each
+// thread owns up to R of those points for all T sub-steps and keeps their
+// coefficients in registers (loaded once, all loads independent). Every
+// node's arithmetic is exactly that of diffuse_stencil2d, so the result is
+// bit-identical to T separate sub-steps. A non-finite value in sub-step q of
+// the tile is keyed (q << 58) | (node << 22): atomicMin yields the earliest
+// sub-step, then the lowest node (the order of separate launches).
+// ---------------------------------------------------------------------------
+template <int T, int TBX, int TBY, int NT>
+__global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D s) {
+  constexpr int VX = TBX + 2 * T, VY = TBY + 2 * T;              // V region
+  constexpr int CX = TBX + 2 * (T - 1), CY = TBY + 2 * (T - 1);  // computed region (sub-step 0)
+  constexpr int R = (CX * CY + NT - 1) / NT;                     // points per thread
+  __shared__ double Vs[2][VY * VX];
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  const long long gx0 = static_cast<long long>(blockIdx.x) * TBX, ly0 = static_cast<long long>(blockIdx.y) * TBY;
+  const long long rows = s.rows, w = s.w;
+  {
+    // V on the tile + T halo; rows outside the sheet are never read (presence flags)
+    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
+    for (int t = threadIdx.x; t < VX * VY; t += NT) {
+      const int cx = t % VX, cy = t / VX;
+      const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
+      const bool in = x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows;
+      Vs[0][t] = in ? vsrc[static_cast<long long>(cy) * w + cx] : 0.0;
+    }
+  }
+  // Slots in ring order: the TBX x TBY tile first, then halo ring 1, 2, ...
+  // so that the points active in sub-step q are a prefix of the slots and
+  // whole warps skip the rest (warp-uniform branch). Per slot: coefficients,
+  // V index, flags (bit0 own, 1 s, 2 n, 3 w, 4 e).
+  double cf[R][10];
+  int vi[R];
+  unsigned fl[R];
+  int px[R], py[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int p = threadIdx.x + r * NT;
+    int rx = 0, ry = 0;
+    bool valid = p < CX * CY;
+    if (p < TBX * TBY) {
+      rx = p % TBX;
+      ry = p / TBX;
+    } else if (valid) {
+      int e = p - TBX * TBY, k = 1;
+      while (e >= 2 * (TBX + 2 * k) + 2 * (TBY + 2 * k - 2)) {
+        e -= 2 * (TBX + 2 * k) + 2 * (TBY + 2 * k - 2);
+        ++k;
+      }
+      const int wr = TBX + 2 * k, hr = TBY + 2 * k - 2;  // ring row length, column length (corners excluded)
+      if (e < wr) {
+        rx = e - k, ry = -k;
+      } else if (e < 2 * wr) {
+        rx = e - wr - k, ry = TBY - 1 + k;
+      } else if (e < 2 * wr + hr) {
+        rx = -k, ry = e - 2 * wr - k + 1;
+      } else {
+        rx = TBX - 1 + k, ry = e - 2 * wr - hr - k + 1;
+      }
+    }
+    px[r] = rx;
+    py[r] = ry;
+    const long long x = gx0 + rx, yl = ly0 + ry, gy = s.row_begin + yl;
+    const bool own = valid && x >= 0 && x < w && yl >= 0 && yl < rows;
+    fl[r] = own ? (1u | (gy > 0 ? 2u : 0u) | (gy + 1 < s.ny1 ? 4u : 0u) | (x > 0 ? 8u : 0u) | (x + 1 < w ? 16u : 0u))
+                : 0u;
+    vi[r] = own ? (ry + T) * VX + (rx + T) : VX + 1;  // inactive slots read a safe in-range cell
+    const long long o = own ? yl * w + x : 0;
+    const double* cp = s.coef + o;
+#pragma unroll
+    for (int c = 0; c < 9; ++c) cf[r][c] = own ? __ldg(cp + c * s.cpitch) : 0.0;
+    cf[r][9] = own ? __ldg(s.cm + o) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < T; ++q) {
+    const double* src = Vs[q & 1];
+    double* dst = Vs[(q + 1) & 1];
+    const int hx = T - 1 - q;
+    const int n_act = (TBX + 2 * hx) * (TBY + 2 * hx);  // active slots: a prefix
+    double out[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      out[r] = 0.0;
+      if (r * NT + (threadIdx.x & ~31) >= n_act) continue;  // warp-uniform
+      const unsigned f = fl[r];
+      const bool act = (f & 1u) && threadIdx.x + r * NT < n_act;
+      const double* sp = src + vi[r];
+      const double v0 = sp[0];
+      const double vsw = sp[-VX - 1], vs = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
+      const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
+      const bool hs = f & 2u, hn = f & 4u, hw = f & 8u, he = f & 16u;
+      // same additions, same order as diffuse_stencil2d; absent terms leave acc untouched
+      double acc = 0.0, tmp;
+      tmp = acc + cf[r][0] * vsw; acc = (hs && hw) ? tmp : acc;
+      tmp = acc + cf[r][1] * vs;  acc = hs ? tmp : acc;
+      tmp = acc + cf[r][2] * vse; acc = (hs && he) ? tmp : acc;
+      tmp = acc + cf[r][3] * vw;  acc = hw ? tmp : acc;
+      acc = acc + cf[r][4] * v0;
+      tmp = acc + cf[r][5] * ve;  acc = he ? tmp : acc;
+      tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
+      tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
+      tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
+      const double o = skip ? v0 : v0 - cf[r][9] * acc;
+      out[r] = o;
+      if (q + 1 < T && act) dst[vi[r]] = o;
+      if (act && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
+        const long long x = gx0 + px[r], yl = ly0 + py[r];
+        record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
+                                  (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2);
+      }
+    }
+    if (q + 1 < T) {
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r * NT >= TBX * TBY) break;
+        if (fl[r] & 1u) a.vout[(ly0 + py[r] + 1) * w + gx0 + px[r]] = out[r];
+      }
+    }
+  }
+}
+
+template <int T, int TBX, int TBY, int NT>
+static cudaError_t launch_tb(const DiffArgs& a, const Stencil2D& s, cudaStream_t st) {
+  const dim3 grid(static_cast<unsigned>((s.w + TBX - 1) / TBX), static_cast<unsigned>((s.rows + TBY - 1) / TBY));
+  diffuse_stencil2d_tb<T, TBX, TBY, NT><<<grid, NT, 0, st>>>(a, s);
+  return cudaGetLastError();
+}
+
+// T fused sub-steps (2..4): 64x16 tiles unless that leaves fewer than 2 blocks per SM
+cudaError_t launch_diffuse_stencil2d_tb(int T, const DiffArgs& a, const Stencil2D& s, int num_sms, cudaStream_t st) {
+  const long long big = ((s.w + 63) / 64) * ((s.rows + 15) / 16);
+  const bool large = big >= 2ll * num_sms;
+  switch (T) {
+    case 2: return large ? launch_tb<2, 64, 16, 512>(a, s, st) : launch_tb<2, 32, 8, 256>(a, s, st);
+    case 3: return large ? launch_tb<3, 64, 16, 512>(a, s, st) : launch_tb<3, 32, 8, 256>(a, s, st);
+    case 4: return large ? launch_tb<4, 64, 16, 512>(a, s, st) : launch_tb<4, 32, 8, 256>(a, s, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Structured 3D slab (EXTENSION): 27-point rows whose coefficients depend only
 // on the node class (x face, y face, z layer); ascending-column order is
 // (dy, dz, dx) lexicographic for the y-outer numbering. 16 B of node traffic

@@ -19,6 +19,7 @@ cudaError_t launch_rates_ord(int kind, long long n, const double* v, const doubl
 
 cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st);
 cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int max_blocks, cudaStream_t st);
+cudaError_t launch_diffuse_stencil2d_tb(int T, const DiffArgs& a, const Stencil2D& s, int num_sms, cudaStream_t st);
 cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st);
 cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st);
 cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,

@@ -146,23 +146,54 @@ __device__ __forceinline__ void gate(SA s, double* ds, int i, double h, double x
   put<R>(s, ds, i, h, (xinf - s[i]) * rate);
 }
 
+// The evaluation is split into composable pieces (prologue, group A, group B,
+// finish) so the two-warp kernel (react_pair.cuh) can run groups A and B in
+// different warps; step() chains them in one thread. Arithmetic is identical
+// either way.
+struct Pro {
+  double ena, ek, eks, camk_b, camkt, fk, nfk, vfrt, e1, e2, xq1, xq2;
+};
+struct CurA {
+  double i_na, i_to, i_cal, i_cana, i_cak;  // i_na includes INaL
+};
+struct CurB {
+  double i_k, inaca_i, inaca_ss, i_nak, i_kb, i_nab, i_cab, i_pca;
+};
+
+// reversal potentials, CaMK, GHK driving terms (reads nai, ki, cass, CaMKt)
+template <int CT, bool FP, class SA>
+__device__ __forceinline__ Pro prologue(double v, SA s) {
+  Pro p;
+  const double nai = s[NAI], ki = s[KI], cass = s[CASS];
+  p.ena = RTF * log(NAO * rcp(nai));
+  p.ek = RTF * log(KO * rcp(ki));
+  p.eks = RTF * log((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
+  p.camkt = s[CAMKT];
+  p.camk_b = 0.05 * (1.0 - p.camkt) * cass * rcp(cass + 0.0015);
+  const double camk_a = p.camk_b + p.camkt;
+  p.fk = camk_a * rcp(camk_a + 0.15);
+  p.nfk = 1.0 - p.fk;
+  p.vfrt = v * FRT;
+  const double vfrt = p.vfrt;
+  // ---------------- GHK driving terms (one expm1 for e^x, e^2x, expm1(2x))
+  const double em1 = expm1(vfrt);
+  p.e1 = em1 + 1.0;
+  p.e2 = p.e1 * p.e1;
+  const double em2 = em1 * (em1 + 2.0);
+  p.xq1 = xem1<FP>(vfrt, em1);
+  p.xq2 = xem1<FP>(2.0 * vfrt, em2);
+
+  return p;
+}
+
+// group A: INa, INaL, Ito, ICaL/ICaNa/ICaK and their 24 gates (reads nass, kss, cass)
 template <int CT, bool R, bool FP, class SA>
-__device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, double gkr_scale, double h,
-                                     double& dv) {
+__device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& pr, double h) {
   using P = Var<CT>;
-  const double nai = s[NAI], nass = s[NASS], ki = s[KI], kss = s[KSS];
-  const double cai = s[CAI], cass = s[CASS], cansr = s[CANSR], cajsr = s[CAJSR];
-
-  const double ena = RTF * log(NAO * rcp(nai));
-  const double ek = RTF * log(KO * rcp(ki));
-  const double eks = RTF * log((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
-  const double camkt = s[CAMKT];
-  const double camk_b = 0.05 * (1.0 - camkt) * cass * rcp(cass + 0.0015);
-  const double camk_a = camk_b + camkt;
-  const double fk = camk_a * rcp(camk_a + 0.15);
-  const double nfk = 1.0 - fk;
-  const double vfrt = v * FRT;
-
+  const double ena = pr.ena, ek = pr.ek, fk = pr.fk, nfk = pr.nfk;
+  const double e1 = pr.e1, e2 = pr.e2, xq1 = pr.xq1, xq2 = pr.xq2;
+  const double nass = s[NASS], kss = s[KSS], cass = s[CASS];
+  CurA o;
   // ---------------- INa + INaL: the 14 V-dependent exponentials in one batch
   double i_na;
   {
@@ -240,14 +271,6 @@ __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, do
     gate<R>(s, ds, ISP, h, i_inf, r_is * r_dr);
   }
 
-  // ---------------- GHK driving terms (one expm1 for e^x, e^2x, expm1(2x))
-  const double em1 = expm1(vfrt);
-  const double e1 = em1 + 1.0;
-  const double e2 = e1 * e1;
-  const double em2 = em1 * (em1 + 2.0);
-  const double xq1 = xem1<FP>(vfrt, em1);
-  const double xq2 = xem1<FP>(2.0 * vfrt, em2);
-
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
@@ -296,6 +319,22 @@ __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, do
     gate<R>(s, ds, FCAFP, h, f_inf, r_fcaf * (1.0 / 2.5));
   }
 
+  o.i_na = i_na;
+  o.i_to = i_to;
+  o.i_cal = i_cal;
+  o.i_cana = i_cana;
+  o.i_cak = i_cak;
+  return o;
+}
+
+// group B: IKr, IKs, IK1 (5 gates), INaCa, INaK, background currents
+template <int CT, bool R, bool FP, class SA>
+__device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& pr, double h, double gkr_scale) {
+  using P = Var<CT>;
+  const double ek = pr.ek, eks = pr.eks, vfrt = pr.vfrt;
+  const double e1 = pr.e1, e2 = pr.e2, xq1 = pr.xq1, xq2 = pr.xq2;
+  const double nai = s[NAI], nass = s[NASS], ki = s[KI], cai = s[CAI], cass = s[CASS];
+  CurB o;
   // ---------------- IKr, IKs, IK1
   double i_k;  // IKr + IKs + IK1
   {
@@ -385,6 +424,28 @@ __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, do
   const double i_cab = (2.5e-8 * 2.0 * F) * (cai * e2 - 0.341 * CAO) * xq2;
   const double i_pca = 0.0005 * cai * rcp(0.0005 + cai);
 
+  o.i_k = i_k;
+  o.inaca_i = inaca_i;
+  o.inaca_ss = inaca_ss;
+  o.i_nak = i_nak;
+  o.i_kb = i_kb;
+  o.i_nab = i_nab;
+  o.i_cab = i_cab;
+  o.i_pca = i_pca;
+  return o;
+}
+
+// SR fluxes (Jrel gates need ICaL), CaMKt, buffers, concentrations, dV
+template <int CT, bool R, class SA>
+__device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& pr, const CurA& A, const CurB& B,
+                                       double ist, double h, double& dv) {
+  using P = Var<CT>;
+  const double fk = pr.fk, nfk = pr.nfk, camk_b = pr.camk_b, camkt = pr.camkt;
+  const double nai = s[NAI], nass = s[NASS], ki = s[KI], kss = s[KSS];
+  const double cai = s[CAI], cass = s[CASS], cansr = s[CANSR], cajsr = s[CAJSR];
+  const double i_na = A.i_na, i_to = A.i_to, i_cal = A.i_cal, i_cana = A.i_cana, i_cak = A.i_cak;
+  const double i_k = B.i_k, inaca_i = B.inaca_i, inaca_ss = B.inaca_ss, i_nak = B.i_nak, i_kb = B.i_kb;
+  const double i_nab = B.i_nab, i_cab = B.i_cab, i_pca = B.i_pca;
   // ---------------- SR release / uptake, buffers
   const double jrel = nfk * s[JRELNP] + fk * s[JRELP];
   {
@@ -437,6 +498,15 @@ __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, do
   if (!R) v = fe(v, h, dv);
 }
 
+template <int CT, bool R, bool FP, class SA>
+__device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, double gkr_scale, double h,
+                                     double& dv) {
+  const Pro pr = prologue<CT, FP>(v, s);
+  const CurA ca = group_a<CT, R, FP>(v, s, ds, pr, h);
+  const CurB cb = group_b<CT, R, FP>(v, s, ds, pr, h, gkr_scale);
+  finish<CT, R>(v, s, ds, pr, ca, cb, ist, h, dv);
+}
+
 // CellModel::rates (no update), for the batched rates entry point / tests
 template <int CT>
 __device__ void rates(double v, const double* s, double ist, double& dv, double* ds) {
@@ -453,11 +523,15 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 // V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep;
 // V = 3: one persistent 512-thread block per SM (<= 128 regs, 16 warps), lockstep;
 // V = 4: like 3 with the node states in shared memory (160 KB);
-// V = 5: like 1 (384 threads) with the node states in shared memory (120 KB).
+// V = 5: like 1 (384 threads) with the node states in shared memory (120 KB);
+// V = 7 / 8: one persistent 288 / 320-thread block per SM (<= 224 / 204 regs):
+//            sized so that a small mesh (C2: 40,401 nodes) needs ONE round of
+//            nodes per lane instead of 1 + a tail.
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = V == 1 || V == 5 ? 384 : (V == 2 ? 256 : (V == 3 || V == 4 ? 512 : 128));
+  static constexpr int kThreads =
+      V == 1 || V == 5 ? 384 : (V == 2 ? 256 : (V == 3 || V == 4 ? 512 : (V == 7 ? 288 : (V == 8 ? 320 : 128))));
   static constexpr int kMinBlocks = V == 0 ? 2 : 1;
   static constexpr bool kBlockSync = V != 0;
   static constexpr bool kSmemStates = V >= 4;
@@ -513,6 +587,27 @@ static int occupancy_t() {
   return b;
 }
 
+}  // namespace cwg
+#include "react_pair.cuh"
+namespace cwg {
+
+template <int CT>
+static cudaError_t launch_pair_t(const ReactArgs& a, int grid, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>((a.khist_len + 3) & ~3) * sizeof(unsigned) + 4 * sizeof(PairShm);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(react_pair_kernel<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  react_pair_kernel<CT><<<grid, kPairWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int CT>
+static int occupancy_pair() {
+  int b = 0;
+  const size_t smem = static_cast<size_t>(2048) * sizeof(unsigned) + 4 * sizeof(PairShm);
+  cudaFuncSetAttribute(react_pair_kernel<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, react_pair_kernel<CT>, kPairWarps * 32, smem);
+  return b;
+}
+
 // Launch-shape variants (see ModelOrd). The host picks one per model bin
 // (cwg_host.cu: choose_ord_variant); CWG_ORD_VARIANT overrides for experiments.
 template <int CT>
@@ -523,6 +618,9 @@ static cudaError_t launch_ct(int variant, const ReactArgs& a, int grid, cudaStre
     case 3: return launch_react_t<ModelOrd<CT, 3>>(a, grid, st);
     case 4: return launch_react_t<ModelOrd<CT, 4>>(a, grid, st);
     case 5: return launch_react_t<ModelOrd<CT, 5>>(a, grid, st);
+    case 6: return launch_pair_t<CT>(a, grid, st);
+    case 7: return launch_react_t<ModelOrd<CT, 7>>(a, grid, st);
+    case 8: return launch_react_t<ModelOrd<CT, 8>>(a, grid, st);
     default: return launch_react_t<ModelOrd<CT, 1>>(a, grid, st);
   }
 }
@@ -543,6 +641,9 @@ int react_ord_threads(int variant) {
     case 3: return ModelOrd<0, 3>::kThreads;
     case 4: return ModelOrd<0, 4>::kThreads;
     case 5: return ModelOrd<0, 5>::kThreads;
+    case 6: return kPairWarps * 16;  // nodes per block (two lanes per node)
+    case 7: return ModelOrd<0, 7>::kThreads;
+    case 8: return ModelOrd<0, 8>::kThreads;
     default: return ModelOrd<0, 1>::kThreads;
   }
 }
@@ -555,6 +656,9 @@ static int occ_ct(int variant) {
     case 3: return occupancy_t<ModelOrd<CT, 3>>();
     case 4: return occupancy_t<ModelOrd<CT, 4>>();
     case 5: return occupancy_t<ModelOrd<CT, 5>>();
+    case 6: return occupancy_pair<CT>();
+    case 7: return occupancy_t<ModelOrd<CT, 7>>();
+    case 8: return occupancy_t<ModelOrd<CT, 8>>();
     default: return occupancy_t<ModelOrd<CT, 1>>();
   }
 }

@@ -1,0 +1,93 @@
+"""Fused (temporally blocked) 2D diffusion sub-steps against the oracle.
+
+With dt = 0.3 ms on an h = 100 um sheet (dt_s ~ 0.012-0.013 ms) the scheme
+runs l = 11..13 sub-steps per half (22..26 per merged step), which the CUDA
+path fuses up to four at a time (diffuse.cu, diffuse_stencil2d_tb). Results must stay bit-identical
+to separate sub-steps, and a non-finite V must be reported at the node and time
+the reference reports (splitting.cpp:60-72 check after every sub-step).
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from helpers import gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _problem(lx, ly, ang, t_end, model="aliev-panfilov"):
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import api, problems
+    sh = cw.Sheet(lx, ly, 0.01, ang, d0_myocyte=0.0017, rho=0.25)
+    nodes = sh.select("x_le", value=0.05)
+    return problems.Problem("tb", sh, [model], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, 100.0, None)],
+                            api.SchemeConfig(dt_ms=0.3, t_end_ms=t_end), [0, sh.n // 2, sh.n - 1])
+
+
+@pytest.mark.parametrize("lx,ly,ang", [(1.3, 0.7, 0.4), (0.33, 0.09, 1.2), (8.0, 4.0, math.pi / 4)])
+def test_fused_substeps_bitwise(lx, ly, ang):
+    import paper_2011_04747_b200 as cw
+    p = _problem(lx, ly, ang, t_end=6.0)
+    assert cw.diffusion_substeps(0.3, p.sheet.op.dt_s, False, cw.Scheme.DAETI).l >= 9  # 18+ fused sub-steps per step
+    res = gpu_run(p)
+    o = oracle_run(p)
+    assert np.array_equal(res.final_state.v, o["v"])
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    for q, tr in enumerate(res.traces):
+        assert np.array_equal(tr.v_mv, o["traces"][q])
+    assert np.array_equal(res.lat_map.valid, o["lat_valid"])
+    assert np.array_equal(res.lat_map.value[o["lat_valid"]], o["lat"][o["lat_valid"]])
+
+
+def test_fused_equals_unfused():
+    p = _problem(1.3, 0.7, 0.4, t_end=9.0)
+    old = os.environ.get("CWG_DIFF_TB")
+    try:
+        os.environ["CWG_DIFF_TB"] = "1"
+        a = gpu_run(p)
+        os.environ["CWG_DIFF_TB"] = "3"
+        b = gpu_run(p)
+    finally:
+        if old is None:
+            os.environ.pop("CWG_DIFF_TB", None)
+        else:
+            os.environ["CWG_DIFF_TB"] = old
+    c = gpu_run(p)
+    for r in (b, c):
+        assert np.array_equal(a.final_state.v, r.final_state.v)
+        assert np.array_equal(a.final_state.s, r.final_state.s)
+
+
+@pytest.mark.parametrize("where", ["interior", "tile_corner", "edge"])
+def test_nonfinite_in_fused_substep_reports_like_oracle(where):
+    """A NaN in the initial V: the first diffusion sub-step of step I spreads it;
+    the reported node is the lowest non-finite one, t = 0 (as in the reference)."""
+    import orapy
+    import paper_2011_04747_b200 as cw
+    from helpers import csr_of
+    p = _problem(1.3, 0.7, 0.4, t_end=3.0)
+    w = p.sheet.nx1
+    x, y = {"interior": (40, 30), "tile_corner": (63, 16), "edge": (0, 55)}[where]
+    node = y * w + x
+    st = p.initial_state()
+    st.v[node] = np.nan
+    with pytest.raises(cw.InstabilityError) as eg:
+        cw.run_simulation(st, p.setup(), p.cfg)
+    st0 = p.initial_state()
+    v0 = st0.v.copy()
+    v0[node] = np.nan
+    with pytest.raises(orapy.OracleInstability) as eo:
+        orapy.run_simulation(csr_of(p), p.sheet.op.dt_s, p.models, p.model_of_node, p.stimuli, dt=0.3, t_end=3.0,
+                             k0_down=p.cfg.k0_down, init=(v0, st0.s.reshape(p.n, -1), st0.last_dvdt))
+    assert eg.value.node_index == eo.value.node
+    assert eg.value.time_ms == eo.value.t == 0.0
+    assert eo.value.node == node - (w + 1 if x > 0 else w)
