@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(React
     if (earlier_failure(a.err, seq)) return;  // uniform across the grid
   }
   for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x) shist[i] = 0u;
+  if constexpr (requires { M::block_init(); }) M::block_init();  // e.g. the exp table (fastmath.cuh)
   __syncthreads();
   react_body<M>(a, shist);
   __syncthreads();

@@ -536,6 +536,7 @@ struct ModelOrd {
   static constexpr bool kBlockSync = V != 0;
   static constexpr bool kSmemStates = V >= 4;
   static constexpr bool kUsesGkr = true;
+  __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
   __device__ __forceinline__ static void advance(double& v, SA s, double ist, double g, double h, double& dv) {
     if (fabs(v) <= 130.0)
@@ -548,6 +549,8 @@ struct ModelOrd {
 template <int CT>
 __global__ void ord_rates_kernel(long long n, const double* v, const double* s, const double* ist, double* dv,
                                  double* ds) {
+  exp_table_init();
+  __syncthreads();
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= n) return;
   double sl[ord::NSTATE], dl[ord::NSTATE];

@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(kPairWarps * 32, 2) react_pair_kernel(ReactArg
   const bool roleB = warp & 1;
   PairShm& P = pshm[pid];
   if (roleB && lane == 0) P.status = 0;
+  exp_table_init();
   __syncthreads();
 
   const long long step = *a.clock + a.step_off;
