@@ -35,10 +35,12 @@ sys.path.insert(0, ROOT)
 METRIC = "node-updates/sec (reaction+diffusion) and simulated ms per wall-s, % roofline"
 UNIT = "node-updates/s"
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
-# Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<1>>
-# (2*DFMA + DMUL + DADD lane ops per evaluation); from the ncu capture in
-# profiles/ (see DESIGN.md "Roofline"). Updated when the kernel changes.
-ORD_FP64_FLOPS_PER_EVAL = 2375.0
+# Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<epi>>
+# (2*DFMA + DMUL + DADD predicated-on lane ops / evaluations), counted by ncu
+# over every reaction launch of a 60-step C2 run (tools/flops_per_eval.py;
+# profiles/r01_flops_per_eval_c2.txt): 1114.3 DFMA + 462.7 DMUL + 334.3 DADD.
+# Updated when the kernel changes.
+ORD_FP64_FLOPS_PER_EVAL = 3025.7
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 

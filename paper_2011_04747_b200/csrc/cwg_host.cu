@@ -622,13 +622,14 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
 int choose_ord_variant(long long count, int num_sms) {
   if (const char* e = getenv("CWG_ORD_VARIANT")) {
     const int v = atoi(e);
-    if (v >= 0 && v <= 8) return v;
+    if (react_ord_variant_valid(v)) return v;
   }
+  const int pf = getenv("CWG_ORD_PREFETCH") && atoi(getenv("CWG_ORD_PREFETCH")) ? 16 : 0;
   const long long warps_per_sm = (count + 32ll * num_sms - 1) / (32ll * num_sms);
-  if (warps_per_sm <= 8) return 2;
-  if (warps_per_sm == 9) return 7;
-  if (warps_per_sm == 10) return 8;
-  return 1;
+  if (warps_per_sm <= 8) return 2 | pf;
+  if (warps_per_sm == 9) return 7 | pf;
+  if (warps_per_sm == 10) return 8 | pf;
+  return 1 | pf;
 }
 
 bool stencil_ok(const cwg_problem* p) {

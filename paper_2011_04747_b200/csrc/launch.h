@@ -13,6 +13,7 @@ cudaError_t launch_rates_exact(int kind, long long n, const double* v, const dou
 
 cudaError_t launch_react_ord(int kind, int variant, const ReactArgs& a, int grid, cudaStream_t st);
 int react_ord_threads(int variant);
+bool react_ord_variant_valid(int variant);
 int react_ord_occupancy(int kind, int variant);
 cudaError_t launch_rates_ord(int kind, long long n, const double* v, const double* s, const double* ist, double* dv,
                              double* ds, cudaStream_t st);

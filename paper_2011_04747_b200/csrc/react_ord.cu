@@ -518,23 +518,24 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 
 }  // namespace ord
 
-// Launch shapes: V = 0: 128-thread blocks, 2 per SM (<= 255 regs), warps free-running;
-// V = 1: one persistent 384-thread block per SM (<= 168 regs, 12 warps), lockstep;
-// V = 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep;
-// V = 3: one persistent 512-thread block per SM (<= 128 regs, 16 warps), lockstep;
-// V = 4: like 3 with the node states in shared memory (160 KB);
-// V = 5: like 1 (384 threads) with the node states in shared memory (120 KB);
-// V = 7 / 8: one persistent 288 / 320-thread block per SM (<= 224 / 204 regs):
-//            sized so that a small mesh (C2: 40,401 nodes) needs ONE round of
-//            nodes per lane instead of 1 + a tail.
+// Launch shapes (V & 15): 0: 128-thread blocks, 2 per SM (<= 255 regs), warps
+// free-running; 1: one persistent 384-thread block per SM (<= 168 regs, 12
+// warps), lockstep; 2: one persistent 256-thread block per SM (<= 255 regs,
+// 8 warps), lockstep; 7 / 8: one persistent 288 / 320-thread block per SM:
+// sized so that a small mesh (C2: 40,401 nodes) needs ONE round of nodes per
+// lane instead of 1 + a tail. V & 16: next-node prefetch (react.cuh).
+// (Measured and dropped: 512-thread blocks, node states in shared memory,
+// a two-warp-per-node split of the rates.)
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
+  static constexpr int kShape = V & 15;
   static constexpr int kThreads =
-      V == 1 || V == 5 ? 384 : (V == 2 ? 256 : (V == 3 || V == 4 ? 512 : (V == 7 ? 288 : (V == 8 ? 320 : 128))));
-  static constexpr int kMinBlocks = V == 0 ? 2 : 1;
-  static constexpr bool kBlockSync = V != 0;
-  static constexpr bool kSmemStates = V >= 4;
+      kShape == 1 ? 384 : (kShape == 2 ? 256 : (kShape == 7 ? 288 : (kShape == 8 ? 320 : 128)));
+  static constexpr int kMinBlocks = kShape == 0 ? 2 : 1;
+  static constexpr bool kBlockSync = kShape != 0;
+  static constexpr bool kSmemStates = false;
+  static constexpr bool kPrefetch = (V & 16) != 0;
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
@@ -564,7 +565,10 @@ __global__ void ord_rates_kernel(long long n, const double* v, const double* s, 
 template <class M>
 static size_t smem_bytes(int khist_len) {
   const size_t hist = static_cast<size_t>((khist_len + 1) & ~1) * sizeof(unsigned);
-  return hist + (M::kSmemStates ? static_cast<size_t>(M::NS) * M::kThreads * sizeof(double) : 0);
+  return hist + (M::kSmemStates ? static_cast<size_t>(M::NS) * M::kThreads * sizeof(double) : 0) +
+         (M::kPrefetch ? static_cast<size_t>(M::NS + 3) * M::kThreads * sizeof(double) +
+                             2ull * M::kThreads * sizeof(int)
+                       : 0);
 }
 
 template <class M>
@@ -590,41 +594,26 @@ static int occupancy_t() {
   return b;
 }
 
-}  // namespace cwg
-#include "react_pair.cuh"
-namespace cwg {
-
-template <int CT>
-static cudaError_t launch_pair_t(const ReactArgs& a, int grid, cudaStream_t st) {
-  const size_t smem = static_cast<size_t>((a.khist_len + 3) & ~3) * sizeof(unsigned) + 4 * sizeof(PairShm);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(react_pair_kernel<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  react_pair_kernel<CT><<<grid, kPairWarps * 32, smem, st>>>(a);
-  return cudaGetLastError();
-}
-
-template <int CT>
-static int occupancy_pair() {
-  int b = 0;
-  const size_t smem = static_cast<size_t>(2048) * sizeof(unsigned) + 4 * sizeof(PairShm);
-  cudaFuncSetAttribute(react_pair_kernel<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, react_pair_kernel<CT>, kPairWarps * 32, smem);
-  return b;
-}
-
 // Launch-shape variants (see ModelOrd). The host picks one per model bin
 // (cwg_host.cu: choose_ord_variant); CWG_ORD_VARIANT overrides for experiments.
+#define CWG_ORD_VARIANTS(X) X(0) X(1) X(2) X(7) X(8) X(16) X(17) X(18) X(23) X(24)
+
+bool react_ord_variant_valid(int v) {
+  switch (v) {
+#define CWG_CASE(n) case n:
+    CWG_ORD_VARIANTS(CWG_CASE) return true;
+#undef CWG_CASE
+    default: return false;
+  }
+}
+
 template <int CT>
 static cudaError_t launch_ct(int variant, const ReactArgs& a, int grid, cudaStream_t st) {
   switch (variant) {
-    case 0: return launch_react_t<ModelOrd<CT, 0>>(a, grid, st);
-    case 2: return launch_react_t<ModelOrd<CT, 2>>(a, grid, st);
-    case 3: return launch_react_t<ModelOrd<CT, 3>>(a, grid, st);
-    case 4: return launch_react_t<ModelOrd<CT, 4>>(a, grid, st);
-    case 5: return launch_react_t<ModelOrd<CT, 5>>(a, grid, st);
-    case 6: return launch_pair_t<CT>(a, grid, st);
-    case 7: return launch_react_t<ModelOrd<CT, 7>>(a, grid, st);
-    case 8: return launch_react_t<ModelOrd<CT, 8>>(a, grid, st);
-    default: return launch_react_t<ModelOrd<CT, 1>>(a, grid, st);
+#define CWG_CASE(n) case n: return launch_react_t<ModelOrd<CT, n>>(a, grid, st);
+    CWG_ORD_VARIANTS(CWG_CASE)
+#undef CWG_CASE
+    default: return cudaErrorInvalidValue;
   }
 }
 
@@ -639,30 +628,20 @@ cudaError_t launch_react_ord(int kind, int variant, const ReactArgs& a, int grid
 
 int react_ord_threads(int variant) {
   switch (variant) {
-    case 0: return ModelOrd<0, 0>::kThreads;
-    case 2: return ModelOrd<0, 2>::kThreads;
-    case 3: return ModelOrd<0, 3>::kThreads;
-    case 4: return ModelOrd<0, 4>::kThreads;
-    case 5: return ModelOrd<0, 5>::kThreads;
-    case 6: return kPairWarps * 16;  // nodes per block (two lanes per node)
-    case 7: return ModelOrd<0, 7>::kThreads;
-    case 8: return ModelOrd<0, 8>::kThreads;
-    default: return ModelOrd<0, 1>::kThreads;
+#define CWG_CASE(n) case n: return ModelOrd<0, n>::kThreads;
+    CWG_ORD_VARIANTS(CWG_CASE)
+#undef CWG_CASE
+    default: return 0;
   }
 }
 
 template <int CT>
 static int occ_ct(int variant) {
   switch (variant) {
-    case 0: return occupancy_t<ModelOrd<CT, 0>>();
-    case 2: return occupancy_t<ModelOrd<CT, 2>>();
-    case 3: return occupancy_t<ModelOrd<CT, 3>>();
-    case 4: return occupancy_t<ModelOrd<CT, 4>>();
-    case 5: return occupancy_t<ModelOrd<CT, 5>>();
-    case 6: return occupancy_pair<CT>();
-    case 7: return occupancy_t<ModelOrd<CT, 7>>();
-    case 8: return occupancy_t<ModelOrd<CT, 8>>();
-    default: return occupancy_t<ModelOrd<CT, 1>>();
+#define CWG_CASE(n) case n: return occupancy_t<ModelOrd<CT, n>>();
+    CWG_ORD_VARIANTS(CWG_CASE)
+#undef CWG_CASE
+    default: return 0;
   }
 }
 
