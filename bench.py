@@ -44,6 +44,15 @@ ORD_FP64_FLOPS_PER_EVAL = 3025.7
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 
+def diffusion_launches(count, fuse):
+    """Launches enqueue_diffusion (cwg_host.cu) uses for `count` sub-steps when
+    up to `fuse` are fused per launch (launch count keeps the parity of count)."""
+    m = -(-count // fuse)
+    if (m - count) % 2:
+        m += 1
+    return m
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -299,8 +308,17 @@ def main():
         pass
     diff_tot_ms = float(diff_ms.sum())
     is3d = args.config in ("c4", "c5")
-    diff_bytes = 16.0 if is3d else DIFF_BYTES_PER_NODE_SUBSTEP  # 3D: V in + out (structured tables are cached)
-    diff_gbs = info.n_local * 2 * info.l * K * diff_bytes / (diff_tot_ms / 1e3) / 1e9
+    # Algorithmic diffusion bytes per step: every launch reads V and writes V
+    # once per node (16 B) plus the node's coefficients -- 80 B of per-node
+    # arrays in 2D, 0 for the cached 3D structured tables; a launch fusing T
+    # sub-steps counts once (fused-traffic bound).
+    fuse = 1 if (is3d or world > 1) else int(os.environ.get("CWG_DIFF_TB", "4"))
+    fuse = max(1, min(4, fuse))
+    launches_per_step = diffusion_launches(2 * info.l, fuse)
+    coef_b = 0.0 if is3d else 80.0
+    diff_bytes_step = info.n_local * launches_per_step * (16.0 + coef_b)
+    diff_bytes = diff_bytes_step / (info.n_local * 2 * info.l)
+    diff_gbs = diff_bytes_step * K / (diff_tot_ms / 1e3) / 1e9
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -316,10 +334,14 @@ def main():
                          "traffic": traffic, "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no "
                                                              "FP64 entry)",
                          "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL},
-            "roofline_diffusion": {"bound": "hbm", "kernel": "diffuse_struct3d" if is3d else "diffuse_stencil2d",
+            "roofline_diffusion": {"bound": "hbm",
+                                   "kernel": "diffuse_struct3d" if is3d else (
+                                       "diffuse_stencil2d_tb" if fuse > 1 and launches_per_step < 2 * info.l
+                                       else "diffuse_stencil2d"),
                                    "achieved": diff_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                    "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                    "peak_source": peak_src, "bytes_per_node_substep": diff_bytes,
+                                   "launches_per_step": launches_per_step,
                                    "note": "phase time includes probe/detector recording"},
             "clocks": clocks.summary(), "gpu_launches": int(launches),
             "launch_mode": "one CUDA graph per step (event-record nodes at step start / after reaction / end)",

@@ -68,26 +68,16 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
 // the tile is keyed (q << 58) | (node << 22): atomicMin yields the earliest
 // sub-step, then the lowest node (the order of separate launches).
 // ---------------------------------------------------------------------------
-template <int T, int TBX, int TBY, int NT>
-__global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D s) {
-  constexpr int VX = TBX + 2 * T, VY = TBY + 2 * T;              // V region
+// EDGE = false: the block's computed region plus one node lies inside the
+// sheet and the rank's rows, so every point has all 8 neighbours (the CSR row
+// is the full 9-point stencil) and no presence flags or selects are needed.
+template <int T, int TBX, int TBY, int NT, bool EDGE>
+__device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, double (*Vs)[(TBY + 2 * T) * (TBX + 2 * T)],
+                                        long long gx0, long long ly0, bool skip, long long seq) {
+  constexpr int VX = TBX + 2 * T;
   constexpr int CX = TBX + 2 * (T - 1), CY = TBY + 2 * (T - 1);  // computed region (sub-step 0)
   constexpr int R = (CX * CY + NT - 1) / NT;                     // points per thread
-  __shared__ double Vs[2][VY * VX];
-  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
-  const bool skip = earlier_failure(a.err, seq);
-  const long long gx0 = static_cast<long long>(blockIdx.x) * TBX, ly0 = static_cast<long long>(blockIdx.y) * TBY;
   const long long rows = s.rows, w = s.w;
-  {
-    // V on the tile + T halo; rows outside the sheet are never read (presence flags)
-    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
-    for (int t = threadIdx.x; t < VX * VY; t += NT) {
-      const int cx = t % VX, cy = t / VX;
-      const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
-      const bool in = x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows;
-      Vs[0][t] = in ? vsrc[static_cast<long long>(cy) * w + cx] : 0.0;
-    }
-  }
   // Slots in ring order: the TBX x TBY tile first, then halo ring 1, 2, ...
   // so that the points active in sub-step q are a prefix of the slots and
   // whole warps skip the rest (warp-uniform branch). Per slot: coefficients,
@@ -100,7 +90,7 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
   for (int r = 0; r < R; ++r) {
     const int p = threadIdx.x + r * NT;
     int rx = 0, ry = 0;
-    bool valid = p < CX * CY;
+    const bool valid = p < CX * CY;
     if (p < TBX * TBY) {
       rx = p % TBX;
       ry = p / TBX;
@@ -124,7 +114,7 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
     px[r] = rx;
     py[r] = ry;
     const long long x = gx0 + rx, yl = ly0 + ry, gy = s.row_begin + yl;
-    const bool own = valid && x >= 0 && x < w && yl >= 0 && yl < rows;
+    const bool own = valid && (!EDGE || (x >= 0 && x < w && yl >= 0 && yl < rows));
     fl[r] = own ? (1u | (gy > 0 ? 2u : 0u) | (gy + 1 < s.ny1 ? 4u : 0u) | (x > 0 ? 8u : 0u) | (x + 1 < w ? 16u : 0u))
                 : 0u;
     vi[r] = own ? (ry + T) * VX + (rx + T) : VX + 1;  // inactive slots read a safe in-range cell
@@ -150,21 +140,36 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
       const bool act = (f & 1u) && threadIdx.x + r * NT < n_act;
       const double* sp = src + vi[r];
       const double v0 = sp[0];
-      const double vsw = sp[-VX - 1], vs = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
-      const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
-      const bool hs = f & 2u, hn = f & 4u, hw = f & 8u, he = f & 16u;
-      // same additions, same order as diffuse_stencil2d; absent terms leave acc untouched
-      double acc = 0.0, tmp;
-      tmp = acc + cf[r][0] * vsw; acc = (hs && hw) ? tmp : acc;
-      tmp = acc + cf[r][1] * vs;  acc = hs ? tmp : acc;
-      tmp = acc + cf[r][2] * vse; acc = (hs && he) ? tmp : acc;
-      tmp = acc + cf[r][3] * vw;  acc = hw ? tmp : acc;
-      acc = acc + cf[r][4] * v0;
-      tmp = acc + cf[r][5] * ve;  acc = he ? tmp : acc;
-      tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
-      tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
-      tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
-      const double o = skip ? v0 : v0 - cf[r][9] * acc;
+      double o;
+      if (!EDGE) {
+        // interior: the full 9-point row, same additions in the same order
+        double acc = 0.0 + cf[r][0] * sp[-VX - 1];
+        acc += cf[r][1] * sp[-VX];
+        acc += cf[r][2] * sp[-VX + 1];
+        acc += cf[r][3] * sp[-1];
+        acc += cf[r][4] * v0;
+        acc += cf[r][5] * sp[1];
+        acc += cf[r][6] * sp[VX - 1];
+        acc += cf[r][7] * sp[VX];
+        acc += cf[r][8] * sp[VX + 1];
+        o = skip ? v0 : v0 - cf[r][9] * acc;
+      } else {
+        const double vsw = sp[-VX - 1], vs = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
+        const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
+        const bool hs = f & 2u, hn = f & 4u, hw = f & 8u, he = f & 16u;
+        // same additions, same order as diffuse_stencil2d; absent terms leave acc untouched
+        double acc = 0.0, tmp;
+        tmp = acc + cf[r][0] * vsw; acc = (hs && hw) ? tmp : acc;
+        tmp = acc + cf[r][1] * vs;  acc = hs ? tmp : acc;
+        tmp = acc + cf[r][2] * vse; acc = (hs && he) ? tmp : acc;
+        tmp = acc + cf[r][3] * vw;  acc = hw ? tmp : acc;
+        acc = acc + cf[r][4] * v0;
+        tmp = acc + cf[r][5] * ve;  acc = he ? tmp : acc;
+        tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
+        tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
+        tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
+        o = skip ? v0 : v0 - cf[r][9] * acc;
+      }
       out[r] = o;
       if (q + 1 < T && act) dst[vi[r]] = o;
       if (act && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
@@ -183,6 +188,31 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
       }
     }
   }
+}
+
+template <int T, int TBX, int TBY, int NT>
+__global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D s) {
+  constexpr int VX = TBX + 2 * T, VY = TBY + 2 * T;  // V region
+  __shared__ double Vs[2][VY * VX];
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  const long long gx0 = static_cast<long long>(blockIdx.x) * TBX, ly0 = static_cast<long long>(blockIdx.y) * TBY;
+  const long long rows = s.rows, w = s.w;
+  {
+    // V on the tile + T halo; rows outside the sheet are never read (presence flags)
+    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
+    for (int t = threadIdx.x; t < VX * VY; t += NT) {
+      const int cx = t % VX, cy = t / VX;
+      const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
+      const bool in = x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows;
+      Vs[0][t] = in ? vsrc[static_cast<long long>(cy) * w + cx] : 0.0;
+    }
+  }
+  const bool interior = gx0 >= T && gx0 + TBX + T <= w && ly0 >= T && ly0 + TBY + T <= rows;
+  if (interior)
+    tb_body<T, TBX, TBY, NT, false>(a, s, Vs, gx0, ly0, skip, seq);
+  else
+    tb_body<T, TBX, TBY, NT, true>(a, s, Vs, gx0, ly0, skip, seq);
 }
 
 template <int T, int TBX, int TBY, int NT>

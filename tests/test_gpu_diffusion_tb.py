@@ -91,3 +91,4 @@ def test_nonfinite_in_fused_substep_reports_like_oracle(where):
     assert eg.value.node_index == eo.value.node
     assert eg.value.time_ms == eo.value.t == 0.0
     assert eo.value.node == node - (w + 1 if x > 0 else w)
+
