@@ -205,6 +205,22 @@ int64_t cwg_reaction_evals(cwg_ctx* ctx);
  * CUDA-event timed. Returns TFLOP/s (2 flops per DFMA) or < 0 on error. */
 double cwg_fp64_peak_tflops(int device, double seconds);
 
+/* pace_to_steady_state (ionic.cpp:122-165, ionic.hpp:74), batched: n
+ * independent single cells of one model kind, request i paced with
+ * cycle_ms[i] / amplitude[i] / duration_ms[i] for n_beats beats, forward Euler
+ * at dt = stable_step / 2, one device thread per request. Outputs (host
+ * buffers, any may be NULL): state_out [n][state_count+1] end-diastolic
+ * [V, s...] of the final beat, apd90_out [n][n_beats] (NaN: no AP),
+ * max_rel_out [n] (change between the last two end-diastolic states),
+ * status_out [n] (CWG_OK / CWG_EINSTABILITY), fail_t_out [n].
+ * Validation as the reference (n_beats >= 1, cycle > 0). Returns
+ * CWG_EINSTABILITY, with err filled from the lowest failing request like the
+ * reference's InstabilityError (node -1, t = beat * cycle + t_in_beat), when
+ * any request diverged; the other requests' outputs are still written. */
+int cwg_pace_cells(int model_kind, int64_t n, const double* cycle_ms, const double* amplitude,
+                   const double* duration_ms, int n_beats, double* state_out, double* apd90_out,
+                   double* max_rel_out, int* status_out, double* fail_t_out, int device, cwg_error* err);
+
 /* ThresholdOptions (stimulus.hpp:60-67) */
 typedef struct {
   double duration_ms;    /* 1.0 */

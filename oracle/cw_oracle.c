@@ -465,6 +465,76 @@ void cwo_rates_batch(int kind, int64_t n, const double* v, const double* s, cons
 }
 
 /* ------------------------------------------------------------------ *
+ * Single-cell pacing (pace_to_steady_state, ionic.cpp:122-165; euler   *
+ * step :74-83; BeatMarkers :86-118). Returns 0, or 1 on validation     *
+ * error, 2 on non-finite V, 3 on |V| > 1000 mV (fail_beat / fail_t set). *
+ * ------------------------------------------------------------------ */
+int cwo_pace(int kind, double cycle_ms, int n_beats, double amp, double dur, double* state_out,
+             double* apd_out, double* max_rel, int* fail_beat, double* fail_t) {
+  if (n_beats < 1 || !(cycle_ms > 0.0)) return 1;
+  const int ns = cwo_state_count(kind);
+  const double dt = cwo_stable_step(kind) / 2.0;
+  const int64_t spb = llround(cycle_ms / dt);
+  double st[64], eds[64], prev[64], ds[64];
+  int have_prev = 0;
+  cwo_rest_state(kind, st);
+  for (int beat = 0; beat < n_beats; ++beat) {
+    const double v_rest = st[0];
+    double max_slope = -INFINITY, t_max = NAN, v_peak = -INFINITY, apd = NAN;
+    int closed = 0;
+    double v_prev = st[0];
+    for (int64_t i = 0; i < spb; ++i) {
+      const double t_in = (double)i * dt;
+      const double ist = t_in < dur ? amp : 0.0;
+      double dv = 0.0;
+      cwo_rates(kind, st[0], st + 1, ist, 1.0, &dv, ds);
+      st[0] += dt * dv;
+      for (int k = 0; k < ns; ++k) st[1 + k] += dt * ds[k];
+      if (!isfinite(st[0]) || fabs(st[0]) > 1000.0) {
+        *fail_beat = beat;
+        *fail_t = (double)beat * cycle_ms + t_in;
+        return isfinite(st[0]) ? 3 : 2;
+      }
+      if (!closed) {
+        const double t = t_in + dt, slope = (st[0] - v_prev) / dt;
+        if (slope > max_slope) {
+          max_slope = slope;
+          t_max = t;
+        }
+        if (st[0] > v_peak) v_peak = st[0];
+        if (isfinite(t_max) && v_peak > 0.0) {
+          const double v90 = v_peak - 0.9 * (v_peak - v_rest);
+          if (st[0] < v90 && v_peak - v_rest > 20.0) {
+            apd = t - t_max;
+            closed = 1;
+          }
+        }
+      }
+      v_prev = st[0];
+    }
+    apd_out[beat] = apd;
+    if (beat > 0) {
+      memcpy(prev, eds, sizeof(double) * (size_t)(ns + 1));
+      have_prev = 1;
+    }
+    memcpy(eds, st, sizeof(double) * (size_t)(ns + 1));
+  }
+  memcpy(state_out, st, sizeof(double) * (size_t)(ns + 1));
+  double mr = 0.0;
+  if (have_prev) {
+    for (int k = 0; k <= ns; ++k) {
+      const double scale = fabs(prev[k]) < fabs(eds[k]) ? fabs(eds[k]) : fabs(prev[k]);
+      if (scale > 1e-12) {
+        const double r = fabs(eds[k] - prev[k]) / scale;
+        if (mr < r) mr = r;
+      }
+    }
+  }
+  *max_rel = mr;
+  return 0;
+}
+
+/* ------------------------------------------------------------------ *
  * Adaptation rules (splitting.cpp:48-72)                               *
  * ------------------------------------------------------------------ */
 int cwo_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max) {

@@ -35,6 +35,8 @@ void cwo_rates(int kind, double v, const double* s, double i_stim, double gkr_sc
 void cwo_rates_batch(int kind, int64_t n, const double* v, const double* s, const double* i_stim,
                      double* dv, double* ds);
 
+int cwo_pace(int kind, double cycle_ms, int n_beats, double amp, double dur, double* state_out,
+             double* apd_out, double* max_rel, int* fail_beat, double* fail_t);
 int cwo_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max);
 int cwo_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad);
 int cwo_k_max_for(double dt, double stable_step);

@@ -44,6 +44,7 @@ def lib():
             "cwo_rest_state": (None, [I, dp]),
             "cwo_rates": (None, [I, D, dp, D, D, dp, dp]),
             "cwo_rates_batch": (None, [I, I64, dp, dp, dp, dp, dp]),
+            "cwo_pace": (I, [I, C.c_double, I, C.c_double, C.c_double, dp, dp, dp, C.POINTER(C.c_int), dp]),
             "cwo_reaction_substeps": (I, [D, I, I, I, I]),
             "cwo_diffusion_substeps": (I, [D, D, I, I, ip, dp]),
             "cwo_k_max_for": (I, [D, D]),
@@ -95,6 +96,23 @@ def rates(model, v, s, i_stim):
     ds = np.zeros_like(s)
     lib().cwo_rates_batch(MODEL_KINDS[model], v.shape[0], _dp(v), _dp(s), _dp(i_stim), _dp(dv), _dp(ds))
     return dv, ds
+
+
+def pace(model, cycle_ms, n_beats, amp, dur):
+    """pace_to_steady_state restatement (ionic.cpp:122-165): (state, max_rel, apd90[n_beats]);
+    raises OracleInstability(msg, -1, t) on divergence, ValueError on bad arguments."""
+    st = np.zeros(64)
+    apd = np.zeros(max(1, n_beats))
+    mr = C.c_double()
+    fb = C.c_int()
+    ft = C.c_double()
+    rc = lib().cwo_pace(MODEL_KINDS[model], cycle_ms, n_beats, amp, dur, _dp(st), _dp(apd), C.byref(mr),
+                        C.byref(fb), C.byref(ft))
+    if rc == 1:
+        raise ValueError("pacing: invalid arguments")
+    if rc in (2, 3):
+        raise OracleInstability(f"pacing: diverged at beat {fb.value}", -1, ft.value)
+    return st[: state_count(model) + 1].copy(), mr.value, apd[:n_beats].copy()
 
 
 def reaction_substeps(dvdt, scheme, k0_up, k0_down, k_max):

@@ -384,6 +384,26 @@ int cwref_rates(const char* name, std::int64_t n, const double* v, const double*
   }
 }
 
+// pace_to_steady_state: 0 ok, 2 validation, 3 instability (t in fail_t)
+int cwref_pace(const char* name, double cycle_ms, int n_beats, double amp, double dur, double* state_out,
+               double* apd_out, double* max_rel, double* fail_t, char* msg, int msg_cap) {
+  try {
+    auto m = make_model(name);
+    const PacingResult r = pace_to_steady_state(*m, cycle_ms, n_beats, amp, dur);
+    for (std::size_t k = 0; k < r.state.size(); ++k) state_out[k] = r.state[k];
+    for (std::size_t b = 0; b < r.apd90_ms.size(); ++b) apd_out[b] = r.apd90_ms[b];
+    *max_rel = r.max_rel_change;
+    return kOk;
+  } catch (const InstabilityError& e) {
+    *fail_t = e.time_ms;
+    std::snprintf(msg, static_cast<std::size_t>(msg_cap), "%s", e.what());
+    return kInstability;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, static_cast<std::size_t>(msg_cap), "%s", e.what());
+    return kValidation;
+  }
+}
+
 double cwref_estimate_dt0(const char* name) { return estimate_dt0(*make_model(name)); }
 
 // ---------------------------------------------------------------- rules

@@ -71,6 +71,7 @@ def lib():
             "cwref_res_maps": (None, [P, dp, CP, dp, CP]),
             "cwref_model_info": (I, [CP, C.POINTER(I), dp, dp, I]),
             "cwref_rates": (I, [CP, I64, dp, dp, dp, dp, dp]),
+            "cwref_pace": (I, [CP, C.c_double, I, C.c_double, C.c_double, dp, dp, dp, dp, C.c_char_p, I]),
             "cwref_estimate_dt0": (D, [CP]),
             "cwref_reaction_substeps": (I, [D, I, I, I, I]),
             "cwref_diffusion_substeps": (I, [D, D, I, I, C.POINTER(I), dp]),
@@ -120,6 +121,20 @@ def rates(name: str, v, s, i_stim):
     if lib().cwref_rates(name.encode(), n, _dp(v), _dp(s), _dp(i_stim), _dp(dv), _dp(ds)) != 0:
         raise RefError(2, f"unknown model {name}")
     return dv, ds
+
+
+def pace(name, cycle_ms, n_beats, amp, dur):
+    """cardwave::pace_to_steady_state: (state, max_rel_change, apd90[n_beats])."""
+    st = np.zeros(64)
+    apd = np.zeros(max(1, n_beats))
+    mr, ft = C.c_double(), C.c_double()
+    msg = C.create_string_buffer(256)
+    rc = lib().cwref_pace(name.encode(), cycle_ms, n_beats, amp, dur, _dp(st), _dp(apd), C.byref(mr), C.byref(ft),
+                          msg, 256)
+    if rc != 0:
+        raise RefError(rc, msg.value.decode(), -1, ft.value)
+    ns = model_info(name)[0]
+    return st[: ns + 1].copy(), mr.value, apd[:n_beats].copy()
 
 
 def reaction_substeps(dvdt, scheme, k0_up, k0_down, k_max):

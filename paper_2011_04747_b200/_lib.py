@@ -89,6 +89,8 @@ _SIGS = {
     "cwg_diffusion_substep": (C.c_int, [C.c_int64, _lp, _lp, _dp, _dp, _dp, C.c_double, _dp, C.c_int,
                                         C.POINTER(cwg_error)]),
     "cwg_rates": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(cwg_error)]),
+    "cwg_pace_cells": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.POINTER(C.c_int), _dp,
+                                 C.c_int, C.POINTER(cwg_error)]),
     "cwg_model_state_count": (C.c_int, [C.c_int]),
     "cwg_model_stable_step": (C.c_double, [C.c_int]),
     "cwg_model_rest_state": (C.c_int, [C.c_int, _dp]),

@@ -187,6 +187,58 @@ def k_max_for(dt_ms: float, model: CellModel) -> int:
 
 
 @dataclass
+class PacingResult:
+    """ionic.hpp:63-68: end-diastolic [V, s...] of the final beat, the relative
+    change between the last two end-diastolic states, APD90 per beat (NaN: none)."""
+    state: np.ndarray
+    max_rel_change: float
+    apd90_ms: np.ndarray
+
+
+def pace_cells(model, cycle_lengths_ms, n_beats: int, stim_amplitude, stim_duration_ms, device=0):
+    """Batched pace_to_steady_state on the device: one single cell per entry of
+    cycle_lengths_ms (amplitude / duration scalars or per-cell arrays), one GPU
+    thread each. Returns (results, errors): errors[i] is None or the
+    InstabilityError the reference would raise for that cell."""
+    m = model if isinstance(model, CellModel) else make_model(model)
+    cl = np.ascontiguousarray(np.atleast_1d(np.asarray(cycle_lengths_ms, np.float64)))
+    n = len(cl)
+    amp = np.ascontiguousarray(np.broadcast_to(np.asarray(stim_amplitude, np.float64), (n,)).copy())
+    dur = np.ascontiguousarray(np.broadcast_to(np.asarray(stim_duration_ms, np.float64), (n,)).copy())
+    ns = m.state_count()
+    st = np.zeros((n, ns + 1))
+    apd = np.zeros((n, max(1, int(n_beats))))
+    mr = np.zeros(n)
+    status = np.zeros(n, np.int32)
+    ft = np.zeros(n)
+    err = L.cwg_error()
+    rc = L.lib().cwg_pace_cells(m.kind, n, L.dp(cl), L.dp(amp), L.dp(dur), int(n_beats), L.dp(st), L.dp(apd),
+                                L.dp(mr), status.ctypes.data_as(C.POINTER(C.c_int)), L.dp(ft), device,
+                                C.byref(err))
+    if rc not in (L.CWG_OK, L.CWG_EINSTABILITY):
+        _raise(rc, err)
+    results, errors = [], []
+    for i in range(n):
+        results.append(PacingResult(st[i].copy(), float(mr[i]), apd[i].copy()))
+        errors.append(None)
+    if rc == L.CWG_EINSTABILITY:
+        for i in np.flatnonzero(status != L.CWG_OK):
+            # per-cell message as the reference's (ionic.cpp:141-147); the C call reports the first
+            errors[i] = InstabilityError(err.msg.decode() if i == np.flatnonzero(status != L.CWG_OK)[0]
+                                         else "pacing: diverged", -1, float(ft[i]))
+    return results, errors
+
+
+def pace_to_steady_state(model, cycle_length_ms: float, n_beats: int, stim_amplitude: float,
+                         stim_duration_ms: float, device=0) -> PacingResult:
+    """pace_to_steady_state (ionic.cpp:122-165) for one cell, on the device."""
+    res, errs = pace_cells(model, [cycle_length_ms], n_beats, stim_amplitude, stim_duration_ms, device)
+    if errs[0] is not None:
+        raise errs[0]
+    return res[0]
+
+
+@dataclass
 class NodeStateArray:
     n_nodes: int = 0
     stride: int = 0

@@ -152,4 +152,22 @@ struct DetDev {
   double threshold;
 };
 
+// single-cell pacing batch (react.cuh: pace_kernel)
+struct PaceArgs {
+  long long n;
+  int n_beats;
+  double dt;
+  const double* cycle;
+  const double* amp;
+  const double* dur;
+  const double* rest;  // [NS + 1]: V, states
+  double* state_out;   // [n][NS + 1]
+  double* apd_out;     // [n][n_beats]
+  double* prev_out;    // [n][NS + 1] scratch: end-diastolic state of beat n_beats - 2
+  double* maxrel_out;  // [n]
+  int* status_out;     // [n]: 0 ok, 2 non-finite V, 3 |V| > 1000 mV
+  int* beat_out;       // [n]: failing beat
+  double* fail_t_out;  // [n]: beat * cycle + t_in_beat at the failure
+};
+
 }  // namespace cwg

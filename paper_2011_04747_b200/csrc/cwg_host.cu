@@ -1770,4 +1770,89 @@ int cwg_rates(int kind, int64_t n, const double* v, const double* s, const doubl
   });
 }
 
+static const char* model_name(int kind) {
+  switch (kind) {
+    case CWG_MODEL_ALIEV_PANFILOV: return "aliev-panfilov";
+    case CWG_MODEL_ORD_ENDO: return "ohara2011-endo";
+    case CWG_MODEL_ORD_EPI: return "ohara2011-epi";
+    case CWG_MODEL_ORD_MID: return "ohara2011-mid";
+    case CWG_MODEL_MACCANNELL: return "maccannell2007";
+    default: return "passive";
+  }
+}
+
+int cwg_pace_cells(int kind, int64_t n, const double* cycle_ms, const double* amplitude, const double* duration_ms,
+                   int n_beats, double* state_out, double* apd90_out, double* max_rel_out, int* status_out,
+                   double* fail_t_out, int device, cwg_error* err) {
+  int first_bad = -1, bad_status = 0, bad_beat = 0;
+  double bad_t = 0.0;
+  const int rc = guarded(err, [&] {
+    validation(state_count(kind) >= 0, "unknown cell model kind");
+    validation(n_beats >= 1, "pacing: n_beats must be >= 1");
+    for (int64_t i = 0; i < n; ++i) validation(cycle_ms[i] > 0.0, "pacing: cycle length must be positive");
+    if (n == 0) return;
+    CUDA_TRY(cudaSetDevice(device));
+    const int ns = state_count(kind);
+    double rest[64];
+    cwg_model_rest_state(kind, rest);
+    PaceArgs a{};
+    a.n = n;
+    a.n_beats = n_beats;
+    a.dt = stable_step(kind) / 2.0;  // ionic.cpp:127
+    a.cycle = upload(cycle_ms, n);
+    a.amp = upload(amplitude, n);
+    a.dur = upload(duration_ms, n);
+    a.rest = upload(rest, static_cast<size_t>(ns) + 1);
+    a.state_out = dev_alloc<double>(static_cast<size_t>(n) * (ns + 1));
+    a.prev_out = dev_alloc<double>(static_cast<size_t>(n) * (ns + 1));
+    a.apd_out = dev_alloc<double>(static_cast<size_t>(n) * n_beats);
+    a.maxrel_out = dev_alloc<double>(n);
+    a.status_out = dev_alloc<int>(n);
+    a.beat_out = dev_alloc<int>(n);
+    a.fail_t_out = dev_alloc<double>(n);
+    CUDA_TRY(is_ord(kind) ? launch_pace_ord(kind, a, nullptr) : launch_pace_exact(kind, a, nullptr));
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<int> st(static_cast<size_t>(n)), beat(static_cast<size_t>(n));
+    std::vector<double> ft(static_cast<size_t>(n));
+    CUDA_TRY(cudaMemcpy(st.data(), a.status_out, n * sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(beat.data(), a.beat_out, n * sizeof(int), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(ft.data(), a.fail_t_out, n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (state_out)
+      CUDA_TRY(cudaMemcpy(state_out, a.state_out, static_cast<size_t>(n) * (ns + 1) * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    if (apd90_out)
+      CUDA_TRY(cudaMemcpy(apd90_out, a.apd_out, static_cast<size_t>(n) * n_beats * sizeof(double),
+                          cudaMemcpyDeviceToHost));
+    if (max_rel_out) CUDA_TRY(cudaMemcpy(max_rel_out, a.maxrel_out, n * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < n; ++i) {
+      if (status_out) status_out[i] = st[static_cast<size_t>(i)] == 0 ? CWG_OK : CWG_EINSTABILITY;
+      if (fail_t_out) fail_t_out[i] = st[static_cast<size_t>(i)] == 0 ? 0.0 : ft[static_cast<size_t>(i)];
+      if (st[static_cast<size_t>(i)] != 0 && first_bad < 0) {
+        first_bad = static_cast<int>(i);
+        bad_status = st[static_cast<size_t>(i)];
+        bad_beat = beat[static_cast<size_t>(i)];
+        bad_t = ft[static_cast<size_t>(i)];
+      }
+    }
+    for (void* p : {(void*)a.cycle, (void*)a.amp, (void*)a.dur, (void*)a.rest, (void*)a.state_out,
+                    (void*)a.prev_out, (void*)a.apd_out, (void*)a.maxrel_out, (void*)a.status_out,
+                    (void*)a.beat_out, (void*)a.fail_t_out})
+      cudaFree(p);
+  });
+  if (rc != CWG_OK || first_bad < 0) return rc;
+  // the reference throws InstabilityError(msg, -1, t) (ionic.cpp:141-147)
+  const std::string msg = bad_status == 2 ? std::string("pacing: ") + model_name(kind) + " diverged at beat " +
+                                                std::to_string(bad_beat)
+                                          : "pacing: |V| > 1000 mV at beat " + std::to_string(bad_beat);
+  g_last_error = msg;
+  if (err) {
+    err->code = CWG_EINSTABILITY;
+    err->node = -1;
+    err->t_ms = bad_t;
+    err->phase = 1;
+    std::snprintf(err->msg, sizeof(err->msg), "%s", msg.c_str());
+  }
+  return CWG_EINSTABILITY;
+}
+
 }  // extern "C"

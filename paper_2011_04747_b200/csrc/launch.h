@@ -7,6 +7,8 @@ namespace cwg {
 
 cudaError_t launch_react_exact(int kind, const ReactArgs& a, int grid, cudaStream_t st);
 int react_exact_threads(int kind);
+cudaError_t launch_pace_exact(int kind, const PaceArgs& a, cudaStream_t st);
+cudaError_t launch_pace_ord(int kind, const PaceArgs& a, cudaStream_t st);
 int react_exact_occupancy(int kind);
 cudaError_t launch_rates_exact(int kind, long long n, const double* v, const double* s, const double* ist,
                                double* dv, double* ds, cudaStream_t st);

@@ -231,3 +231,97 @@ __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(React
 }
 
 }  // namespace cwg
+
+namespace cwg {
+
+// ---------------------------------------------------------------------------
+// Single-cell pacing to steady state (pace_to_steady_state, ionic.cpp:122-165),
+// batched: one thread per request (model kind fixed per launch; cycle length,
+// amplitude and duration per request). Forward Euler at dt = dt0 / 2 through
+// the same M::advance as the reaction pass; per-beat APD90 markers
+// (BeatMarkers, ionic.cpp:86-118) with the reference's operation order, every
+// product and sum rounded explicitly so the TU's contraction setting does not
+// matter.
+// ---------------------------------------------------------------------------
+
+template <class M>
+__global__ void __launch_bounds__(64) pace_kernel(PaceArgs a) {
+  if constexpr (requires { M::block_init(); }) M::block_init();
+  __syncthreads();
+  const long long r = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (r >= a.n) return;
+  constexpr int NS = M::NS > 0 ? M::NS : 1;
+  double s[NS];
+  double v = a.rest[0];
+#pragma unroll
+  for (int q = 0; q < M::NS; ++q) s[q] = a.rest[1 + q];
+  const double cycle = a.cycle[r], amp = a.amp[r], dur = a.dur[r], dt = a.dt;
+  const long long spb = llround(cycle / dt);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll), nan = __longlong_as_double(0x7ff8000000000000ll);
+  a.status_out[r] = 0;
+  for (int beat = 0; beat < a.n_beats; ++beat) {
+    const double v_rest = v;
+    double max_slope = -inf, t_max = nan, v_peak = -inf, apd = nan;
+    bool closed = false;
+    double v_prev = v;
+    for (long long i = 0; i < spb; ++i) {
+      const double t_in = __dmul_rn(static_cast<double>(i), dt);
+      const double ist = t_in < dur ? amp : 0.0;
+      double dv;
+      M::advance(v, s, ist, 1.0, dt, dv);
+      if (!isfinite(v) || fabs(v) > 1000.0) {
+        a.status_out[r] = isfinite(v) ? 3 : 2;
+        a.beat_out[r] = beat;
+        a.fail_t_out[r] = __dadd_rn(__dmul_rn(static_cast<double>(beat), cycle), t_in);
+        return;
+      }
+      if (!closed) {
+        const double t = __dadd_rn(t_in, dt);
+        const double slope = __ddiv_rn(__dsub_rn(v, v_prev), dt);
+        if (slope > max_slope) {
+          max_slope = slope;
+          t_max = t;
+        }
+        if (v > v_peak) v_peak = v;
+        if (isfinite(t_max) && v_peak > 0.0) {
+          const double v90 = __dsub_rn(v_peak, __dmul_rn(0.9, __dsub_rn(v_peak, v_rest)));
+          if (v < v90 && __dsub_rn(v_peak, v_rest) > 20.0) {
+            apd = __dsub_rn(t, t_max);
+            closed = true;
+          }
+        }
+      }
+      v_prev = v;
+    }
+    a.apd_out[r * a.n_beats + beat] = apd;
+    if (beat == a.n_beats - 2) {
+      double* pv = a.prev_out + r * (M::NS + 1);
+      pv[0] = v;
+#pragma unroll
+      for (int q = 0; q < M::NS; ++q) pv[1 + q] = s[q];
+    }
+  }
+  double* out = a.state_out + r * (M::NS + 1);
+  out[0] = v;
+#pragma unroll
+  for (int q = 0; q < M::NS; ++q) out[1 + q] = s[q];
+  double max_rel = 0.0;
+  if (a.n_beats >= 2) {
+    const double* pv = a.prev_out + r * (M::NS + 1);
+    for (int k = 0; k <= M::NS; ++k) {
+      const double e = out[k], p = pv[k];
+      const double scale = fmax(fabs(p), fabs(e));
+      if (scale > 1e-12) max_rel = fmax(max_rel, __ddiv_rn(fabs(__dsub_rn(e, p)), scale));
+    }
+  }
+  a.maxrel_out[r] = max_rel;
+}
+
+template <class M>
+cudaError_t launch_pace_t(const PaceArgs& a, cudaStream_t st) {
+  if (a.n == 0) return cudaSuccess;
+  pace_kernel<M><<<static_cast<unsigned>((a.n + 63) / 64), 64, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace cwg

@@ -133,6 +133,15 @@ cudaError_t launch_react_exact(int kind, const ReactArgs& a, int grid, cudaStrea
   }
 }
 
+cudaError_t launch_pace_exact(int kind, const PaceArgs& a, cudaStream_t st) {
+  switch (kind) {
+    case 0: return launch_pace_t<ModelAP>(a, st);
+    case 4: return launch_pace_t<ModelMac>(a, st);
+    case 5: return launch_pace_t<ModelPassive>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 int react_exact_threads(int) { return 256; }
 
 int react_exact_occupancy(int kind) {

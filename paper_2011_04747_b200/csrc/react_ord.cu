@@ -654,6 +654,15 @@ int react_ord_occupancy(int kind, int variant) {
   }
 }
 
+cudaError_t launch_pace_ord(int kind, const PaceArgs& a, cudaStream_t st) {
+  switch (kind) {
+    case 1: return launch_pace_t<ModelOrd<0, 0>>(a, st);
+    case 2: return launch_pace_t<ModelOrd<1, 0>>(a, st);
+    case 3: return launch_pace_t<ModelOrd<2, 0>>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_rates_ord(int kind, long long n, const double* v, const double* s, const double* ist, double* dv,
                              double* ds, cudaStream_t st) {
   if (n == 0) return cudaSuccess;

@@ -100,8 +100,27 @@ def runs_fixture():
     np.savez_compressed(os.path.join(HERE, "runs.npz"), **out)
 
 
+PACE_CASES = [("aliev-panfilov", 500.0, 3, 0.5, 1.0), ("maccannell2007", 400.0, 2, 10.0, 1.0),
+              ("ohara2011-endo", 300.0, 2, 80.0, 1.0), ("ohara2011-epi", 400.0, 3, 60.0, 0.5),
+              ("ohara2011-mid", 250.0, 2, 80.0, 1.0)]
+
+
+def pace_fixture():
+    """cardwave::pace_to_steady_state (ionic.cpp:122-165) outputs + one |V| > 1000 abort."""
+    out = {}
+    for i, (m, cl, nb, amp, dur) in enumerate(PACE_CASES):
+        st, mr, apd = refpy.pace(m, cl, nb, amp, dur)
+        out.update({f"c{i}_state": st, f"c{i}_max_rel": np.array([mr]), f"c{i}_apd": apd})
+    try:
+        refpy.pace("ohara2011-epi", 300.0, 2, 3000.0, 2.0)
+        out["abort_t"] = np.array([np.nan])
+    except refpy.RefError as e:
+        out["abort_t"] = np.array([e.t])
+    np.savez_compressed(os.path.join(HERE, "pace.npz"), **out)
+
+
 if __name__ == "__main__":
-    rates_fixture()
-    rules_fixture()
-    runs_fixture()
+    which = sys.argv[1:] or ["rates", "rules", "runs", "pace"]
+    for name in which:
+        globals()[name + "_fixture"]()
     print("wrote", sorted(f for f in os.listdir(HERE) if f.endswith(".npz")))

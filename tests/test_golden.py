@@ -109,3 +109,49 @@ def test_gpu_rates_golden(gold, model):
         assert np.array_equal(dv, g[k + "_dv"]) and np.array_equal(ds, g[k + "_ds"])
     else:
         np.testing.assert_allclose(dv, g[k + "_dv"], rtol=1e-11, atol=1e-12)
+
+
+# ----------------------------------------------------------------------------- single-cell pacing
+def _pace_cases():
+    src = open(os.path.join(G, "make_golden.py")).read()
+    ns = {}
+    exec(src[src.index("PACE_CASES ="):src.index("def pace_fixture")], ns)  # the case table only
+    return ns["PACE_CASES"]
+
+
+def _check_pace(model, st, mr, apd, g, i, dt, exact):
+    if exact:
+        assert np.array_equal(st, g[f"c{i}_state"]) and mr == g[f"c{i}_max_rel"][0]
+        assert np.array_equal(apd, g[f"c{i}_apd"], equal_nan=True)
+    else:  # transcendental models: libm / device exp differ by ulps; crossings are quantised to dt
+        np.testing.assert_allclose(st, g[f"c{i}_state"], rtol=1e-8, atol=1e-12)
+        assert abs(mr - g[f"c{i}_max_rel"][0]) < 1e-6
+        ga = g[f"c{i}_apd"]
+        assert np.array_equal(np.isnan(apd), np.isnan(ga))
+        assert np.all(np.abs(apd[~np.isnan(ga)] - ga[~np.isnan(ga)]) <= dt * 1.0000001)
+
+
+def test_oracle_pace_golden(ora):
+    g = np.load(os.path.join(G, "pace.npz"))
+    for i, (m, cl, nb, amp, dur) in enumerate(_pace_cases()):
+        st, mr, apd = ora.pace(m, cl, nb, amp, dur)
+        _check_pace(m, st, mr, apd, g, i, ora.stable_step(m) / 2, exact=(m == "aliev-panfilov"))
+    with pytest.raises(ora.OracleInstability) as e:
+        ora.pace("ohara2011-epi", 300.0, 2, 3000.0, 2.0)
+    assert e.value.t == g["abort_t"][0]
+
+
+@pytest.mark.gpu
+def test_gpu_pace_golden():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2011_04747_b200 as cw
+    g = np.load(os.path.join(G, "pace.npz"))
+    for i, (m, cl, nb, amp, dur) in enumerate(_pace_cases()):
+        r = cw.pace_to_steady_state(m, cl, nb, amp, dur)
+        _check_pace(m, r.state, r.max_rel_change, r.apd90_ms, g, i, cw.make_model(m).stable_step() / 2,
+                    exact=(m == "aliev-panfilov"))
+    with pytest.raises(cw.InstabilityError) as e:
+        cw.pace_to_steady_state("ohara2011-epi", 300.0, 2, 3000.0, 2.0)
+    assert e.value.time_ms == g["abort_t"][0] and e.value.node_index == -1
