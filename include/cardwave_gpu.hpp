@@ -244,21 +244,51 @@ inline SimulationResult run_simulation(NodeStateArray state, const SimulationSet
           : 0;
   const std::int64_t every_prog = setup.progress_every > 0 && setup.on_progress ? setup.progress_every : 0;
   if (every_snap) setup.on_snapshot(0.0, state.v);
+  // Snapshots are asynchronous: the V copy of snapshot N is enqueued after the
+  // steps up to it, the next chunk of steps is enqueued, and only then does
+  // the host wait for the copy and run on_snapshot -- the callback (e.g. the
+  // reference's write_vtk_snapshot) overlaps the device computing the next
+  // chunk. cwg_snapshot_wait reports a failure that happened before the
+  // snapshot point, so no snapshot after the reference's throw is delivered.
+  std::vector<double> snap;
+  bool registered = false;
+  if (every_snap) {
+    snap.assign(state.v.size(), 0.0);
+    registered = cwg_host_register(snap.data(), snap.size() * sizeof(double)) == CWG_OK;
+  }
+  struct Unregister {
+    bool on;
+    double* p;
+    ~Unregister() {
+      if (on) cwg_host_unregister(p);
+    }
+  } unreg{registered, snap.data()};
+  bool pending = false;
+  double pending_t = 0.0;
   std::int64_t s = 0;
   cwg_error e{};
+  auto deliver = [&] {
+    const int rc = cwg_snapshot_wait(ctx, &e);
+    if (rc != CWG_OK) detail::rethrow(rc, e);
+    pending = false;
+    setup.on_snapshot(pending_t, snap);
+  };
   while (s < n_steps) {
     std::int64_t next = n_steps;
     if (every_snap) next = std::min(next, (s / every_snap + 1) * every_snap);
     if (every_prog) next = std::min(next, (s / every_prog + 1) * every_prog);
     detail::check(cwg_run_steps(ctx, s, next - s));
+    if (pending) deliver();
     s = next;
-    if ((every_snap && s % every_snap == 0) || (every_prog && s % every_prog == 0) || s == n_steps) {
+    if (every_snap && s % every_snap == 0) {
+      detail::check(cwg_snapshot_begin(ctx, snap.data()));
+      pending = true;
+      pending_t = static_cast<double>(s) * dt;
+    }
+    if ((every_prog && s % every_prog == 0) || s == n_steps) {
+      if (pending) deliver();
       const int rc = cwg_run_sync(ctx, &e);
       if (rc != CWG_OK) detail::rethrow(rc, e);
-      if (every_snap && s % every_snap == 0) {
-        detail::check(cwg_download_state(ctx, state.v.data(), nullptr, state.stride, nullptr));
-        setup.on_snapshot(static_cast<double>(s) * dt, state.v);
-      }
       if (every_prog && s % every_prog == 0) {
         integ.refresh();
         TimingBreakdown tb = integ.timing();
@@ -267,6 +297,7 @@ inline SimulationResult run_simulation(NodeStateArray state, const SimulationSet
       }
     }
   }
+  if (pending) deliver();
   SimulationResult r;
   r.dt_effective = dt;
   r.dt_s = setup.op->dt_s;

@@ -152,6 +152,24 @@ int cwg_download_state(cwg_ctx* ctx, double* v, double* s_aos, int stride, doubl
 /* make_initial_state from the models' rest states directly on the device
  * (no host arrays; for 10^8-node slabs). last_dvdt = 0, V = rest V. */
 int cwg_init_rest_state(cwg_ctx* ctx);
+/* Asynchronous V snapshot for on_snapshot (splitting.cpp:267-277): enqueue,
+ * after the steps issued so far, a device-side copy of V and of the failure
+ * record, then their transfer to host_v[global node] on a side stream; the
+ * solver stream continues with the next steps meanwhile. host_v must stay
+ * valid until cwg_snapshot_wait returns (pinned or cwg_host_register-ed
+ * memory makes the copy asynchronous). One snapshot in flight per context.
+ * cwg_snapshot_wait blocks until host_v is complete; it returns
+ * CWG_EINSTABILITY (err filled as by cwg_run_sync) when the run had already
+ * failed at the snapshot point, so no snapshot later than the reference's
+ * throw is ever delivered. (world > 1: synchronous, the failure agreement is
+ * a collective.) */
+int cwg_snapshot_begin(cwg_ctx* ctx, double* host_v);
+int cwg_snapshot_wait(cwg_ctx* ctx, cwg_error* err);
+/* cudaHostRegister / cudaHostUnregister for caller-owned buffers
+ * (e.g. the std::vector handed to on_snapshot). */
+int cwg_host_register(void* p, size_t bytes);
+int cwg_host_unregister(void* p);
+
 /* Pinned staging for host<->device copies (e2e path); returns host pointers
  * owned by ctx of the sizes of the local slab. */
 int cwg_pinned_buffers(cwg_ctx* ctx, double** v, double** s_aos, double** last_dvdt);

@@ -227,7 +227,7 @@ class OracleInstability(RuntimeError):
 
 def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt=0.1, t_end=1.0, k0_up=5,
                    k0_down=1, strict=False, record_interval=1.0, map_interval=1.0, probes=(), lat_threshold=0.0,
-                   init=None, gkr_scale=None, stride=None):
+                   init=None, gkr_scale=None, stride=None, snapshot_interval=0.0):
     """Restatement of run_simulation (splitting.cpp:219-294) + StrangIntegrator (:74-181).
 
     models: list of model names (model id -> name); model_of_node: uint8[n].
@@ -266,6 +266,8 @@ def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt
     spr = max(1, int(round_half_away(record_interval / dt_eff)))
     spm = max(1, int(round_half_away(map_interval / dt_eff)))
     det = Detector(n, lat_threshold)
+    sps = max(1, int(round_half_away(snapshot_interval / dt_eff))) if snapshot_interval > 0.0 else 0
+    snaps = [(0.0, v.copy())] if sps else []
     traces_t = [0.0]
     traces_v = [[float(v[p]) for p in probes]]
     det.observe(0.0, v)
@@ -298,8 +300,10 @@ def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt
             traces_v.append([float(v[p]) for p in probes])
         if (step + 1) % spm == 0:
             det.observe(t_next, v)
+        if sps and (step + 1) % sps == 0:  # on_snapshot (splitting.cpp:276-277)
+            snaps.append((t_next, v.copy()))
     lat, lv, apd, av = det.maps()
-    return dict(v=v, s=s, last_dvdt=last, k_histogram=khist, n_steps=n_steps, l=l, dt_ad=dt_ad,
+    return dict(v=v, s=s, last_dvdt=last, k_histogram=khist, n_steps=n_steps, l=l, dt_ad=dt_ad, snapshots=snaps,
                 dt_effective=dt_eff, trace_t=np.array(traces_t), traces=np.array(traces_v).T.copy(),
                 lat=lat, lat_valid=lv, apd90=apd, apd_valid=av)
 

@@ -52,6 +52,14 @@ int main(int argc, char** argv) {
   cfg.t_end_ms = ap ? 100.0 : 20.0;
   cfg.k0_down = mode == "abort" ? 1 : (ap ? 1 : 3);
   NodeStateArray s0 = make_initial_state(mesh, models, {0});
+  // snapshots (asynchronous in the drop-in) and progress callbacks
+  std::vector<std::pair<double, std::vector<double>>> snaps[2];
+  int which = 0;
+  long progress_calls[2] = {0, 0};
+  setup.snapshot_interval_ms = ap ? 5.0 : (mode == "abort" ? 0.5 : 2.0);
+  setup.on_snapshot = [&](double t, const std::vector<double>& v) { snaps[which].emplace_back(t, v); };
+  setup.progress_every = 37;
+  setup.on_progress = [&](std::int64_t, double, const TimingBreakdown&) { ++progress_calls[which]; };
 
   long ref_node = -1, gpu_node = -1;
   double ref_t = 0, gpu_t = 0;
@@ -64,6 +72,7 @@ int main(int argc, char** argv) {
     ref_node = e.node_index;
     ref_t = e.time_ms;
   }
+  which = 1;
   try {
     b = gpu::run_simulation(s0, setup, cfg);
   } catch (const InstabilityError& e) {
@@ -71,10 +80,23 @@ int main(int argc, char** argv) {
     gpu_node = e.node_index;
     gpu_t = e.time_ms;
   }
+  // snapshot series: same count and times; V bit-exact for AP, <= 1e-6 mV for ORd
+  bool snaps_same = snaps[0].size() == snaps[1].size() && progress_calls[0] == progress_calls[1];
+  double snap_dv = 0.0;
+  for (std::size_t k = 0; snaps_same && k < snaps[0].size(); ++k) {
+    snaps_same = snaps[0][k].first == snaps[1][k].first;
+    for (std::size_t i = 0; i < snaps[0][k].second.size(); ++i)
+      snap_dv = std::max(snap_dv, std::abs(snaps[0][k].second[i] - snaps[1][k].second[i]));
+  }
+  // (abort mode: the last snapshots precede a blow-up, where ulp differences
+  // are amplified without bound -- there only count and times are compared)
+  if (mode != "abort") snaps_same = snaps_same && (ap ? snap_dv == 0.0 : snap_dv <= 1e-6);
   if (!ref_ok || !gpu_ok) {
-    const bool same = !ref_ok && !gpu_ok && ref_node == gpu_node && ref_t == gpu_t;
-    std::printf("{\"mode\":\"%s\",\"ref_abort\":[%ld,%.17g],\"gpu_abort\":[%ld,%.17g],\"match\":%s}\n", mode.c_str(),
-                ref_node, ref_t, gpu_node, gpu_t, same ? "true" : "false");
+    const bool same = !ref_ok && !gpu_ok && ref_node == gpu_node && ref_t == gpu_t && snaps_same;
+    std::printf("{\"mode\":\"%s\",\"ref_abort\":[%ld,%.17g],\"gpu_abort\":[%ld,%.17g],\"snapshots\":[%zu,%zu],"
+                "\"match\":%s}\n",
+                mode.c_str(), ref_node, ref_t, gpu_node, gpu_t, snaps[0].size(), snaps[1].size(),
+                same ? "true" : "false");
     return same ? 0 : 1;
   }
   double dv = 0, dl = 0;
@@ -86,10 +108,13 @@ int main(int argc, char** argv) {
   for (std::size_t i = 0; i < a.lat_map.value.size(); ++i)
     if (a.lat_map.valid[i]) dl = std::max(dl, std::abs(a.lat_map.value[i] - b.lat_map.value[i]));
   const bool kh = a.k_histogram == b.k_histogram;
-  const bool pass = ap ? (dv == 0.0 && dl == 0.0 && kh && valid_same) : (dv <= 1e-6 && dl < 1e-6 && kh && valid_same);
+  const bool pass = snaps_same && (ap ? (dv == 0.0 && dl == 0.0 && kh && valid_same)
+                                       : (dv <= 1e-6 && dl < 1e-6 && kh && valid_same));
   std::printf("{\"mode\":\"%s\",\"max_dV_mV\":%.3e,\"max_dLAT_ms\":%.3e,\"khist_equal\":%s,\"lat_valid_equal\":%s,"
+              "\"snapshots\":[%zu,%zu],\"snapshot_max_dV\":%.3e,\"progress_calls\":[%ld,%ld],"
               "\"pass\":%s,\"ref_ms\":%.1f,\"gpu_ms\":%.1f}\n",
-              mode.c_str(), dv, dl, kh ? "true" : "false", valid_same ? "true" : "false", pass ? "true" : "false",
+              mode.c_str(), dv, dl, kh ? "true" : "false", valid_same ? "true" : "false", snaps[0].size(),
+              snaps[1].size(), snap_dv, progress_calls[0], progress_calls[1], pass ? "true" : "false",
               a.timing.total_ms, b.timing.total_ms);
   return pass ? 0 : 1;
 }

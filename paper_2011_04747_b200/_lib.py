@@ -89,6 +89,10 @@ _SIGS = {
     "cwg_diffusion_substep": (C.c_int, [C.c_int64, _lp, _lp, _dp, _dp, _dp, C.c_double, _dp, C.c_int,
                                         C.POINTER(cwg_error)]),
     "cwg_rates": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(cwg_error)]),
+    "cwg_snapshot_begin": (C.c_int, [C.c_void_p, _dp]),
+    "cwg_snapshot_wait": (C.c_int, [C.c_void_p, C.POINTER(cwg_error)]),
+    "cwg_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),
+    "cwg_host_unregister": (C.c_int, [C.c_void_p]),
     "cwg_pace_cells": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, C.c_int, _dp, _dp, _dp, C.POINTER(C.c_int), _dp,
                                  C.c_int, C.POINTER(cwg_error)]),
     "cwg_model_state_count": (C.c_int, [C.c_int]),

@@ -30,7 +30,7 @@ import ctypes as C
 import enum
 import math
 from dataclasses import dataclass, field
-from typing import List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
@@ -517,6 +517,11 @@ class SimulationSetup:
     lat_threshold_mv: float = 0.0
     map_interval_ms: float = 1.0
     gkr_scale: Optional[np.ndarray] = None  # extension: per-node ORd GKr multiplier
+    # splitting.hpp:90-93: snapshot cadence + callbacks
+    snapshot_interval_ms: float = 0.0       # 0: no snapshots
+    on_snapshot: Optional[Callable[[float, np.ndarray], None]] = None
+    progress_every: int = 0
+    on_progress: Optional[Callable[[int, float, "TimingBreakdown"], None]] = None
 
 
 @dataclass
@@ -700,6 +705,65 @@ class StrangIntegrator:
         return ScalarMap(lat, lv.astype(bool)), ScalarMap(apd, av.astype(bool))
 
 
+def round_half_away(x: float) -> int:
+    """std::llround."""
+    return int(math.floor(x + 0.5)) if x >= 0 else -int(math.floor(-x + 0.5))
+
+
+def _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog, t0):
+    """The run loop with on_snapshot / on_progress (splitting.cpp:265-283).
+    Snapshots are asynchronous (cwg_snapshot_begin): snapshot N's copy drains
+    and its callback runs while the device computes the next chunk; a failure
+    before the snapshot point raises instead of delivering it."""
+    import time
+    lib = L.lib()
+    snap = None
+    if every_snap:
+        snap = np.zeros(state.n_nodes)
+        registered = lib.cwg_host_register(snap.ctypes.data, snap.nbytes) == L.CWG_OK
+        setup.on_snapshot(0.0, state.v.copy())
+    pending, pending_t = False, 0.0
+
+    def deliver():
+        err = L.cwg_error()
+        _check(lib.cwg_snapshot_wait(integ._h, C.byref(err)), err)
+        setup.on_snapshot(pending_t, snap.copy())
+
+    try:
+        s = 0
+        while s < n_steps:
+            nxt = n_steps
+            if every_snap:
+                nxt = min(nxt, (s // every_snap + 1) * every_snap)
+            if every_prog:
+                nxt = min(nxt, (s // every_prog + 1) * every_prog)
+            integ.run_steps(s, nxt - s)
+            if pending:
+                pending = False
+                deliver()
+            s = nxt
+            if every_snap and s % every_snap == 0:
+                _check(lib.cwg_snapshot_begin(integ._h, L.dp(snap)))
+                pending, pending_t = True, s * dt
+            if (every_prog and s % every_prog == 0) or s == n_steps:
+                if pending:
+                    pending = False
+                    deliver()
+                integ.run_sync()
+                if every_prog and s % every_prog == 0:
+                    tb = integ.timing()
+                    tb.total_ms = (time.perf_counter() - t0) * 1e3
+                    setup.on_progress(s, s * dt, tb)
+        if pending:
+            pending = False
+            deliver()
+    finally:
+        if pending:  # an exception left a copy in flight: drain it before the buffer goes away
+            lib.cwg_snapshot_wait(integ._h, None)
+        if every_snap and registered:
+            lib.cwg_host_unregister(snap.ctypes.data)
+
+
 def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeConfig, device=0,
                    integrator: StrangIntegrator = None) -> SimulationResult:
     """run_simulation (splitting.cpp:219-294) on the GPU; raises InstabilityError like the reference."""
@@ -708,8 +772,15 @@ def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeCon
     integ = integrator or StrangIntegrator(setup, cfg, model_of_node=state.model_of_node, device=device)
     integ.upload(state)
     integ.run_begin()
-    integ.run_steps(0, integ.info.n_steps)
-    integ.run_sync()
+    n_steps, dt = integ.info.n_steps, integ.dt_effective()
+    every_snap = (max(1, int(round_half_away(setup.snapshot_interval_ms / dt)))
+                  if setup.snapshot_interval_ms > 0.0 and setup.on_snapshot else 0)
+    every_prog = setup.progress_every if setup.progress_every > 0 and setup.on_progress else 0
+    if not every_snap and not every_prog:
+        integ.run_steps(0, n_steps)
+        integ.run_sync()
+    else:
+        _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog, t0)
     final = state.copy()
     integ.download(final)
     t, v = integ.traces()

@@ -254,6 +254,14 @@ struct cwg_ctx {
   // multi-GPU
   ncclComm_t comm = nullptr;
 
+  // asynchronous V snapshots (cwg_snapshot_begin / _wait)
+  double* d_snap = nullptr;
+  ErrRec* d_snap_err = nullptr;
+  ErrRec* h_snap_err = nullptr;  // pinned
+  cudaStream_t snap_stream = nullptr;
+  cudaEvent_t ev_vready = nullptr, ev_snapdone = nullptr;
+  bool snap_pending = false;
+
   // stats / timing
   long long launches = 0;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -321,6 +329,13 @@ void ctx_free(cwg_ctx* c) {
   if (c->h_v) cudaFreeHost(c->h_v);
   if (c->h_s) cudaFreeHost(c->h_s);
   if (c->h_last) cudaFreeHost(c->h_last);
+  if (c->snap_pending && c->ev_snapdone) cudaEventSynchronize(c->ev_snapdone);
+  dev_free(c->d_snap);
+  dev_free(c->d_snap_err);
+  if (c->h_snap_err) cudaFreeHost(c->h_snap_err);
+  if (c->ev_vready) cudaEventDestroy(c->ev_vready);
+  if (c->ev_snapdone) cudaEventDestroy(c->ev_snapdone);
+  if (c->snap_stream) cudaStreamDestroy(c->snap_stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->comm && g_nccl.destroy) g_nccl.destroy(c->comm);
@@ -1216,6 +1231,75 @@ int cwg_download_state(cwg_ctx* c, double* v, double* s_aos, int stride, double*
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   });
+}
+
+int cwg_snapshot_begin(cwg_ctx* c, double* host_v) {
+  return guarded(nullptr, [&] {
+    validation(host_v != nullptr, "snapshot: no destination");
+    validation(!c->snap_pending, "snapshot: the previous snapshot was not waited for");
+    CUDA_TRY(cudaSetDevice(c->device));
+    if (c->world > 1) {  // the failure agreement is a collective on the solver stream: stay synchronous
+      CUDA_TRY(cudaMemcpyAsync(host_v + c->own_global0, c->d_v[c->cur] + c->halo, c->n_own * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+      c->snap_pending = true;
+      return;
+    }
+    if (!c->d_snap) {
+      c->d_snap = dev_alloc<double>(std::max<long long>(c->n_own, 1));
+      c->d_snap_err = dev_alloc<ErrRec>(1);
+      CUDA_TRY(cudaMallocHost(&c->h_snap_err, sizeof(ErrRec)));
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->snap_stream, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_vready, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_snapdone, cudaEventDisableTiming));
+    }
+    // device-side copy on the solver stream (V and the failure record at this
+    // point of the run), then the D2H on a side stream: the solver stream
+    // moves on to the next steps while the copy drains
+    CUDA_TRY(cudaMemcpyAsync(c->d_snap, c->d_v[c->cur] + c->halo, c->n_own * sizeof(double),
+                             cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->d_snap_err, c->d_err, sizeof(ErrRec), cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_TRY(cudaEventRecord(c->ev_vready, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->snap_stream, c->ev_vready, 0));
+    CUDA_TRY(cudaMemcpyAsync(host_v + c->own_global0, c->d_snap, c->n_own * sizeof(double), cudaMemcpyDeviceToHost,
+                             c->snap_stream));
+    CUDA_TRY(cudaMemcpyAsync(c->h_snap_err, c->d_snap_err, sizeof(ErrRec), cudaMemcpyDeviceToHost, c->snap_stream));
+    CUDA_TRY(cudaEventRecord(c->ev_snapdone, c->snap_stream));
+    c->snap_pending = true;
+  });
+}
+
+int cwg_snapshot_wait(cwg_ctx* c, cwg_error* err) {
+  bool failed = false;
+  cwg_error e{};
+  const int rc = guarded(err, [&] {
+    validation(c->snap_pending, "snapshot: nothing to wait for");
+    CUDA_TRY(cudaSetDevice(c->device));
+    c->snap_pending = false;
+    if (c->world > 1) {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      failed = fetch_error(c, false, 0.0, &e);
+      return;
+    }
+    CUDA_TRY(cudaEventSynchronize(c->ev_snapdone));
+    if (c->h_snap_err->key != kNoError) {  // the run failed at or before this point: report it like run_sync
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      failed = fetch_error(c, false, 0.0, &e);
+    }
+  });
+  if (rc != CWG_OK) return rc;
+  if (failed) {
+    if (err) *err = e;
+    return CWG_EINSTABILITY;
+  }
+  return CWG_OK;
+}
+
+int cwg_host_register(void* p, size_t bytes) {
+  return guarded(nullptr, [&] { CUDA_TRY(cudaHostRegister(p, bytes, cudaHostRegisterDefault)); });
+}
+
+int cwg_host_unregister(void* p) {
+  return guarded(nullptr, [&] { CUDA_TRY(cudaHostUnregister(p)); });
 }
 
 int cwg_pinned_buffers(cwg_ctx* c, double** v, double** s_aos, double** last) {

@@ -255,3 +255,38 @@ def test_slab3d_ord_sites_tolerance(cw, ora, problems):
     p = problems.slab(0.6, 0.4, 0.2, 0.02, t_end=8.0, stim="sites", n_sites=3, site_radius=0.1, amplitude=150.0)
     res, o = run_both(p)
     _compare_tol(res, o, p.sheet.nx1, p.probes)
+
+
+# ----------------------------------------------------------------------------- callbacks (splitting.cpp:265-283)
+def test_async_snapshots_bitwise(cw, ora, problems):
+    """on_snapshot receives V at every snapshot time, bit-identical to the oracle
+    run stopped at that time; on_progress fires at its cadence."""
+    p = problems.c1(model="aliev-panfilov", t_end=20.0, k0_down=1)
+    setup = p.setup()
+    snaps, prog = [], []
+    setup.snapshot_interval_ms = 2.0
+    setup.on_snapshot = lambda t, v: snaps.append((t, v))
+    setup.progress_every = 45
+    setup.on_progress = lambda step, t, tb: prog.append(step)
+    res = cw.run_simulation(p.initial_state(), setup, p.cfg)
+    assert [round(t, 9) for t, _ in snaps] == [round(2.0 * k, 9) for k in range(11)]
+    assert prog == [45, 90, 135, 180]
+    assert np.array_equal(snaps[-1][1], res.final_state.v)
+    o = oracle_run(p, snapshot_interval=2.0)
+    assert len(o["snapshots"]) == len(snaps)
+    for (tg, vg), (to, vo) in zip(snaps, o["snapshots"]):
+        assert tg == to and np.array_equal(vg, vo), tg
+
+
+def test_async_snapshots_stop_at_abort(cw, ora, problems):
+    """The reference throws at node 16, t = 2.04 ms: snapshots up to t = 2.0 are
+    delivered, none after (the drop-in checks the failure record at each one)."""
+    p = problems.c1(t_end=10.0, k0_down=1)
+    setup = p.setup()
+    snaps = []
+    setup.snapshot_interval_ms = 0.5
+    setup.on_snapshot = lambda t, v: snaps.append(t)
+    with pytest.raises(cw.InstabilityError) as e:
+        cw.run_simulation(p.initial_state(), setup, p.cfg)
+    assert (e.value.node_index, e.value.time_ms) == (16, 2.04)
+    assert [round(t, 9) for t in snaps] == [0.0, 0.5, 1.0, 1.5, 2.0]

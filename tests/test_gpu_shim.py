@@ -21,3 +21,6 @@ def test_cpp_dropin_matches_reference(mode):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     if mode == "abort":
         assert line["ref_abort"][0] == 16 and line["match"]
+        assert line["snapshots"][0] == line["snapshots"][1] == 5  # t = 0, 0.5, ..., 2.0
+    elif mode in ("ap", "ord"):
+        assert line["snapshots"][0] == line["snapshots"][1] > 1 and line["pass"]
