@@ -152,6 +152,14 @@ int cwg_download_state(cwg_ctx* ctx, double* v, double* s_aos, int stride, doubl
 /* make_initial_state from the models' rest states directly on the device
  * (no host arrays; for 10^8-node slabs). last_dvdt = 0, V = rest V. */
 int cwg_init_rest_state(cwg_ctx* ctx);
+/* Reconfigure the scheme of an existing context -- cli_compare
+ * (runner.cpp:254-324) runs OST / OSTAR / DAETI on one prepared problem, so
+ * the device-resident operator, stimulus, probes and model bins are kept
+ * while dt_eff, l, dt_ad (and dt/m), k_max, n_steps and the record cadences
+ * are recomputed exactly as by cwg_create; cached graphs are dropped.
+ * Upload the initial state and call cwg_run_begin afterwards. */
+int cwg_set_scheme(cwg_ctx* ctx, int scheme, double dt_ms, double t_end_ms, int k0_up, int k0_down,
+                   int strict_substeps, cwg_error* err);
 /* Asynchronous V snapshot for on_snapshot (splitting.cpp:267-277): enqueue,
  * after the steps issued so far, a device-side copy of V and of the failure
  * record, then their transfer to host_v[global node] on a side stream; the

@@ -18,6 +18,7 @@
 #include "cardwave/fem.hpp"
 #include "cardwave/ionic.hpp"
 #include "cardwave/mesh.hpp"
+#include "cardwave/postprocess.hpp"
 #include "cardwave/splitting.hpp"
 #include "cardwave/stimulus.hpp"
 
@@ -400,6 +401,59 @@ int cwref_pace(const char* name, double cycle_ms, int n_beats, double amp, doubl
     return kInstability;
   } catch (const std::exception& e) {
     std::snprintf(msg, static_cast<std::size_t>(msg_cap), "%s", e.what());
+    return kValidation;
+  }
+}
+
+// ---------------------------------------------------------------- postprocess metrics (postprocess.cpp:98-236)
+namespace {
+Trace make_trace(const double* t, const double* v, std::int64_t n) {
+  Trace tr;
+  tr.t_ms.assign(t, t + n);
+  tr.v_mv.assign(v, v + n);
+  return tr;
+}
+ScalarMap make_map(std::int64_t n, const double* value, const char* valid) {
+  ScalarMap m;
+  m.value.assign(value, value + n);
+  m.valid.assign(valid, valid + n);
+  return m;
+}
+}  // namespace
+
+// 1: APD90 written, 0: none
+int cwref_compute_apd90(const double* t, const double* v, std::int64_t n, double* out) {
+  const auto r = compute_apd90(make_trace(t, v, n));
+  if (r) *out = *r;
+  return r ? 1 : 0;
+}
+
+int cwref_compute_cv(cwref_problem* p, const double* lat, const char* valid, std::int64_t a, std::int64_t b,
+                     double* out) {
+  try {
+    *out = compute_cv(p->mesh, make_map(p->mesh.node_count(), lat, valid), a, b);
+    return kOk;
+  } catch (const std::exception&) {
+    return kValidation;
+  }
+}
+
+int cwref_nrmse(std::int64_t n, const double* rv, const char* rvalid, const double* cv, const char* cvalid,
+                double* out) {
+  try {
+    *out = nrmse(make_map(n, rv, rvalid), make_map(n, cv, cvalid));
+    return kOk;
+  } catch (const std::exception&) {
+    return kValidation;
+  }
+}
+
+int cwref_align_and_diff(const double* ta, const double* va, std::int64_t na, const double* tb, const double* vb,
+                         std::int64_t nb, double* out) {
+  try {
+    *out = align_and_diff(make_trace(ta, va, na), make_trace(tb, vb, nb));
+    return kOk;
+  } catch (const std::exception&) {
     return kValidation;
   }
 }

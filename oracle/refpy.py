@@ -71,6 +71,10 @@ def lib():
             "cwref_res_maps": (None, [P, dp, CP, dp, CP]),
             "cwref_model_info": (I, [CP, C.POINTER(I), dp, dp, I]),
             "cwref_rates": (I, [CP, I64, dp, dp, dp, dp, dp]),
+            "cwref_compute_apd90": (I, [dp, dp, I64, dp]),
+            "cwref_compute_cv": (I, [C.c_void_p, dp, C.c_char_p, I64, I64, dp]),
+            "cwref_nrmse": (I, [I64, dp, C.c_char_p, dp, C.c_char_p, dp]),
+            "cwref_align_and_diff": (I, [dp, dp, I64, dp, dp, I64, dp]),
             "cwref_pace": (I, [CP, C.c_double, I, C.c_double, C.c_double, dp, dp, dp, dp, C.c_char_p, I]),
             "cwref_estimate_dt0": (D, [CP]),
             "cwref_reaction_substeps": (I, [D, I, I, I, I]),
@@ -121,6 +125,40 @@ def rates(name: str, v, s, i_stim):
     if lib().cwref_rates(name.encode(), n, _dp(v), _dp(s), _dp(i_stim), _dp(dv), _dp(ds)) != 0:
         raise RefError(2, f"unknown model {name}")
     return dv, ds
+
+
+def compute_apd90(t, v):
+    t, v = np.ascontiguousarray(t, np.float64), np.ascontiguousarray(v, np.float64)
+    out = C.c_double()
+    return out.value if lib().cwref_compute_apd90(_dp(t), _dp(v), len(t), C.byref(out)) else None
+
+
+def _u8(a):
+    return np.ascontiguousarray(a, np.uint8).tobytes()
+
+
+def compute_cv(sheet, lat, valid, a, b):
+    lat = np.ascontiguousarray(lat, np.float64)
+    out = C.c_double()
+    if lib().cwref_compute_cv(sheet.p, _dp(lat), _u8(valid), a, b, C.byref(out)) != 0:
+        raise RefError(2, "compute_cv: validation error")
+    return out.value
+
+
+def nrmse(rv, rvalid, cv, cvalid):
+    rv, cv = np.ascontiguousarray(rv, np.float64), np.ascontiguousarray(cv, np.float64)
+    out = C.c_double()
+    if lib().cwref_nrmse(len(rv), _dp(rv), _u8(rvalid), _dp(cv), _u8(cvalid), C.byref(out)) != 0:
+        raise RefError(2, "nrmse: validation error")
+    return out.value
+
+
+def align_and_diff(ta, va, tb, vb):
+    ta, va, tb, vb = (np.ascontiguousarray(x, np.float64) for x in (ta, va, tb, vb))
+    out = C.c_double()
+    if lib().cwref_align_and_diff(_dp(ta), _dp(va), len(ta), _dp(tb), _dp(vb), len(tb), C.byref(out)) != 0:
+        raise RefError(2, "align: validation error")
+    return out.value
 
 
 def pace(name, cycle_ms, n_beats, amp, dur):

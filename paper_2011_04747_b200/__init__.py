@@ -17,4 +17,9 @@ from .api import (  # noqa: E402
     scheme_from_string, slab_plan,
 )
 
+from . import postprocess  # noqa: E402
+from .postprocess import (  # noqa: E402
+    CompareReport, SchemeComparison, align_and_diff, compare_schemes, compute_apd90, compute_cv, nrmse,
+)
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -89,6 +89,8 @@ _SIGS = {
     "cwg_diffusion_substep": (C.c_int, [C.c_int64, _lp, _lp, _dp, _dp, _dp, C.c_double, _dp, C.c_int,
                                         C.POINTER(cwg_error)]),
     "cwg_rates": (C.c_int, [C.c_int, C.c_int64, _dp, _dp, _dp, _dp, _dp, C.c_int, C.POINTER(cwg_error)]),
+    "cwg_set_scheme": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                                 C.POINTER(cwg_error)]),
     "cwg_snapshot_begin": (C.c_int, [C.c_void_p, _dp]),
     "cwg_snapshot_wait": (C.c_int, [C.c_void_p, C.POINTER(cwg_error)]),
     "cwg_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),

@@ -626,6 +626,20 @@ class StrangIntegrator:
 
     __del__ = close
 
+    def set_scheme(self, cfg: SchemeConfig):
+        """Reconfigure scheme / dt / T / k0 on the same device-resident operator
+        (cwg_set_scheme; cli_compare, runner.cpp:254-324). The record interval
+        given at construction is kept. Upload a state and run_begin() next."""
+        cfg.validate()
+        err = L.cwg_error()
+        _check(L.lib().cwg_set_scheme(self._h, int(cfg.scheme), cfg.dt_ms, cfg.t_end_ms, cfg.k0_up, cfg.k0_down,
+                                      int(cfg.strict_substeps), C.byref(err)), err)
+        self.cfg = cfg
+        info = L.cwg_info()
+        L.lib().cwg_get_info(self._h, C.byref(info))
+        self.info = info
+        self._state_id = None
+
     # --- reference accessors
     def dt_effective(self):
         return self.info.dt_effective

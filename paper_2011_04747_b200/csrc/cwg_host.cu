@@ -217,7 +217,8 @@ struct cwg_ctx {
   long long s3_nx1 = 0, s3_nz1 = 0;  // struct3d
   double* d_coef = nullptr;  // stencil: [9][n_own]; struct3d: [classes][27]
   double* d_cm = nullptr;    // dt_ad / m_i
-  double* d_mass = nullptr;  // lumped mass of the owned rows (2D)
+  double* d_mass = nullptr;  // lumped mass: owned rows (2D / CSR) or node classes (3D)
+  long long n_mass = 0;
   long long* d_rp = nullptr;
   long long* d_col = nullptr;
   double* d_val = nullptr;
@@ -680,6 +681,44 @@ void infer_grid(cwg_problem* q) {
   q->grid_ny1 = q->n / w;
 }
 
+// Scheme-dependent quantities (StrangIntegrator ctor, splitting.cpp:74-93;
+// run_simulation's step counts and record cadences, :225-240).
+void configure_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int k0_up, int k0_down, int strict) {
+  validation(dt_ms > 0.0, "scheme: dt must be positive");
+  validation(t_end_ms >= dt_ms, "scheme: T must be >= dt");
+  validation(k0_down >= 1 && k0_up >= k0_down, "scheme: need k0_up >= k0_down >= 1");
+  validation(scheme >= CWG_OST && scheme <= CWG_DAETI, "scheme: unknown scheme");
+  c->scheme = scheme;
+  c->dt = dt_ms;
+  c->t_end = t_end_ms;
+  c->k0_up = k0_up;
+  c->k0_down = k0_down;
+  c->strict = strict;
+  c->dt_eff = c->scheme == CWG_OSTAR ? std::min(c->dt, c->dt_s) : c->dt;
+  {
+    int l = 0;
+    double dt_ad = 0;
+    cwg_diffusion_substeps(c->dt_eff, c->dt_s, c->strict, c->scheme, &l, &dt_ad);
+    c->l = l;
+    c->dt_ad = dt_ad;
+  }
+  c->evs = 3ll * c->l + 2;
+  c->kmax_of_model.clear();
+  c->kmax_global = 0;
+  for (int kind : c->model_kind) {
+    c->kmax_of_model.push_back(kmax_for(c->dt_eff, kind));
+    c->kmax_global = std::max(c->kmax_global, c->kmax_of_model.back());
+  }
+  validation(c->kmax_global < 2048, "integrator: k_max >= 2048 is not supported");
+  c->khist_len = c->kmax_global + 1;
+  c->n_steps = static_cast<long long>(std::ceil(c->t_end / c->dt_eff - 1e-9));
+  c->spr = std::max<long long>(1, llround_ref(c->record_interval / c->dt_eff));
+  c->spm = std::max<long long>(1, llround_ref(c->map_interval / c->dt_eff));
+  c->n_samples = c->n_steps / c->spr + 1;
+  const long long G = lcm_ll(c->spr, c->spm);  // graph block: a multiple of both record cadences
+  c->G = G <= 200 ? G : 0;
+}
+
 void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   validation(p_in != nullptr, "integrator: empty problem");
   cwg_problem pc = *p_in;
@@ -688,11 +727,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   validation(p->n > 0, "integrator: empty problem");
   validation(p->lumped_mass != nullptr || p->op_kind == CWG_OP_STRUCT3D, "integrator: missing assembled operator");
   validation(p->n_models > 0 && p->model_kind, "integrator: no cell models");
-  validation(p->dt_ms > 0.0, "scheme: dt must be positive");
-  validation(p->t_end_ms >= p->dt_ms, "scheme: T must be >= dt");
-  validation(p->k0_down >= 1 && p->k0_up >= p->k0_down, "scheme: need k0_up >= k0_down >= 1");
   validation(p->record_interval_ms > 0.0, "scheme: record interval must be positive");
-  validation(p->scheme >= CWG_OST && p->scheme <= CWG_DAETI, "scheme: unknown scheme");
   validation(p->dt_s > 0.0, "diffusion sub-steps: dt and dt_s must be positive");
   validation(p->world >= 1 && p->rank >= 0 && p->rank < p->world, "placement: bad rank/world");
   validation(p->n < (1ll << 40), "integrator: at most 2^40 nodes");
@@ -708,37 +743,16 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
 
   // ---- scheme (StrangIntegrator ctor, splitting.cpp:74-93)
-  c->scheme = p->scheme;
-  c->dt = p->dt_ms;
   c->dt_s = p->dt_s;
-  c->t_end = p->t_end_ms;
-  c->k0_up = p->k0_up;
-  c->k0_down = p->k0_down;
-  c->strict = p->strict_substeps;
   c->record_interval = p->record_interval_ms;
   c->map_interval = p->map_interval_ms > 0.0 ? p->map_interval_ms : 1.0;
-  c->dt_eff = c->scheme == CWG_OSTAR ? std::min(c->dt, c->dt_s) : c->dt;
-  {
-    int l = 0;
-    double dt_ad = 0;
-    cwg_diffusion_substeps(c->dt_eff, c->dt_s, c->strict, c->scheme, &l, &dt_ad);
-    c->l = l;
-    c->dt_ad = dt_ad;
-  }
-  c->evs = 3ll * c->l + 2;
   c->model_kind.assign(p->model_kind, p->model_kind + p->n_models);
   c->stride = 1;
   for (int m = 0; m < p->n_models; ++m) {
     validation(state_count(c->model_kind[m]) >= 0, "integrator: unknown model kind " + std::to_string(c->model_kind[m]));
-    c->kmax_of_model.push_back(kmax_for(c->dt_eff, c->model_kind[m]));
-    c->kmax_global = std::max(c->kmax_global, c->kmax_of_model.back());
     c->stride = std::max(c->stride, state_count(c->model_kind[m]));
   }
-  validation(c->kmax_global < 2048, "integrator: k_max >= 2048 is not supported");
-  c->khist_len = c->kmax_global + 1;
-  c->n_steps = static_cast<long long>(std::ceil(c->t_end / c->dt_eff - 1e-9));
-  c->spr = std::max<long long>(1, llround_ref(c->record_interval / c->dt_eff));
-  c->spm = std::max<long long>(1, llround_ref(c->map_interval / c->dt_eff));
+  configure_scheme(c, p->scheme, p->dt_ms, p->t_end_ms, p->k0_up, p->k0_down, p->strict_substeps);
 
   // ---- partition and operator layout
   std::vector<double> s3_coef, s3_mass;
@@ -812,16 +826,17 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
 
   // ---- operator upload
   if (kind == CWG_OP_STRUCT3D) {
-    double* d_mass = upload(s3_mass.data(), s3_mass.size());
+    c->d_mass = upload(s3_mass.data(), s3_mass.size());
+    c->n_mass = static_cast<long long>(s3_mass.size());
     c->d_cm = dev_alloc<double>(s3_mass.size());
-    CUDA_TRY(launch_mass_factor(d_mass, static_cast<long long>(s3_mass.size()), c->dt_ad, c->d_cm, c->stream));
+    CUDA_TRY(launch_mass_factor(c->d_mass, c->n_mass, c->dt_ad, c->d_cm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    dev_free(d_mass);
     c->d_coef = upload(s3_coef.data(), s3_coef.size());
   } else {
     validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
     std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
     c->d_mass = upload(mass_own.data(), mass_own.size());
+    c->n_mass = c->n_own;
     c->d_cm = dev_alloc<double>(c->n_own);
     CUDA_TRY(launch_mass_factor(c->d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -925,7 +940,6 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   // ---- recording
   c->lat_threshold = p->lat_threshold_mv;
   c->n_probes = p->n_probes;
-  c->n_samples = c->n_steps / c->spr + 1;
   if (c->n_probes > 0) {
     std::vector<long long> loc(static_cast<size_t>(c->n_probes), -1);
     for (int q = 0; q < c->n_probes; ++q) {
@@ -944,10 +958,6 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->det.has_lat = dev_alloc<unsigned char>(c->n_own);
   c->det.has_apd = dev_alloc<unsigned char>(c->n_own);
   c->det.threshold = c->lat_threshold;
-
-  // ---- graph block length: a multiple of both record cadences
-  const long long G = lcm_ll(c->spr, c->spm);
-  c->G = G <= 200 ? G : 0;
 
   // ---- NCCL communicator for the halo exchange
   if (c->world > 1) {
@@ -1049,7 +1059,7 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
 // recompute cm = dt_ad / m after dt_ad changed (fixed-step mode)
 cudaError_t launch_mass_factor_fix(cwg_ctx* c) {
   if (!c->d_mass) return cudaErrorNotSupported;
-  const cudaError_t e = launch_mass_factor(c->d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream);
+  const cudaError_t e = launch_mass_factor(c->d_mass, c->n_mass, c->dt_ad, c->d_cm, c->stream);
   if (e != cudaSuccess) return e;
   return cudaStreamSynchronize(c->stream);
 }
@@ -1230,6 +1240,31 @@ int cwg_download_state(cwg_ctx* c, double* v, double* s_aos, int stride, double*
       }
     }
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int cwg_set_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int k0_up, int k0_down,
+                   int strict_substeps, cwg_error* err) {
+  return guarded(err, [&] {
+    validation(!c->fixed_step, "scheme: not available on a threshold probe context");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const long long old_khist = c->khist_len, old_samples = c->n_samples;
+    configure_scheme(c, scheme, dt_ms, t_end_ms, k0_up, k0_down, strict_substeps);
+    if (c->khist_len != old_khist) {
+      dev_free(c->d_khist);
+      c->d_khist = dev_alloc<unsigned long long>(c->khist_len);
+    }
+    CUDA_TRY(cudaMemset(c->d_khist, 0, c->khist_len * sizeof(unsigned long long)));
+    if (c->n_probes > 0 && c->n_samples != old_samples) {
+      dev_free(c->d_traces);
+      c->d_traces = dev_alloc<double>(static_cast<size_t>(c->n_samples) * c->n_probes);
+    }
+    CUDA_TRY(launch_mass_factor_fix(c));  // cm = dt_ad / m for the new dt_ad (same division)
+    if (c->graph) {
+      cudaGraphExecDestroy(c->graph);
+      c->graph = nullptr;
+    }
   });
 }
 

@@ -290,3 +290,34 @@ def test_async_snapshots_stop_at_abort(cw, ora, problems):
         cw.run_simulation(p.initial_state(), setup, p.cfg)
     assert (e.value.node_index, e.value.time_ms) == (16, 2.04)
     assert [round(t, 9) for t in snaps] == [0.0, 0.5, 1.0, 1.5, 2.0]
+
+
+def test_compare_schemes_one_device_operator(cw, ora, problems):
+    """cli_compare (runner.cpp:254-324) on one integrator: each scheme's run,
+    after cwg_set_scheme on the resident operator, equals a fresh integrator's
+    run bit for bit, and the metrics are the reference's functions of them."""
+    from paper_2011_04747_b200 import postprocess as pp
+    p = problems.c1(model="aliev-panfilov", t_end=400.0, k0_down=1)  # long enough to repolarise (APD maps)
+    p.probes = [p.sheet.nearest(0.2, 0.5), p.sheet.nearest(0.8, 0.5)]
+    setup = p.setup()
+    rep = pp.compare_schemes(p.initial_state(), setup, p.cfg, p.sheet.coords, reference="OST",
+                             model_of_node=p.model_of_node)
+    assert rep.reference == "OST" and [c.scheme for c in rep.schemes] == ["OST", "OSTAR", "DAETI"]
+    for c in rep.schemes:
+        sch = cw.scheme_from_string(c.scheme)
+        sc = cw.SchemeConfig(scheme=sch, dt_ms=0.01 if sch == cw.Scheme.OST else 0.1, t_end_ms=400.0,
+                             k0_up=p.cfg.k0_up, k0_down=p.cfg.k0_down)
+        fresh = cw.run_simulation(p.initial_state(), setup, sc)
+        assert np.array_equal(c.result.final_state.v, fresh.final_state.v), c.scheme
+        assert np.array_equal(c.result.k_histogram, fresh.k_histogram), c.scheme
+        assert np.array_equal(c.result.traces[0].v_mv, fresh.traces[0].v_mv), c.scheme
+        if c.scheme == "DAETI":  # and against the oracle
+            o = oracle_run(p, scheme="DAETI", dt=0.1, t_end=400.0)
+            assert np.array_equal(c.result.final_state.v, o["v"])
+        assert c.cv_cm_per_ms > 0 and math.isfinite(c.cv_cm_per_ms)
+    ost = rep.schemes[0]
+    assert ost.e_lat == 0.0 and ost.max_dv_per_probe == [0.0, 0.0]
+    for c in rep.schemes[1:]:
+        assert c.e_lat == pp.nrmse(ost.result.lat_map, c.result.lat_map) and 0.0 < c.e_lat < 0.5
+        assert c.e_apd == pp.nrmse(ost.result.apd90_map, c.result.apd90_map)
+        assert all(math.isfinite(a) for a in c.apd90_per_probe) and all(d >= 0 for d in c.max_dv_per_probe)
