@@ -18,6 +18,7 @@
 #include "cardwave/fem.hpp"
 #include "cardwave/ionic.hpp"
 #include "cardwave/mesh.hpp"
+#include "cardwave/output.hpp"
 #include "cardwave/postprocess.hpp"
 #include "cardwave/splitting.hpp"
 #include "cardwave/stimulus.hpp"
@@ -455,6 +456,56 @@ int cwref_align_and_diff(const double* ta, const double* va, std::int64_t na, co
     return kOk;
   } catch (const std::exception&) {
     return kValidation;
+  }
+}
+
+// ---------------------------------------------------------------- writers (output.cpp, ionic.cpp:13-57)
+int cwref_write_vtk_snapshot(cwref_problem* p, const double* v, double t, const char* path) {
+  try {
+    write_vtk_snapshot(p->mesh, std::vector<double>(v, v + p->mesh.node_count()), t, path);
+    return kOk;
+  } catch (const std::exception&) {
+    return kIo;
+  }
+}
+
+int cwref_write_map(cwref_problem* p, const double* value, const char* valid, const char* name, int vtk,
+                    const char* path) {
+  try {
+    const ScalarMap m = make_map(p->mesh.node_count(), value, valid);
+    if (vtk)
+      write_map_vtk(p->mesh, m, name, path);
+    else
+      write_map_csv(p->mesh, m, path);
+    return kOk;
+  } catch (const std::exception&) {
+    return kIo;
+  }
+}
+
+int cwref_write_trace_csv(const double* t, const double* v, std::int64_t n, const char* path) {
+  try {
+    write_trace_csv(make_trace(t, v, n), path);
+    return kOk;
+  } catch (const std::exception&) {
+    return kIo;
+  }
+}
+
+int cwref_state_save(std::int64_t n, int stride, const double* v, const double* s, const double* last,
+                     const std::uint8_t* mon, const char* path) {
+  try {
+    NodeStateArray a;
+    a.n_nodes = n;
+    a.stride = stride;
+    a.v.assign(v, v + n);
+    a.s.assign(s, s + n * stride);
+    a.last_dvdt.assign(last, last + n);
+    a.model_of_node.assign(mon, mon + n);
+    a.save(path);
+    return kOk;
+  } catch (const std::exception&) {
+    return kIo;
   }
 }
 

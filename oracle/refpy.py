@@ -75,6 +75,10 @@ def lib():
             "cwref_compute_cv": (I, [C.c_void_p, dp, C.c_char_p, I64, I64, dp]),
             "cwref_nrmse": (I, [I64, dp, C.c_char_p, dp, C.c_char_p, dp]),
             "cwref_align_and_diff": (I, [dp, dp, I64, dp, dp, I64, dp]),
+            "cwref_write_vtk_snapshot": (I, [C.c_void_p, dp, C.c_double, CP]),
+            "cwref_write_map": (I, [C.c_void_p, dp, C.c_char_p, CP, I, CP]),
+            "cwref_write_trace_csv": (I, [dp, dp, I64, CP]),
+            "cwref_state_save": (I, [I64, I, dp, dp, dp, C.c_char_p, CP]),
             "cwref_pace": (I, [CP, C.c_double, I, C.c_double, C.c_double, dp, dp, dp, dp, C.c_char_p, I]),
             "cwref_estimate_dt0": (D, [CP]),
             "cwref_reaction_substeps": (I, [D, I, I, I, I]),
@@ -159,6 +163,26 @@ def align_and_diff(ta, va, tb, vb):
     if lib().cwref_align_and_diff(_dp(ta), _dp(va), len(ta), _dp(tb), _dp(vb), len(tb), C.byref(out)) != 0:
         raise RefError(2, "align: validation error")
     return out.value
+
+
+def write_vtk_snapshot(sheet, v, t, path):
+    v = np.ascontiguousarray(v, np.float64)
+    assert lib().cwref_write_vtk_snapshot(sheet.p, _dp(v), t, path.encode()) == 0
+
+
+def write_map(sheet, value, valid, name, vtk, path):
+    value = np.ascontiguousarray(value, np.float64)
+    assert lib().cwref_write_map(sheet.p, _dp(value), _u8(valid), name.encode(), int(vtk), path.encode()) == 0
+
+
+def write_trace_csv(t, v, path):
+    t, v = np.ascontiguousarray(t, np.float64), np.ascontiguousarray(v, np.float64)
+    assert lib().cwref_write_trace_csv(_dp(t), _dp(v), len(t), path.encode()) == 0
+
+
+def state_save(n, stride, v, s, last, mon, path):
+    v, s, last = (np.ascontiguousarray(x, np.float64) for x in (v, s, last))
+    assert lib().cwref_state_save(n, stride, _dp(v), _dp(s), _dp(last), _u8(mon), path.encode()) == 0
 
 
 def pace(name, cycle_ms, n_beats, amp, dur):

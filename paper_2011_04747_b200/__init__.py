@@ -17,7 +17,7 @@ from .api import (  # noqa: E402
     scheme_from_string, slab_plan,
 )
 
-from . import postprocess  # noqa: E402
+from . import output, postprocess  # noqa: E402
 from .postprocess import (  # noqa: E402
     CompareReport, SchemeComparison, align_and_diff, compare_schemes, compute_apd90, compute_cv, nrmse,
 )
