@@ -46,11 +46,8 @@ DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt
 
 def diffusion_launches(count, fuse):
     """Launches enqueue_diffusion (cwg_host.cu) uses for `count` sub-steps when
-    up to `fuse` are fused per launch (launch count keeps the parity of count)."""
-    m = -(-count // fuse)
-    if (m - count) % 2:
-        m += 1
-    return m
+    up to `fuse` are fused per launch."""
+    return -(-count // fuse)
 
 
 def load_peaks():

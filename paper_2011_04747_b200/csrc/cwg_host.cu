@@ -247,7 +247,11 @@ struct cwg_ctx {
 
   // graphs
   long long G = 0;
-  cudaGraphExec_t graph = nullptr;
+  // one G-step graph per starting V-buffer parity (a block may flip it when
+  // fused diffusion launches make the per-step launch count odd)
+  cudaGraphExec_t graph_p[2] = {nullptr, nullptr};
+  int graph_cur_after[2] = {0, 0};
+  bool graph_built = false;
   long long graph_base_mod = 0;
   long long graph_launches = 0;
   long long clock_at = -1;  // host knowledge of *d_clock, -1 unknown
@@ -290,7 +294,8 @@ namespace {
 void ctx_free(cwg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto& gx : c->graph_p)
+    if (gx) cudaGraphExecDestroy(gx);
   for (auto& b : c->bins) {
     dev_free(b.d_list);
     dev_free(b.d_counter);
@@ -375,11 +380,10 @@ int diffusion_fuse(const cwg_ctx* c) {
 }
 
 void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
-  // Launches m >= ceil(count / fuse) with m = count (mod 2): every launch flips
-  // the V double buffer, and captured step graphs must keep its parity.
+  // m = ceil(count / fuse) launches with balanced group sizes; every launch
+  // flips the V double buffer (graphs are kept per starting parity).
   const int fuse = diffusion_fuse(c);
-  int m = (count + fuse - 1) / fuse;
-  if ((m - count) & 1) ++m;
+  const int m = (count + fuse - 1) / fuse;
   for (int q = 0, launch = 0; q < count; ++launch) {
     const int left = m - launch;
     const int T = (count - q + left - 1) / left;  // balanced group sizes
@@ -503,10 +507,12 @@ void build_graph(cwg_ctx* c, long long b0) {
   CUDA_TRY(cudaStreamEndCapture(c->stream, &g));
   c->graph_launches = c->launches - l0 + 1;
   c->launches = l0;
-  CUDA_TRY(cudaGraphInstantiate(&c->graph, g, 0));
+  CUDA_TRY(cudaGraphInstantiate(&c->graph_p[cur0], g, 0));
   cudaGraphDestroy(g);
-  if (c->cur != cur0) throw Fail{CWG_ECUDA, "graph block must preserve the V buffer parity"};
+  c->graph_cur_after[cur0] = c->cur;  // capture only recorded the flips
+  c->cur = cur0;
   c->graph_base_mod = ((b0 % c->G) + c->G) % c->G;
+  c->graph_built = true;
 }
 
 // One middle step as a graph (bench timing: the production launch path,
@@ -519,6 +525,7 @@ struct StepGraph {
   cudaGraphExec_t exec = nullptr;
   cudaGraphNode_t ev_nodes[3] = {nullptr, nullptr, nullptr};
   long long launches = 0;
+  int cur_after = 0;
 };
 
 void free_step_graph(StepGraph& sg) {
@@ -532,7 +539,7 @@ void free_step_graph(StepGraph& sg) {
 StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   const long long S = step + 1;
   const int flags = ((c->n_probes > 0 && S % c->spr == 0) ? 1 : 0) | (S % c->spm == 0 ? 2 : 0);
-  StepGraph& sg = cache[flags];
+  StepGraph& sg = cache[flags | (c->cur << 2)];  // per recording pattern and starting V-buffer parity
   if (sg.exec) return sg;
   cudaGraph_t g = nullptr;
   const int cur0 = c->cur;
@@ -587,7 +594,8 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   }
   if (found != 3) throw Fail{CWG_ECUDA, "step graph: event nodes not found"};
   CUDA_TRY(cudaGraphInstantiate(&sg.exec, g, 0));
-  if (c->cur != cur0) throw Fail{CWG_ECUDA, "step graph must preserve the V buffer parity"};
+  sg.cur_after = c->cur;
+  c->cur = cur0;
   return sg;
 }
 
@@ -1261,10 +1269,12 @@ int cwg_set_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int k0
       c->d_traces = dev_alloc<double>(static_cast<size_t>(c->n_samples) * c->n_probes);
     }
     CUDA_TRY(launch_mass_factor_fix(c));  // cm = dt_ad / m for the new dt_ad (same division)
-    if (c->graph) {
-      cudaGraphExecDestroy(c->graph);
-      c->graph = nullptr;
-    }
+    for (auto& gx : c->graph_p)
+      if (gx) {
+        cudaGraphExecDestroy(gx);
+        gx = nullptr;
+      }
+    c->graph_built = false;
   });
 }
 
@@ -1414,11 +1424,12 @@ int cwg_run_steps(cwg_ctx* c, int64_t first, int64_t count) {
     const long long end = first + count;
     while (s < end) {
       const bool block_ok = c->G > 0 && s >= 1 && s + c->G <= c->n_steps - 1 && s + c->G <= end &&
-                            (c->graph == nullptr ? (s % c->G == 1 % c->G) : (s % c->G == c->graph_base_mod));
+                            (!c->graph_built ? (s % c->G == 1 % c->G) : (s % c->G == c->graph_base_mod));
       if (block_ok) {
         set_clock(c, s);
-        if (!c->graph) build_graph(c, s);
-        CUDA_TRY(cudaGraphLaunch(c->graph, c->stream));
+        if (!c->graph_p[c->cur]) build_graph(c, s);
+        CUDA_TRY(cudaGraphLaunch(c->graph_p[c->cur], c->stream));
+        c->cur = c->graph_cur_after[c->cur];
         c->launches += c->graph_launches;
         c->clock_at = s + c->G;
         s += c->G;
@@ -1562,7 +1573,7 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
       c->flush_bytes = static_cast<size_t>(flush_bytes);
     }
     constexpr int kChunk = 256;
-    StepGraph graphs[4];
+    StepGraph graphs[8];
     std::vector<cudaEvent_t> ev(3 * kChunk);
     for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
     try {
@@ -1580,6 +1591,7 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
             for (int q = 0; q < 3; ++q)
               CUDA_TRY(cudaGraphExecEventRecordNodeSetEvent(sg.exec, sg.ev_nodes[q], ev[3 * i + q]));
             CUDA_TRY(cudaGraphLaunch(sg.exec, c->stream));
+            c->cur = sg.cur_after;
             c->launches += sg.launches;
             continue;
           }
