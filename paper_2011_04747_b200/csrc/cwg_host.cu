@@ -638,11 +638,14 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
   c->d_coef = upload(coef.data(), coef.size());
 }
 
-// ORd launch shape: one persistent lockstep block per SM. Latency regime
-// (the bin fits into <= 10 warps per SM, e.g. C2's 40k nodes): the smallest
-// block that holds EVERY node in one round (256 / 288 / 320 threads with
-// 252 / 224 / 204 registers) -- a second round of nodes per lane would double
-// the step's makespan. Throughput regime: 384 threads x 168 registers.
+// ORd launch shape. Throughput regime (many nodes per lane): one persistent
+// 384-thread block per SM (<= 168 registers) whose warps advance in lockstep
+// -- free-running warps drift apart and thrash the 32 KB L1.5 instruction
+// cache with the ~40 KB body (C3: 0.65 ms lockstep vs 1.12 ms free-running).
+// Latency regime (the bin fits into <= 10 warps per SM, e.g. C2's 40k nodes:
+// about one node per lane): two free-running 128-thread blocks per SM with up
+// to 255 registers -- there the per-evaluation barrier only adds waiting (C2
+// reaction 53.6 us vs 59.0 us for the best lockstep shape).
 int choose_ord_variant(long long count, int num_sms) {
   if (const char* e = getenv("CWG_ORD_VARIANT")) {
     const int v = atoi(e);
@@ -650,9 +653,7 @@ int choose_ord_variant(long long count, int num_sms) {
   }
   const int pf = getenv("CWG_ORD_PREFETCH") && atoi(getenv("CWG_ORD_PREFETCH")) ? 16 : 0;
   const long long warps_per_sm = (count + 32ll * num_sms - 1) / (32ll * num_sms);
-  if (warps_per_sm <= 8) return 2 | pf;
-  if (warps_per_sm == 9) return 7 | pf;
-  if (warps_per_sm == 10) return 8 | pf;
+  if (warps_per_sm <= 10) return 0 | pf;
   return 1 | pf;
 }
 
