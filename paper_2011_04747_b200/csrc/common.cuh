@@ -137,6 +137,7 @@ struct Struct3D {
   long long planes;           // owned y-planes
   long long row_begin;        // global y of owned plane 0
   long long ny1;
+  int ychunk = 16;            // y-planes marched per block (launch_diffuse_struct3d)
 };
 
 struct CsrDev {

@@ -410,7 +410,7 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
         CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
     } else if (c->op_kind == CWG_OP_STRUCT3D) {
       Struct3D s{c->d_coef, c->d_cm, c->s3_nx1, c->s3_nz1, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
-      CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms * 16, c->stream));
+      CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms, c->stream));
     } else {
       CsrDev m{c->d_rp, c->d_col, c->d_val, c->d_cm};
       CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));

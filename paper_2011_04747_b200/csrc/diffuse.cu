@@ -3,6 +3,10 @@
 // like the reference's x86-64 build, so diffusion is bit-identical to
 // diffusion_substep (fem.cpp:194-207) and the detector to
 // ActivationDetector::observe (postprocess.cpp:18-66).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
 #include "launch.h"
 
 namespace cwg {
@@ -246,71 +250,125 @@ cudaError_t launch_diffuse_stencil2d_tb(int T, const DiffArgs& a, const Stencil2
 // a shared-memory ring, so each V value is fetched from global memory ~1.3x
 // per sub-step instead of up to 27x. No 64-bit division: (x, z, y) come from
 // the launch geometry.
-constexpr int S3_TX = 32, S3_TZ = 8, S3_YCHUNK = 16;
+constexpr int S3_TX = 32, S3_TZ = 8;
 
-__global__ void __launch_bounds__(S3_TX * S3_TZ) diffuse_struct3d(DiffArgs a, Struct3D s) {
+__global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a, Struct3D s) {
+  constexpr int NT = S3_TX * S3_TZ;
   constexpr int PX = S3_TX + 2, PZ = S3_TZ + 2, PL = PX * PZ;
-  __shared__ double ring[3][PL];
+  constexpr int PR = (PL + NT - 1) / NT;  // plane values per thread
+  __shared__ double ring[4][PL];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
   const int tx = threadIdx.x % S3_TX, tz = threadIdx.x / S3_TX;
-  const long long x0 = static_cast<long long>(blockIdx.x) * S3_TX, z0 = static_cast<long long>(blockIdx.y) * S3_TZ;
-  const long long ix = x0 + tx, iz = z0 + tz;
-  const long long nx = s.nx1 - 1, nz = s.nz1 - 1;
-  const long long yb = static_cast<long long>(blockIdx.z) * S3_YCHUNK;
-  const long long ye = yb + S3_YCHUNK < s.planes ? yb + S3_YCHUNK : s.planes;
-  const bool inside = ix < s.nx1 && iz < s.nz1;
-  // load local plane yl (-1..planes) into ring slot (halo planes are valid memory)
-  auto load = [&](long long yl, int slot) {
-    const long long base = (yl + 1) * s.plane;  // local index of (0, yl, 0)
-    for (int t = threadIdx.x; t < PL; t += S3_TX * S3_TZ) {
-      const long long lx = x0 - 1 + t % PX, lz = z0 - 1 + t / PX;
-      double val = 0.0;
-      if (lx >= 0 && lx < s.nx1 && lz >= 0 && lz < s.nz1) val = a.vin[base + lz * s.nx1 + lx];
-      ring[slot][t] = val;
-    }
+  const int x0 = blockIdx.x * S3_TX, z0 = blockIdx.y * S3_TZ;
+  const int ix = x0 + tx, iz = z0 + tz;
+  const int nx1 = static_cast<int>(s.nx1), nz1 = static_cast<int>(s.nz1);
+  const int nx = nx1 - 1, nz = nz1 - 1;
+  const long long yb = static_cast<long long>(blockIdx.z) * s.ychunk;
+  const long long ye = yb + s.ychunk < s.planes ? yb + s.ychunk : s.planes;
+  const bool inside = ix < nx1 && iz < nz1;
+  // this thread's share of a (tile + halo) plane: offsets within the plane, or -1
+  int off[PR];
+#pragma unroll
+  for (int r = 0; r < PR; ++r) {
+    const int t = threadIdx.x + r * NT;
+    const int lx = x0 - 1 + t % PX, lz = z0 - 1 + t / PX;
+    off[r] = (t < PL && lx >= 0 && lx < nx1 && lz >= 0 && lz < nz1) ? lz * nx1 + lx : -1;
+  }
+  // planes yl = -1 .. planes are valid memory (halo planes); beyond: zeros
+  auto fetch = [&](long long yl, double (&reg)[PR]) {
+    const double* src = a.vin + (yl + 1) * s.plane;
+#pragma unroll
+    for (int r = 0; r < PR; ++r) reg[r] = (off[r] >= 0 && yl <= s.planes) ? src[off[r]] : 0.0;
+  };
+  auto put = [&](const double (&reg)[PR], double* dst) {
+#pragma unroll
+    for (int r = 0; r < PR; ++r)
+      if (threadIdx.x + r * NT < PL) dst[threadIdx.x + r * NT] = reg[r];
   };
   const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
-  load(yb - 1, (yb + 2) % 3);
-  load(yb, yb % 3);
+  // Interior in x and z: all 27 neighbours exist on every y-interior plane;
+  // the row's class (by = 1, bx, iz) is fixed for the whole march. Its
+  // coefficients are read through the read-only cache: a warp spans one z
+  // layer, so every load is a warp-uniform broadcast (registers would cut the
+  // occupancy this latency-bound loop needs).
+  const bool xz_interior = inside && bx == 1 && iz > 0 && iz < nz;
+  const double* cfi = s.coef + ((3 + bx) * static_cast<long long>(nz1) + iz) * 27;
+  const double* cmp = s.cm + (3 + bx) * static_cast<long long>(nz1) + iz;
+  // 4-slot ring: planes y-1, y, y+1 are read while y+2 (prefetched into
+  // registers one trip earlier) is written -- one barrier per plane, and the
+  // global loads of a plane overlap the previous plane's arithmetic.
+  double* pm = ring[0];  // y - 1
+  double* p0 = ring[1];  // y
+  double* pp = ring[2];  // y + 1
+  double* pw = ring[3];  // y + 2 (being written)
+  double reg[PR];
+  fetch(yb - 1, reg);
+  put(reg, pm);
+  fetch(yb, reg);
+  put(reg, p0);
+  fetch(yb + 1, reg);
+  put(reg, pp);
+  fetch(yb + 2, reg);
+  __syncthreads();
+  const int c0 = (tz + 1) * PX + (tx + 1);
   for (long long yl = yb; yl < ye; ++yl) {
-    load(yl + 1, (yl + 1) % 3);
-    __syncthreads();
     if (inside) {
-      const long long i = (yl + 1) * s.plane + iz * s.nx1 + ix;
-      const double* pc = ring[yl % 3];
-      const int c0 = (tz + 1) * PX + (tx + 1);
-      const double vi = pc[c0];
+      const long long i = (yl + 1) * s.plane + static_cast<long long>(iz) * nx1 + ix;
+      const double vi = p0[c0];
+      const long long gy = s.row_begin + yl;
+      const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
       if (skip) {
         a.vout[i] = vi;
       } else {
-        const long long gy = s.row_begin + yl;
-        const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
-        const long long cls = (by * 3 + bx) * s.nz1 + iz;
-        const double* cf = s.coef + cls * 27;
-        double acc = 0.0;
+        double out;
+        const double* pl[3] = {pm, p0, pp};
+        if (xz_interior && by == 1) {
+          // the full 27-point row in ascending column order (dy, dz, dx)
+          double acc = 0.0;
 #pragma unroll
-        for (int dy = -1; dy <= 1; ++dy) {
-          if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
-          const double* pl = ring[(yl + 3 + dy) % 3];
+          for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-          for (int dz = -1; dz <= 1; ++dz) {
-            if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+            for (int dz = -1; dz <= 1; ++dz)
 #pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-              if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
-              const int q = (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1);
-              acc += __ldg(cf + q) * pl[c0 + dz * PX + dx];
+              for (int dx = -1; dx <= 1; ++dx)
+                acc += __ldg(cfi + dy * 9 + (dz + 1) * 3 + (dx + 1)) * pl[dy][c0 + dz * PX + dx];
+          out = vi - __ldg(cmp) * acc;
+        } else {
+          const long long cls = (by * 3 + bx) * static_cast<long long>(nz1) + iz;
+          const double* cf = s.coef + cls * 27;
+          double acc = 0.0;
+#pragma unroll
+          for (int dy = -1; dy <= 1; ++dy) {
+            if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+#pragma unroll
+            for (int dz = -1; dz <= 1; ++dz) {
+              if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+#pragma unroll
+              for (int dx = -1; dx <= 1; ++dx) {
+                if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
+                const int q = (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1);
+                acc += __ldg(cf + q) * pl[dy + 1][c0 + dz * PX + dx];
+              }
             }
           }
+          out = vi - __ldg(s.cm + cls) * acc;
         }
-        const double out = vi - __ldg(s.cm + cls) * acc;
         a.vout[i] = out;
         if (!isfinite(out))
           record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2);
       }
     }
-    __syncthreads();  // slot (yl+2)%3 is overwritten next trip
+    if (yl + 1 < ye) {
+      put(reg, pw);        // plane yl + 2
+      fetch(yl + 3, reg);  // in flight during the next trip
+    }
+    __syncthreads();
+    double* t = pm;
+    pm = p0;
+    p0 = pp;
+    pp = pw;
+    pw = t;
   }
 }
 
@@ -495,9 +553,33 @@ cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int 
   return cudaGetLastError();
 }
 
-cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int, cudaStream_t st) {
+// The y-chunk trades halo-plane reloads (a block loads chunk + 3 planes)
+// against parallelism for this latency-bound loop: the largest chunk in
+// [4, 16] that still gives >= 4 waves of resident blocks (C4: 4, C5: 16;
+// measured C4 0.140 / 0.153 / 0.163 ms per step at 4 / 8 / 16, C5 flat).
+// CWG_S3_YCHUNK overrides for experiments.
+cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s_in, int num_sms, cudaStream_t st) {
+  static int capacity = 0;
+  if (capacity == 0) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, diffuse_struct3d, S3_TX * S3_TZ, 0);
+    capacity = std::max(1, per_sm) * num_sms;
+  }
+  static const int forced = [] {
+    const char* e = getenv("CWG_S3_YCHUNK");
+    return e ? atoi(e) : 0;
+  }();
+  Struct3D s = s_in;
+  const long long xz = ((s.nx1 + S3_TX - 1) / S3_TX) * ((s.nz1 + S3_TZ - 1) / S3_TZ);
+  s.ychunk = 4;
+  for (int ch = 16; ch >= 4; --ch)
+    if (xz * ((s.planes + ch - 1) / ch) >= 4ll * capacity) {
+      s.ychunk = ch;
+      break;
+    }
+  if (forced > 0) s.ychunk = forced;
   const dim3 grid(static_cast<unsigned>((s.nx1 + S3_TX - 1) / S3_TX), static_cast<unsigned>((s.nz1 + S3_TZ - 1) / S3_TZ),
-                  static_cast<unsigned>((s.planes + S3_YCHUNK - 1) / S3_YCHUNK));
+                  static_cast<unsigned>((s.planes + s.ychunk - 1) / s.ychunk));
   diffuse_struct3d<<<grid, S3_TX * S3_TZ, 0, st>>>(a, s);
   return cudaGetLastError();
 }
