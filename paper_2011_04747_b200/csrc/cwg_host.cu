@@ -4,6 +4,7 @@
 // outer loop with its record cadence (splitting.cpp:219-294), replayed as
 // CUDA graphs; y-slab halo exchange over NCCL for world > 1.
 #include <dlfcn.h>
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -217,6 +218,12 @@ struct cwg_ctx {
   long long s3_nx1 = 0, s3_nz1 = 0;  // struct3d
   double* d_coef = nullptr;  // stencil: [9][n_own]; struct3d: [classes][27]
   double* d_cm = nullptr;    // dt_ad / m_i
+  // padded coefficient tensor for the TMA diffusion kernel (2D, one device):
+  // [10][rows][w_pad], planes 0..8 = coef, 9 = dt/m; tensor maps for T = 2..4
+  double* d_coefp = nullptr;
+  long long w_pad = 0;
+  CUtensorMap tmap[5];
+  bool tma_ok = false;
   double* d_mass = nullptr;  // lumped mass: owned rows (2D / CSR) or node classes (3D)
   long long n_mass = 0;
   long long* d_rp = nullptr;
@@ -308,6 +315,7 @@ void ctx_free(cwg_ctx* c) {
   dev_free(c->d_coef);
   dev_free(c->d_cm);
   dev_free(c->d_mass);
+  dev_free(c->d_coefp);
   dev_free(c->d_rp);
   dev_free(c->d_col);
   dev_free(c->d_val);
@@ -372,6 +380,54 @@ void halo_exchange(cwg_ctx* c, double* buf) {
   NCCL_TRY(g_nccl.gend());
 }
 
+// Build the padded coefficient tensor and its TMA descriptors (2D sheet on
+// one device). Any failure just leaves the register-loading kernel in charge.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+void refresh_padded_cm(cwg_ctx* c) {
+  if (!c->d_coefp) return;
+  CUDA_TRY(launch_pad_planes(c->d_cm, 0, 1, c->w, c->row_end - c->row_begin, c->d_coefp, c->w_pad, 9, c->stream));
+}
+
+void setup_tma(cwg_ctx* c) {
+  const char* e = getenv("CWG_TB_TMA");
+  if (e && e[0] == '0') return;
+  if (c->op_kind != CWG_OP_STENCIL2D || c->world > 1 || !c->d_coef) return;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  const long long rows = c->row_end - c->row_begin;
+  unsigned bx0 = 0, by0 = 0;
+  int margin = 0;
+  tbm_box(4, &bx0, &by0, &margin);
+  c->w_pad = (c->w + margin + 1) / 2 * 2;  // zeroed left margin; 16-byte row pitch
+  c->d_coefp = dev_alloc<double>(static_cast<size_t>(10 * rows * c->w_pad));
+  CUDA_TRY(cudaMemsetAsync(c->d_coefp, 0, static_cast<size_t>(10 * rows * c->w_pad) * sizeof(double), c->stream));
+  CUDA_TRY(launch_pad_planes(c->d_coef, c->n_own, 9, c->w, rows, c->d_coefp, c->w_pad, 0, c->stream));
+  refresh_padded_cm(c);
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->w + margin), static_cast<cuuint64_t>(rows), 10};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->w_pad) * 8, static_cast<cuuint64_t>(rows * c->w_pad) * 8};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  bool ok = true;
+  for (int T = 2; T <= 4 && ok; ++T) {
+    unsigned cx = 0, cy = 0;
+    tbm_box(T, &cx, &cy, &margin);
+    const cuuint32_t box[3] = {cx, cy, 10};
+    ok = reinterpret_cast<EncodeTiledFn>(fn)(&c->tmap[T], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->d_coefp, dims, strides,
+                                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->tma_ok = ok;
+}
+
 // sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides)
 int diffusion_fuse(const cwg_ctx* c) {
   if (c->op_kind != CWG_OP_STENCIL2D || c->world > 1) return 1;  // T-row halos are not exchanged
@@ -404,7 +460,10 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     a.node_offset = c->own_global0;
     if (c->op_kind == CWG_OP_STENCIL2D) {
       Stencil2D s{c->d_coef, c->n_own, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
-      if (T > 1)
+      const bool big = ((c->w + 63) / 64) * ((s.rows + 15) / 16) >= 2ll * c->num_sms;
+      if (T > 1 && c->tma_ok && big)
+        CUDA_TRY(launch_diffuse_stencil2d_tbm(T, a, s, c->tmap[T], c->num_sms, c->stream));
+      else if (T > 1)
         CUDA_TRY(launch_diffuse_stencil2d_tb(T, a, s, c->num_sms, c->stream));
       else
         CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
@@ -854,6 +913,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     // tables uploaded above
   } else if (kind == CWG_OP_STENCIL2D) {
     build_stencil(c, p);
+    setup_tma(c);
   } else {
     validation(p->row_ptr && p->col && p->val, "operator: CSR arrays missing");
     const long long r0 = c->own_global0, r1 = c->own_global0 + c->n_own;
@@ -1068,8 +1128,12 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
 // recompute cm = dt_ad / m after dt_ad changed (fixed-step mode)
 cudaError_t launch_mass_factor_fix(cwg_ctx* c) {
   if (!c->d_mass) return cudaErrorNotSupported;
-  const cudaError_t e = launch_mass_factor(c->d_mass, c->n_mass, c->dt_ad, c->d_cm, c->stream);
+  cudaError_t e = launch_mass_factor(c->d_mass, c->n_mass, c->dt_ad, c->d_cm, c->stream);
   if (e != cudaSuccess) return e;
+  if (c->d_coefp) {
+    e = launch_pad_planes(c->d_cm, 0, 1, c->w, c->row_end - c->row_begin, c->d_coefp, c->w_pad, 9, c->stream);
+    if (e != cudaSuccess) return e;
+  }
   return cudaStreamSynchronize(c->stream);
 }
 

@@ -3,6 +3,8 @@
 // like the reference's x86-64 build, so diffusion is bit-identical to
 // diffusion_substep (fem.cpp:194-207) and the detector to
 // ActivationDetector::observe (postprocess.cpp:18-66).
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -10,6 +12,8 @@
 #include "launch.h"
 
 namespace cwg {
+
+static inline int blocks_for(long long n, int t, int cap);
 
 // ---------------------------------------------------------------------------
 // Stencil-2D: a regular sheet's 9-point rows with per-node coefficients taken
@@ -217,6 +221,277 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
     tb_body<T, TBX, TBY, NT, false>(a, s, Vs, gx0, ly0, skip, seq);
   else
     tb_body<T, TBX, TBY, NT, true>(a, s, Vs, gx0, ly0, skip, seq);
+}
+
+// ---------------------------------------------------------------------------
+// Persistent temporal blocking with TMA: one CTA per SM walks the tiles. The
+// coefficients live in a padded copy [10][rows][w_pad] (planes 0..8 = the 9
+// stencil coefficients, 9 = dt/m; even row pitch so every global stride is a
+// multiple of 16 bytes) described by a 3D tensor map; one thread issues ONE
+// cp.async.bulk.tensor per tile for the whole (CX x CY x 10) box -- TMA
+// zero-fills outside the sheet -- completing on an mbarrier while the CTA
+// computes the previous tile. V regions (odd row pitch) come in by per-thread
+// cp.async into a third buffer. Arithmetic, slot order and failure keys are
+// those of diffuse_stencil2d_tb.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// TMA geometry. The padded tensor stores node (x, y) at column x + kTmaMargin
+// (a zeroed left margin), and a box must start at a 16-byte aligned,
+// non-negative inner coordinate: boxes start SX = 2*ceil((T-1)/2) columns
+// left of the tile (even), BXW columns wide (even, covers the CX needed).
+constexpr int kTmaMargin = 4;
+template <int T, int TBX, int TBY, int NT>
+struct TbmGeom {
+  static constexpr int VX = TBX + 2 * T, VY = TBY + 2 * T, VXY = VX * VY;
+  static constexpr int CX = TBX + 2 * (T - 1), CY = TBY + 2 * (T - 1);
+  static constexpr int SX = 2 * ((T - 1 + 1) / 2);
+  static constexpr int BXW = ((SX + TBX + (T - 1)) + 1) / 2 * 2;
+  static constexpr int R = (CX * CY + NT - 1) / NT;
+  static constexpr int BOX = 10 * BXW * CY;  // doubles per TMA box
+  static_assert(SX <= kTmaMargin && (BXW * 8) % 16 == 0, "TMA box alignment");
+  static constexpr size_t smem = (static_cast<size_t>(BOX) + 3ull * VXY) * sizeof(double) + 16;
+};
+
+template <int T, int TBX, int TBY, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    diffuse_stencil2d_tbm(DiffArgs a, Stencil2D s, const __grid_constant__ CUtensorMap tmap, int tiles_x, int n_tiles) {
+  using G = TbmGeom<T, TBX, TBY, NT>;
+  constexpr int VX = G::VX, VXY = G::VXY, CX = G::CX, CY = G::CY, R = G::R, BOX = G::BOX, BXW = G::BXW, SX = G::SX;
+  extern __shared__ __align__(128) double tbm_smem[];
+  double* cfs = tbm_smem;  // [10][CY][BXW]: the TMA box
+  double* vb0 = cfs + BOX;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(vb0 + 3 * VXY);
+  const unsigned bar_a = smem_u32(bar);
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  const bool skip = earlier_failure(a.err, seq);
+  const long long rows = s.rows, w = s.w;
+  int px[R], py[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int p = threadIdx.x + r * NT;
+    int rx = 0, ry = 0;
+    if (p < TBX * TBY) {
+      rx = p % TBX;
+      ry = p / TBX;
+    } else if (p < CX * CY) {
+      int e = p - TBX * TBY, k = 1;
+      while (e >= 2 * (TBX + 2 * k) + 2 * (TBY + 2 * k - 2)) {
+        e -= 2 * (TBX + 2 * k) + 2 * (TBY + 2 * k - 2);
+        ++k;
+      }
+      const int wr = TBX + 2 * k, hr = TBY + 2 * k - 2;
+      if (e < wr) {
+        rx = e - k, ry = -k;
+      } else if (e < 2 * wr) {
+        rx = e - wr - k, ry = TBY - 1 + k;
+      } else if (e < 2 * wr + hr) {
+        rx = -k, ry = e - 2 * wr - k + 1;
+      } else {
+        rx = TBX - 1 + k, ry = e - 2 * wr - hr - k + 1;
+      }
+    }
+    px[r] = rx;
+    py[r] = ry;
+  }
+  auto issue_box = [&](int tile) {  // thread 0 only
+    const int gx0 = (tile % tiles_x) * TBX, ly0 = (tile / tiles_x) * TBY;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of cfs before the async write
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(BOX * 8) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(cfs)),
+        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(ly0 - (T - 1)), "r"(0), "r"(bar_a)
+        : "memory");
+  };
+  auto fetch_v = [&](int tile, double* vdst) {
+    const long long gx0 = static_cast<long long>(tile % tiles_x) * TBX, ly0 = static_cast<long long>(tile / tiles_x) * TBY;
+    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
+    for (int t = threadIdx.x; t < VXY; t += NT) {
+      const int cx = t % VX, cy = t / VX;
+      const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
+      if (x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows)
+        cp_async8(vdst + t, vsrc + static_cast<long long>(cy) * w + cx);
+      else
+        vdst[t] = 0.0;  // outside the sheet: never read (presence flags)
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (tile < n_tiles) {
+    if (threadIdx.x == 0) issue_box(tile);
+    fetch_v(tile, vb0);
+  }
+  int cur = 0;
+  unsigned parity = 0;
+  for (; tile < n_tiles; tile += gridDim.x) {
+    const long long gx0 = static_cast<long long>(tile % tiles_x) * TBX, ly0 = static_cast<long long>(tile / tiles_x) * TBY;
+    mbar_wait(bar_a, parity);
+    parity ^= 1u;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const bool interior = gx0 >= T && gx0 + TBX + T <= w && ly0 >= T && ly0 + TBY + T <= rows;
+    double cf[R][10];
+    int vi[R];
+    unsigned fl[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const long long x = gx0 + px[r], yl = ly0 + py[r], gy = s.row_begin + yl;
+      const bool own = threadIdx.x + r * NT < CX * CY && x >= 0 && x < w && yl >= 0 && yl < rows;
+      fl[r] = own ? (1u | (gy > 0 ? 2u : 0u) | (gy + 1 < s.ny1 ? 4u : 0u) | (x > 0 ? 8u : 0u) | (x + 1 < w ? 16u : 0u))
+                  : 0u;
+      vi[r] = own ? (py[r] + T) * VX + (px[r] + T) : VX + 1;
+      const int bi = (py[r] + T - 1) * BXW + (px[r] + SX);
+#pragma unroll
+      for (int c = 0; c < 10; ++c) cf[r][c] = own ? cfs[c * BXW * CY + bi] : 0.0;
+    }
+    __syncthreads();  // cfs and the spare V buffer are free: start the next tile's copies
+    const int nxt = tile + static_cast<int>(gridDim.x);
+    double* vnext = vb0 + ((cur + 2) % 3) * VXY;
+    if (nxt < n_tiles) {
+      if (threadIdx.x == 0) issue_box(nxt);
+      fetch_v(nxt, vnext);
+    }
+    double* va = vb0 + cur * VXY;
+    double* vs = vb0 + ((cur + 1) % 3) * VXY;
+#pragma unroll
+    for (int q = 0; q < T; ++q) {
+      const double* src = (q & 1) ? vs : va;
+      double* dst = (q & 1) ? va : vs;
+      const int hx = T - 1 - q;
+      const int n_act = (TBX + 2 * hx) * (TBY + 2 * hx);
+      double out[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        out[r] = 0.0;
+        if (r * NT + (threadIdx.x & ~31) >= n_act) continue;  // warp-uniform
+        const unsigned f = fl[r];
+        const bool act = (f & 1u) && threadIdx.x + r * NT < n_act;
+        const double* sp = src + vi[r];
+        const double v0 = sp[0];
+        double o;
+        if (interior) {
+          double acc = 0.0 + cf[r][0] * sp[-VX - 1];
+          acc += cf[r][1] * sp[-VX];
+          acc += cf[r][2] * sp[-VX + 1];
+          acc += cf[r][3] * sp[-1];
+          acc += cf[r][4] * v0;
+          acc += cf[r][5] * sp[1];
+          acc += cf[r][6] * sp[VX - 1];
+          acc += cf[r][7] * sp[VX];
+          acc += cf[r][8] * sp[VX + 1];
+          o = skip ? v0 : v0 - cf[r][9] * acc;
+        } else {
+          const double vsw = sp[-VX - 1], vss = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
+          const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
+          const bool hs = f & 2u, hn = f & 4u, hw = f & 8u, he = f & 16u;
+          double acc = 0.0, tmp;
+          tmp = acc + cf[r][0] * vsw; acc = (hs && hw) ? tmp : acc;
+          tmp = acc + cf[r][1] * vss; acc = hs ? tmp : acc;
+          tmp = acc + cf[r][2] * vse; acc = (hs && he) ? tmp : acc;
+          tmp = acc + cf[r][3] * vw;  acc = hw ? tmp : acc;
+          acc = acc + cf[r][4] * v0;
+          tmp = acc + cf[r][5] * ve;  acc = he ? tmp : acc;
+          tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
+          tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
+          tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
+          o = skip ? v0 : v0 - cf[r][9] * acc;
+        }
+        out[r] = o;
+        if (q + 1 < T && act) dst[vi[r]] = o;
+        if (act && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
+          const long long x = gx0 + px[r], yl = ly0 + py[r];
+          record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
+                                    (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2);
+        }
+      }
+      if (q + 1 < T) {
+        __syncthreads();
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (r * NT >= TBX * TBY) break;
+          if (fl[r] & 1u) a.vout[(ly0 + py[r] + 1) * w + gx0 + px[r]] = out[r];
+        }
+      }
+    }
+    cur = (cur + 2) % 3;
+  }
+}
+
+template <int T>
+static cudaError_t launch_tbm_t(const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm, int num_sms,
+                                cudaStream_t st) {
+  using G = TbmGeom<T, 64, 16, 512>;
+  static bool set = false;
+  if (!set) {
+    cudaFuncSetAttribute(diffuse_stencil2d_tbm<T, 64, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(G::smem));
+    set = true;
+  }
+  const int tiles_x = static_cast<int>((s.w + 63) / 64);
+  const int n_tiles = tiles_x * static_cast<int>((s.rows + 15) / 16);
+  diffuse_stencil2d_tbm<T, 64, 16, 512><<<std::min(num_sms, n_tiles), 512, G::smem, st>>>(a, s, tm, tiles_x, n_tiles);
+  return cudaGetLastError();
+}
+
+// TMA box of the padded coefficient tensor for T fused sub-steps (64 x 16 tiles)
+void tbm_box(int T, unsigned* cx, unsigned* cy, int* margin) {
+  *margin = kTmaMargin;
+  switch (T) {
+    case 2: *cx = TbmGeom<2, 64, 16, 512>::BXW, *cy = TbmGeom<2, 64, 16, 512>::CY; break;
+    case 3: *cx = TbmGeom<3, 64, 16, 512>::BXW, *cy = TbmGeom<3, 64, 16, 512>::CY; break;
+    default: *cx = TbmGeom<4, 64, 16, 512>::BXW, *cy = TbmGeom<4, 64, 16, 512>::CY; break;
+  }
+}
+
+cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm,
+                                         int num_sms, cudaStream_t st) {
+  switch (T) {
+    case 2: return launch_tbm_t<2>(a, s, tm, num_sms, st);
+    case 3: return launch_tbm_t<3>(a, s, tm, num_sms, st);
+    case 4: return launch_tbm_t<4>(a, s, tm, num_sms, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// dst[(c*rows + y)*w_pad + margin + x] = src[c*src_pitch + y*w + x] (padded coefficient planes)
+__global__ void pad_planes(const double* src, long long src_pitch, int n_planes, long long w, long long rows,
+                           double* dst, long long w_pad, int dst_plane0) {
+  const long long n = w * rows;
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < n * n_planes;
+       o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long c = o / n, r = o - c * n, y = r / w, x = r - y * w;
+    dst[((c + dst_plane0) * rows + y) * w_pad + kTmaMargin + x] = src[c * src_pitch + r];
+  }
+}
+
+cudaError_t launch_pad_planes(const double* src, long long src_pitch, int n_planes, long long w, long long rows,
+                              double* dst, long long w_pad, int dst_plane0, cudaStream_t st) {
+  pad_planes<<<blocks_for(w * rows * n_planes, 256, 148 * 32), 256, 0, st>>>(src, src_pitch, n_planes, w, rows, dst,
+                                                                            w_pad, dst_plane0);
+  return cudaGetLastError();
 }
 
 template <int T, int TBX, int TBY, int NT>

@@ -1,6 +1,8 @@
 // Host-side declarations of the kernel launchers (defined in the .cu files).
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace cwg {
@@ -23,6 +25,11 @@ cudaError_t launch_rates_ord(int kind, long long n, const double* v, const doubl
 cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int max_blocks, cudaStream_t st);
 cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int max_blocks, cudaStream_t st);
 cudaError_t launch_diffuse_stencil2d_tb(int T, const DiffArgs& a, const Stencil2D& s, int num_sms, cudaStream_t st);
+void tbm_box(int T, unsigned* cx, unsigned* cy, int* margin);
+cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm,
+                                         int num_sms, cudaStream_t st);
+cudaError_t launch_pad_planes(const double* src, long long src_pitch, int n_planes, long long w, long long rows,
+                              double* dst, long long w_pad, int dst_plane0, cudaStream_t st);
 cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st);
 cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st);
 cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,
