@@ -710,10 +710,8 @@ int choose_ord_variant(long long count, int num_sms) {
     const int v = atoi(e);
     if (react_ord_variant_valid(v)) return v;
   }
-  const int pf = getenv("CWG_ORD_PREFETCH") && atoi(getenv("CWG_ORD_PREFETCH")) ? 16 : 0;
   const long long warps_per_sm = (count + 32ll * num_sms - 1) / (32ll * num_sms);
-  if (warps_per_sm <= 10) return 0 | pf;
-  return 1 | pf;
+  return warps_per_sm <= 10 ? 0 : 1;
 }
 
 bool stencil_ok(const cwg_problem* p) {

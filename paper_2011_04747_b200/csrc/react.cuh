@@ -25,36 +25,6 @@ namespace cwg {
 // 32 KB L1.5 instruction cache; warps that drift to different PCs thrash it
 // (ncu: ~35% of stall cycles were instruction fetch). In lockstep every
 // fetched line serves all warps.
-// Per-thread state column in shared memory (M::kSmemStates): s[q] is
-// sst[q * kThreads + tid]. Frees the ~80 registers the 40 ORd states would
-// pin, so more exponentials can be in flight (the kernel is FP64-latency
-// bound). The stride is a compile-time constant, so the compiler knows the
-// columns never alias.
-template <int STRIDE>
-struct SmemCol {
-  double* p;
-  __device__ __forceinline__ double& operator[](int q) const { return p[q * STRIDE]; }
-};
-
-template <class M, bool SM = M::kSmemStates>
-struct StateStore;
-
-template <class M>
-struct StateStore<M, false> {
-  double s[M::NS > 0 ? M::NS : 1];
-  __device__ __forceinline__ StateStore(unsigned*, int) {}
-  __device__ __forceinline__ double* acc() { return s; }
-};
-
-template <class M>
-struct StateStore<M, true> {
-  SmemCol<M::kThreads> col;
-  __device__ __forceinline__ StateStore(unsigned* smem_after_hist, int) {
-    col.p = reinterpret_cast<double*>(smem_after_hist) + threadIdx.x;
-  }
-  __device__ __forceinline__ SmemCol<M::kThreads> acc() { return col; }
-};
-
 template <class M>
 __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
   const int lane = threadIdx.x & 31;
@@ -67,48 +37,9 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   bool open = true;  // may still receive work
   int k = 0, j = 0, p0 = 0, p1 = 0;
   double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
-  StateStore<M> store(shist + ((a.khist_len + 1) & ~1), 0);
-  auto s = store.acc();
-  // Prefetch slot (M::kPrefetch): a lane whose node finishes with the current
-  // evaluation claims its next node one trip early and copies that node's
-  // states, V, last dV/dt, GKr scale and stimulus range into its own shared
-  // memory column with cp.async while the evaluation runs; the refill then
-  // reads shared memory instead of waiting on HBM. nxt: -2 nothing claimed,
-  // -1 claimed but the work list was exhausted, >= 0 the prefetched node.
-  long long nxt = -2;
-  double* pf = nullptr;
-  int* pfi = nullptr;
-  if constexpr (M::kPrefetch) {
-    double* base = reinterpret_cast<double*>(shist + ((a.khist_len + 1) & ~1)) + (M::kSmemStates ? M::NS * M::kThreads : 0);
-    pf = base + threadIdx.x;                                           // pf[q * kThreads], q < NS + 3
-    pfi = reinterpret_cast<int*>(base + (M::NS + 3) * M::kThreads) + threadIdx.x;  // pfi[0 / kThreads]
-  }
+  double s[M::NS > 0 ? M::NS : 1];  // the lane's node states (registers)
 
   while (true) {
-    if constexpr (M::kPrefetch) {
-      if (node < 0 && open && nxt != -2) {
-        if (nxt >= 0) {
-          asm volatile("cp.async.wait_all;" ::: "memory");
-          node = nxt;
-#pragma unroll
-          for (int q = 0; q < M::NS; ++q) s[q] = pf[q * M::kThreads];
-          v = pf[M::NS * M::kThreads];
-          k = substeps(pf[(M::NS + 1) * M::kThreads], a.scheme, a.k0_up, a.k0_down, a.kmax);
-          h = a.dt / static_cast<double>(k);  // dt_ar (splitting.cpp:117)
-          j = 0;
-          dv = 0.0;
-          if (M::kUsesGkr) g = a.gkr ? pf[(M::NS + 2) * M::kThreads] : 1.0;
-          if (a.stim.node_ptr) {
-            p0 = pfi[0];
-            p1 = pfi[M::kThreads];
-          }
-          atomicAdd(shist + k, 1u);
-        } else {
-          open = false;
-        }
-        nxt = -2;
-      }
-    }
     const bool need = node < 0 && open;
     const unsigned m = __ballot_sync(kFull, need);
     if (m) {
@@ -143,44 +74,6 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
       if (!__syncthreads_or(node >= 0)) break;
     } else if (!__any_sync(kFull, node >= 0)) {
       break;
-    }
-    if constexpr (M::kPrefetch) {
-      const bool want = node >= 0 && j + 1 == k && open && nxt == -2;
-      const unsigned mw = __ballot_sync(kFull, want);
-      if (mw) {
-        const int leader = __ffs(mw) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(mw)));
-        base = __shfl_sync(kFull, base, leader);
-        if (want) {
-          const long long pos = static_cast<long long>(base) + __popc(mw & lt);
-          if (pos < a.count) {
-            const long long nn = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
-            nxt = nn;
-            const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(pf));
-#pragma unroll
-            for (int q = 0; q < M::NS; ++q)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sp + q * M::kThreads * 8),
-                           "l"(a.S + q * a.pitch + nn) : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sp + M::NS * M::kThreads * 8),
-                         "l"(a.v + nn) : "memory");
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sp + (M::NS + 1) * M::kThreads * 8),
-                         "l"(a.last + nn) : "memory");
-            if (M::kUsesGkr && a.gkr)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sp + (M::NS + 2) * M::kThreads * 8),
-                           "l"(a.gkr + nn) : "memory");
-            if (a.stim.node_ptr) {
-              const unsigned si = static_cast<unsigned>(__cvta_generic_to_shared(pfi));
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(si), "l"(a.stim.node_ptr + nn) : "memory");
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(si + M::kThreads * 4),
-                           "l"(a.stim.node_ptr + nn + 1) : "memory");
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-          } else {
-            nxt = -1;
-          }
-        }
-      }
     }
     if (node >= 0) {
       const double ts = __dadd_rn(t, __dmul_rn(static_cast<double>(j), h));  // t + j*dt_ar, never contracted

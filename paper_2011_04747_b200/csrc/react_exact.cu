@@ -13,8 +13,6 @@ struct ModelAP {
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
   static constexpr bool kBlockSync = false;
-  static constexpr bool kSmemStates = false;
-  static constexpr bool kPrefetch = false;
   __device__ __forceinline__ static void rates(double v, const double* s, double ist, double& dv, double* ds) {
     const double u = (v - (-80.0)) / 100.0;
     const double w = s[0];
@@ -39,8 +37,6 @@ struct ModelMac {
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
   static constexpr bool kBlockSync = false;
-  static constexpr bool kSmemStates = false;
-  static constexpr bool kPrefetch = false;
   __device__ __forceinline__ static void rates(double v, const double* s, double ist, double& dv, double* ds) {
     const double rtf = 8314.0 * 306.15 / 96485.0;
     const double e_k = rtf * log(5.4 / 129.4349);
@@ -81,8 +77,6 @@ struct ModelPassive {
   static constexpr int kMinBlocks = 4;
   static constexpr bool kUsesGkr = false;
   static constexpr bool kBlockSync = false;
-  static constexpr bool kSmemStates = false;
-  static constexpr bool kPrefetch = false;
   __device__ __forceinline__ static void rates(double v, const double*, double ist, double& dv, double*) {
     dv = -0.01 * (v - (-85.0)) + ist;
   }

@@ -518,26 +518,20 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 
 }  // namespace ord
 
-// Launch shapes (V & 15): 0: 128-thread blocks, 2 per SM (<= 255 regs), warps
+// Launch shapes: 0: 128-thread blocks, 2 per SM (<= 255 regs), warps
 // free-running (latency regime default); 1: one persistent 384-thread block
 // per SM (<= 168 regs, 12 warps), lockstep (throughput regime default);
-// 2: one persistent 256-thread block per SM (<= 255 regs, 8 warps), lockstep;
-// 7 / 8: one persistent 288 / 320-thread lockstep block per SM (sized so a
-// C2-sized mesh needs one round of nodes per lane); 9 / 10: 288 / 256
-// threads free-running. V & 16: next-node prefetch (react.cuh).
-// (Measured and dropped: 512-thread blocks, node states in shared memory,
-// a two-warp-per-node split of the rates.)
+// 2 / 7: one persistent 256 / 288-thread lockstep block per SM (alternatives
+// for the latency regime, selectable with CWG_ORD_VARIANT). Measured and
+// dropped: 512-thread blocks, node states in shared memory, a
+// two-warp-per-node split of the rates, a cp.async next-node prefetch,
+// free-running 256/288-thread blocks, lockstep in warp groups.
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kShape = V & 15;
-  static constexpr int kThreads =
-      kShape == 1 ? 384
-                  : (kShape == 2 || kShape == 10 ? 256 : (kShape == 7 || kShape == 9 ? 288 : (kShape == 8 ? 320 : 128)));
-  static constexpr int kMinBlocks = kShape == 0 ? 2 : 1;
-  static constexpr bool kBlockSync = kShape != 0 && kShape != 9 && kShape != 10;
-  static constexpr bool kSmemStates = false;
-  static constexpr bool kPrefetch = (V & 16) != 0;
+  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 7 ? 288 : 128));
+  static constexpr int kMinBlocks = V == 0 ? 2 : 1;
+  static constexpr bool kBlockSync = V != 0;
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
@@ -567,10 +561,7 @@ __global__ void ord_rates_kernel(long long n, const double* v, const double* s, 
 template <class M>
 static size_t smem_bytes(int khist_len) {
   const size_t hist = static_cast<size_t>((khist_len + 1) & ~1) * sizeof(unsigned);
-  return hist + (M::kSmemStates ? static_cast<size_t>(M::NS) * M::kThreads * sizeof(double) : 0) +
-         (M::kPrefetch ? static_cast<size_t>(M::NS + 3) * M::kThreads * sizeof(double) +
-                             2ull * M::kThreads * sizeof(int)
-                       : 0);
+  return hist;
 }
 
 template <class M>
@@ -598,7 +589,7 @@ static int occupancy_t() {
 
 // Launch-shape variants (see ModelOrd). The host picks one per model bin
 // (cwg_host.cu: choose_ord_variant); CWG_ORD_VARIANT overrides for experiments.
-#define CWG_ORD_VARIANTS(X) X(0) X(1) X(2) X(7) X(8) X(9) X(10) X(16) X(17) X(18) X(23) X(24)
+#define CWG_ORD_VARIANTS(X) X(0) X(1) X(2) X(7)
 
 bool react_ord_variant_valid(int v) {
   switch (v) {
