@@ -227,19 +227,24 @@ def main():
     torch.cuda.set_device(local)
     dist = None
     nccl_id = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("gloo", init_method="env://")
-        obj = [os.urandom(0)]
+
+    def new_nccl_id():
+        """A fresh ncclUniqueId from rank 0 for every communicator (an id
+        bootstraps exactly one communicator); gloo carries the 128 bytes."""
+        obj = [b""]
         if rank == 0:
-            # ncclGetUniqueId through the torch-bundled NCCL (plumbing only)
             import ctypes
-            nc = ctypes.CDLL("libnccl.so.2")
+            nc = ctypes.CDLL("libnccl.so.2")  # the torch-bundled NCCL (plumbing only)
             buf = (ctypes.c_ubyte * 128)()
             assert nc.ncclGetUniqueId(buf) == 0
             obj = [bytes(buf)]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo", init_method="env://")
+        nccl_id = new_nccl_id()
 
     prob = build_problem(args.config, world, rank)
     setup = prob.setup()
@@ -360,12 +365,13 @@ def main():
         # builds its own integrator, as the reference's run_simulation does
         walls, creates = [], []
         for _rep in range(3):
+            e_id = new_nccl_id() if dist else None
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e_integ = cw.StrangIntegrator(setup, e2e_cfg, model_of_node=prob.model_of_node, device=local, rank=rank,
-                                          world=world, nccl_id=nccl_id)
+                                          world=world, nccl_id=e_id)
             creates.append(time.perf_counter() - t0)
             res = cw.run_simulation(st0, setup, e2e_cfg, device=local, integrator=e_integ)
             torch.cuda.synchronize()
