@@ -92,3 +92,26 @@ def test_nonfinite_in_fused_substep_reports_like_oracle(where):
     assert eg.value.time_ms == eo.value.t == 0.0
     assert eo.value.node == node - (w + 1 if x > 0 else w)
 
+
+
+def test_set_scheme_refreshes_fused_coefficients():
+    """cwg_set_scheme changes dt_ad, hence dt/m -- also in the padded tensor the
+    TMA-fed kernel reads. A reconfigured integrator must equal a fresh one."""
+    import paper_2011_04747_b200 as cw
+    p = _problem(8.0, 4.0, math.pi / 4, t_end=3.0)
+    setup = p.setup()
+    cfg_a = cw.SchemeConfig(dt_ms=0.3, t_end_ms=3.0)
+    cfg_b = cw.SchemeConfig(dt_ms=0.2, t_end_ms=3.0)  # different l and dt_ad
+    assert (cw.diffusion_substeps(0.3, p.sheet.op.dt_s, False, cw.Scheme.DAETI).dt_ad
+            != cw.diffusion_substeps(0.2, p.sheet.op.dt_s, False, cw.Scheme.DAETI).dt_ad)
+    integ = cw.StrangIntegrator(setup, cfg_a, model_of_node=p.model_of_node)
+    try:
+        cw.run_simulation(p.initial_state(), setup, cfg_a, integrator=integ)
+        integ.set_scheme(cfg_b)
+        r = cw.run_simulation(p.initial_state(), setup, cfg_b, integrator=integ)
+    finally:
+        integ.close()
+    fresh = cw.run_simulation(p.initial_state(), setup, cfg_b)
+    assert np.array_equal(r.final_state.v, fresh.final_state.v)
+    o = oracle_run(p, dt=0.2, t_end=3.0)
+    assert np.array_equal(fresh.final_state.v, o["v"])
