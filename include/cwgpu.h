@@ -160,6 +160,16 @@ int cwg_init_rest_state(cwg_ctx* ctx);
  * Upload the initial state and call cwg_run_begin afterwards. */
 int cwg_set_scheme(cwg_ctx* ctx, int scheme, double dt_ms, double t_end_ms, int k0_up, int k0_down,
                    int strict_substeps, cwg_error* err);
+/* Testing hook for the multi-GPU decomposition on ONE device: contexts
+ * created with world = N, rank r, no NCCL id and CWG_LOOPBACK=1 in the
+ * environment skip the communicator; this call runs steps [first,
+ * first+count) of all N ranks interleaved on rank 0's stream, copying the
+ * one-row (2D) / one-plane (3D) halos between the ranks' V buffers before
+ * every diffusion sub-step exactly where halo_exchange's ncclSend/ncclRecv
+ * would. Everything but the transport (slab kernels, offsets, failure keys,
+ * recording) runs as on N GPUs. Call cwg_run_begin on each rank first. */
+int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t count);
+
 /* Asynchronous V snapshot for on_snapshot (splitting.cpp:267-277): enqueue,
  * after the steps issued so far, a device-side copy of V and of the failure
  * record, then their transfer to host_v[global node] on a side stream; the

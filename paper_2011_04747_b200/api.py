@@ -602,11 +602,12 @@ class StrangIntegrator:
         p.k0_up, p.k0_down, p.strict_substeps = cfg.k0_up, cfg.k0_down, int(cfg.strict_substeps)
         p.record_interval_ms = cfg.record_interval_ms
         p.device, p.rank, p.world = device, rank, world
-        if world > 1:
-            if nccl_id is None or len(nccl_id) != 128:
+        if world > 1 and nccl_id is not None:
+            if len(nccl_id) != 128:
                 raise ValidationError("placement: world > 1 needs a 128-byte NCCL unique id")
             keep["nid"] = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
             p.nccl_id = C.cast(keep["nid"], C.POINTER(C.c_ubyte))
+        # (world > 1 without an id: only the CWG_LOOPBACK testing mode, cwg_loopback_steps)
         err = L.cwg_error()
         h = C.c_void_p()
         _check(L.lib().cwg_create(C.byref(p), C.byref(h), C.byref(err)), err)

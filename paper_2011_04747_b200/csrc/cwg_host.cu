@@ -265,6 +265,7 @@ struct cwg_ctx {
 
   // multi-GPU
   ncclComm_t comm = nullptr;
+  bool loopback = false;  // world > 1 without NCCL: halos copied by cwg_loopback_steps (testing hook)
 
   // asynchronous V snapshots (cwg_snapshot_begin / _wait)
   double* d_snap = nullptr;
@@ -366,7 +367,7 @@ T* upload(const T* h, size_t count) {
 
 // ---------------------------------------------------------------- step pieces
 void halo_exchange(cwg_ctx* c, double* buf) {
-  if (c->world <= 1) return;
+  if (c->world <= 1 || c->loopback) return;
   const size_t w = static_cast<size_t>(c->w);
   NCCL_TRY(g_nccl.gstart());
   if (c->rank > 0) {
@@ -1027,7 +1028,9 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->det.threshold = c->lat_threshold;
 
   // ---- NCCL communicator for the halo exchange
-  if (c->world > 1) {
+  if (c->world > 1 && p->nccl_id == nullptr && getenv("CWG_LOOPBACK") && atoi(getenv("CWG_LOOPBACK"))) {
+    c->loopback = true;  // ranks share one process and device; cwg_loopback_steps drives them
+  } else if (c->world > 1) {
     validation(p->nccl_id != nullptr, "placement: world > 1 needs an NCCL unique id");
     if (!g_nccl.load()) throw Fail{CWG_ECUDA, "NCCL library (libnccl.so.2) not loadable"};
     ncclUniqueId id;
@@ -1075,7 +1078,7 @@ bool ev_is_reaction(const cwg_ctx* c, long long seq) { return seq % c->evs == c-
 bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
   ErrRec r{};
   CUDA_TRY(cudaMemcpy(&r, c->d_err, sizeof(r), cudaMemcpyDeviceToHost));
-  if (c->world > 1) {
+  if (c->world > 1 && !c->loopback) {
     long long* tmp = dev_alloc<long long>(2);
     long long h[2] = {r.key == kNoError ? (1ll << 62) : r.seq, 0};
     CUDA_TRY(cudaMemcpy(tmp, h, sizeof(long long), cudaMemcpyHostToDevice));
@@ -1341,6 +1344,74 @@ int cwg_set_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int k0
   });
 }
 
+int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t count) {
+  return guarded(nullptr, [&] {
+    validation(ranks && world >= 2, "loopback: need >= 2 rank contexts");
+    for (int r = 0; r < world; ++r)
+      validation(ranks[r] && ranks[r]->loopback && ranks[r]->world == world && ranks[r]->rank == r,
+                 "loopback: contexts must be ranks 0..world-1 created with CWG_LOOPBACK=1");
+    cwg_ctx* c0 = ranks[0];
+    CUDA_TRY(cudaSetDevice(c0->device));
+    const cudaStream_t shared = c0->stream;
+    std::vector<cudaStream_t> own(static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+      own[static_cast<size_t>(r)] = ranks[r]->stream;
+      CUDA_TRY(cudaStreamSynchronize(ranks[r]->stream));
+      ranks[r]->stream = shared;  // one stream: every rank's work is ordered as enqueued below
+    }
+    // the halo exchange of halo_exchange(), as device copies between the ranks' current V buffers
+    auto exchange = [&] {
+      for (int r = 0; r < world; ++r) {
+        cwg_ctx* c = ranks[r];
+        double* buf = c->d_v[c->cur];
+        const size_t w = static_cast<size_t>(c->w);
+        if (r > 0) {
+          cwg_ctx* b = ranks[r - 1];
+          CUDA_TRY(cudaMemcpyAsync(buf, b->d_v[b->cur] + b->n_own, w * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   shared));
+        }
+        if (r + 1 < world) {
+          cwg_ctx* t = ranks[r + 1];
+          CUDA_TRY(cudaMemcpyAsync(buf + c->n_own + w, t->d_v[t->cur] + w, w * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, shared));
+        }
+      }
+    };
+    try {
+      for (long long s = first; s < first + count; ++s) {
+        for (int r = 0; r < world; ++r) set_clock(ranks[r], s);
+        const int l = c0->l;
+        if (s == 0)
+          for (int q = 0; q < l; ++q) {  // step I
+            exchange();
+            for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], 1, 0, q);
+          }
+        for (int r = 0; r < world; ++r) enqueue_reaction(ranks[r], 0, l, false, 0.0);  // step A
+        const int cnt = s == c0->n_steps - 1 ? l : 2 * l;
+        for (int q = 0; q < cnt; ++q) {  // step III / merged B
+          exchange();
+          for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], 1, 0, l + 1 + q);
+        }
+        const long long S = s + 1;
+        for (int r = 0; r < world; ++r) {
+          cwg_ctx* c = ranks[r];
+          if (c->n_probes > 0 && S % c->spr == 0)
+            CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, 1,
+                                          c->spr, shared));
+          if (S % c->spm == 0)
+            CUDA_TRY(launch_detector_observe(c->d_v[c->cur] + c->halo, c->n_own, 0, c->det, c->d_clock, 1, c->spm,
+                                             c->dt_eff, shared));
+        }
+      }
+      CUDA_TRY(cudaStreamSynchronize(shared));
+    } catch (...) {
+      for (int r = 0; r < world; ++r) ranks[r]->stream = own[static_cast<size_t>(r)];
+      throw;
+    }
+    for (int r = 0; r < world; ++r) ranks[r]->stream = own[static_cast<size_t>(r)];
+  });
+}
+
 int cwg_snapshot_begin(cwg_ctx* c, double* host_v) {
   return guarded(nullptr, [&] {
     validation(host_v != nullptr, "snapshot: no destination");
@@ -1549,7 +1620,7 @@ int cwg_get_khist(cwg_ctx* c, int64_t* out, int len) {
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (c->world > 1) {
+    if (c->world > 1 && !c->loopback) {
       unsigned long long* tmp = dev_alloc<unsigned long long>(c->khist_len);
       NCCL_TRY(g_nccl.allreduce(c->d_khist, tmp, c->khist_len, ncclUint64, ncclSum, c->comm, c->stream));
       CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1574,7 +1645,7 @@ int cwg_get_traces(cwg_ctx* c, double* t_ms, double* v) {
     const size_t cnt = static_cast<size_t>(c->n_samples) * c->n_probes;
     double* src = c->d_traces;
     double* tmp = nullptr;
-    if (c->world > 1) {  // non-owned probes are 0 on each rank
+    if (c->world > 1 && !c->loopback) {  // non-owned probes are 0 on each rank
       tmp = dev_alloc<double>(cnt);
       NCCL_TRY(g_nccl.allreduce(c->d_traces, tmp, cnt, ncclDouble, ncclSum, c->comm, c->stream));
       CUDA_TRY(cudaStreamSynchronize(c->stream));

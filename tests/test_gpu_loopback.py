@@ -1,0 +1,99 @@
+"""The multi-GPU decomposition on one device.
+
+N slab contexts (world = N, rank r) run in loopback mode: no NCCL, the halo
+rows/planes are copied between the ranks' V buffers before every diffusion
+sub-step exactly where halo_exchange's ncclSend/ncclRecv would
+(cwg_loopback_steps). The slab kernels, node offsets, model bins and
+recording run as on N GPUs; the gathered final state must equal the
+single-context run bit for bit."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    old = os.environ.get("CWG_LOOPBACK")
+    os.environ["CWG_LOOPBACK"] = "1"
+    yield
+    if old is None:
+        os.environ.pop("CWG_LOOPBACK", None)
+    else:
+        os.environ["CWG_LOOPBACK"] = old
+
+
+def _loopback(p, world):
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import _lib as L
+    setup = p.setup()
+    integs = [cw.StrangIntegrator(setup, p.cfg, model_of_node=p.model_of_node, rank=r, world=world)
+              for r in range(world)]
+    try:
+        st = p.initial_state()
+        for it in integs:
+            it.upload(st)
+            it.run_begin()
+        n = integs[0].info.n_steps
+        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
+        rc = L.lib().cwg_loopback_steps(hs, world, 0, n)
+        assert rc == 0, L.lib().cwg_last_error().decode()
+        out = p.initial_state()
+        for it in integs:
+            it.download(out)
+        kh = sum(it.k_histogram() for it in integs)
+        return out, kh
+    finally:
+        for it in integs:
+            it.close()
+
+
+def _single(p):
+    import paper_2011_04747_b200 as cw
+    os.environ["CWG_LOOPBACK"] = "0"
+    try:
+        return cw.run_simulation(p.initial_state(), p.setup(), p.cfg)
+    finally:
+        os.environ["CWG_LOOPBACK"] = "1"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_2d_aliev_panfilov(world):
+    from paper_2011_04747_b200 import problems
+    p = problems.c1(model="aliev-panfilov", t_end=15.0, k0_down=1)
+    out, kh = _loopback(p, world)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v)
+    assert np.array_equal(out.s, ref.final_state.s)
+    assert np.array_equal(kh, ref.k_histogram)
+
+
+def test_loopback_2d_ord_and_fibrosis():
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import api, problems
+    p = problems.c1(t_end=4.0)
+    out, kh = _loopback(p, 2)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
+    sh = cw.Sheet(1.0, 0.5, 0.02, 0.3, d0_myocyte=0.0017, d0_fibrotic=0.00066, rho=0.25, fib_fraction=0.2, seed=5)
+    nodes = sh.select("x_le", value=0.05)
+    q = problems.Problem("fib", sh, ["ohara2011-epi", "maccannell2007"], sh.tags.astype(np.uint8),
+                         [(nodes, 0.0, 1.0, 80.0, None)], api.SchemeConfig(dt_ms=0.1, t_end_ms=3.0, k0_down=3), [0])
+    out, kh = _loopback(q, 3)
+    ref = _single(q)
+    assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
+
+
+def test_loopback_3d_slab():
+    from paper_2011_04747_b200 import problems
+    p = problems.slab(0.4, 0.3, 0.2, 0.02, model="aliev-panfilov", t_end=10.0, amplitude=100.0)
+    out, kh = _loopback(p, 2)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v)
+    assert np.array_equal(kh, ref.k_histogram)
