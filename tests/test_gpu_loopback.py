@@ -97,3 +97,20 @@ def test_loopback_3d_slab():
     ref = _single(p)
     assert np.array_equal(out.v, ref.final_state.v)
     assert np.array_equal(kh, ref.k_histogram)
+
+
+def test_loopback_thin_slabs():
+    """Slabs of 2-3 rows with several diffusion sub-steps per step: every
+    sub-step's halo row is exchanged; still bit-identical."""
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import api, problems
+    sh = cw.Sheet(1.0, 0.1, 0.02, 0.3, d0_myocyte=0.0017, rho=0.25)  # 6 rows
+    nodes = sh.select("x_le", value=0.05)
+    p = problems.Problem("thin", sh, ["aliev-panfilov"], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, 100.0, None)],
+                         api.SchemeConfig(dt_ms=0.3, t_end_ms=6.0), [0])
+    assert cw.diffusion_substeps(0.3, sh.op.dt_s, False, cw.Scheme.DAETI).l >= 2
+    for world in (2, 3):  # 3 and 2 rows per rank
+        out, kh = _loopback(p, world)
+        ref = _single(p)
+        assert np.array_equal(out.v, ref.final_state.v), world
+        assert np.array_equal(kh, ref.k_histogram)
