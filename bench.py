@@ -314,8 +314,8 @@ def main():
     # once per node (16 B) plus the node's coefficients -- 80 B of per-node
     # arrays in 2D, 0 for the cached 3D structured tables; a launch fusing T
     # sub-steps counts once (fused-traffic bound).
-    fuse = 1 if (is3d or world > 1) else int(os.environ.get("CWG_DIFF_TB", "4"))
-    fuse = max(1, min(4, fuse))
+    fuse = 1 if is3d else int(os.environ.get("CWG_DIFF_TB", "4"))
+    fuse = max(1, min(4, fuse))  # (multi-rank 2D: halo depth min(4, rows per rank) >= 4 in every bench config)
     launches_per_step = diffusion_launches(2 * info.l, fuse)
     coef_b = 0.0 if is3d else 80.0
     diff_bytes_step = info.n_local * launches_per_step * (16.0 + coef_b)

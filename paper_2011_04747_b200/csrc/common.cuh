@@ -127,6 +127,12 @@ struct Stencil2D {
   long long rows;       // owned rows
   long long row_begin;  // global index of owned row 0
   long long ny1;        // global rows
+  // Local layouts: V has hrows_v halo rows each side of the owned rows (owned
+  // row r at (r + hrows_v) * w); coef / cm cover hrows_c rows each side (owned
+  // row r at (r + hrows_c) * w). One GPU: 1 / 0. Multi-rank fused diffusion:
+  // H / H, so halo points can be advanced through the fused sub-steps.
+  long long hrows_v = 1;
+  long long hrows_c = 0;
 };
 
 // Structured 3D slab (EXTENSION): per-class 27-point coefficients

@@ -194,6 +194,8 @@ struct cwg_ctx {
   int rank = 0, world = 1;
   long long row_begin = 0, row_end = 0;  // owned rows (stencil / slab)
   long long n_own = 0, halo = 0, n_alloc = 0;
+  int hrows_v = 1, hrows_c = 0;  // 2D: halo rows of V / of the coefficient arrays per side (Stencil2D)
+  long long n_coef = 0;          // 2D: nodes covered by coef / cm ((rows + 2 hrows_c) * w)
   long long node_offset = 0;  // global index of local index 0
   long long own_global0 = 0;  // global index of the first owned node
 
@@ -366,17 +368,21 @@ T* upload(const T* h, size_t count) {
 }
 
 // ---------------------------------------------------------------- step pieces
-void halo_exchange(cwg_ctx* c, double* buf) {
+// Exchange `rows` halo rows (planes) with both neighbours: my first / last
+// `rows` owned rows go down / up, theirs land in the halo rows adjacent to my
+// slab. Local V layout: [hrows_v halo | owned | hrows_v halo] rows of w nodes.
+void halo_exchange(cwg_ctx* c, double* buf, int rows) {
   if (c->world <= 1 || c->loopback) return;
-  const size_t w = static_cast<size_t>(c->w);
+  const size_t n = static_cast<size_t>(c->w) * static_cast<size_t>(rows);
+  const size_t own0 = static_cast<size_t>(c->halo), own1 = own0 + static_cast<size_t>(c->n_own);
   NCCL_TRY(g_nccl.gstart());
   if (c->rank > 0) {
-    NCCL_TRY(g_nccl.send(buf + w, w, ncclDouble, c->rank - 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(buf, w, ncclDouble, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.send(buf + own0, n, ncclDouble, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(buf + own0 - n, n, ncclDouble, c->rank - 1, c->comm, c->stream));
   }
   if (c->rank + 1 < c->world) {
-    NCCL_TRY(g_nccl.send(buf + c->n_own, w, ncclDouble, c->rank + 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(buf + c->n_own + w, w, ncclDouble, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.send(buf + own1 - n, n, ncclDouble, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(buf + own1, n, ncclDouble, c->rank + 1, c->comm, c->stream));
   }
   NCCL_TRY(g_nccl.gend());
 }
@@ -431,22 +437,34 @@ void setup_tma(cwg_ctx* c) {
 
 // sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides)
 int diffusion_fuse(const cwg_ctx* c) {
-  if (c->op_kind != CWG_OP_STENCIL2D || c->world > 1) return 1;  // T-row halos are not exchanged
-  if (const char* e = getenv("CWG_DIFF_TB")) return std::max(1, std::min(4, atoi(e)));
-  return 4;
+  if (c->op_kind != CWG_OP_STENCIL2D) return 1;
+  int f = 4;
+  if (const char* e = getenv("CWG_DIFF_TB")) f = std::max(1, std::min(4, atoi(e)));
+  return c->world > 1 ? std::min(f, c->hrows_c) : f;  // T fused sub-steps need T halo rows (V and coefficients)
+}
+
+// fused-launch group sizes for `count` sub-steps: ceil(count/fuse) launches, balanced
+std::vector<int> diffusion_groups(const cwg_ctx* c, int count) {
+  const int fuse = diffusion_fuse(c);
+  const int m = (count + fuse - 1) / fuse;
+  std::vector<int> g;
+  for (int q = 0, launch = 0; q < count; ++launch) {
+    const int T = (count - q + (m - launch) - 1) / (m - launch);
+    g.push_back(T);
+    q += T;
+  }
+  return g;
 }
 
 void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
-  // m = ceil(count / fuse) launches with balanced group sizes; every launch
-  // flips the V double buffer (graphs are kept per starting parity).
-  const int fuse = diffusion_fuse(c);
-  const int m = (count + fuse - 1) / fuse;
-  for (int q = 0, launch = 0; q < count; ++launch) {
-    const int left = m - launch;
-    const int T = (count - q + left - 1) / left;  // balanced group sizes
+  // ceil(count / fuse) launches with balanced group sizes; every launch flips
+  // the V double buffer (graphs are kept per starting parity)
+  const std::vector<int> groups = diffusion_groups(c, count);
+  for (int gi = 0, q = 0; gi < static_cast<int>(groups.size()); ++gi) {
+    const int T = groups[static_cast<size_t>(gi)];
     double* vin = c->d_v[c->cur];
     double* vout = c->d_v[c->cur ^ 1];
-    halo_exchange(c, vin);
+    halo_exchange(c, vin, T);
     DiffArgs a{};
     a.vin = vin;
     a.vout = vout;
@@ -460,7 +478,8 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     a.ev = ev0 + q;
     a.node_offset = c->own_global0;
     if (c->op_kind == CWG_OP_STENCIL2D) {
-      Stencil2D s{c->d_coef, c->n_own, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
+      Stencil2D s{c->d_coef, c->n_coef, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1,
+                  c->hrows_v, c->hrows_c};
       const bool big = ((c->w + 63) / 64) * ((s.rows + 15) / 16) >= 2ll * c->num_sms;
       if (T > 1 && c->tma_ok && big)
         CUDA_TRY(launch_diffuse_stencil2d_tbm(T, a, s, c->tmap[T], c->num_sms, c->stream));
@@ -668,12 +687,16 @@ namespace {
 
 void build_stencil(cwg_ctx* c, const cwg_problem* p) {
   // Per-node 9 coefficients taken verbatim from the CSR rows; a row must hold
-  // exactly its in-grid 9-neighbourhood in ascending order.
+  // exactly its in-grid 9-neighbourhood in ascending order. Covers the owned
+  // rows plus hrows_c rows each side (multi-rank fused diffusion).
   const long long w = c->w;
-  std::vector<double> coef(static_cast<size_t>(9 * c->n_own), 0.0);
+  const long long n_coef = c->n_coef;
+  const long long g0 = (c->row_begin - c->hrows_c) * w;  // global index of local coefficient 0
+  std::vector<double> coef(static_cast<size_t>(9 * n_coef), 0.0);
   const long long offs[9] = {-w - 1, -w, -w + 1, -1, 0, 1, w - 1, w, w + 1};
-  for (long long o = 0; o < c->n_own; ++o) {
-    const long long i = c->own_global0 + o;
+  for (long long o = 0; o < n_coef; ++o) {
+    const long long i = g0 + o;
+    if (i < 0 || i >= p->n) continue;  // beyond the sheet: never read
     const long long y = i / w, x = i - y * w;
     int slot = 0;
     for (long long p_ = p->row_ptr[i]; p_ < p->row_ptr[i + 1]; ++p_) {
@@ -683,7 +706,7 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
       const long long gy = y + (slot / 3) - 1, gx = x + (slot % 3) - 1;
       if (gy < 0 || gy >= c->ny1 || gx < 0 || gx >= w)
         throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " couples outside the grid"};
-      coef[static_cast<size_t>(slot) * c->n_own + o] = p->val[p_];
+      coef[static_cast<size_t>(slot) * n_coef + o] = p->val[p_];
       ++slot;
     }
     // every in-grid neighbour must be present (absent ones would be read as 0)
@@ -865,7 +888,14 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->row_begin = rb;
     c->row_end = re;
     c->n_own = (re - rb) * c->w;
-    c->halo = c->w;
+    // Multi-rank stencil: H = min(4, thinnest slab) halo rows of V and of the
+    // coefficients, so a launch can fuse up to H sub-steps: it advances the
+    // neighbours' boundary rows itself and exchanges H rows once per launch.
+    if (c->world > 1 && kind == CWG_OP_STENCIL2D) {
+      c->hrows_v = static_cast<int>(std::max<long long>(1, std::min<long long>(4, c->ny1 / c->world)));
+      c->hrows_c = c->hrows_v;
+    }
+    c->halo = c->hrows_v * c->w;
     c->own_global0 = rb * c->w;
     c->node_offset = c->own_global0 - c->halo;
   } else {
@@ -901,11 +931,18 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->d_coef = upload(s3_coef.data(), s3_coef.size());
   } else {
     validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
-    std::vector<double> mass_own(p->lumped_mass + c->own_global0, p->lumped_mass + c->own_global0 + c->n_own);
+    // lumped mass of the coefficient rows (owned rows, plus hrows_c halo rows
+    // each side for a multi-rank stencil; rows beyond the sheet: 1, never read)
+    const long long rows_c = (c->row_end - c->row_begin) + 2ll * c->hrows_c;
+    c->n_coef = kind == CWG_OP_STENCIL2D ? rows_c * c->w : c->n_own;
+    std::vector<double> mass_own(static_cast<size_t>(c->n_coef), 1.0);
+    const long long g0 = kind == CWG_OP_STENCIL2D ? (c->row_begin - c->hrows_c) * c->w : c->own_global0;
+    for (long long o = 0; o < c->n_coef; ++o)
+      if (g0 + o >= 0 && g0 + o < p->n) mass_own[static_cast<size_t>(o)] = p->lumped_mass[g0 + o];
     c->d_mass = upload(mass_own.data(), mass_own.size());
-    c->n_mass = c->n_own;
-    c->d_cm = dev_alloc<double>(c->n_own);
-    CUDA_TRY(launch_mass_factor(c->d_mass, c->n_own, c->dt_ad, c->d_cm, c->stream));
+    c->n_mass = c->n_coef;
+    c->d_cm = dev_alloc<double>(c->n_coef);
+    CUDA_TRY(launch_mass_factor(c->d_mass, c->n_coef, c->dt_ad, c->d_cm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
   if (kind == CWG_OP_STRUCT3D) {
@@ -1360,38 +1397,39 @@ int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t 
       ranks[r]->stream = shared;  // one stream: every rank's work is ordered as enqueued below
     }
     // the halo exchange of halo_exchange(), as device copies between the ranks' current V buffers
-    auto exchange = [&] {
+    auto exchange = [&](int rows) {
       for (int r = 0; r < world; ++r) {
         cwg_ctx* c = ranks[r];
         double* buf = c->d_v[c->cur];
-        const size_t w = static_cast<size_t>(c->w);
+        const size_t n = static_cast<size_t>(c->w) * static_cast<size_t>(rows);
+        const size_t own0 = static_cast<size_t>(c->halo), own1 = own0 + static_cast<size_t>(c->n_own);
         if (r > 0) {
           cwg_ctx* b = ranks[r - 1];
-          CUDA_TRY(cudaMemcpyAsync(buf, b->d_v[b->cur] + b->n_own, w * sizeof(double), cudaMemcpyDeviceToDevice,
-                                   shared));
+          CUDA_TRY(cudaMemcpyAsync(buf + own0 - n, b->d_v[b->cur] + b->halo + b->n_own - n, n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, shared));
         }
         if (r + 1 < world) {
           cwg_ctx* t = ranks[r + 1];
-          CUDA_TRY(cudaMemcpyAsync(buf + c->n_own + w, t->d_v[t->cur] + w, w * sizeof(double),
+          CUDA_TRY(cudaMemcpyAsync(buf + own1, t->d_v[t->cur] + t->halo, n * sizeof(double),
                                    cudaMemcpyDeviceToDevice, shared));
         }
+      }
+    };
+    auto diffuse_all = [&](int count, int ev0) {
+      int q = 0;
+      for (int T : diffusion_groups(c0, count)) {
+        exchange(T);
+        for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], T, 0, ev0 + q);
+        q += T;
       }
     };
     try {
       for (long long s = first; s < first + count; ++s) {
         for (int r = 0; r < world; ++r) set_clock(ranks[r], s);
         const int l = c0->l;
-        if (s == 0)
-          for (int q = 0; q < l; ++q) {  // step I
-            exchange();
-            for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], 1, 0, q);
-          }
+        if (s == 0) diffuse_all(l, 0);                                                   // step I
         for (int r = 0; r < world; ++r) enqueue_reaction(ranks[r], 0, l, false, 0.0);  // step A
-        const int cnt = s == c0->n_steps - 1 ? l : 2 * l;
-        for (int q = 0; q < cnt; ++q) {  // step III / merged B
-          exchange();
-          for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], 1, 0, l + 1 + q);
-        }
+        diffuse_all(s == c0->n_steps - 1 ? l : 2 * l, l + 1);                         // step III / merged B
         const long long S = s + 1;
         for (int r = 0; r < world; ++r) {
           cwg_ctx* c = ranks[r];

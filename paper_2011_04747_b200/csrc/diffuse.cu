@@ -32,7 +32,8 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
   const bool skip = earlier_failure(a.err, seq);
   for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown;
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long i = o + s.w;  // local index
+    const long long i = o + s.hrows_v * s.w;  // local V index
+    const long long oc = o + s.hrows_c * s.w;  // local coefficient index
     const double vi = a.vin[i];
     if (skip) {
       a.vout[i] = vi;
@@ -41,7 +42,7 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
     const long long r = o / s.w, x = o - r * s.w;
     const long long gy = s.row_begin + r;
     const bool has_s = gy > 0, has_n = gy + 1 < s.ny1, has_w = x > 0, has_e = x + 1 < s.w;
-    const double* c = s.coef + o;
+    const double* c = s.coef + oc;
     const long long P = s.cpitch;
     double acc = 0.0;
     if (has_s) {
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
       acc += c[7 * P] * a.vin[i + s.w];
       if (has_e) acc += c[8 * P] * a.vin[i + s.w + 1];
     }
-    const double out = vi - s.cm[o] * acc;
+    const double out = vi - s.cm[oc] * acc;
     a.vout[i] = out;
     if (!isfinite(out))
       record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.w) << 22, seq, 2);
@@ -122,11 +123,17 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
     px[r] = rx;
     py[r] = ry;
     const long long x = gx0 + rx, yl = ly0 + ry, gy = s.row_begin + yl;
-    const bool own = valid && (!EDGE || (x >= 0 && x < w && yl >= 0 && yl < rows));
-    fl[r] = own ? (1u | (gy > 0 ? 2u : 0u) | (gy + 1 < s.ny1 ? 4u : 0u) | (x > 0 ? 8u : 0u) | (x + 1 < w ? 16u : 0u))
+    // computed: inside the sheet and within the local coefficient rows (with
+    // hrows_c > 0, halo points of a neighbouring rank are advanced too);
+    // owned: written back and failure-checked
+    const bool own = valid && (!EDGE || (x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -s.hrows_c &&
+                                         yl < rows + s.hrows_c));
+    const bool mine = yl >= 0 && yl < rows;
+    fl[r] = own ? (1u | (gy > 0 ? 2u : 0u) | (gy + 1 < s.ny1 ? 4u : 0u) | (x > 0 ? 8u : 0u) | (x + 1 < w ? 16u : 0u) |
+                   (mine ? 32u : 0u))
                 : 0u;
     vi[r] = own ? (ry + T) * VX + (rx + T) : VX + 1;  // inactive slots read a safe in-range cell
-    const long long o = own ? yl * w + x : 0;
+    const long long o = own ? (yl + s.hrows_c) * w + x : 0;
     const double* cp = s.coef + o;
 #pragma unroll
     for (int c = 0; c < 9; ++c) cf[r][c] = own ? __ldg(cp + c * s.cpitch) : 0.0;
@@ -180,7 +187,7 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
       }
       out[r] = o;
       if (q + 1 < T && act) dst[vi[r]] = o;
-      if (act && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
+      if (act && (f & 32u) && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
         const long long x = gx0 + px[r], yl = ly0 + py[r];
         record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
                                   (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2);
@@ -192,7 +199,7 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r * NT >= TBX * TBY) break;
-        if (fl[r] & 1u) a.vout[(ly0 + py[r] + 1) * w + gx0 + px[r]] = out[r];
+        if (fl[r] & 32u) a.vout[(ly0 + py[r] + s.hrows_v) * w + gx0 + px[r]] = out[r];
       }
     }
   }
@@ -208,11 +215,11 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
   const long long rows = s.rows, w = s.w;
   {
     // V on the tile + T halo; rows outside the sheet are never read (presence flags)
-    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
+    const double* vsrc = a.vin + (ly0 - T + s.hrows_v) * w + gx0 - T;
     for (int t = threadIdx.x; t < VX * VY; t += NT) {
       const int cx = t % VX, cy = t / VX;
       const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
-      const bool in = x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows;
+      const bool in = x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -s.hrows_v && yl < rows + s.hrows_v;
       Vs[0][t] = in ? vsrc[static_cast<long long>(cy) * w + cx] : 0.0;
     }
   }
@@ -322,11 +329,11 @@ __global__ void __launch_bounds__(NT, 1)
   };
   auto fetch_v = [&](int tile, double* vdst) {
     const long long gx0 = static_cast<long long>(tile % tiles_x) * TBX, ly0 = static_cast<long long>(tile / tiles_x) * TBY;
-    const double* vsrc = a.vin + (ly0 - T + 1) * w + gx0 - T;
+    const double* vsrc = a.vin + (ly0 - T + s.hrows_v) * w + gx0 - T;
     for (int t = threadIdx.x; t < VXY; t += NT) {
       const int cx = t % VX, cy = t / VX;
       const long long x = gx0 - T + cx, gy = s.row_begin + ly0 - T + cy, yl = ly0 - T + cy;
-      if (x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -1 && yl <= rows)
+      if (x >= 0 && x < w && gy >= 0 && gy < s.ny1 && yl >= -s.hrows_v && yl < rows + s.hrows_v)
         cp_async8(vdst + t, vsrc + static_cast<long long>(cy) * w + cx);
       else
         vdst[t] = 0.0;  // outside the sheet: never read (presence flags)
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (r * NT >= TBX * TBY) break;
-          if (fl[r] & 1u) a.vout[(ly0 + py[r] + 1) * w + gx0 + px[r]] = out[r];
+          if (fl[r] & 1u) a.vout[(ly0 + py[r] + s.hrows_v) * w + gx0 + px[r]] = out[r];
         }
       }
     }
