@@ -114,3 +114,16 @@ def test_loopback_thin_slabs():
         ref = _single(p)
         assert np.array_equal(out.v, ref.final_state.v), world
         assert np.array_equal(kh, ref.k_histogram)
+
+
+def test_loopback_c2_single_substep_launches():
+    """C2 geometry: l = 1, so step I is a single plain-kernel sub-step and the
+    merged steps are one fused launch of 2 -- both with the multi-rank halo
+    offsets."""
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import problems
+    p = problems.c2(t_end=3.0)
+    assert cw.diffusion_substeps(0.1, p.sheet.op.dt_s, False, cw.Scheme.DAETI).l == 1
+    out, kh = _loopback(p, 2)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
