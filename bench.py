@@ -317,6 +317,10 @@ def main():
     fuse = 1 if is3d else int(os.environ.get("CWG_DIFF_TB", "4"))
     fuse = max(1, min(4, fuse))  # (multi-rank 2D: halo depth min(4, rows per rank) >= 4 in every bench config)
     launches_per_step = diffusion_launches(2 * info.l, fuse)
+    # large one-GPU 2D sheets run the TMA-fed persistent kernel (cwg_host.cu enqueue_diffusion)
+    sheet = getattr(prob, "sheet", None)
+    tma_path = (not is3d and world == 1 and sheet is not None and os.environ.get("CWG_TB_TMA", "1") != "0"
+                and -(-sheet.nx1 // 64) * -(-sheet.ny1 // 16) >= 2 * 148)
     coef_b = 0.0 if is3d else 80.0
     diff_bytes_step = info.n_local * launches_per_step * (16.0 + coef_b)
     diff_bytes = diff_bytes_step / (info.n_local * 2 * info.l)
@@ -338,8 +342,8 @@ def main():
                          "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
-                                       "diffuse_stencil2d_tb" if fuse > 1 and launches_per_step < 2 * info.l
-                                       else "diffuse_stencil2d"),
+                                       ("diffuse_stencil2d_tbm (TMA)" if tma_path else "diffuse_stencil2d_tb")
+                                       if fuse > 1 and launches_per_step < 2 * info.l else "diffuse_stencil2d"),
                                    "achieved": diff_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                                    "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                    "peak_source": peak_src, "bytes_per_node_substep": diff_bytes,

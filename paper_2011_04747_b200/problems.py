@@ -78,13 +78,16 @@ def c2(model="ohara2011-epi", t_end=500.0, k0_down=3, amplitude=C2_AMPLITUDE, ra
     return Problem("C2", sh, [model], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, amplitude, None)], cfg, probes)
 
 
-def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size=5.0) -> Problem:
+def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size=5.0, amplitude_s2=80.0) -> Problem:
     """Pathological sheet (EXTENSION; parity pinned to the C oracle only).
 
     Central scar (r = 1 cm): elements with D = 0 and passive nodes; border
     zone (1-1.5 cm): D x 0.5 and per-node GKr x U(0.8, 1.2) drawn with
-    numpy's PCG64(seed). S1: left edge x <= 0 at t = 0; S2: quadrant
-    [0, size/2]^2 at t = 300 ms.
+    numpy's PCG64(seed). S1: left edge x <= 0 at t = 0 (2x the line
+    threshold, as C1); S2: quadrant [0, size/2]^2 at t = 300 ms with
+    amplitude_s2 = 80 mV/ms -- a whole region has no diffusive drain, and at
+    the S1 amplitude its corner node diverges under forward Euler (in the
+    oracle as on the GPU: node 0, t = 300.36 ms).
     """
     nx = int(round(size / h))
     c = size / 2.0
@@ -105,7 +108,7 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
     cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
     probes = [sh.nearest(0.5, c), sh.nearest(c, 0.5), sh.nearest(size - 0.5, c)]
     return Problem("C3", sh, ["ohara2011-epi", "passive"], model_of_node,
-                   [(s1, 0.0, 1.0, amplitude, None), (s2, 300.0, 1.0, amplitude, None)], cfg, probes, gkr,
+                   [(s1, 0.0, 1.0, amplitude, None), (s2, 300.0, 1.0, amplitude_s2, None)], cfg, probes, gkr,
                    notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)")
 
 
