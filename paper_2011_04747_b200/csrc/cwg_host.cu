@@ -367,6 +367,21 @@ T* upload(const T* h, size_t count) {
   return d;
 }
 
+// Frees the temporary device buffers of a one-shot entry point on every exit
+// path, including a CUDA_TRY / validation throw half-way through.
+struct DevScope {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* keep(T* p) {
+    ptrs.push_back(p);
+    return p;
+  }
+  ~DevScope() {
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
 // ---------------------------------------------------------------- step pieces
 // Exchange `rows` halo rows (planes) with both neighbours: my first / last
 // `rows` owned rows go down / up, theirs land in the halo rows adjacent to my
@@ -1814,7 +1829,8 @@ double cwg_fp64_peak_tflops(int device, double seconds) {
     int occ = 0;
     occ = 8;  // 8 x 256 threads per SM
     const int blocks = prop.multiProcessorCount * occ;
-    double* out = dev_alloc<double>(1);
+    DevScope scope;
+    double* out = scope.keep(dev_alloc<double>(1));
     cudaEvent_t a, b;
     CUDA_TRY(cudaEventCreate(&a));
     CUDA_TRY(cudaEventCreate(&b));
@@ -1843,7 +1859,6 @@ double cwg_fp64_peak_tflops(int device, double seconds) {
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    dev_free(out);
     result = best;
   });
   return result;
@@ -1861,11 +1876,11 @@ bool propagates(cwg_ctx* c, double amp, long long steps, cudaGraphExec_t& graph,
   for (const auto& b : c->bins) {
     double rest[64] = {0};
     cwg_model_rest_state(b.kind, rest);
-    double* d_rest = upload(rest, 64);
+    DevScope scope;
+    double* d_rest = scope.keep(upload(rest, 64));
     CUDA_TRY(launch_init_rest(c->d_v[0], c->d_S, c->pitch, c->d_last, b.d_list, b.first, b.count, d_rest,
                               state_count(b.kind), c->stride, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    dev_free(d_rest);
   }
   ErrRec none{kNoError, -1, 0, 0};
   CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
@@ -2031,21 +2046,16 @@ int cwg_diffusion_substep(int64_t n, const int64_t* rp, const int64_t* col, cons
   return guarded(err, [&] {
     CUDA_TRY(cudaSetDevice(device));
     const long long nnz = rp[n];
-    long long* d_rp = upload(reinterpret_cast<const long long*>(rp), n + 1);
-    long long* d_col = upload(reinterpret_cast<const long long*>(col), nnz);
-    double* d_val = upload(val, nnz);
-    double* d_m = upload(mass, n);
-    double* d_v = upload(v, n);
-    double* d_o = dev_alloc<double>(n);
+    DevScope ds;
+    long long* d_rp = ds.keep(upload(reinterpret_cast<const long long*>(rp), n + 1));
+    long long* d_col = ds.keep(upload(reinterpret_cast<const long long*>(col), nnz));
+    double* d_val = ds.keep(upload(val, nnz));
+    double* d_m = ds.keep(upload(mass, n));
+    double* d_v = ds.keep(upload(v, n));
+    double* d_o = ds.keep(dev_alloc<double>(n));
     CUDA_TRY(launch_diffuse_csr_plain(n, d_rp, d_col, d_val, d_m, d_v, dt_sub, d_o, nullptr));
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpy(out, d_o, n * sizeof(double), cudaMemcpyDeviceToHost));
-    dev_free(d_rp);
-    dev_free(d_col);
-    dev_free(d_val);
-    dev_free(d_m);
-    dev_free(d_v);
-    dev_free(d_o);
   });
 }
 
@@ -2055,21 +2065,17 @@ int cwg_rates(int kind, int64_t n, const double* v, const double* s, const doubl
     validation(state_count(kind) >= 0, "unknown cell model kind");
     CUDA_TRY(cudaSetDevice(device));
     const int ns = state_count(kind);
-    double* d_v = upload(v, n);
-    double* d_s = upload(s, static_cast<size_t>(n) * ns);
-    double* d_i = upload(ist, n);
-    double* d_dv = dev_alloc<double>(n);
-    double* d_ds = dev_alloc<double>(static_cast<size_t>(n) * ns);
+    DevScope scope;
+    double* d_v = scope.keep(upload(v, n));
+    double* d_s = scope.keep(upload(s, static_cast<size_t>(n) * ns));
+    double* d_i = scope.keep(upload(ist, n));
+    double* d_dv = scope.keep(dev_alloc<double>(n));
+    double* d_ds = scope.keep(dev_alloc<double>(static_cast<size_t>(n) * ns));
     CUDA_TRY(is_ord(kind) ? launch_rates_ord(kind, n, d_v, d_s, d_i, d_dv, d_ds, nullptr)
                           : launch_rates_exact(kind, n, d_v, d_s, d_i, d_dv, d_ds, nullptr));
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpy(dv, d_dv, n * sizeof(double), cudaMemcpyDeviceToHost));
     if (ns) CUDA_TRY(cudaMemcpy(ds, d_ds, static_cast<size_t>(n) * ns * sizeof(double), cudaMemcpyDeviceToHost));
-    dev_free(d_v);
-    dev_free(d_s);
-    dev_free(d_i);
-    dev_free(d_dv);
-    dev_free(d_ds);
   });
 }
 
@@ -2102,17 +2108,18 @@ int cwg_pace_cells(int kind, int64_t n, const double* cycle_ms, const double* am
     a.n = n;
     a.n_beats = n_beats;
     a.dt = stable_step(kind) / 2.0;  // ionic.cpp:127
-    a.cycle = upload(cycle_ms, n);
-    a.amp = upload(amplitude, n);
-    a.dur = upload(duration_ms, n);
-    a.rest = upload(rest, static_cast<size_t>(ns) + 1);
-    a.state_out = dev_alloc<double>(static_cast<size_t>(n) * (ns + 1));
-    a.prev_out = dev_alloc<double>(static_cast<size_t>(n) * (ns + 1));
-    a.apd_out = dev_alloc<double>(static_cast<size_t>(n) * n_beats);
-    a.maxrel_out = dev_alloc<double>(n);
-    a.status_out = dev_alloc<int>(n);
-    a.beat_out = dev_alloc<int>(n);
-    a.fail_t_out = dev_alloc<double>(n);
+    DevScope scope;
+    a.cycle = scope.keep(upload(cycle_ms, n));
+    a.amp = scope.keep(upload(amplitude, n));
+    a.dur = scope.keep(upload(duration_ms, n));
+    a.rest = scope.keep(upload(rest, static_cast<size_t>(ns) + 1));
+    a.state_out = scope.keep(dev_alloc<double>(static_cast<size_t>(n) * (ns + 1)));
+    a.prev_out = scope.keep(dev_alloc<double>(static_cast<size_t>(n) * (ns + 1)));
+    a.apd_out = scope.keep(dev_alloc<double>(static_cast<size_t>(n) * n_beats));
+    a.maxrel_out = scope.keep(dev_alloc<double>(n));
+    a.status_out = scope.keep(dev_alloc<int>(n));
+    a.beat_out = scope.keep(dev_alloc<int>(n));
+    a.fail_t_out = scope.keep(dev_alloc<double>(n));
     CUDA_TRY(is_ord(kind) ? launch_pace_ord(kind, a, nullptr) : launch_pace_exact(kind, a, nullptr));
     CUDA_TRY(cudaDeviceSynchronize());
     std::vector<int> st(static_cast<size_t>(n)), beat(static_cast<size_t>(n));
@@ -2137,10 +2144,6 @@ int cwg_pace_cells(int kind, int64_t n, const double* cycle_ms, const double* am
         bad_t = ft[static_cast<size_t>(i)];
       }
     }
-    for (void* p : {(void*)a.cycle, (void*)a.amp, (void*)a.dur, (void*)a.rest, (void*)a.state_out,
-                    (void*)a.prev_out, (void*)a.apd_out, (void*)a.maxrel_out, (void*)a.status_out,
-                    (void*)a.beat_out, (void*)a.fail_t_out})
-      cudaFree(p);
   });
   if (rc != CWG_OK || first_bad < 0) return rc;
   // the reference throws InstabilityError(msg, -1, t) (ionic.cpp:141-147)
