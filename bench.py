@@ -339,7 +339,12 @@ def main():
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak if fp64_peak > 0 else None,
                          "traffic": traffic, "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no "
                                                              "FP64 entry)",
-                         "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL},
+                         "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL,
+                         "note": ("latency regime: ~1 node per lane (8 warps/SM at >168 registers), each node's k "
+                                  "sub-steps sequential, so the step's largest k sets the critical path; see "
+                                  "DESIGN.md 3.1 / 5" if args.config in ("c1", "c2") else
+                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe ~51% of "
+                                  "active cycles (profiles/r01_react_c3_full.txt)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
                                        ("diffuse_stencil2d_tbm (TMA)" if tma_path else "diffuse_stencil2d_tb")
