@@ -1,9 +1,11 @@
 // TEST INFRASTRUCTURE: the C++ drop-in (include/cardwave_gpu.hpp) side by side
 // with the unmodified reference, on the same reference-built problem.
 //   shim_parity ap|ord|abort|diffusion   -> one JSON line; exit 0 on parity
+//   shim_parity c2 [t_end_ms]            -> the bench workload (BASELINE configs[1]) end to end
 // Built by oracle/Makefile (target `shim`) into oracle/_ref/shim_parity,
 // linked against the reference objects and ../paper_2011_04747_b200/libcwgpu.so.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -19,8 +21,11 @@ using namespace cardwave;
 
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "ap";
-  Mesh mesh = build_regular_sheet(1.0, 1.0, 0.01, 0.0);
-  AssembledOperator op = assemble(mesh, build_diffusion_field(mesh, 0.001, 0.00066, 1.0));
+  const bool c2 = mode == "c2";
+  // C2: 5 x 5 cm, h = 0.025, fibres 45 deg, D_l 0.0012 / rho 0.25, ORd-epi, corner disc r = 0.15 at 100 mV/ms
+  Mesh mesh = c2 ? build_regular_sheet(5.0, 5.0, 0.025, M_PI / 4) : build_regular_sheet(1.0, 1.0, 0.01, 0.0);
+  AssembledOperator op = c2 ? assemble(mesh, build_diffusion_field(mesh, 0.0012, 0.00066, 0.25))
+                            : assemble(mesh, build_diffusion_field(mesh, 0.001, 0.00066, 1.0));
   if (mode == "diffusion") {
     std::vector<double> v(op.rows()), a, b;
     for (std::size_t i = 0; i < v.size(); ++i) v[i] = -80.0 + 100.0 * std::sin(0.37 * static_cast<double>(i));
@@ -35,10 +40,16 @@ int main(int argc, char** argv) {
   RegionSelector sel;
   sel.kind = RegionSelector::Kind::half_plane_x_le;
   sel.value = ap ? 0.05 : 0.0;
+  if (c2) {
+    sel.kind = RegionSelector::Kind::disc;
+    sel.cx = 0.0;
+    sel.cy = 0.0;
+    sel.radius = 0.15;
+  }
   Protocol prot;
   Stimulus st;
   st.nodes = select_nodes(mesh, sel);
-  st.amplitude = ap ? 100.0 : 592.0;
+  st.amplitude = ap || c2 ? 100.0 : 592.0;
   prot.entries.push_back(st);
   ProtocolIndex index(prot, mesh.node_count());
   SimulationSetup setup;
@@ -46,10 +57,14 @@ int main(int argc, char** argv) {
   setup.models = models;
   setup.protocol = &index;
   setup.probes = {Probe{5050, "mid"}, Probe{10200, "far"}};
+  if (c2)
+    setup.probes = {Probe{mesh.nearest_node(0.0, 0.0), "corner"}, Probe{mesh.nearest_node(2.5, 2.5), "centre"},
+                    Probe{mesh.nearest_node(5.0, 5.0), "far"}};
   SchemeConfig cfg;
   cfg.scheme = Scheme::DAETI;
   cfg.dt_ms = 0.1;
   cfg.t_end_ms = ap ? 100.0 : 20.0;
+  if (c2) cfg.t_end_ms = argc > 2 ? std::atof(argv[2]) : 500.0;
   cfg.k0_down = mode == "abort" ? 1 : (ap ? 1 : 3);
   NodeStateArray s0 = make_initial_state(mesh, models, {0});
   // snapshots (asynchronous in the drop-in) and progress callbacks
