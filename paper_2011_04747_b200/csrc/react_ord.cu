@@ -197,13 +197,15 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- INa + INaL: the 14 V-dependent exponentials in one batch
   double i_na;
   {
-    double e[14] = {-(v + 39.57) * (1.0 / 9.871),   (v + 11.64) * (1.0 / 34.77),  -(v + 77.42) * (1.0 / 5.955),
+    double e[12] = {-(v + 39.57) * (1.0 / 9.871),   (v + 11.64) * (1.0 / 34.77),  -(v + 77.42) * (1.0 / 5.955),
                     (v + 82.90) * (1.0 / 6.086),    -(v + 1.196) * (1.0 / 6.285), (v + 0.5096) * (1.0 / 20.27),
                     -(v + 17.95) * (1.0 / 28.05),   (v + 5.730) * (1.0 / 56.66),  -(v + 100.6) * (1.0 / 8.281),
-                    (v + 0.9941) * (1.0 / 38.45),   (v + 89.1) * (1.0 / 6.086),   -(v + 42.85) * (1.0 / 5.264),
-                    (v + 87.61) * (1.0 / 7.488),    (v + 93.81) * (1.0 / 7.488)};
+                    (v + 0.9941) * (1.0 / 38.45),   -(v + 42.85) * (1.0 / 5.264), (v + 87.61) * (1.0 / 7.488)};
     vexp_n<FP>(e);
-    double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e[10], 1.0 + e[11], 1.0 + e[12], 1.0 + e[13],
+    // e^((v+89.1)/6.086) = e^((v+82.9)/6.086) e^(6.2/6.086), e^((v+93.81)/7.488) = e^((v+87.61)/7.488) e^(6.2/7.488)
+    const double e_hp = FP ? e[3] * 2.7696792380394113 : vexp<FP>((v + 89.1) * (1.0 / 6.086));
+    const double e_hlp = FP ? e[11] * 2.288717124596482 : vexp<FP>((v + 93.81) * (1.0 / 7.488));
+    double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e_hp, 1.0 + e[10], 1.0 + e[11], 1.0 + e_hlp,
                    0.02136 * e[8] + 0.3052 * e[9]};
     vrcp_n<FP>(q);
     const double m_inf = q[0], h_inf = q[1], hp_inf = q[2];
@@ -232,15 +234,17 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- Ito
   double i_to;
   {
-    double e[14] = {-(v - 14.34) * (1.0 / 14.82),     -(v - 18.4099) * (1.0 / 29.3814), (v + 100.0) * (1.0 / 29.3814),
+    double e[13] = {-(v - 14.34) * (1.0 / 14.82),     -(v - 18.4099) * (1.0 / 29.3814), (v + 100.0) * (1.0 / 29.3814),
                     (v + 43.94) * (1.0 / 5.711),      -(v + 100.0) * (1.0 / 100.0),     (v + 50.0) * (1.0 / 16.59),
                     -(v + 96.52) * (1.0 / 59.05),     (v + 114.1) * (1.0 / 8.079),      (v + 70.0) * (1.0 / 5.0),
-                    (v - 213.6) * (1.0 / 151.2),      -(v - 24.34) * (1.0 / 14.82),     (v - 167.4) * (1.0 / 15.89),
-                    -(v - 12.23) * (1.0 / 0.2154),    (v + 70.0) * (1.0 / 20.0)};
+                    (v - 213.6) * (1.0 / 151.2),      (v - 167.4) * (1.0 / 15.89),      -(v - 12.23) * (1.0 / 0.2154),
+                    (v + 70.0) * (1.0 / 20.0)};
     vexp_n<FP>(e);
+    // e^(-(v-24.34)/14.82) = e^(-(v-14.34)/14.82) e^(10/14.82)
+    const double e_ap = FP ? e[0] * 1.9635691902911017 : vexp<FP>(-(v - 24.34) * (1.0 / 14.82));
     double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), 1.0 + e[2], 1.0 + e[3],
                     0.3933 * e[4] + 0.08004 * e[5], 0.001416 * e[6] + 1.780e-8 * e[7], 1.0 + e[8],
-                    1.0 + e[9], 1.0 + e[10], e[11] + e[12], 1.0 + e[13]};
+                    1.0 + e[9], 1.0 + e_ap, e[10] + e[11], 1.0 + e[12]};
     vrcp_n<FP>(q);
     const double a_inf = q[0];
     const double r_a = (1.0 / 1.0515) * (q[1] + 3.5 * q[2]);
@@ -274,14 +278,16 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
-    double e[11] = {-(v + 3.940) * (1.0 / 4.230), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
+    double e[10] = {-(v + 3.940) * (1.0 / 4.230), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
                     (v + 19.58) * (1.0 / 3.696),  (v + 20.0) * (1.0 / 10.0),  -(v + 5.0) * (1.0 / 4.0),
                     (v + 5.0) * (1.0 / 6.0),      (v - 4.0) * (1.0 / 7.0),    -v * (1.0 / 3.0),
-                    v * (1.0 / 7.0),              (v - 10.0) * (1.0 / 10.0)};
+                    v * (1.0 / 7.0)};
     vexp_n<FP>(e);
     const double eff = e[4], efc = e[7];
+    // e^((v-10)/10) = e^((v+20)/10) e^-3
+    const double e_fca = FP ? e[4] * 0.049787068367863944 : vexp<FP>((v - 10.0) * (1.0 / 10.0));
     double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, 0.000035 * e[5] + 0.000035 * e[6], efc,
-                   0.00012 * e[8] + 0.00012 * e[9], 1.0 + e[10]};
+                   0.00012 * e[8] + 0.00012 * e[9], 1.0 + e_fca};
     vrcp_n<FP>(q);
     double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
     vrcp_n<FP>(q2);
