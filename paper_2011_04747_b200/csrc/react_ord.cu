@@ -165,9 +165,9 @@ template <int CT, bool FP, class SA>
 __device__ __forceinline__ Pro prologue(double v, SA s) {
   Pro p;
   const double nai = s[NAI], ki = s[KI], cass = s[CASS];
-  p.ena = RTF * log(NAO * rcp(nai));
-  p.ek = RTF * log(KO * rcp(ki));
-  p.eks = RTF * log((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
+  p.ena = RTF * flog(NAO * rcp(nai));
+  p.ek = RTF * flog(KO * rcp(ki));
+  p.eks = RTF * flog((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
   p.camkt = s[CAMKT];
   p.camk_b = 0.05 * (1.0 - p.camkt) * cass * rcp(cass + 0.0015);
   const double camk_a = p.camk_b + p.camkt;
@@ -369,7 +369,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     const double xs_inf = p[0];
     const double r_xs1 = vrcp<FP>(817.3 + p[1]);
     const double r_xs2 = 0.01 * f[3] + 0.0193 * f[4];
-    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - log(cai))) /* log(3.8e-5) */);
+    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - flog(cai))) /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
