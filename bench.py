@@ -38,9 +38,9 @@ FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<epi>>
 # (2*DFMA + DMUL + DADD predicated-on lane ops / evaluations), counted by ncu
 # over every reaction launch of a 60-step C2 run (tools/flops_per_eval.py;
-# profiles/r01_flops_per_eval_c2.txt): 1086.3 DFMA + 454.6 DMUL + 323.3 DADD.
+# profiles/r01_flops_per_eval_c2.txt): 1054.3 DFMA + 442.6 DMUL + 299.3 DADD.
 # Updated when the kernel changes.
-ORD_FP64_FLOPS_PER_EVAL = 2950.6
+ORD_FP64_FLOPS_PER_EVAL = 2850.6
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 
