@@ -321,3 +321,26 @@ def test_compare_schemes_one_device_operator(cw, ora, problems):
         assert c.e_lat == pp.nrmse(ost.result.lat_map, c.result.lat_map) and 0.0 < c.e_lat < 0.5
         assert c.e_apd == pp.nrmse(ost.result.apd90_map, c.result.apd90_map)
         assert all(math.isfinite(a) for a in c.apd90_per_probe) and all(d >= 0 for d in c.max_dv_per_probe)
+
+
+@pytest.mark.parametrize("model", ["aliev-panfilov", "ohara2011-epi"])
+def test_generic_csr_operator_run(cw, ora, problems, model):
+    """The generic CSR operator path (any mesh; diffuse_csr) through a whole run:
+    bit-identical to the stencil path and to the oracle for AP, within
+    tolerance for ORd."""
+    from paper_2011_04747_b200 import _lib as L
+    p = problems.c1(model=model, t_end=8.0, k0_down=1 if model == "aliev-panfilov" else 3)
+    setup = p.setup()
+    integ = cw.StrangIntegrator(setup, p.cfg, model_of_node=p.model_of_node, op_kind=L.OP_CSR)
+    try:
+        r_csr = cw.run_simulation(p.initial_state(), setup, p.cfg, integrator=integ)
+    finally:
+        integ.close()
+    r_st = gpu_run(p)
+    o = oracle_run(p)
+    assert np.array_equal(r_csr.final_state.v, r_st.final_state.v)
+    assert np.array_equal(r_csr.k_histogram, o["k_histogram"])
+    if model == "aliev-panfilov":
+        assert np.array_equal(r_csr.final_state.v, o["v"])
+    else:
+        assert np.max(np.abs(r_csr.final_state.v - o["v"])) <= V_TOL_MV
