@@ -146,10 +146,11 @@ __device__ __forceinline__ void gate(SA s, double* ds, int i, double h, double x
   put<R>(s, ds, i, h, (xinf - s[i]) * rate);
 }
 
-// The evaluation is split into composable pieces (prologue, group A, group B,
-// finish) so the two-warp kernel (react_pair.cuh) can run groups A and B in
-// different warps; step() chains them in one thread. Arithmetic is identical
-// either way.
+// The evaluation is split into composable pieces (prologue, group A: INa,
+// INaL, Ito, ICaL; group B: IKr, IKs, IK1, NaCa, NaK, background; finish:
+// fluxes, concentrations, V); step() chains them in one thread. (A two-warp
+// variant that ran groups A and B in different warps was measured slower and
+// dropped; the split keeps each piece's live ranges short.)
 struct Pro {
   double ena, ek, eks, camk_b, camkt, fk, nfk, vfrt, e1, e2, xq1, xq2;
 };
