@@ -2,6 +2,7 @@
 // with the unmodified reference, on the same reference-built problem.
 //   shim_parity ap|ord|abort|diffusion   -> one JSON line; exit 0 on parity
 //   shim_parity c2 [t_end_ms]            -> the bench workload (BASELINE configs[1]) end to end
+//   shim_parity c1 [t_end_ms]            -> BASELINE configs[0] (ORd-epi, C1 line at 592 mV/ms), default 400 ms
 // Built by oracle/Makefile (target `shim`) into oracle/_ref/shim_parity,
 // linked against the reference objects and ../paper_2011_04747_b200/libcwgpu.so.
 #include <cmath>
@@ -65,6 +66,7 @@ int main(int argc, char** argv) {
   cfg.dt_ms = 0.1;
   cfg.t_end_ms = ap ? 100.0 : 20.0;
   if (c2) cfg.t_end_ms = argc > 2 ? std::atof(argv[2]) : 500.0;
+  if (mode == "c1") cfg.t_end_ms = argc > 2 ? std::atof(argv[2]) : 400.0;
   cfg.k0_down = mode == "abort" ? 1 : (ap ? 1 : 3);
   NodeStateArray s0 = make_initial_state(mesh, models, {0});
   // snapshots (asynchronous in the drop-in) and progress callbacks
