@@ -137,9 +137,11 @@ typedef struct {
 /* StrangIntegrator ctor (splitting.cpp:74-93): validates, uploads the operator,
  * stimulus tables and model lists, derives dt_eff, plan and k_max. */
 int cwg_create(const cwg_problem* prob, cwg_ctx** out, cwg_error* err);
+/* StrangIntegrator destructor (splitting.hpp:101-127): frees the device context. */
 void cwg_destroy(cwg_ctx* ctx);
 
-/* Use an external CUDA stream (e.g. torch's current stream); NULL = own stream. */
+/* No reference counterpart (stream plumbing): use an external CUDA stream
+ * (e.g. torch's current stream); NULL = own stream. cwg_stream returns it. */
 int cwg_set_stream(cwg_ctx* ctx, void* cuda_stream);
 void* cwg_stream(cwg_ctx* ctx);
 
@@ -148,9 +150,12 @@ void* cwg_stream(cwg_ctx* ctx);
  * For world > 1 the arrays are the GLOBAL arrays; each rank copies its slab. */
 int cwg_upload_state(cwg_ctx* ctx, const double* v, const double* s_aos, int stride,
                      const double* last_dvdt);
+/* SimulationResult::final_state (splitting.cpp:292) / the state advance()
+ * mutates in place (splitting.cpp:171-181): device SoA -> host AoS. */
 int cwg_download_state(cwg_ctx* ctx, double* v, double* s_aos, int stride, double* last_dvdt);
-/* make_initial_state from the models' rest states directly on the device
- * (no host arrays; for 10^8-node slabs). last_dvdt = 0, V = rest V. */
+/* make_initial_state (splitting.cpp:183-217) from the models' rest states
+ * directly on the device (no host arrays; for 10^8-node slabs). last_dvdt = 0,
+ * V = rest V. */
 int cwg_init_rest_state(cwg_ctx* ctx);
 /* Reconfigure the scheme of an existing context -- cli_compare
  * (runner.cpp:254-324) runs OST / OSTAR / DAETI on one prepared problem, so
@@ -182,14 +187,17 @@ int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t 
  * throw is ever delivered. (world > 1: synchronous, the failure agreement is
  * a collective.) */
 int cwg_snapshot_begin(cwg_ctx* ctx, double* host_v);
+/* Completes cwg_snapshot_begin (see above; splitting.cpp:276-277 delivery). */
 int cwg_snapshot_wait(cwg_ctx* ctx, cwg_error* err);
-/* cudaHostRegister / cudaHostUnregister for caller-owned buffers
- * (e.g. the std::vector handed to on_snapshot). */
+/* No reference counterpart (host memory plumbing): cudaHostRegister /
+ * cudaHostUnregister for caller-owned buffers (e.g. the std::vector handed
+ * to on_snapshot). */
 int cwg_host_register(void* p, size_t bytes);
 int cwg_host_unregister(void* p);
 
-/* Pinned staging for host<->device copies (e2e path); returns host pointers
- * owned by ctx of the sizes of the local slab. */
+/* No reference counterpart (host memory plumbing): pinned staging for
+ * host<->device copies (e2e path); returns host pointers owned by ctx of the
+ * sizes of the local slab. */
 int cwg_pinned_buffers(cwg_ctx* ctx, double** v, double** s_aos, double** last_dvdt);
 
 /* StrangIntegrator::advance (splitting.cpp:171-181): one outer step at t_ms.
@@ -215,17 +223,25 @@ typedef struct {
   int64_t n_local, node_begin; /* this rank's slab */
   int op_kind;                 /* resolved CWG_OP_* */
 } cwg_info;
+/* dt_effective / plan / k_max_global (splitting.hpp:108-110) and the
+ * SimulationResult scalars (splitting.hpp:64-75) */
 int cwg_get_info(cwg_ctx* ctx, cwg_info* info);
-int cwg_get_khist(cwg_ctx* ctx, int64_t* out, int len);            /* cumulative, index k */
+/* k_histogram (splitting.hpp:111): cumulative, index k */
+int cwg_get_khist(cwg_ctx* ctx, int64_t* out, int len);
+/* SimulationResult::traces (splitting.hpp:64-75; recorded at splitting.cpp:271-275) */
 int cwg_get_traces(cwg_ctx* ctx, double* t_ms, double* v /* [probe][sample] */);
+/* SimulationResult lat_map / apd90_map = ActivationDetector::lat / apd90
+ * (postprocess.hpp:45-46, postprocess.cpp:68-90); this rank's slab */
 int cwg_get_maps(cwg_ctx* ctx, double* lat, uint8_t* lat_valid, double* apd90, uint8_t* apd_valid);
 /* reaction / diffusion / recording device time (ms, CUDA events) of the last
  * cwg_advance calls (TimingBreakdown, splitting.hpp:57-62) */
 int cwg_get_timing(cwg_ctx* ctx, double* reaction_ms, double* diffusion_ms, double* recording_ms);
-/* Kernel launches issued by this context so far (for the bench's gpu_launches). */
+/* No reference counterpart (measurement): kernel launches issued by this
+ * context so far (for the bench's gpu_launches). */
 int64_t cwg_launch_count(cwg_ctx* ctx);
 
-/* Benchmark driver (bench.py): enqueue steps [first, first+count) one at a
+/* Benchmark driver (bench.py; the role of the reference's BM_strang_step,
+ * bench_core.cpp:70-75): enqueue steps [first, first+count) one at a
  * time, each preceded by an (untimed) write of flush_bytes to a scratch
  * buffer that evicts L2, and bracketed by CUDA events on the context stream.
  * split_phases = 0: each middle step is one single-step CUDA graph (the
@@ -234,11 +250,13 @@ int64_t cwg_launch_count(cwg_ctx* ctx);
  * the diffusion sub-steps + recording: react_ms[i], diff_ms[i]. */
 int cwg_bench_steps(cwg_ctx* ctx, int64_t first, int64_t count, int64_t flush_bytes, int split_phases,
                     double* step_ms, double* react_ms, double* diff_ms);
-/* Reaction node-updates (rates evaluations) so far = sum_k k * khist[k]. */
+/* Reaction node-updates (rates evaluations) so far = sum_k k * khist[k]
+ * (the reference's k_histogram, splitting.hpp:111, weighted by k). */
 int64_t cwg_reaction_evals(cwg_ctx* ctx);
 
-/* Measured FP64 peak of this device: a DFMA-chain kernel at full occupancy,
- * CUDA-event timed. Returns TFLOP/s (2 flops per DFMA) or < 0 on error. */
+/* No reference counterpart (measurement): FP64 peak of this device, a
+ * DFMA-chain kernel at full occupancy, CUDA-event timed. Returns TFLOP/s
+ * (2 flops per DFMA) or < 0 on error. */
 double cwg_fp64_peak_tflops(int device, double seconds);
 
 /* pace_to_steady_state (ionic.cpp:122-165, ionic.hpp:74), batched: n
@@ -289,23 +307,27 @@ int cwg_diffusion_substep(int64_t n, const int64_t* row_ptr, const int64_t* col,
 int cwg_rates(int model_kind, int64_t n, const double* v, const double* s_aos, const double* i_stim,
               double* dv, double* ds_aos, int device, cwg_error* err);
 
-/* Model metadata (CellModel::state_count / stable_step / rest_state) */
+/* Model metadata: CellModel::state_count (ionic.hpp:23), stable_step
+ * (ionic.hpp:28), rest_state (ionic.hpp:26) */
 int cwg_model_state_count(int model_kind);
 double cwg_model_stable_step(int model_kind);
 int cwg_model_rest_state(int model_kind, double* out /* state_count+1 */);
 int cwg_model_kind_from_name(const char* name); /* -1 if unknown (make_model, ionic.cpp:59) */
 
 /* Adaptation rules (splitting.cpp:48-72), host-side, exported for parity tests */
-int cwg_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max);
-int cwg_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad);
-int cwg_k_max_for(double dt, int model_kind);
+int cwg_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max); /* splitting.cpp:48-54 */
+int cwg_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad); /* :56-67 */
+int cwg_k_max_for(double dt, int model_kind);                                                /* :69-72 */
 
-/* y-slab plan for world ranks over ny1 node rows:
- * [row_begin, row_end) owned rows; balanced by node count. No GPU needed. */
+/* No reference counterpart (new: the reference is single-process OpenMP):
+ * y-slab plan for world ranks over ny1 node rows,
+ * [row_begin, row_end) owned rows, balanced by node count. No GPU needed. */
 int cwg_slab_plan(int64_t ny1, int world, int rank, int64_t* row_begin, int64_t* row_end);
 
+/* No reference counterpart: library version string. */
 const char* cwg_version(void);
-/* Message of the last failed call on this host thread ("" if none). */
+/* No reference counterpart (the reference throws): message of the last failed
+ * call on this host thread ("" if none). */
 const char* cwg_last_error(void);
 
 #ifdef __cplusplus

@@ -35,20 +35,26 @@ enum {
   CWG_SEL_RECT = 4, CWG_SEL_NODE_SET = 5, CWG_SEL_DISC = 6
 };
 
-/* build_regular_sheet + assign_fibrosis (fib_fraction > 0) + build_diffusion_field
- * + assemble. elem_scale: optional [n_elements] multiplier of D (extension). */
+/* build_regular_sheet (mesh.cpp:72-98) + assign_fibrosis (mesh.cpp:100-122,
+ * fib_fraction > 0) + build_diffusion_field (fem.cpp:21-51) + assemble
+ * (fem.cpp:63-176). elem_scale: optional [n_elements] multiplier of D
+ * (extension). cwg_sheet_free releases it. */
 int cwg_sheet_build(double lx_cm, double ly_cm, double h_cm, double fiber_angle_rad,
                     double d0_myocyte, double d0_fibrotic, double rho, double fib_fraction,
                     uint64_t seed, const double* elem_scale, cwg_sheet** out, cwg_error* err);
 void cwg_sheet_free(cwg_sheet* s);
 
+/* Mesh::node_count / element_count (mesh.hpp), AssembledOperator nnz /
+ * rows / dt_s (fem.hpp:23-32), grid node counts of build_regular_sheet */
 int64_t cwg_sheet_nodes(const cwg_sheet* s);
 int64_t cwg_sheet_elements(const cwg_sheet* s);
 int64_t cwg_sheet_nnz(const cwg_sheet* s);
 int64_t cwg_sheet_nx1(const cwg_sheet* s);
 int64_t cwg_sheet_ny1(const cwg_sheet* s);
 double cwg_sheet_dt_s(const cwg_sheet* s);
-/* zero-copy views valid for the sheet's lifetime */
+/* zero-copy views valid for the sheet's lifetime: AssembledOperator row_ptr /
+ * col / val / lumped_mass (fem.hpp:23-32), Mesh::node_coords and node tags
+ * (mesh.hpp) */
 const int64_t* cwg_sheet_row_ptr(const cwg_sheet* s);
 const int64_t* cwg_sheet_col(const cwg_sheet* s);
 const double* cwg_sheet_val(const cwg_sheet* s);
@@ -56,10 +62,11 @@ const double* cwg_sheet_mass(const cwg_sheet* s);
 const double* cwg_sheet_coords(const cwg_sheet* s); /* [n][2] */
 const int32_t* cwg_sheet_tags(const cwg_sheet* s);  /* per node; 0 myocyte-epi, 1 fibroblast */
 
-/* prm = {value, x0, x1, y0, y1, cx, cy, radius}; returns count (writes <= cap) */
+/* select_nodes (mesh.cpp:124-180); prm = {value, x0, x1, y0, y1, cx, cy,
+ * radius}; returns count (writes <= cap) */
 int64_t cwg_sheet_select(const cwg_sheet* s, int kind, const double* prm, const int64_t* set_nodes,
                          int64_t n_set, int64_t* out, int64_t cap);
-int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y);
+int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y); /* Mesh::nearest_node (mesh.cpp:43-57) */
 
 /* ---- 3D slab (EXTENSION for BASELINE configs 4-5; parity pinned to the C
  * oracle's independent CSR assembly, oracle/cw_oracle.c cwo_assemble_slab3d).
