@@ -247,12 +247,22 @@ int64_t cwg_launch_count(cwg_ctx* ctx);
  * split_phases = 0: each middle step is one single-step CUDA graph (the
  * production launch path), step_ms[i] = the step; split_phases = 1: direct
  * launches with an extra event between the reaction kernels (step A) and
- * the diffusion sub-steps + recording: react_ms[i], diff_ms[i]. */
+ * the diffusion sub-steps + recording: react_ms[i], diff_ms[i];
+ * split_phases = 2: the step graph without event nodes, events recorded on
+ * the stream around its launch (react_ms[i] = the step, diff_ms[i] = the
+ * cost of one more stream event record). */
 int cwg_bench_steps(cwg_ctx* ctx, int64_t first, int64_t count, int64_t flush_bytes, int split_phases,
                     double* step_ms, double* react_ms, double* diff_ms);
 /* Reaction node-updates (rates evaluations) so far = sum_k k * khist[k]
  * (the reference's k_histogram, splitting.hpp:111, weighted by k). */
 int64_t cwg_reaction_evals(cwg_ctx* ctx);
+
+/* No reference counterpart (diagnostics): with CWG_REACT_TRACE set in the
+ * environment, every reaction launch stamps %globaltimer per block (slot 15:
+ * block start, slot 0: the block's reaction done; 16 slots per block, at most
+ * 4096 blocks, overwritten by the next launch). Copies the first n slots of
+ * the last launch's stamps. Returns CWG_EVALIDATION when tracing is off. */
+int cwg_react_trace(uint64_t* out, int n);
 
 /* No reference counterpart (measurement): FP64 peak of this device, a
  * DFMA-chain kernel at full occupancy, CUDA-event timed. Returns TFLOP/s

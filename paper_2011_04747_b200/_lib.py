@@ -83,6 +83,7 @@ _SIGS = {
     "cwg_launch_count": (C.c_int64, [C.c_void_p]),
     "cwg_bench_steps": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int, _dp, _dp, _dp]),
     "cwg_reaction_evals": (C.c_int64, [C.c_void_p]),
+    "cwg_react_trace": (C.c_int, [C.c_void_p, C.c_int]),
     "cwg_fp64_peak_tflops": (C.c_double, [C.c_int, C.c_double]),
     "cwg_diastolic_threshold": (C.c_int, [C.POINTER(cwg_problem), _dp, _lp, C.c_int64,
                                           C.POINTER(cwg_threshold_options), _dp, _lp, C.POINTER(cwg_error)]),

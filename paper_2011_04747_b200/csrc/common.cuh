@@ -86,6 +86,7 @@ struct ReactArgs {
   unsigned int* counter;  // work counter (self-resetting)
   unsigned int* done;     // finished-block counter (self-resetting)
   long long node_offset;  // local -> global node index
+  unsigned long long* trace;  // diagnostics (CWG_REACT_TRACE): per block 16 globaltimer slots, or nullptr
 };
 
 struct DiffArgs {

@@ -515,41 +515,59 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
   }
 }
 
+unsigned long long* g_react_trace = nullptr;  // diagnostics only (CWG_REACT_TRACE, cwg_react_trace)
+
+ReactArgs react_args(const cwg_ctx* c, const Bin& b, long long step_off, int ev, bool use_t, double t_fixed) {
+  ReactArgs a{};
+  a.v = c->d_v[c->cur];
+  a.S = c->d_S;
+  a.pitch = c->pitch;
+  a.last = c->d_last;
+  a.list = b.d_list;
+  a.first = b.first;
+  a.count = b.count;
+  a.stim = StimDev{c->d_stim_ptr, c->d_stim_ids, c->d_st0, c->d_sdur, c->d_samp, c->d_sper};
+  a.gkr = c->d_gkr;
+  a.dt = c->dt_eff;
+  a.t_fixed = t_fixed;
+  a.use_t_fixed = use_t ? 1 : 0;
+  a.clock = c->d_clock;
+  a.step_off = step_off;
+  a.scheme = c->scheme;
+  a.k0_up = c->k0_up;
+  a.k0_down = c->k0_down;
+  a.kmax = c->kmax_of_model[b.model];
+  a.khist = c->d_khist;
+  a.khist_len = c->khist_len;
+  a.err = c->d_err;
+  a.evs = c->evs;
+  a.ev = ev;
+  a.counter = b.d_counter;
+  a.done = b.d_counter + 1;
+  a.node_offset = c->node_offset;
+  return a;
+}
+
 void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double t_fixed) {
   for (auto& b : c->bins) {
     if (b.count == 0) continue;
-    ReactArgs a{};
-    a.v = c->d_v[c->cur];
-    a.S = c->d_S;
-    a.pitch = c->pitch;
-    a.last = c->d_last;
-    a.list = b.d_list;
-    a.first = b.first;
-    a.count = b.count;
-    a.stim = StimDev{c->d_stim_ptr, c->d_stim_ids, c->d_st0, c->d_sdur, c->d_samp, c->d_sper};
-    a.gkr = c->d_gkr;
-    a.dt = c->dt_eff;
-    a.t_fixed = t_fixed;
-    a.use_t_fixed = use_t ? 1 : 0;
-    a.clock = c->d_clock;
-    a.step_off = step_off;
-    a.scheme = c->scheme;
-    a.k0_up = c->k0_up;
-    a.k0_down = c->k0_down;
-    a.kmax = c->kmax_of_model[b.model];
-    a.khist = c->d_khist;
-    a.khist_len = c->khist_len;
-    a.err = c->d_err;
-    a.evs = c->evs;
-    a.ev = ev;
-    a.counter = b.d_counter;
-    a.done = b.d_counter + 1;
-    a.node_offset = c->node_offset;
+    ReactArgs a = react_args(c, b, step_off, ev, use_t, t_fixed);
+    if (getenv("CWG_REACT_TRACE") && b.grid <= 4096) {
+      if (!g_react_trace) CUDA_TRY(cudaMalloc(&g_react_trace, 16 * 4096 * sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemsetAsync(g_react_trace, 0, 16 * 4096 * sizeof(unsigned long long), c->stream));
+      a.trace = g_react_trace;
+    }
     cudaError_t e = is_ord(b.kind) ? launch_react_ord(b.kind, b.variant, a, b.grid, c->stream)
                                    : launch_react_exact(b.kind, a, b.grid, c->stream);
     CUDA_TRY(e);
     ++c->launches;
   }
+}
+
+// Reaction then the step's merged diffusion sub-steps (steps A and B/III).
+void enqueue_react_then_diffuse(cwg_ctx* c, long long step_off, int count, bool use_t, double t_fixed) {
+  enqueue_reaction(c, step_off, c->l, use_t, t_fixed);
+  enqueue_diffusion(c, count, step_off, c->l + 1);
 }
 
 // One outer step (StrangIntegrator::advance, splitting.cpp:171-181) at
@@ -559,8 +577,7 @@ void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double
 void enqueue_step(cwg_ctx* c, long long base, long long off, bool record, bool use_t, double t_fixed) {
   const long long step = base + off;
   if (step == 0) enqueue_diffusion(c, c->l, off, 0);  // step I
-  enqueue_reaction(c, off, c->l, use_t, t_fixed);     // step A
-  enqueue_diffusion(c, step == c->n_steps - 1 ? c->l : 2 * c->l, off, c->l + 1);  // step III / merged B
+  enqueue_react_then_diffuse(c, off, step == c->n_steps - 1 ? c->l : 2 * c->l, use_t, t_fixed);  // A, III / merged B
   if (!record) return;
   const long long S = step + 1;
   if (c->n_probes > 0 && S % c->spr == 0) {
@@ -630,7 +647,7 @@ void free_step_graph(StepGraph& sg) {
   sg = StepGraph{};
 }
 
-StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
+StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache, bool events = true) {
   const long long S = step + 1;
   const int flags = ((c->n_probes > 0 && S % c->spr == 0) ? 1 : 0) | (S % c->spm == 0 ? 2 : 0);
   StepGraph& sg = cache[flags | (c->cur << 2)];  // per recording pattern and starting V-buffer parity
@@ -642,9 +659,9 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
   for (int q = 0; q < 3; ++q) CUDA_TRY(cudaEventCreate(&tmp[q]));
   CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
-    CUDA_TRY(cudaEventRecordWithFlags(tmp[0], c->stream, cudaEventRecordExternal));
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(tmp[0], c->stream, cudaEventRecordExternal));
     enqueue_reaction(c, 0, c->l, false, 0.0);
-    CUDA_TRY(cudaEventRecordWithFlags(tmp[1], c->stream, cudaEventRecordExternal));
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(tmp[1], c->stream, cudaEventRecordExternal));
     const long long base = step;
     enqueue_diffusion(c, 2 * c->l, 0, c->l + 1);
     if (flags & 1) {
@@ -658,7 +675,7 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
       ++c->launches;
     }
     (void)base;
-    CUDA_TRY(cudaEventRecordWithFlags(tmp[2], c->stream, cudaEventRecordExternal));
+    if (events) CUDA_TRY(cudaEventRecordWithFlags(tmp[2], c->stream, cudaEventRecordExternal));
   } catch (...) {
     cudaStreamEndCapture(c->stream, &g);
     if (g) cudaGraphDestroy(g);
@@ -686,7 +703,7 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache) {
         ++found;
       }
   }
-  if (found != 3) throw Fail{CWG_ECUDA, "step graph: event nodes not found"};
+  if (events && found != 3) throw Fail{CWG_ECUDA, "step graph: event nodes not found"};
   CUDA_TRY(cudaGraphInstantiate(&sg.exec, g, 0));
   sg.cur_after = c->cur;
   c->cur = cur0;
@@ -1741,6 +1758,13 @@ int cwg_get_timing(cwg_ctx* c, double* r, double* d, double* rec) {
 
 int64_t cwg_launch_count(cwg_ctx* c) { return c->launches; }
 
+int cwg_react_trace(uint64_t* out, int n) {
+  if (!g_react_trace || n < 0 || n > 16 * 4096) return CWG_EVALIDATION;
+  if (cudaDeviceSynchronize() != cudaSuccess) return CWG_ECUDA;
+  return cudaMemcpy(out, g_react_trace, static_cast<size_t>(n) * sizeof(uint64_t), cudaMemcpyDeviceToHost) ==
+                 cudaSuccess ? CWG_OK : CWG_ECUDA;
+}
+
 int64_t cwg_reaction_evals(cwg_ctx* c) {
   std::vector<int64_t> h(static_cast<size_t>(c->khist_len));
   if (cwg_get_khist(c, h.data(), c->khist_len) != CWG_OK) return -1;
@@ -1773,6 +1797,16 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
                                      c->stream));
           set_clock(c, step);
           const bool middle = step >= 1 && step < c->n_steps - 1;
+          if (middle && split_phases == 2) {  // plain step graph, events recorded on the stream around it
+            StepGraph& sg = step_graph(c, step, graphs, false);
+            CUDA_TRY(cudaEventRecord(ev[3 * i], c->stream));
+            CUDA_TRY(cudaGraphLaunch(sg.exec, c->stream));
+            CUDA_TRY(cudaEventRecord(ev[3 * i + 1], c->stream));
+            CUDA_TRY(cudaEventRecord(ev[3 * i + 2], c->stream));
+            c->cur = sg.cur_after;
+            c->launches += sg.launches;
+            continue;
+          }
           if (middle && split_phases == 0) {
             StepGraph& sg = step_graph(c, step, graphs);
             for (int q = 0; q < 3; ++q)

@@ -39,16 +39,27 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
   double s[M::NS > 0 ? M::NS : 1];  // the lane's node states (registers)
 
+  // First round: position = global thread index (no atomic: ~1,200 warps
+  // claiming from one counter at once serialise in L2; ncu put 4% of the C2
+  // kernel's stall samples on that claim). Refills then take positions
+  // nthreads, nthreads + 1, ... from the counter.
+  const unsigned nthreads = gridDim.x * blockDim.x;
+  bool first = true;
   while (true) {
     const bool need = node < 0 && open;
     const unsigned m = __ballot_sync(kFull, need);
     if (m) {
       const int leader = __ffs(m) - 1;
       unsigned base = 0;
-      if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(m)));
-      base = __shfl_sync(kFull, base, leader);
+      if (first) {
+        base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+      } else {
+        if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(m))) + nthreads;
+        base = __shfl_sync(kFull, base, leader);
+      }
+      first = false;
       if (need) {
-        const long long pos = static_cast<long long>(base) + __popc(m & lt);
+        const long long pos = static_cast<long long>(base) + __popc(m & lt);  // first trip: m is full, so + lane
         if (pos < a.count) {
           node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
           v = a.v[node];
@@ -98,9 +109,16 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   }
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 template <class M>
 __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(ReactArgs a) {
   extern __shared__ __align__(16) unsigned shist[];
+  if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 16 + 15] = gtimer();  // block start
   {
     const long long seq = (*a.clock + a.step_off) * a.evs + a.ev;
     if (earlier_failure(a.err, seq)) return;  // uniform across the grid
@@ -112,13 +130,15 @@ __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(React
   __syncthreads();
   for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x)
     if (shist[i]) atomicAdd(a.khist + i, static_cast<unsigned long long>(shist[i]));
+  if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 16] = gtimer();  // block's reaction done
   if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned prev = atomicAdd(a.done, 1u);
+    // acq_rel: this block's claims happen before its arrival; the last block
+    // to arrive sees every block's claims before it resets the counters
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(a.done) : "memory");
     if (prev == gridDim.x - 1) {  // last block out resets the work counter for the next launch
       *a.counter = 0u;
       *a.done = 0u;
-      __threadfence();
     }
   }
 }
