@@ -103,3 +103,24 @@ def test_slab3d_tables_match_oracle_csr(ora):
     assert abs(mass.sum() - 0.14 * 0.1 * 0.08) < 1e-15
     rs = np.add.reduceat(val, rp[:-1])
     assert np.abs(rs).max() < 1e-18
+
+
+@pytest.mark.parametrize("which", ["c1", "c2"])
+def test_spectral_bound_of_gershgorin_step(which):
+    """The reference's spectral-bound oracle (tests/oracles/oracles.cpp:11-60, power iteration) restated
+    with a Lanczos eigensolver: lambda_max(M^-1 K) * dt_s <= 0.9 (Gershgorin discs, fem.cpp:178-192).
+    C1's 0.675 puts 3 dt_s past 2, the divergence the GPU test checks (test_gpu_properties.py)."""
+    import scipy.sparse as sp
+    import scipy.sparse.linalg as sla
+    if which == "c1":
+        sh = cw.Sheet(1.0, 1.0, 0.01, 0.0, d0_myocyte=0.001, rho=1.0)
+    else:
+        sh = cw.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0_myocyte=0.0012, rho=0.25)
+    op = sh.op
+    k = sp.csr_matrix((op.val, op.col, op.row_ptr), shape=(sh.n, sh.n))
+    mh = sp.diags(1.0 / np.sqrt(np.asarray(op.lumped_mass)))
+    a = mh @ k @ mh
+    lam = sla.eigsh((a + a.T) * 0.5, k=1, which="LA", return_eigenvectors=False)[0]
+    assert 0.0 < lam * op.dt_s <= 0.9 + 1e-12
+    if which == "c1":
+        assert abs(lam * op.dt_s - 0.675) < 1e-9 and 3.0 * op.dt_s * lam > 2.0
