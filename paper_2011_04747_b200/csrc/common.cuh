@@ -87,6 +87,7 @@ struct ReactArgs {
   unsigned int* done;     // finished-block counter (self-resetting)
   long long node_offset;  // local -> global node index
   unsigned long long* trace;  // diagnostics (CWG_REACT_TRACE): per block 16 globaltimer slots, or nullptr
+  int preclaim;         // claim a finishing lane's next node one trip ahead (react.cuh)
 };
 
 struct DiffArgs {

@@ -545,6 +545,11 @@ ReactArgs react_args(const cwg_ctx* c, const Bin& b, long long step_off, int ev,
   a.counter = b.d_counter;
   a.done = b.d_counter + 1;
   a.node_offset = c->node_offset;
+  static const int preclaim = [] {
+    const char* e = getenv("CWG_PRECLAIM");
+    return e ? atoi(e) : 1;
+  }();
+  a.preclaim = preclaim;
   return a;
 }
 

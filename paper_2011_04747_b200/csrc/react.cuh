@@ -25,6 +25,15 @@ namespace cwg {
 // 32 KB L1.5 instruction cache; warps that drift to different PCs thrash it
 // (ncu: ~35% of stall cycles were instruction fetch). In lockstep every
 // fetched line serves all warps.
+// Launch shapes opt in to the one-trip-ahead claim (M::kPreclaim): it helps
+// the latency regime (C2 reaction 53.2 -> 52.3 us) but adds spills to the
+// 168-register lockstep shape (C3 +1.1%, C4 -0.6%).
+template <class M>
+__host__ __device__ constexpr bool preclaim_of() {
+  if constexpr (requires { M::kPreclaim; }) return M::kPreclaim;
+  return false;
+}
+
 template <class M>
 __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
   const int lane = threadIdx.x & 31;
@@ -42,12 +51,19 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   // First round: position = global thread index (no atomic: ~1,200 warps
   // claiming from one counter at once serialise in L2; ncu put 4% of the C2
   // kernel's stall samples on that claim). Refills then take positions
-  // nthreads, nthreads + 1, ... from the counter.
+  // nthreads, nthreads + 1, ... from the counter, claimed one trip ahead:
+  // lanes that will finish their node in this trip (j + 1 == k) claim their
+  // next position before the evaluation, so the atomic's round trip hides
+  // behind it (shapes with M::kPreclaim; CWG_PRECLAIM=0 claims at refill
+  // time instead).
   const unsigned nthreads = gridDim.x * blockDim.x;
   bool first = true;
+  long long nxt = -1;  // pre-claimed next position, -1: none
   while (true) {
     const bool need = node < 0 && open;
-    const unsigned m = __ballot_sync(kFull, need);
+    const bool need_claim = need && nxt < 0;
+    const unsigned m = __ballot_sync(kFull, need_claim);
+    long long pos = nxt;
     if (m) {
       const int leader = __ffs(m) - 1;
       unsigned base = 0;
@@ -57,9 +73,12 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(m))) + nthreads;
         base = __shfl_sync(kFull, base, leader);
       }
-      first = false;
-      if (need) {
-        const long long pos = static_cast<long long>(base) + __popc(m & lt);  // first trip: m is full, so + lane
+      if (need_claim) pos = static_cast<long long>(base) + __popc(m & lt);  // first trip: m is full, so + lane
+    }
+    first = false;
+    if (need) {
+      nxt = -1;
+      {
         if (pos < a.count) {
           node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
           v = a.v[node];
@@ -79,6 +98,17 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         } else {
           open = false;
         }
+      }
+    }
+    if (preclaim_of<M>() && a.preclaim) {
+      const bool want = node >= 0 && j + 1 == k && open;
+      const unsigned m2 = __ballot_sync(kFull, want);
+      if (m2) {
+        const int leader = __ffs(m2) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(a.counter, static_cast<unsigned>(__popc(m2))) + nthreads;
+        base = __shfl_sync(kFull, base, leader);
+        if (want) nxt = static_cast<long long>(base) + __popc(m2 & lt);
       }
     }
     if (M::kBlockSync) {

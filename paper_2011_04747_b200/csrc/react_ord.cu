@@ -539,6 +539,7 @@ struct ModelOrd {
   static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 7 ? 288 : 128));
   static constexpr int kMinBlocks = V == 0 ? 2 : 1;
   static constexpr bool kBlockSync = V != 0;
+  static constexpr bool kPreclaim = V == 0;  // react.cuh: claim the next node one trip ahead
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
