@@ -341,10 +341,11 @@ def main():
                                                              "FP64 entry)",
                          "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL,
                          "note": ("latency regime: ~1 node per lane (8 warps/SM at >168 registers), each node's k "
-                                  "sub-steps sequential, so the step's largest k sets the critical path; see "
-                                  "DESIGN.md 3.1 / 5" if args.config in ("c1", "c2") else
-                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe ~51% of "
-                                  "active cycles (profiles/r01_react_c3_full.txt)")},
+                                  "sub-steps sequential, so the step's largest k sets the critical path; the "
+                                  "event-timed phase includes ~10 us of launch/completion latency around a ~42 us "
+                                  "kernel span (tools/react_trace.py, DESIGN.md 3.5)" if args.config in ("c1", "c2") else
+                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 56% of "
+                                  "active cycles on C4 (profiles/r01_react_c4_digest.txt)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
                                        ("diffuse_stencil2d_tbm (TMA)" if tma_path else "diffuse_stencil2d_tb")
@@ -353,7 +354,8 @@ def main():
                                    "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                    "peak_source": peak_src, "bytes_per_node_substep": diff_bytes,
                                    "launches_per_step": launches_per_step,
-                                   "note": "phase time includes probe/detector recording"},
+                                   "note": "phase time includes probe/detector recording and the ~6 us that any "
+                                           "kernel between two CUDA events costs here (DESIGN.md 3.5)"},
             "clocks": clocks.summary(), "gpu_launches": int(launches),
             "launch_mode": "one CUDA graph per step (event-record nodes at step start / after reaction / end)",
             "ord_min_blocks": int(os.environ.get("CWG_ORD_MINB", "2"))}
