@@ -302,11 +302,14 @@ def main():
     local_evals = reaction_evals / world
     react_tot_ms = float(react_ms.sum())
     achieved = ORD_FP64_FLOPS_PER_EVAL * local_evals / (react_tot_ms / 1e3) / 1e12
-    traffic = None
+    traffic, pipe_ncu = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            traffic = json.load(f).get("react_dram_bytes_per_launch")
-    except OSError:
+            summ = json.load(f)
+        traffic = summ.get("react_dram_bytes_per_launch")
+        pipe = summ.get("fp64_pipe_active_pct_of_active", {})
+        pipe_ncu = pipe.get("c2_latency_shape" if args.config in ("c1", "c2") else "c4_throughput_shape")
+    except (OSError, ValueError):
         pass
     diff_tot_ms = float(diff_ms.sum())
     is3d = args.config in ("c4", "c5")
@@ -340,6 +343,7 @@ def main():
                          "traffic": traffic, "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no "
                                                              "FP64 entry)",
                          "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL,
+                         "fp64_pipe_active_ncu": pipe_ncu / 100.0 if pipe_ncu is not None else None,
                          "note": ("latency regime: ~1 node per lane (8 warps/SM at >168 registers), each node's k "
                                   "sub-steps sequential, so the step's largest k sets the critical path; the "
                                   "event-timed phase includes ~10 us of launch/completion latency around a ~42 us "
