@@ -362,7 +362,9 @@ def main():
                                            "kernel between two CUDA events costs here (DESIGN.md 3.5)"},
             "clocks": clocks.summary(), "gpu_launches": int(launches),
             "launch_mode": "one CUDA graph per step (event-record nodes at step start / after reaction / end)",
-            "ord_min_blocks": int(os.environ.get("CWG_ORD_MINB", "2"))}
+            "ord_launch_shape": ("2 x 128-thread free-running blocks per SM, 254 registers (latency regime)"
+                                 if args.config in ("c1", "c2") else
+                                 "one 384-thread lockstep block per SM, 168 registers (throughput regime)")}
 
     # --- end to end through the public API (run_simulation) with pinned host state
     if big:
