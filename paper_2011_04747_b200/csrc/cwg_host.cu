@@ -730,21 +730,25 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
   const long long n_coef = c->n_coef;
   const long long g0 = (c->row_begin - c->hrows_c) * w;  // global index of local coefficient 0
   std::vector<double> coef(static_cast<size_t>(9 * n_coef), 0.0);
-  const long long offs[9] = {-w - 1, -w, -w + 1, -1, 0, 1, w - 1, w, w + 1};
   for (long long o = 0; o < n_coef; ++o) {
     const long long i = g0 + o;
     if (i < 0 || i >= p->n) continue;  // beyond the sheet: never read
     const long long y = i / w, x = i - y * w;
-    int slot = 0;
+    int prev = -1;
     for (long long p_ = p->row_ptr[i]; p_ < p->row_ptr[i + 1]; ++p_) {
-      const long long d = p->col[p_] - i;
-      while (slot < 9 && offs[slot] != d) ++slot;
-      if (slot == 9) throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " is not a 9-point grid row"};
-      const long long gy = y + (slot / 3) - 1, gx = x + (slot % 3) - 1;
-      if (gy < 0 || gy >= c->ny1 || gx < 0 || gx >= w)
+      // the slot from the column's grid coordinates, not from the index
+      // offset: for w = 2 the offsets -w+1 / -1 and 1 / w-1 coincide
+      const long long j = p->col[p_];
+      if (j < 0 || j >= p->n)
         throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " couples outside the grid"};
+      const long long dy = j / w - y, dx = j % w - x;
+      if (dy < -1 || dy > 1 || dx < -1 || dx > 1)
+        throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " is not a 9-point grid row"};
+      const int slot = static_cast<int>((dy + 1) * 3 + (dx + 1));
+      if (slot <= prev)
+        throw Fail{CWG_EVALIDATION, "stencil: row " + std::to_string(i) + " columns are not ascending"};
+      prev = slot;
       coef[static_cast<size_t>(slot) * n_coef + o] = p->val[p_];
-      ++slot;
     }
     // every in-grid neighbour must be present (absent ones would be read as 0)
     int expect = 0;

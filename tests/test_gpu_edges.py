@@ -1,0 +1,78 @@
+"""Edge cases of the hot path on the CUDA side, each against the CPU oracle.
+
+Degenerate and ragged geometries (a single element, one-element-wide strips,
+a 1-row-of-elements sheet), the shortest runs (one outer step: step I, A and
+III at once, splitting.cpp:171-181), runs without a stimulus or without
+probes, and a stimulus that is still on when the run ends. Aliev-Panfilov
+cases are bit-exact; ORd ones are held to the 1e-6 mV contract.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+V_TOL_MV = 1e-6
+
+
+@pytest.fixture(scope="module")
+def cw():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2011_04747_b200 as cw
+    return cw
+
+
+def _problem(cw, lx, ly, h, model="aliev-panfilov", t_end=5.0, dt=0.1, stim=True, probes=True, amp=100.0,
+             dur=1.0, ang=0.3, k0_down=3):
+    from paper_2011_04747_b200 import api, problems
+    sh = cw.Sheet(lx, ly, h, ang, d0_myocyte=0.0012, rho=0.25)
+    stims = [(sh.select("x_le", value=0.0), 0.0, dur, amp, None)] if stim else []
+    pr = [0, sh.n - 1] if probes else []
+    return problems.Problem("edge", sh, [model], np.zeros(sh.n, np.uint8), stims,
+                            api.SchemeConfig(dt_ms=dt, t_end_ms=t_end, k0_down=k0_down), pr)
+
+
+def _exact(res, o):
+    assert np.array_equal(res.final_state.v, o["v"])
+    assert np.array_equal(res.final_state.s.reshape(o["s"].shape), o["s"])
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    for q, tr in enumerate(res.traces):
+        assert np.array_equal(tr.v_mv, o["traces"][q])
+    assert np.array_equal(res.lat_map.valid, o["lat_valid"])
+    assert np.array_equal(res.lat_map.value[o["lat_valid"]], o["lat"][o["lat_valid"]])
+
+
+@pytest.mark.parametrize("lx,ly,h", [(0.02, 0.02, 0.02),    # one element, 4 nodes
+                                     (0.02, 0.5, 0.02),     # a strip one element wide in x
+                                     (0.5, 0.02, 0.02),     # one row of elements
+                                     (0.07, 0.13, 0.01)])   # ragged 8 x 14 nodes
+def test_degenerate_and_ragged_sheets_bitwise(cw, lx, ly, h):
+    p = _problem(cw, lx, ly, h, t_end=8.0)
+    _exact(gpu_run(p), oracle_run(p))
+
+
+@pytest.mark.parametrize("t_end", [0.1, 0.2])  # one step (I + A + III), two steps (I + A + B, then A + III)
+def test_shortest_runs_bitwise(cw, t_end):
+    p = _problem(cw, 0.3, 0.2, 0.01, t_end=t_end)
+    _exact(gpu_run(p), oracle_run(p))
+
+
+def test_no_stimulus_no_probes_bitwise(cw):
+    p = _problem(cw, 0.3, 0.2, 0.01, stim=False, probes=False, t_end=3.0)
+    res, o = gpu_run(p), oracle_run(p)
+    _exact(res, o)
+    assert not res.lat_map.valid.any()  # nothing activates
+
+
+def test_stimulus_on_at_the_end_ord(cw):
+    """ORd, the stimulus window still open when the run stops (t_end inside [t0, t0 + dur))."""
+    p = _problem(cw, 0.3, 0.3, 0.02, model="ohara2011-epi", t_end=1.5, dur=5.0, amp=80.0)
+    res, o = gpu_run(p), oracle_run(p)
+    assert np.max(np.abs(res.final_state.v - o["v"])) <= V_TOL_MV
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    for q, tr in enumerate(res.traces):
+        assert np.max(np.abs(tr.v_mv - o["traces"][q])) <= V_TOL_MV
