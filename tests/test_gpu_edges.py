@@ -76,3 +76,12 @@ def test_stimulus_on_at_the_end_ord(cw):
     assert np.array_equal(res.k_histogram, o["k_histogram"])
     for q, tr in enumerate(res.traces):
         assert np.max(np.abs(tr.v_mv - o["traces"][q])) <= V_TOL_MV
+
+
+@pytest.mark.parametrize("lx,ly,lz", [(0.02, 0.12, 0.02),   # one element in x and z
+                                      (0.3, 0.02, 0.04),    # one element in y (the slab axis)
+                                      (0.06, 0.1, 0.02)])   # one element layer in z (fibre angle +60 only)
+def test_degenerate_3d_slabs_bitwise(cw, lx, ly, lz):
+    from paper_2011_04747_b200 import problems
+    p = problems.slab(lx, ly, lz, 0.02, model="aliev-panfilov", t_end=6.0, amplitude=100.0)
+    _exact(gpu_run(p), oracle_run(p))
