@@ -150,16 +150,22 @@ def cpu_reference_steps(config, steps, warmup, budget_s, threads):
     """Time the reference's own StrangIntegrator::advance (oracle/_ref/libcwref.so) on host cores."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy
-    if config != "c2":
-        raise SystemExit("reference arm implemented for c2/c1")
-    p = refpy.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0=0.0012, rho=0.25)
     from paper_2011_04747_b200 import problems
-    nodes = p.select("disc", cx=0.0, cy=0.0, radius=problems.C2_RADIUS)
+    if config == "c2":
+        p = refpy.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0=0.0012, rho=0.25)
+        nodes = p.select("disc", cx=0.0, cy=0.0, radius=problems.C2_RADIUS)
+        amp, t_end = problems.C2_AMPLITUDE, 500.0
+    elif config == "c1":  # BASELINE configs[0]: 1 x 1 cm isotropic, left-edge line at 2x threshold, 400 ms
+        p = refpy.Sheet(1.0, 1.0, 0.01, 0.0, d0=0.001, rho=1.0)
+        nodes = p.select("x_le", value=0.0)
+        amp, t_end = problems.C1_AMPLITUDE, 400.0
+    else:
+        raise SystemExit("reference arm implemented for c1 and c2 (the reference cannot express c3-c5)")
     p.set_models(["ohara2011-epi"])
-    p.add_stimulus(nodes, 0.0, 1.0, problems.C2_AMPLITUDE)
+    p.add_stimulus(nodes, 0.0, 1.0, amp)
     p.init_state()
-    n_total = 5000
-    p.integrator(scheme="DAETI", dt=0.1, t_end=500.0, k0_up=5, k0_down=3, workers=threads)
+    n_total = int(round(t_end / 0.1))
+    p.integrator(scheme="DAETI", dt=0.1, t_end=t_end, k0_up=5, k0_down=3, workers=threads)
     for s in range(warmup):
         p.advance(s * 0.1, s, n_total)
     kh0 = p.integrator_khist().copy()
@@ -187,11 +193,12 @@ def run_reference_arm(args):
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["wall_s"] * 1e3 / max(r["steps"], 1),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2 (BASELINE configs[1]) through cardwave::StrangIntegrator::advance",
+            "config": {"workload": ("C2 (BASELINE configs[1])" if args.config == "c2" else "C1 (BASELINE configs[0])")
+                                   + " through cardwave::StrangIntegrator::advance",
                        "nodes": r["n"], "threads": threads},
             "sim_ms_per_s": r["sim_ms_per_s"],
             "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                             "sample": f"C2 outer steps {args.warmup}..{args.warmup + r['steps']} "
+                             "sample": f"{args.config.upper()} outer steps {args.warmup}..{args.warmup + r['steps']} "
                                        f"({r['steps']} x 0.1 ms) after {args.warmup} warm-up steps, "
                                        f"OpenMP {threads} threads, -O3 reference build"},
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -416,12 +423,12 @@ def main():
                        "create_s_all": creates}
 
     # --- CPU baseline: the reference itself on this host (rank 0, N = 1)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "c2":
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c2"):
         try:
             threads = len(os.sched_getaffinity(0))
-            r = cpu_reference_steps("c2", 100000, args.warmup, 15.0, threads)
+            r = cpu_reference_steps(args.config, 100000, args.warmup, 15.0, threads)
             line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                                    "sample": f"C2 outer steps {args.warmup}..{args.warmup + r['steps']} through "
+                                    "sample": f"{args.config.upper()} outer steps {args.warmup}..{args.warmup + r['steps']} through "
                                               f"cardwave::StrangIntegrator::advance (oracle/_ref), ~15 s budget",
                                     "sim_ms_per_s": r["sim_ms_per_s"]}
         except Exception as e:  # the checker library is a build artefact; report its absence
