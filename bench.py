@@ -324,13 +324,15 @@ def main():
     # once per node (16 B) plus the node's coefficients -- 80 B of per-node
     # arrays in 2D, 0 for the cached 3D structured tables; a launch fusing T
     # sub-steps counts once (fused-traffic bound).
-    fuse = 1 if is3d else int(os.environ.get("CWG_DIFF_TB", "4"))
-    fuse = max(1, min(4, fuse))  # (multi-rank 2D: halo depth min(4, rows per rank) >= 4 in every bench config)
-    launches_per_step = diffusion_launches(2 * info.l, fuse)
-    # large one-GPU 2D sheets run the TMA-fed persistent kernel (cwg_host.cu enqueue_diffusion)
+    # large one-GPU 2D sheets run the TMA-fed persistent kernel (cwg_host.cu enqueue_diffusion), which
+    # fuses up to 6 sub-steps per launch; the register-loading kernel up to 4
     sheet = getattr(prob, "sheet", None)
     tma_path = (not is3d and world == 1 and sheet is not None and os.environ.get("CWG_TB_TMA", "1") != "0"
                 and -(-sheet.nx1 // 64) * -(-sheet.ny1 // 16) >= 2 * 148)
+    cap = 6 if tma_path else 4
+    fuse = 1 if is3d else int(os.environ.get("CWG_DIFF_TB", str(cap)))
+    fuse = max(1, min(cap, fuse))  # (multi-rank 2D: halo depth min(4, rows per rank) >= 4 in every bench config)
+    launches_per_step = diffusion_launches(2 * info.l, fuse)
     coef_b = 0.0 if is3d else 80.0
     diff_bytes_step = info.n_local * launches_per_step * (16.0 + coef_b)
     diff_bytes = diff_bytes_step / (info.n_local * 2 * info.l)

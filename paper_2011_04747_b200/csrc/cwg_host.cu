@@ -224,7 +224,7 @@ struct cwg_ctx {
   // [10][rows][w_pad], planes 0..8 = coef, 9 = dt/m; tensor maps for T = 2..4
   double* d_coefp = nullptr;
   long long w_pad = 0;
-  CUtensorMap tmap[5];
+  CUtensorMap tmap[7];  // TMA diffusion: one map per fused depth T = 2..6
   bool tma_ok = false;
   double* d_mass = nullptr;  // lumped mass: owned rows (2D / CSR) or node classes (3D)
   long long n_mass = 0;
@@ -437,7 +437,7 @@ void setup_tma(cwg_ctx* c) {
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->w_pad) * 8, static_cast<cuuint64_t>(rows * c->w_pad) * 8};
   const cuuint32_t estr[3] = {1, 1, 1};
   bool ok = true;
-  for (int T = 2; T <= 4 && ok; ++T) {
+  for (int T = 2; T <= 6 && ok; ++T) {
     unsigned cx = 0, cy = 0;
     tbm_box(T, &cx, &cy, &margin);
     const cuuint32_t box[3] = {cx, cy, 10};
@@ -450,11 +450,19 @@ void setup_tma(cwg_ctx* c) {
   c->tma_ok = ok;
 }
 
-// sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides)
+// Large one-GPU sheets take the TMA-fed persistent kernel (enqueue_diffusion).
+bool tma_path(const cwg_ctx* c) {
+  return c->tma_ok && ((c->w + 63) / 64) * ((c->row_end - c->row_begin + 15) / 16) >= 2ll * c->num_sms;
+}
+
+// sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides): up to
+// 6 in the TMA kernel (its 64 x 16 tile plus a 6-deep halo still fits shared memory; fewer launches
+// re-read the coefficients fewer times), 4 in the register-loading kernel
 int diffusion_fuse(const cwg_ctx* c) {
   if (c->op_kind != CWG_OP_STENCIL2D) return 1;
-  int f = 4;
-  if (const char* e = getenv("CWG_DIFF_TB")) f = std::max(1, std::min(4, atoi(e)));
+  const int cap = tma_path(c) ? 6 : 4;
+  int f = cap;
+  if (const char* e = getenv("CWG_DIFF_TB")) f = std::max(1, std::min(cap, atoi(e)));
   return c->world > 1 ? std::min(f, c->hrows_c) : f;  // T fused sub-steps need T halo rows (V and coefficients)
 }
 
@@ -495,8 +503,7 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     if (c->op_kind == CWG_OP_STENCIL2D) {
       Stencil2D s{c->d_coef, c->n_coef, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1,
                   c->hrows_v, c->hrows_c};
-      const bool big = ((c->w + 63) / 64) * ((s.rows + 15) / 16) >= 2ll * c->num_sms;
-      if (T > 1 && c->tma_ok && big)
+      if (T > 1 && tma_path(c))
         CUDA_TRY(launch_diffuse_stencil2d_tbm(T, a, s, c->tmap[T], c->num_sms, c->stream));
       else if (T > 1)
         CUDA_TRY(launch_diffuse_stencil2d_tb(T, a, s, c->num_sms, c->stream));

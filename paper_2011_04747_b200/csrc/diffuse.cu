@@ -263,7 +263,7 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 // (a zeroed left margin), and a box must start at a 16-byte aligned,
 // non-negative inner coordinate: boxes start SX = 2*ceil((T-1)/2) columns
 // left of the tile (even), BXW columns wide (even, covers the CX needed).
-constexpr int kTmaMargin = 4;
+constexpr int kTmaMargin = 6;  // >= SX for T <= 6
 template <int T, int TBX, int TBY, int NT>
 struct TbmGeom {
   static constexpr int VX = TBX + 2 * T, VY = TBY + 2 * T, VXY = VX * VY;
@@ -469,7 +469,9 @@ void tbm_box(int T, unsigned* cx, unsigned* cy, int* margin) {
   switch (T) {
     case 2: *cx = TbmGeom<2, 64, 16, 512>::BXW, *cy = TbmGeom<2, 64, 16, 512>::CY; break;
     case 3: *cx = TbmGeom<3, 64, 16, 512>::BXW, *cy = TbmGeom<3, 64, 16, 512>::CY; break;
-    default: *cx = TbmGeom<4, 64, 16, 512>::BXW, *cy = TbmGeom<4, 64, 16, 512>::CY; break;
+    case 4: *cx = TbmGeom<4, 64, 16, 512>::BXW, *cy = TbmGeom<4, 64, 16, 512>::CY; break;
+    case 5: *cx = TbmGeom<5, 64, 16, 512>::BXW, *cy = TbmGeom<5, 64, 16, 512>::CY; break;
+    default: *cx = TbmGeom<6, 64, 16, 512>::BXW, *cy = TbmGeom<6, 64, 16, 512>::CY; break;
   }
 }
 
@@ -479,6 +481,8 @@ cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil
     case 2: return launch_tbm_t<2>(a, s, tm, num_sms, st);
     case 3: return launch_tbm_t<3>(a, s, tm, num_sms, st);
     case 4: return launch_tbm_t<4>(a, s, tm, num_sms, st);
+    case 5: return launch_tbm_t<5>(a, s, tm, num_sms, st);
+    case 6: return launch_tbm_t<6>(a, s, tm, num_sms, st);
     default: return cudaErrorInvalidValue;
   }
 }
