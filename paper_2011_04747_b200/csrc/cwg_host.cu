@@ -386,18 +386,41 @@ struct DevScope {
 // Exchange `rows` halo rows (planes) with both neighbours: my first / last
 // `rows` owned rows go down / up, theirs land in the halo rows adjacent to my
 // slab. Local V layout: [hrows_v halo | owned | hrows_v halo] rows of w nodes.
+// The halo exchange of `rows` rows (2D) or planes (3D) of a V buffer: what
+// this rank sends to / receives from each neighbour. Shared by the NCCL
+// transport (halo_exchange) and the one-GPU loopback (cwg_loopback_steps), so
+// the loopback tests exercise the same buffer arithmetic.
+struct HaloPlan {
+  size_t n = 0;                                          // doubles per direction
+  bool lo = false, hi = false;                           // neighbours rank - 1 / rank + 1 exist
+  double *send_lo = nullptr, *recv_lo = nullptr;         // first owned rows / the halo below
+  double *send_hi = nullptr, *recv_hi = nullptr;         // last owned rows / the halo above
+};
+
+HaloPlan halo_plan(const cwg_ctx* c, double* buf, int rows) {
+  HaloPlan h;
+  h.n = static_cast<size_t>(c->w) * static_cast<size_t>(rows);
+  const size_t own0 = static_cast<size_t>(c->halo), own1 = own0 + static_cast<size_t>(c->n_own);
+  h.lo = c->rank > 0;
+  h.hi = c->rank + 1 < c->world;
+  h.send_lo = buf + own0;
+  h.recv_lo = buf + own0 - h.n;
+  h.send_hi = buf + own1 - h.n;
+  h.recv_hi = buf + own1;
+  return h;
+}
+
 void halo_exchange(cwg_ctx* c, double* buf, int rows) {
   if (c->world <= 1 || c->loopback) return;
-  const size_t n = static_cast<size_t>(c->w) * static_cast<size_t>(rows);
-  const size_t own0 = static_cast<size_t>(c->halo), own1 = own0 + static_cast<size_t>(c->n_own);
+  const HaloPlan h = halo_plan(c, buf, rows);
   NCCL_TRY(g_nccl.gstart());
-  if (c->rank > 0) {
-    NCCL_TRY(g_nccl.send(buf + own0, n, ncclDouble, c->rank - 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(buf + own0 - n, n, ncclDouble, c->rank - 1, c->comm, c->stream));
+  if (h.lo) {
+    NCCL_TRY(g_nccl.send(h.send_lo, h.n, ncclDouble, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(h.recv_lo, h.n, ncclDouble, c->rank - 1, c->comm, c->stream));
   }
-  if (c->rank + 1 < c->world) {
-    NCCL_TRY(g_nccl.send(buf + own1 - n, n, ncclDouble, c->rank + 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(buf + own1, n, ncclDouble, c->rank + 1, c->comm, c->stream));
+  if (h.hi) {
+    NCCL_TRY(g_nccl.send(h.send_hi, h.n, ncclDouble, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.recv(h.recv_hi, h.n, ncclDouble, c->rank + 1, c->comm, c->stream));
   }
   NCCL_TRY(g_nccl.gend());
 }
@@ -1444,22 +1467,20 @@ int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t 
       CUDA_TRY(cudaStreamSynchronize(ranks[r]->stream));
       ranks[r]->stream = shared;  // one stream: every rank's work is ordered as enqueued below
     }
-    // the halo exchange of halo_exchange(), as device copies between the ranks' current V buffers
+    // halo_exchange()'s plan with the NCCL send/recv pairs as device copies between the ranks' current
+    // V buffers: rank r's halo below <- rank r-1's last rows, its halo above <- rank r+1's first rows
     auto exchange = [&](int rows) {
       for (int r = 0; r < world; ++r) {
-        cwg_ctx* c = ranks[r];
-        double* buf = c->d_v[c->cur];
-        const size_t n = static_cast<size_t>(c->w) * static_cast<size_t>(rows);
-        const size_t own0 = static_cast<size_t>(c->halo), own1 = own0 + static_cast<size_t>(c->n_own);
-        if (r > 0) {
-          cwg_ctx* b = ranks[r - 1];
-          CUDA_TRY(cudaMemcpyAsync(buf + own0 - n, b->d_v[b->cur] + b->halo + b->n_own - n, n * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, shared));
+        const HaloPlan h = halo_plan(ranks[r], ranks[r]->d_v[ranks[r]->cur], rows);
+        if (h.lo) {
+          const HaloPlan b = halo_plan(ranks[r - 1], ranks[r - 1]->d_v[ranks[r - 1]->cur], rows);
+          validation(b.n == h.n && b.hi, "loopback: halo plans of ranks r-1 and r disagree");
+          CUDA_TRY(cudaMemcpyAsync(h.recv_lo, b.send_hi, h.n * sizeof(double), cudaMemcpyDeviceToDevice, shared));
         }
-        if (r + 1 < world) {
-          cwg_ctx* t = ranks[r + 1];
-          CUDA_TRY(cudaMemcpyAsync(buf + own1, t->d_v[t->cur] + t->halo, n * sizeof(double),
-                                   cudaMemcpyDeviceToDevice, shared));
+        if (h.hi) {
+          const HaloPlan t = halo_plan(ranks[r + 1], ranks[r + 1]->d_v[ranks[r + 1]->cur], rows);
+          validation(t.n == h.n && t.lo, "loopback: halo plans of ranks r and r+1 disagree");
+          CUDA_TRY(cudaMemcpyAsync(h.recv_hi, t.send_lo, h.n * sizeof(double), cudaMemcpyDeviceToDevice, shared));
         }
       }
     };
