@@ -85,3 +85,36 @@ def test_degenerate_3d_slabs_bitwise(cw, lx, ly, lz):
     from paper_2011_04747_b200 import problems
     p = problems.slab(lx, ly, lz, 0.02, model="aliev-panfilov", t_end=6.0, amplitude=100.0)
     _exact(gpu_run(p), oracle_run(p))
+
+
+@pytest.mark.parametrize("model", ["ohara2011-endo", "ohara2011-mid", "maccannell2007"])
+def test_other_cell_models_full_runs(cw, model):
+    """Whole DAETI runs of the other registered models (ohara_rudy_2011.cpp:86-87 cell types,
+    maccannell_2007.cpp) on the C1 sheet -- the tolerance contract, identical k-histograms."""
+    from paper_2011_04747_b200 import problems
+    p = problems.c1(model=model, t_end=12.0, amplitude=600.0 if model != "maccannell2007" else 100.0)
+    res, o = gpu_run(p), oracle_run(p)
+    assert np.max(np.abs(res.final_state.v - o["v"])) <= V_TOL_MV
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+    for q, tr in enumerate(res.traces):
+        assert np.max(np.abs(tr.v_mv - o["traces"][q])) <= V_TOL_MV
+
+
+@pytest.mark.parametrize("scheme,dt,strict", [("OSTAR", 0.1, False), ("DAETI", 0.1, True), ("OST", 0.02, False)])
+def test_ord_schemes_and_strict_substeps(cw, scheme, dt, strict):
+    """ORd under the other schemes and the strict (ceil) diffusion sub-step rule (splitting.cpp:56-67)."""
+    from paper_2011_04747_b200 import api, problems
+    p = problems.c1(t_end=8.0, scheme=api.Scheme[scheme], dt=dt)
+    p.cfg.strict_substeps = strict
+    res, o = gpu_run(p), oracle_run(p)
+    assert np.max(np.abs(res.final_state.v - o["v"])) <= V_TOL_MV
+    assert np.array_equal(res.k_histogram, o["k_histogram"])
+
+
+def test_record_interval_not_a_multiple_of_dt(cw):
+    """Traces every llround(rec / dt) steps (splitting.cpp:274-279) with rec = 0.35 ms at dt = 0.1 (AP, bit-exact)."""
+    p = _problem(cw, 0.3, 0.2, 0.01, t_end=6.0)
+    p.cfg.record_interval_ms = 0.35
+    res, o = gpu_run(p), oracle_run(p)
+    _exact(res, o)
+    assert len(res.traces[0].v_mv) == len(o["traces"][0])

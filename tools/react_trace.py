@@ -1,4 +1,4 @@
-"""Diagnostic: where one C2 step's device time goes (CWG_REACT_TRACE=1 python tools/react_trace.py [step]).
+"""Diagnostic: where one step's device time goes (CWG_REACT_TRACE=1 python tools/react_trace.py [cN] [step ...]).
 
 Runs the C2 problem to `step`, then times that step the way bench.py does
 (256 MiB L2 flush, then the step graph between CUDA events) while the
@@ -18,12 +18,14 @@ from paper_2011_04747_b200 import _lib as L, problems  # noqa: E402
 
 assert os.environ.get("CWG_REACT_TRACE"), "set CWG_REACT_TRACE=1"
 lib = L.lib()
-p = problems.c2()
+args = sys.argv[1:]
+cfg = args.pop(0) if args and args[0].startswith("c") else "c2"
+p = getattr(problems, cfg)()
 integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=p.model_of_node)
 integ.upload(p.initial_state())
 integ.run_begin()
 pos = 0
-for step in sorted(int(a) for a in sys.argv[1:]) or [2000, 4000]:
+for step in sorted(int(a) for a in args) or [2000, 4000]:
     integ.run_steps(pos, step - pos)  # bring the wave to this step
     integ.run_sync()
     pos = step + 1
@@ -36,7 +38,7 @@ for step in sorted(int(a) for a in sys.argv[1:]) or [2000, 4000]:
     t = t[t[:, 15] > 0]
     t0 = t[:, 15].min()
     done = (t[:, 0] - t0) / 1e3
-    print(f"step {step}: reaction phase {re[0] * 1e3:.1f} us event-timed; kernel span {done.max():.1f} us "
+    print(f"{cfg} step {step}: reaction phase {re[0] * 1e3:.1f} us event-timed; kernel span {done.max():.1f} us "
           f"({len(t)} blocks start within {(t[:, 15].max() - t0) / 1e3:.2f} us; block done: min {done.min():.1f}, "
           f"median {np.median(done):.1f}, max {done.max():.1f} us); diffusion + recording {di[0] * 1e3:.1f} us")
 integ.close()
