@@ -1832,7 +1832,11 @@ int cwg_bench_steps(cwg_ctx* c, int64_t first, int64_t count, int64_t flush_byte
           if (flush_bytes > 0)
             CUDA_TRY(cudaMemsetAsync(c->d_flush, static_cast<int>(step & 0xff), static_cast<size_t>(flush_bytes),
                                      c->stream));
-          set_clock(c, step);
+          {
+            const long long l0 = c->launches;  // the clock write sits outside the timed events: not counted
+            set_clock(c, step);
+            c->launches = l0;
+          }
           const bool middle = step >= 1 && step < c->n_steps - 1;
           if (middle && split_phases == 2) {  // plain step graph, events recorded on the stream around it
             StepGraph& sg = step_graph(c, step, graphs, false);
