@@ -41,4 +41,8 @@ for step in sorted(int(a) for a in args) or [2000, 4000]:
     print(f"{cfg} step {step}: reaction phase {re[0] * 1e3:.1f} us event-timed; kernel span {done.max():.1f} us "
           f"({len(t)} blocks start within {(t[:, 15].max() - t0) / 1e3:.2f} us; block done: min {done.min():.1f}, "
           f"median {np.median(done):.1f}, max {done.max():.1f} us); diffusion + recording {di[0] * 1e3:.1f} us")
+    late = np.sort(done[done > np.median(done) + 3.0])
+    if len(late):
+        print(f"  {len(late)} blocks finish > 3 us after the median (a second lane round): "
+              f"done at {', '.join(f'{x:.1f}' for x in np.percentile(late, [0, 25, 50, 75, 100]))} us (0/25/50/75/100%)")
 integ.close()
