@@ -1,19 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the DAETI hot path on B200 (one JSON line on rank 0).
 
-Workload (N = 1): BASELINE.json configs[1] ("C2"): 5x5 cm anisotropic sheet,
-201x201 nodes, fibres 45 deg, D_l 0.0012 / D_t 0.0003, ORd-epi from rest,
-corner-disc stimulus (r 0.15 cm, 100 mV/ms, 1 ms), DAETI dt 0.1 ms
-(k0_up 5, k0_down 3), fp64. A "step" is one outer Strang step (the
-adaptive reaction pass + 2l diffusion sub-steps + the record cadence).
-The default run is the whole 500 ms simulation: W warm-up steps, then
-K = 5000 - W timed steps. N > 1 (torchrun): weak scaling, rank r owns a
-201-row y-slab of a 5 x 5N cm sheet, halo exchange per diffusion sub-step.
+Workload (default, N = 1): BASELINE.json configs[3] ("C4"), the largest
+configuration that fits one GPU: 3D ventricular slab 5 x 5 x 1 cm, h = 0.02
+cm (251 x 251 x 51 = 3,213,051 nodes), fibres rotating +60 -> -60 deg from
+endocardium to epicardium, D_l 0.0012 / D_t 0.0003 cm^2/ms, ORd-epi from
+rest, endocardial-face stimulus (z = 0, 150 mV/ms for 1 ms), DAETI dt 0.1 ms
+(k0_up 5, k0_down 3; the paper's k0_down = 1 aborts in the reference for
+ORd), fp64. A "step" is one outer Strang step (the adaptive
+reaction pass + 2l diffusion sub-steps + the record cadence). Default run:
+the whole 500 ms simulation (W warm-up steps, then K = 5000 - W timed).
+N > 1 (torchrun): strong scaling of the same C4 grid -- rank r owns a
+contiguous y-slab, halo exchange of the fused diffusion launches over NCCL
+(--scaling weak stacks one C4 per rank instead). --config c1/c2/c3/c5 pick
+the other BASELINE configurations.
 
 metric: node-updates/s = (reaction rates evaluations + diffusion node
 sub-steps) per second, whole job. Timing: CUDA events per step on the
 solver's stream, with a 256 MiB L2-evicting write before every timed step
 (untimed); max over ranks.
+
+--impl reference: the reference's own CPU path on this host's physical
+cores (OMP_PROC_BIND=close). C1/C2: the UNMODIFIED reference library
+(oracle/_ref/libcwref.so, cardwave::StrangIntegrator::advance). C3-C5 are not
+expressible in the reference (3D, scar, jitter -- SURVEY.md s0), so they run
+the C restatement oracle (oracle/cw_oracle.c, pinned bit-exact to the
+reference on C1/C2), kind "port". This arm never imports the product package.
 """
 from __future__ import annotations
 
@@ -42,6 +54,48 @@ FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # Updated when the kernel changes.
 ORD_FP64_FLOPS_PER_EVAL = 2850.6
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
+
+
+# Problem constants of the reference arm, restated so that arm never imports
+# the product package (tests/test_bench_host.py checks them against problems.py).
+C1_AMPLITUDE = 592.0   # 2 x the reference's diastolic threshold on the C1 line (296 mV/ms)
+C2_AMPLITUDE = 100.0
+C2_RADIUS = 0.15
+SLAB_AMPLITUDE = 150.0  # C4/C5 endocardial stimulus, 1 ms
+
+
+def host_cpu():
+    """(physical cores available to this process, logical CPUs, CPU model) from /proc/cpuinfo."""
+    allowed = os.sched_getaffinity(0)
+    cores, model, cpu, phys, core = set(), "unknown", None, None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f.read().splitlines() + [""]:
+                if not line.strip():
+                    if cpu is not None and cpu in allowed:
+                        cores.add((phys, core if core is not None else cpu))
+                    cpu, phys, core = None, None, None
+                    continue
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "processor":
+                    cpu = int(v)
+                elif k == "physical id":
+                    phys = v
+                elif k == "core id":
+                    core = v
+                elif k == "model name":
+                    model = v
+    except OSError:
+        pass
+    return max(1, len(cores) or len(allowed)), len(allowed), model
+
+
+def pin_openmp(threads):
+    """OpenMP placement for the CPU legs; must run before the oracle/reference library is loaded."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    os.environ["OMP_PROC_BIND"] = "close"
+    os.environ["OMP_PLACES"] = "cores"
 
 
 def diffusion_launches(count, fuse):
@@ -103,8 +157,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def build_problem(config, world, rank):
+def build_problem(config, world, rank, scaling="strong"):
     from paper_2011_04747_b200 import problems
+    if config == "c4" and (world == 1 or scaling == "strong"):
+        return problems.c4()  # N > 1: every rank gets the full grid and keeps its own y-slab (cwg_slab_plan)
     if config == "c2":
         if world == 1:
             return problems.c2()
@@ -135,32 +191,81 @@ def config_block(config, prob, world, l):
                    "corner stimulus, ORd-epi, DAETI dt 0.1 ms, 500 ms",
              "c1": "BASELINE configs[0]: 2D isotropic 1x1 cm, 101x101 nodes, ORd-epi, left-edge 2x threshold",
              "c3": "BASELINE configs[2] (extension): 1001x1001 scar/border-zone sheet",
-             "c4": "BASELINE configs[3] (extension): 3D slab 5x5x1 cm, 251x251x51 nodes per GPU, fibres +60..-60 deg, "
-                   "endocardial face stimulus, ORd-epi",
+             "c4": "BASELINE configs[3] (extension): 3D slab 5x5x1 cm, 251x251x51 nodes (3,213,051), fibres +60..-60 "
+                   "deg, endocardial face stimulus, ORd-epi, DAETI dt 0.1 ms, 500 ms",
              "c5": "BASELINE configs[4] (extension): 3D slab 10x10x2 cm, 1001x1001x201 nodes per GPU, 16 random "
                    "endocardial sites, ORd-epi"}
     return {"workload": names[config], "nodes": int(prob.n), "nodes_per_gpu": int(prob.n // max(world, 1)),
             "cell_model": prob.models[0], "scheme": "DAETI", "dt_ms": prob.cfg.dt_ms, "k0_up": prob.cfg.k0_up,
             "k0_down": prob.cfg.k0_down, "diffusion_substeps_per_step": 2 * l,
             "l2": "flushed (256 MiB write) before every timed step",
-            "parallelism": f"y-slab x{world}" if world > 1 else "single GPU"}
+            "parallelism": f"y-slab x{world}" if world > 1 else "single GPU",
+            "data": "synthetic tissue (no dataset exists); random-free except the seeded std::mt19937_64 draws of C3/C5"}
+
+
+def oracle_slab(config):
+    """C4 / C5 for the CPU legs on the oracle alone (no product import): the structured slab operator
+    (orapy.Slab3DOp, the oracle's own assembly), face / seeded-site endocardial stimulus, ORd-epi."""
+    import orapy
+    if config == "c4":
+        op = orapy.Slab3DOp(250, 250, 50, 0.02)
+        iy, ix = np.meshgrid(np.arange(op.ny1), np.arange(op.nx1), indexing="ij")
+        nodes = np.sort(op.index(ix, iy, 0).ravel())
+        t_end = 500.0
+    else:
+        # c5: a y-sub-slab of the 1001 x 1001 x 201 grid (y <= 0.2 cm, 1001 x 21 x 201 = 4.2M nodes: the
+        # full slab's state alone is ~70 GB of host memory) with the full slab's 16 seeded sites
+        # (problems.site_centers: std::mt19937_64(2011)); node-updates/s is a per-node rate
+        op = orapy.Slab3DOp(1000, 20, 200, 0.01)
+        u = orapy.uniform_mt64(2011, 32, 0.0, 1.0)
+        iy, ix = np.meshgrid(np.arange(op.ny1), np.arange(op.nx1), indexing="ij")
+        x, y = ix * op.h, iy * op.h
+        sel = np.zeros(ix.shape, bool)
+        for k in range(16):
+            sel |= np.sqrt((x - 10.0 * u[2 * k]) ** 2 + (y - 10.0 * u[2 * k + 1]) ** 2) <= 0.1 + 1e-9
+        nodes = np.sort(op.index(ix[sel], iy[sel], 0))
+        t_end = 5.0
+    return op, nodes, t_end
 
 
 def cpu_reference_steps(config, steps, warmup, budget_s, threads):
-    """Time the reference's own StrangIntegrator::advance (oracle/_ref/libcwref.so) on host cores."""
+    """Time the reference's own StrangIntegrator::advance (oracle/_ref/libcwref.so) on host cores -- or,
+    for the configurations the reference cannot express (C4, C5), the oracle's restatement of it."""
+    pin_openmp(threads)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    if config in ("c4", "c5"):
+        import orapy
+        op, nodes, t_end = oracle_slab(config)
+        it = orapy.Integrator(op, op.dt_s, ["ohara2011-epi"], np.zeros(op.n, np.uint8),
+                              [(nodes, 0.0, 1.0, SLAB_AMPLITUDE, None)], scheme="DAETI", dt=0.1, k0_up=5, k0_down=3)
+        n_total = int(round(t_end / 0.1))
+        for st in range(warmup):
+            it.advance(st * 0.1, st, n_total)
+        kh0 = it.khist.copy()
+        t0 = time.perf_counter()
+        done = 0
+        for st in range(warmup, min(warmup + steps, n_total)):
+            it.advance(st * 0.1, st, n_total)
+            done += 1
+            if time.perf_counter() - t0 > budget_s:
+                break
+        wall = time.perf_counter() - t0
+        evals = int(np.sum((it.khist - kh0) * np.arange(len(it.khist))))
+        diff = done * it.n * 2 * it.l
+        return {"steps": done, "wall_s": wall, "evals": evals, "diff": diff, "n": it.n, "l": it.l,
+                "value": (evals + diff) / wall, "sim_ms_per_s": done * 0.1 / wall, "kind": "port",
+                "what": "oracle restatement of StrangIntegrator::advance (oracle/cw_oracle.c, OpenMP)"}
     import refpy
-    from paper_2011_04747_b200 import problems
     if config == "c2":
         p = refpy.Sheet(5.0, 5.0, 0.025, math.pi / 4, d0=0.0012, rho=0.25)
-        nodes = p.select("disc", cx=0.0, cy=0.0, radius=problems.C2_RADIUS)
-        amp, t_end = problems.C2_AMPLITUDE, 500.0
+        nodes = p.select("disc", cx=0.0, cy=0.0, radius=C2_RADIUS)
+        amp, t_end = C2_AMPLITUDE, 500.0
     elif config == "c1":  # BASELINE configs[0]: 1 x 1 cm isotropic, left-edge line at 2x threshold, 400 ms
         p = refpy.Sheet(1.0, 1.0, 0.01, 0.0, d0=0.001, rho=1.0)
         nodes = p.select("x_le", value=0.0)
-        amp, t_end = problems.C1_AMPLITUDE, 400.0
+        amp, t_end = C1_AMPLITUDE, 400.0
     else:
-        raise SystemExit("reference arm implemented for c1 and c2 (the reference cannot express c3-c5)")
+        raise SystemExit("reference arm implemented for c1, c2, c4 and c5")
     p.set_models(["ohara2011-epi"])
     p.add_stimulus(nodes, 0.0, 1.0, amp)
     p.init_state()
@@ -181,26 +286,34 @@ def cpu_reference_steps(config, steps, warmup, budget_s, threads):
     evals = int(np.sum((kh1 - kh0) * np.arange(len(kh1))))
     diff = done * p.n * 2 * p.l
     return {"steps": done, "wall_s": wall, "evals": evals, "diff": diff, "n": p.n, "l": p.l,
-            "value": (evals + diff) / wall, "sim_ms_per_s": done * 0.1 / wall}
+            "value": (evals + diff) / wall, "sim_ms_per_s": done * 0.1 / wall, "kind": "reference",
+            "what": "cardwave::StrangIntegrator::advance (oracle/_ref/libcwref.so, unmodified reference)"}
+
+
+WORKLOAD = {"c1": "C1 (BASELINE configs[0])", "c2": "C2 (BASELINE configs[1])",
+            "c4": "C4 (BASELINE configs[3], 251x251x51 slab)", "c5": "C5 (BASELINE configs[4], 1001x1001x201 slab)"}
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    threads = len(os.sched_getaffinity(0))
+    threads, logical, model = host_cpu()
     r = cpu_reference_steps(args.config, args.steps, args.warmup, args.ref_budget, threads)
     line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
             "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["wall_s"] * 1e3 / max(r["steps"], 1),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": ("C2 (BASELINE configs[1])" if args.config == "c2" else "C1 (BASELINE configs[0])")
-                                   + " through cardwave::StrangIntegrator::advance",
-                       "nodes": r["n"], "threads": threads},
+            "higher_is_better": True, "scaling": "strong" if args.config == "c4" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD[args.config] + " through " + r["what"],
+                       "nodes": r["n"], "threads": threads, "cpu_model": model, "logical_cpus": logical,
+                       "omp": "OMP_PROC_BIND=close OMP_PLACES=cores"},
             "sim_ms_per_s": r["sim_ms_per_s"],
-            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads, "kind": r["kind"],
+                             "cpu_model": model,
                              "sample": f"{args.config.upper()} outer steps {args.warmup}..{args.warmup + r['steps']} "
                                        f"({r['steps']} x 0.1 ms) after {args.warmup} warm-up steps, "
-                                       f"OpenMP {threads} threads, -O3 reference build"},
+                                       f"OpenMP {threads} threads on physical cores ({logical} logical CPUs), "
+                                       f"{r['what']}"},
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -212,7 +325,9 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c2", "c1", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1 with --config c4: split one C4 grid (strong) or one C4 per rank (weak)")
     ap.add_argument("--ref-budget", type=float, default=20.0, help="seconds of reference CPU work per arm")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -253,7 +368,7 @@ def main():
         dist.init_process_group("gloo", init_method="env://")
         nccl_id = new_nccl_id()
 
-    prob = build_problem(args.config, world, rank)
+    prob = build_problem(args.config, world, rank, args.scaling)
     setup = prob.setup()
     n_total = int(math.ceil(prob.cfg.t_end_ms / prob.cfg.dt_ms - 1e-9))
     if args.steps is None:
@@ -339,7 +454,8 @@ def main():
     diff_gbs = diff_bytes_step * K / (diff_tot_ms / 1e3) / 1e9
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-            "ms_per_step": t_dev_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": t_dev_ms / K, "higher_is_better": True,
+            "scaling": "strong" if (args.config == "c4" and args.scaling == "strong") else "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": config_block(args.config, prob, world, info.l),
             "sim_ms_per_s": K * prob.cfg.dt_ms / (t_dev_ms / 1e3),
             "reaction_node_updates_per_s": reaction_evals / (t_dev_ms / 1e3),
@@ -425,13 +541,16 @@ def main():
                        "create_s_all": creates}
 
     # --- CPU baseline: the reference itself on this host (rank 0, N = 1)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c2"):
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in ("c1", "c2", "c4", "c5"):
+        threads, logical, model = host_cpu()
         try:
-            threads = len(os.sched_getaffinity(0))
             r = cpu_reference_steps(args.config, 100000, args.warmup, 15.0, threads)
-            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
-                                    "sample": f"{args.config.upper()} outer steps {args.warmup}..{args.warmup + r['steps']} through "
-                                              f"cardwave::StrangIntegrator::advance (oracle/_ref), ~15 s budget",
+            line["cpu_baseline"] = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": r["kind"],
+                                    "cpu_model": model,
+                                    "sample": f"{args.config.upper()} outer steps {args.warmup}.."
+                                              f"{args.warmup + r['steps']} ({r['n']} nodes) through {r['what']}, "
+                                              f"~15 s budget, OpenMP {threads} threads on physical cores "
+                                              f"({logical} logical CPUs, OMP_PROC_BIND=close)",
                                     "sim_ms_per_s": r["sim_ms_per_s"]}
         except Exception as e:  # the checker library is a build artefact; report its absence
             line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",

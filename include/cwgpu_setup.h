@@ -83,6 +83,13 @@ int64_t cwg_sheet_nearest(const cwg_sheet* s, double x, double y); /* Mesh::near
  * n_classes = 9*(nz+1). Returns dt_s (Gershgorin, fem.cpp:178-192) or < 0. */
 double cwg_struct3d_tables(const cwg_struct3d* s, double* coef, double* mass);
 
+/* Seeded uniform draws for the synthetic configurations (EXTENSION; the
+ * reference's RNG, std::mt19937_64 as in assign_fibrosis mesh.cpp:112):
+ * out[i] = lo + (hi - lo) * ((x_i >> 11) * 2^-53) with x_i the i-th output
+ * of std::mt19937_64(seed). Used for C3's per-node GKr jitter and C5's
+ * stimulus sites; restated in the oracle (cwo_uniform_mt64). */
+void cwg_uniform_mt64(uint64_t seed, int64_t n, double lo, double hi, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -637,6 +637,63 @@ int64_t cwo_reaction_step(int64_t n, int stride, double* v, double* s, double* l
   return bad;
 }
 
+/* Same pass with the node loop spread over OpenMP threads, as the
+ * reference's own `#pragma omp parallel for` (splitting.cpp:104-149): every
+ * node is independent, so any schedule gives the same bits; the k-histogram
+ * is summed per thread and the lowest failing node wins. */
+int64_t cwo_reaction_step_omp(int64_t n, int stride, double* v, double* s, double* last_dvdt,
+                              const uint8_t* model_of_node, const int* model_kind, const int* k_max,
+                              const double* gkr_scale, const cwo_protocol* prot, int scheme, int k0_up,
+                              int k0_down, double dt, double t, int64_t* khist, int khist_len, double* bad_t) {
+  int64_t bad = -1;
+  double bt = 0.0;
+#pragma omp parallel
+  {
+    int64_t lh[64] = {0};
+    int64_t lbad = -1;
+    double lbt = 0.0;
+#pragma omp for schedule(dynamic, 256)
+    for (int64_t i = 0; i < n; ++i) {
+      const int mid = model_of_node[i];
+      const int kind = model_kind[mid];
+      const int k = cwo_reaction_substeps(last_dvdt[i], scheme, k0_up, k0_down, k_max[mid]);
+      lh[k] += 1;
+      const double h = dt / (double)k;
+      const int ns = cwo_state_count(kind);
+      const double g = gkr_scale ? gkr_scale[i] : 1.0;
+      double vi = v[i];
+      double* si = s + i * stride;
+      double dv = 0.0, ds[64];
+      for (int j = 0; j < k; ++j) {
+        const double ts = t + (double)j * h;
+        const double cur = cwo_stim_current(prot, i, ts);
+        cwo_rates(kind, vi, si, cur, g, &dv, ds);
+        vi += h * dv;
+        for (int q = 0; q < ns; ++q) si[q] += h * ds[q];
+        if (!isfinite(vi)) {
+          if (lbad < 0 || i < lbad) {
+            lbad = i;
+            lbt = ts;
+          }
+          break;
+        }
+      }
+      v[i] = vi;
+      last_dvdt[i] = dv;
+    }
+#pragma omp critical
+    {
+      for (int q = 0; q < khist_len && q < 64; ++q) khist[q] += lh[q];
+      if (lbad >= 0 && (bad < 0 || lbad < bad)) {
+        bad = lbad;
+        bt = lbt;
+      }
+    }
+  }
+  if (bad_t) *bad_t = bt;
+  return bad;
+}
+
 /* ------------------------------------------------------------------ *
  * Activation detector (postprocess.cpp:15-66)                          *
  * ------------------------------------------------------------------ */
@@ -807,3 +864,118 @@ double cwo_assemble_slab3d(int64_t nx, int64_t ny, int64_t nz, double h, double 
 }
 
 void cwo_free(void* p) { free(p); }
+
+/* Node-class tables of the slab operator, from the oracle's own CSR assembly
+ * of a 2 x 2 x nz-element slab: every class (x face 0 / interior / nx, y
+ * face likewise, z layer) has a representative row there, and a row's
+ * coefficients are sums of its own elements' contributions in ascending
+ * element index, whatever the slab's extent in x and y. Layout as the
+ * structured operator: cls = (by*3 + bx)*(nz+1) + iz, slot q = (dy+1)*9 +
+ * (dz+1)*3 + (dx+1) (absent neighbours 0). Returns dt_s of any slab with
+ * nx, ny >= 2 (Gershgorin over the class rows, which are all its rows). */
+double cwo_slab3d_classes(int64_t nz, double h, double d_long, double rho, const double* angle_of_layer,
+                          double* coef, double* mass_out) {
+  int64_t *rp, *col;
+  double *val, *mass;
+  const double dt_s = cwo_assemble_slab3d(2, 2, nz, h, d_long, rho, angle_of_layer, &rp, &col, &val, &mass);
+  const int64_t nz1 = nz + 1, plane = nz1 * 3;
+  for (int by = 0; by < 3; ++by)
+    for (int bx = 0; bx < 3; ++bx)
+      for (int64_t iz = 0; iz < nz1; ++iz) {
+        const int64_t cls = (by * 3 + bx) * nz1 + iz;
+        const int64_t i = (by * nz1 + iz) * 3 + bx;
+        double* cf = coef + cls * 27;
+        for (int q = 0; q < 27; ++q) cf[q] = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+          /* (dy, dz, dx) from the column's grid coordinates (offsets alone are ambiguous for thin slabs) */
+          const int64_t cy = col[p] / plane, cz = (col[p] % plane) / 3, cx = col[p] % 3;
+          const int64_t dy = cy - by, dz = cz - iz, dx = cx - bx;
+          cf[(dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)] = val[p];
+        }
+        mass_out[cls] = mass[i];
+      }
+  free(rp);
+  free(col);
+  free(val);
+  free(mass);
+  return dt_s;
+}
+
+/* diffusion_substep (fem.cpp:194-207) on the structured slab: the same row
+ * sum in ascending column order ((dy, dz, dx) lexicographic for the y-outer
+ * numbering) over the present neighbours, then v - dt/m * acc. OpenMP over
+ * nodes (fem.cpp:198). */
+void cwo_diffusion_substep_slab3d(int64_t nx1, int64_t ny1, int64_t nz1, const double* coef, const double* mass,
+                                  const double* v, double dt_sub, double* out) {
+  const int64_t plane = nx1 * nz1;
+#pragma omp parallel for schedule(static) collapse(2)
+  for (int64_t iy = 0; iy < ny1; ++iy)
+    for (int64_t iz = 0; iz < nz1; ++iz) {
+      const int by = iy == 0 ? 0 : (iy == ny1 - 1 ? 2 : 1);
+      for (int64_t ix = 0; ix < nx1; ++ix) {
+        const int bx = ix == 0 ? 0 : (ix == nx1 - 1 ? 2 : 1);
+        const int64_t cls = (by * 3 + bx) * nz1 + iz;
+        const double* cf = coef + cls * 27;
+        const int64_t i = iy * plane + iz * nx1 + ix;
+        double acc = 0.0;
+        for (int dy = -1; dy <= 1; ++dy) {
+          if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+          for (int dz = -1; dz <= 1; ++dz) {
+            if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz1 - 1)) continue;
+            for (int dx = -1; dx <= 1; ++dx) {
+              if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
+              acc += cf[(dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)] * v[i + dy * plane + dz * nx1 + dx];
+            }
+          }
+        }
+        out[i] = v[i] - dt_sub / mass[cls] * acc;
+      }
+    }
+}
+
+/* MT19937-64 (Matsumoto & Nishimura 2004; the generator behind the
+ * reference's std::mt19937_64, mesh.cpp:112): 312-word state, seeded by
+ * x_i = 6364136223846793005 * (x_{i-1} ^ (x_{i-1} >> 62)) + i. */
+typedef struct {
+  uint64_t mt[312];
+  int mti;
+} cwo_mt64;
+
+static void mt64_seed(cwo_mt64* g, uint64_t seed) {
+  g->mt[0] = seed;
+  for (int i = 1; i < 312; ++i) g->mt[i] = 6364136223846793005ull * (g->mt[i - 1] ^ (g->mt[i - 1] >> 62)) + (uint64_t)i;
+  g->mti = 312;
+}
+
+static uint64_t mt64_next(cwo_mt64* g) {
+  const uint64_t A = 0xB5026F5AA96619E9ull, UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
+  if (g->mti >= 312) {
+    for (int i = 0; i < 312; ++i) {
+      const uint64_t x = (g->mt[i] & UM) | (g->mt[(i + 1) % 312] & LM);
+      g->mt[i] = g->mt[(i + 156) % 312] ^ (x >> 1) ^ ((x & 1ull) ? A : 0ull);
+    }
+    g->mti = 0;
+  }
+  uint64_t x = g->mt[g->mti++];
+  x ^= (x >> 29) & 0x5555555555555555ull;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+  x ^= (x << 37) & 0xFFF7EEE000000000ull;
+  x ^= x >> 43;
+  return x;
+}
+
+/* raw outputs (known-answer pin: the C++ standard requires the 10000th output
+ * of a default-seeded (5489) mt19937_64 to be 9981545732273789042) */
+void cwo_mt64_raw(uint64_t seed, int64_t n, uint64_t* out) {
+  cwo_mt64 g;
+  mt64_seed(&g, seed);
+  for (int64_t k = 0; k < n; ++k) out[k] = mt64_next(&g);
+}
+
+/* uniform draws lo + (hi - lo) * ((x >> 11) * 2^-53) for the synthetic configurations */
+void cwo_uniform_mt64(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  cwo_mt64 g;
+  mt64_seed(&g, seed);
+  const double w = hi - lo;
+  for (int64_t k = 0; k < n; ++k) out[k] = lo + w * ((double)(mt64_next(&g) >> 11) * 0x1.0p-53);
+}

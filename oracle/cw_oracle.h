@@ -91,6 +91,23 @@ double cwo_assemble_slab3d(int64_t nx, int64_t ny, int64_t nz, double h, double 
                            double** mass);
 void cwo_free(void* p);
 
+/* OpenMP variant of cwo_reaction_step (same results for any thread count). */
+int64_t cwo_reaction_step_omp(int64_t n, int stride, double* v, double* s, double* last_dvdt,
+                              const uint8_t* model_of_node, const int* model_kind, const int* k_max,
+                              const double* gkr_scale, const cwo_protocol* prot, int scheme, int k0_up,
+                              int k0_down, double dt, double t, int64_t* khist, int khist_len, double* bad_t);
+
+/* Slab node-class tables (coef[9*(nz+1)][27], mass[9*(nz+1)]) from a small CSR assembly; returns dt_s. */
+double cwo_slab3d_classes(int64_t nz, double h, double d_long, double rho, const double* angle_of_layer,
+                          double* coef, double* mass);
+/* Structured slab diffusion sub-step over those tables (OpenMP). */
+void cwo_diffusion_substep_slab3d(int64_t nx1, int64_t ny1, int64_t nz1, const double* coef, const double* mass,
+                                  const double* v, double dt_sub, double* out);
+
+/* MT19937-64 (std::mt19937_64): raw outputs and uniform draws lo + (hi-lo)*((x >> 11) * 2^-53). */
+void cwo_mt64_raw(uint64_t seed, int64_t n, uint64_t* out);
+void cwo_uniform_mt64(uint64_t seed, int64_t n, double lo, double hi, double* out);
+
 #ifdef __cplusplus
 }
 #endif

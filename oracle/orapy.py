@@ -57,6 +57,12 @@ def lib():
             "cwo_assemble_slab3d": (D, [I64, I64, I64, D, D, D, dp, C.POINTER(lp), C.POINTER(lp), C.POINTER(dp),
                                         C.POINTER(dp)]),
             "cwo_free": (None, [C.c_void_p]),
+            "cwo_reaction_step_omp": (I64, [I64, I, dp, dp, dp, u8p, ip, ip, dp, C.c_void_p, I, I, I, D, D, lp, I,
+                                            dp]),
+            "cwo_slab3d_classes": (D, [I64, D, D, D, dp, dp, dp]),
+            "cwo_diffusion_substep_slab3d": (None, [I64, I64, I64, dp, dp, dp, D, dp]),
+            "cwo_mt64_raw": (None, [C.c_uint64, I64, C.POINTER(C.c_uint64)]),
+            "cwo_uniform_mt64": (None, [C.c_uint64, I64, D, D, dp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -148,7 +154,47 @@ def assemble_slab3d(nx, ny, nz, h, d_long, rho, angles):
     return out, dt_s
 
 
+def mt64_raw(seed, n):
+    out = np.zeros(n, np.uint64)
+    lib().cwo_mt64_raw(seed, n, out.ctypes.data_as(C.POINTER(C.c_uint64)))
+    return out
+
+
+def uniform_mt64(seed, n, lo, hi):
+    out = np.zeros(n)
+    lib().cwo_uniform_mt64(seed, n, lo, hi, _dp(out))
+    return out
+
+
+class Slab3DOp:
+    """Structured 3D slab operator (EXTENSION, BASELINE configs 4-5) for the oracle run loop: node-class
+    tables from the oracle's own CSR assembly of a 2 x 2 x nz-element slab (cwo_slab3d_classes), applied
+    matrix-free (cwo_diffusion_substep_slab3d), so 10^6-10^8-node slabs need no CSR. Node index
+    (iy*(nz+1) + iz)*(nx+1) + ix; fibre angle per element layer linear in z (endo -> epi)."""
+
+    def __init__(self, nx, ny, nz, h, d_long=0.0012, rho=0.25, angle_endo_deg=60.0, angle_epi_deg=-60.0):
+        self.nx, self.ny, self.nz, self.h = nx, ny, nz, h
+        self.nx1, self.ny1, self.nz1 = nx + 1, ny + 1, nz + 1
+        self.n = self.nx1 * self.ny1 * self.nz1
+        self.angles = np.deg2rad(angle_endo_deg + (angle_epi_deg - angle_endo_deg) * (np.arange(nz) + 0.5) / nz)
+        self.coef = np.zeros(9 * self.nz1 * 27)
+        self.mass = np.zeros(9 * self.nz1)
+        self.dt_s = lib().cwo_slab3d_classes(nz, h, d_long, rho, _dp(self.angles), _dp(self.coef), _dp(self.mass))
+
+    def index(self, ix, iy, iz):
+        return (np.asarray(iy) * self.nz1 + np.asarray(iz)) * self.nx1 + np.asarray(ix)
+
+    def substep(self, v, dt_sub):
+        v = np.ascontiguousarray(v, np.float64)
+        out = np.empty_like(v)
+        lib().cwo_diffusion_substep_slab3d(self.nx1, self.ny1, self.nz1, _dp(self.coef), _dp(self.mass), _dp(v),
+                                           dt_sub, _dp(out))
+        return out
+
+
 def diffusion_substep(csr, v, dt_sub):
+    if hasattr(csr, "substep"):
+        return csr.substep(v, dt_sub)
     rp, col, val, mass = csr
     v = np.ascontiguousarray(v, np.float64)
     out = np.empty_like(v)
@@ -167,13 +213,15 @@ class Protocol:
 
     def __init__(self, n, stimuli):
         # stimuli: list of (nodes, t_start, duration, amplitude, period|None)
-        lists = [[] for _ in range(n)]
-        for eid, st in enumerate(stimuli):
-            for node in st[0]:
-                lists[int(node)].append(eid)
+        # per node, entry ids in entry order (stimulus.cpp:17-31 appends entry by entry)
+        nodes = [np.asarray(st[0], np.int64).ravel() for st in stimuli]
+        eids = [np.full(len(nd), e, np.int32) for e, nd in enumerate(nodes)]
+        nd = np.concatenate(nodes) if nodes else np.zeros(0, np.int64)
+        ed = np.concatenate(eids) if eids else np.zeros(0, np.int32)
+        order = np.argsort(nd, kind="stable")
         self.node_ptr = np.zeros(n + 1, np.int32)
-        self.node_ptr[1:] = np.cumsum([len(x) for x in lists])
-        self.ids = np.array([e for x in lists for e in x] or [0], np.int32)
+        self.node_ptr[1:] = np.cumsum(np.bincount(nd, minlength=n)[:n])
+        self.ids = ed[order].astype(np.int32) if ed.size else np.array([0], np.int32)
         self.t_start = np.array([s[1] for s in stimuli] or [0.0])
         self.duration = np.array([s[2] for s in stimuli] or [0.0])
         self.amplitude = np.array([s[3] for s in stimuli] or [0.0])
@@ -236,7 +284,7 @@ def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt
     Raises OracleInstability like the reference's InstabilityError.
     """
     L = lib()
-    n = len(csr[3])
+    n = csr.n if hasattr(csr, "substep") else len(csr[3])
     kinds = np.array([MODEL_KINDS[m] for m in models], np.int32)
     sc = SCHEMES[scheme]
     dt_eff = min(dt, dt_s) if scheme == "OSTAR" else dt
@@ -287,10 +335,10 @@ def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt
         t = float(step) * dt_eff
         if step == 0:
             diffuse(l, t)
-        bad = L.cwo_reaction_step(n, stride, _dp(v), _dp(s), _dp(last), model_of_node.ctypes.data_as(u8p),
-                                  kinds.ctypes.data_as(ip), kmax.ctypes.data_as(ip),
-                                  None if gk is None else _dp(gk), C.byref(prot.c), sc, k0_up, k0_down,
-                                  dt_eff, t, _lp(khist), C.byref(bad_t))
+        bad = L.cwo_reaction_step_omp(n, stride, _dp(v), _dp(s), _dp(last), model_of_node.ctypes.data_as(u8p),
+                                      kinds.ctypes.data_as(ip), kmax.ctypes.data_as(ip),
+                                      None if gk is None else _dp(gk), C.byref(prot.c), sc, k0_up, k0_down,
+                                      dt_eff, t, _lp(khist), len(khist), C.byref(bad_t))
         if bad >= 0:
             raise OracleInstability("reaction step produced non-finite V", int(bad), bad_t.value)
         diffuse(l if step == n_steps - 1 else 2 * l, t)
@@ -306,6 +354,58 @@ def run_simulation(csr, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt
     return dict(v=v, s=s, last_dvdt=last, k_histogram=khist, n_steps=n_steps, l=l, dt_ad=dt_ad, snapshots=snaps,
                 dt_effective=dt_eff, trace_t=np.array(traces_t), traces=np.array(traces_v).T.copy(),
                 lat=lat, lat_valid=lv, apd90=apd, apd_valid=av)
+
+
+class Integrator:
+    """StrangIntegrator restatement with the reference's per-step surface (splitting.hpp:101-127):
+    advance(t, step, n_steps) runs splitting.cpp:171-181 on the oracle kernels (OpenMP reaction and
+    diffusion). Used by bench.py's CPU legs on configurations the reference cannot express."""
+
+    def __init__(self, op, dt_s, models, model_of_node, stimuli, scheme="DAETI", dt=0.1, k0_up=5, k0_down=1,
+                 strict=False, gkr_scale=None):
+        self.op = op
+        self.n = op.n if hasattr(op, "substep") else len(op[3])
+        self.kinds = np.array([MODEL_KINDS[m] for m in models], np.int32)
+        self.sc = SCHEMES[scheme]
+        self.dt_eff = min(dt, dt_s) if scheme == "OSTAR" else dt
+        self.l, self.dt_ad = diffusion_substeps(self.dt_eff, dt_s, strict, scheme)
+        self.kmax = np.array([max(1, int(math.floor(self.dt_eff / stable_step(m)))) for m in models], np.int32)
+        self.khist = np.zeros(max(1, int(self.kmax.max())) + 1, np.int64)
+        self.stride = max([1] + [state_count(m) for m in models])
+        self.mon = np.ascontiguousarray(model_of_node, np.uint8)
+        self.k0_up, self.k0_down = k0_up, k0_down
+        self.gk = None if gkr_scale is None else np.ascontiguousarray(gkr_scale, np.float64)
+        self.prot = Protocol(self.n, stimuli)
+        self.v = np.zeros(self.n)
+        self.s = np.zeros((self.n, self.stride))
+        self.last = np.zeros(self.n)
+        for mid, m in enumerate(models):  # make_initial_state (splitting.cpp:183-217), rest states
+            r = rest_state(m)
+            sel = self.mon == mid
+            self.v[sel] = r[0]
+            self.s[np.ix_(sel, np.arange(len(r) - 1))] = r[1:]
+
+    def _diffuse(self, count, t):
+        for _ in range(count):
+            self.v = diffusion_substep(self.op, self.v, self.dt_ad)
+            bad = np.flatnonzero(~np.isfinite(self.v))
+            if bad.size:
+                raise OracleInstability("diffusion sub-step produced non-finite V", int(bad[0]), t)
+
+    def advance(self, t, step, n_steps):
+        if step == 0:
+            self._diffuse(self.l, t)
+        bad_t = C.c_double()
+        bad = lib().cwo_reaction_step_omp(self.n, self.stride, _dp(self.v), _dp(self.s), _dp(self.last),
+                                          self.mon.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                          self.kinds.ctypes.data_as(C.POINTER(C.c_int)),
+                                          self.kmax.ctypes.data_as(C.POINTER(C.c_int)),
+                                          None if self.gk is None else _dp(self.gk), C.byref(self.prot.c), self.sc,
+                                          self.k0_up, self.k0_down, self.dt_eff, t, _lp(self.khist),
+                                          len(self.khist), C.byref(bad_t))
+        if bad >= 0:
+            raise OracleInstability("reaction step produced non-finite V", int(bad), bad_t.value)
+        self._diffuse(self.l if step == n_steps - 1 else 2 * self.l, t)
 
 
 def round_half_away(x):

@@ -126,6 +126,7 @@ _SIGS = {
     "cwg_sheet_tags": (_i32p, [C.c_void_p]),
     "cwg_sheet_select": (C.c_int64, [C.c_void_p, C.c_int, _dp, _lp, C.c_int64, _lp, C.c_int64]),
     "cwg_sheet_nearest": (C.c_int64, [C.c_void_p, C.c_double, C.c_double]),
+    "cwg_uniform_mt64": (None, [C.c_uint64, C.c_int64, C.c_double, C.c_double, _dp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -8,17 +8,26 @@ namespace cwg {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kNoError = ~0ull;
+constexpr long long kNoSeq = 0x7fffffffffffffffll;  // ErrRec::seq before any failure
 
 // Error record, one per context. key = node << 22 | k << 11 | j (reaction) or
 // node << 22 (diffusion); atomicMin gives the reference's "lowest node"
 // (splitting.cpp:129-140, :162-166). seq = program-order event id of the
-// first failing event; kernels of later events skip their work so the state
-// stays exactly where the reference would have thrown.
+// first failing event (atomicMin, kNoSeq before any failure); kernels of
+// later events skip their work so the state stays exactly where the
+// reference would have thrown.
+// The failing launch also records its V buffers and fused depth T, so the
+// host can put V exactly where the reference stops (later events skip their
+// work without writing): the reaction's in-place V, a diffusion launch's
+// output, or -- for a launch that fused T sub-steps and failed in sub-step
+// q < T-1 -- a replay of q+1 sub-steps from its (untouched) input.
 struct ErrRec {
   unsigned long long key;
   long long seq;
   int phase;  // 1 reaction, 2 diffusion
-  int pad;
+  int T;      // sub-steps fused by the failing launch (1: unfused / reaction)
+  const double* vin;
+  double* vout;
 };
 
 // Flattened ProtocolIndex (stimulus.hpp:35-50)
@@ -109,16 +118,29 @@ __device__ __forceinline__ long long cur_seq(const long long* clock, long long s
   return (*clock + step_off) * evs + ev;
 }
 
-// True when an earlier event already failed: skip the work (state frozen at the throw).
+// True when a STRICTLY earlier event already failed: skip the work (state
+// frozen at the throw). Only seq decides: a failure of the current event
+// (written concurrently by this launch) carries seq == the current seq and
+// never makes a block skip, so every block of a launch agrees (an earlier
+// event's record was complete at its kernel boundary).
+// err == nullptr: an unchecked launch (diastolic_threshold probe runs, whose
+// diffusion has no NaN scan, stimulus.cpp:106) -- never skips, never records.
 __device__ __forceinline__ bool earlier_failure(const ErrRec* err, long long seq) {
+  if (!err) return false;
   const volatile ErrRec* e = err;
-  return e->key != kNoError && e->seq != seq;
+  return e->seq < seq;
 }
 
-__device__ __forceinline__ void record_failure(ErrRec* err, unsigned long long key, long long seq, int phase) {
+__device__ __forceinline__ void record_failure(ErrRec* err, unsigned long long key, long long seq, int phase,
+                                               int T, const double* vin, double* vout) {
+  if (!err) return;
+  atomicMin(reinterpret_cast<unsigned long long*>(&err->seq), static_cast<unsigned long long>(seq));  // seq >= 0
   atomicMin(&err->key, key);
-  err->seq = seq;  // all failing threads of this event write the same values
+  // all failing threads of this event write the same values
   err->phase = phase;
+  err->T = T;
+  err->vin = vin;
+  err->vout = vout;
 }
 
 struct Stencil2D {

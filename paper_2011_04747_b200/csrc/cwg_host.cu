@@ -264,6 +264,7 @@ struct cwg_ctx {
   long long graph_base_mod = 0;
   long long graph_launches = 0;
   long long clock_at = -1;  // host knowledge of *d_clock, -1 unknown
+  long long restored_seq = -1;  // failure whose state restore_failed_state already put in place
 
   // multi-GPU
   ncclComm_t comm = nullptr;
@@ -296,7 +297,8 @@ struct cwg_ctx {
   // pinned staging
   double *h_v = nullptr, *h_s = nullptr, *h_last = nullptr;
   double* d_stage = nullptr;
-  long long stage_nodes = 0;
+  long long stage_nodes = 0;  // nodes per staging chunk at the current caller stride
+  long long stage_cap = 0;    // doubles allocated in d_stage
 };
 
 namespace {
@@ -502,6 +504,40 @@ std::vector<int> diffusion_groups(const cwg_ctx* c, int count) {
   return g;
 }
 
+// One diffusion launch of T fused sub-steps vin -> vout (err == nullptr: unchecked).
+void launch_diffusion_group(cwg_ctx* c, int T, const double* vin, double* vout, ErrRec* err, long long step_off,
+                            int ev) {
+  DiffArgs a{};
+  a.vin = vin;
+  a.vout = vout;
+  a.n = c->n_own;
+  a.halo = c->halo;
+  a.dt_sub = c->dt_ad;
+  a.err = err;
+  a.clock = c->d_clock;
+  a.step_off = step_off;
+  a.evs = c->evs;
+  a.ev = ev;
+  a.node_offset = c->own_global0;
+  if (c->op_kind == CWG_OP_STENCIL2D) {
+    Stencil2D s{c->d_coef, c->n_coef, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1,
+                c->hrows_v, c->hrows_c};
+    if (T > 1 && tma_path(c))
+      CUDA_TRY(launch_diffuse_stencil2d_tbm(T, a, s, c->tmap[T], c->num_sms, c->stream));
+    else if (T > 1)
+      CUDA_TRY(launch_diffuse_stencil2d_tb(T, a, s, c->num_sms, c->stream));
+    else
+      CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
+  } else if (c->op_kind == CWG_OP_STRUCT3D) {
+    Struct3D s{c->d_coef, c->d_cm, c->s3_nx1, c->s3_nz1, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
+    CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms, c->stream));
+  } else {
+    CsrDev m{c->d_rp, c->d_col, c->d_val, c->d_cm};
+    CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));
+  }
+  ++c->launches;
+}
+
 void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
   // ceil(count / fuse) launches with balanced group sizes; every launch flips
   // the V double buffer (graphs are kept per starting parity)
@@ -511,38 +547,36 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     double* vin = c->d_v[c->cur];
     double* vout = c->d_v[c->cur ^ 1];
     halo_exchange(c, vin, T);
-    DiffArgs a{};
-    a.vin = vin;
-    a.vout = vout;
-    a.n = c->n_own;
-    a.halo = c->halo;
-    a.dt_sub = c->dt_ad;
-    a.err = c->fixed_step ? c->d_err_dummy : c->d_err;
-    a.clock = c->d_clock;
-    a.step_off = step_off;
-    a.evs = c->evs;
-    a.ev = ev0 + q;
-    a.node_offset = c->own_global0;
-    if (c->op_kind == CWG_OP_STENCIL2D) {
-      Stencil2D s{c->d_coef, c->n_coef, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1,
-                  c->hrows_v, c->hrows_c};
-      if (T > 1 && tma_path(c))
-        CUDA_TRY(launch_diffuse_stencil2d_tbm(T, a, s, c->tmap[T], c->num_sms, c->stream));
-      else if (T > 1)
-        CUDA_TRY(launch_diffuse_stencil2d_tb(T, a, s, c->num_sms, c->stream));
-      else
-        CUDA_TRY(launch_diffuse_stencil2d(a, s, c->num_sms * 16, c->stream));
-    } else if (c->op_kind == CWG_OP_STRUCT3D) {
-      Struct3D s{c->d_coef, c->d_cm, c->s3_nx1, c->s3_nz1, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1};
-      CUDA_TRY(launch_diffuse_struct3d(a, s, c->num_sms, c->stream));
-    } else {
-      CsrDev m{c->d_rp, c->d_col, c->d_val, c->d_cm};
-      CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));
-    }
-    ++c->launches;
+    // threshold probe runs: no NaN scan after diffusion (stimulus.cpp:106) -> unchecked launch
+    launch_diffusion_group(c, T, vin, vout, c->fixed_step ? nullptr : c->d_err, step_off, ev0 + q);
     c->cur ^= 1;
     q += T;
   }
+}
+
+// After a failure: put the state where the reference stops (splitting.cpp:
+// 129-140 reaction: every node finished, V in place; :162-166 diffusion: the
+// failing sub-step's output). Later events skipped without writing, so the
+// failing launch's buffers are intact: copy its output into the current V
+// buffer, or -- when it fused T sub-steps and failed in sub-step q < T-1 --
+// replay q+1 sub-steps from its input first (bit-identical kernels,
+// unchecked). One device only: with y-slabs a neighbour's halo may have
+// moved on. Idempotent per failure (restored_seq).
+void restore_failed_state(cwg_ctx* c, const ErrRec& r) {
+  if (r.key == kNoError || r.seq == c->restored_seq || !r.vout) return;
+  double* dst = c->d_v[c->cur];
+  const double* src = r.vout;
+  if (r.phase == 2 && r.T > 1 && c->world == 1) {
+    const int q = static_cast<int>(r.key >> 58);
+    if (q < r.T - 1) {
+      launch_diffusion_group(c, q + 1, r.vin, r.vout, nullptr, 0, 0);
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+  }
+  if (src != dst)
+    CUDA_TRY(cudaMemcpyAsync(dst, src, c->n_alloc * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->restored_seq = r.seq;
 }
 
 unsigned long long* g_react_trace = nullptr;  // diagnostics only (CWG_REACT_TRACE, cwg_react_trace)
@@ -1107,7 +1141,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->d_err = dev_alloc<ErrRec>(1);
   c->d_clock = dev_alloc<long long>(1);
   c->d_khist = dev_alloc<unsigned long long>(c->khist_len);
-  ErrRec none{kNoError, -1, 0, 0};
+  ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
   CUDA_TRY(cudaMemcpy(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemset(c->d_clock, 0, sizeof(long long)));
   c->clock_at = 0;
@@ -1174,8 +1208,13 @@ int guarded(cwg_error* err, F&& f) {
 }
 
 void reset_error(cwg_ctx* c) {
-  ErrRec none{kNoError, -1, 0, 0};
+  ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
+  c->restored_seq = -1;
   CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
+  // the reaction bins' work/done counters reset themselves at the end of
+  // every launch; zero them here too so no earlier launch can leave them stale
+  for (const auto& b : c->bins)
+    if (b.d_counter) CUDA_TRY(cudaMemsetAsync(b.d_counter, 0, 2 * sizeof(unsigned), c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 }
 
@@ -1186,6 +1225,7 @@ bool ev_is_reaction(const cwg_ctx* c, long long seq) { return seq % c->evs == c-
 bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
   ErrRec r{};
   CUDA_TRY(cudaMemcpy(&r, c->d_err, sizeof(r), cudaMemcpyDeviceToHost));
+  const ErrRec local = r;
   if (c->world > 1 && !c->loopback) {
     long long* tmp = dev_alloc<long long>(2);
     long long h[2] = {r.key == kNoError ? (1ll << 62) : r.seq, 0};
@@ -1203,6 +1243,7 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
     r.seq = h[0];
   }
   if (r.key == kNoError) return false;
+  restore_failed_state(c, local);
   // diffusion keys carry the fused sub-step index in bits 58..63 (temporal blocking)
   const long long node = static_cast<long long>(r.key >> 22) & (ev_is_reaction(c, r.seq) ? -1ll : (1ll << 36) - 1);
   const long long step = r.seq / c->evs;
@@ -1252,10 +1293,21 @@ void normalise_parity(cwg_ctx* c) {
   c->cur = 0;
 }
 
-void ensure_stage(cwg_ctx* c) {
-  if (c->d_stage) return;
-  c->stage_nodes = std::min<long long>(c->n_own, 1ll << 20);
-  c->d_stage = dev_alloc<double>(static_cast<size_t>(std::max<long long>(c->stage_nodes, 1)) * c->stride);
+// AoS staging buffer for a caller state of `stride` doubles per node (any
+// stride >= c->stride: a wider model list, a checkpoint): up to 2^20 nodes
+// per chunk, reallocated when a wider stride needs more room.
+void ensure_stage(cwg_ctx* c, int stride) {
+  const long long nodes = std::max<long long>(1, std::min<long long>(c->n_own, 1ll << 20));
+  const long long need = nodes * stride;
+  if (c->d_stage && c->stage_cap >= need) {
+    c->stage_nodes = c->stage_cap / stride;
+    if (c->stage_nodes > nodes) c->stage_nodes = nodes;
+    return;
+  }
+  dev_free(c->d_stage);
+  c->d_stage = dev_alloc<double>(static_cast<size_t>(need));
+  c->stage_cap = need;
+  c->stage_nodes = nodes;
 }
 
 }  // namespace
@@ -1371,7 +1423,7 @@ int cwg_upload_state(cwg_ctx* c, const double* v, const double* s_aos, int strid
                              c->stream));
     CUDA_TRY(cudaMemcpyAsync(c->d_last + c->halo, last + g0, c->n_own * sizeof(double), cudaMemcpyHostToDevice,
                              c->stream));
-    ensure_stage(c);
+    ensure_stage(c, stride);
     for (long long o = 0; o < c->n_own; o += c->stage_nodes) {
       const long long cnt = std::min(c->stage_nodes, c->n_own - o);
       CUDA_TRY(cudaMemcpyAsync(c->d_stage, s_aos + (g0 + o) * stride, cnt * stride * sizeof(double),
@@ -1412,7 +1464,7 @@ int cwg_download_state(cwg_ctx* c, double* v, double* s_aos, int stride, double*
       CUDA_TRY(cudaMemcpyAsync(last + g0, c->d_last + c->halo, c->n_own * sizeof(double), cudaMemcpyDeviceToHost,
                                c->stream));
     if (s_aos) {
-      ensure_stage(c);
+      ensure_stage(c, stride);
       for (long long o = 0; o < c->n_own; o += c->stage_nodes) {
         const long long cnt = std::min(c->stage_nodes, c->n_own - o);
         CUDA_TRY(launch_soa_to_aos(c->d_S, c->pitch, c->halo + o, c->stride, cnt, c->d_stage, stride, c->stream));
@@ -1957,7 +2009,7 @@ bool propagates(cwg_ctx* c, double amp, long long steps, cudaGraphExec_t& graph,
                               state_count(b.kind), c->stride, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
-  ErrRec none{kNoError, -1, 0, 0};
+  ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
   CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
   CUDA_TRY(cudaMemcpyAsync(c->d_err_dummy, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
   const long long never = 0x7fffffffffffffffll;
@@ -2076,7 +2128,7 @@ extern "C" int cwg_diastolic_threshold(const cwg_problem* prob, const double* co
     CUDA_TRY(launch_mass_factor_fix(c));
     c->d_err_dummy = dev_alloc<ErrRec>(1);
     {
-      const ErrRec none{kNoError, -1, 0, 0};
+      const ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
       CUDA_TRY(cudaMemcpy(c->d_err_dummy, &none, sizeof(none), cudaMemcpyHostToDevice));
     }
     c->d_cross = dev_alloc<long long>(1);

@@ -34,11 +34,8 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = o + s.hrows_v * s.w;  // local V index
     const long long oc = o + s.hrows_c * s.w;  // local coefficient index
+    if (skip) return;  // an earlier event failed: leave V where it stopped (host: restore_failed_state)
     const double vi = a.vin[i];
-    if (skip) {
-      a.vout[i] = vi;
-      continue;
-    }
     const long long r = o / s.w, x = o - r * s.w;
     const long long gy = s.row_begin + r;
     const bool has_s = gy > 0, has_n = gy + 1 < s.ny1, has_w = x > 0, has_e = x + 1 < s.w;
@@ -61,7 +58,7 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
     const double out = vi - s.cm[oc] * acc;
     a.vout[i] = out;
     if (!isfinite(out))
-      record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.w) << 22, seq, 2);
+      record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.w) << 22, seq, 2, 1, a.vin, a.vout);
   }
 }
 
@@ -82,7 +79,7 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
 // is the full 9-point stencil) and no presence flags or selects are needed.
 template <int T, int TBX, int TBY, int NT, bool EDGE>
 __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, double (*Vs)[(TBY + 2 * T) * (TBX + 2 * T)],
-                                        long long gx0, long long ly0, bool skip, long long seq) {
+                                        long long gx0, long long ly0, long long seq) {
   constexpr int VX = TBX + 2 * T;
   constexpr int CX = TBX + 2 * (T - 1), CY = TBY + 2 * (T - 1);  // computed region (sub-step 0)
   constexpr int R = (CX * CY + NT - 1) / NT;                     // points per thread
@@ -167,7 +164,7 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
         acc += cf[r][6] * sp[VX - 1];
         acc += cf[r][7] * sp[VX];
         acc += cf[r][8] * sp[VX + 1];
-        o = skip ? v0 : v0 - cf[r][9] * acc;
+        o = v0 - cf[r][9] * acc;
       } else {
         const double vsw = sp[-VX - 1], vs = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
         const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
@@ -183,14 +180,15 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
         tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
         tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
         tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
-        o = skip ? v0 : v0 - cf[r][9] * acc;
+        o = v0 - cf[r][9] * acc;
       }
       out[r] = o;
       if (q + 1 < T && act) dst[vi[r]] = o;
-      if (act && (f & 32u) && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
+      if (act && (f & 32u) && threadIdx.x + r * NT < TBX * TBY && !isfinite(o)) {
         const long long x = gx0 + px[r], yl = ly0 + py[r];
         record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
-                                  (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2);
+                                  (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2, T,
+                       a.vin, a.vout);
       }
     }
     if (q + 1 < T) {
@@ -211,6 +209,7 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
   __shared__ double Vs[2][VY * VX];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
+  if (skip) return;  // block-uniform: an earlier event failed, V stays where it stopped
   const long long gx0 = static_cast<long long>(blockIdx.x) * TBX, ly0 = static_cast<long long>(blockIdx.y) * TBY;
   const long long rows = s.rows, w = s.w;
   {
@@ -225,9 +224,9 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
   }
   const bool interior = gx0 >= T && gx0 + TBX + T <= w && ly0 >= T && ly0 + TBY + T <= rows;
   if (interior)
-    tb_body<T, TBX, TBY, NT, false>(a, s, Vs, gx0, ly0, skip, seq);
+    tb_body<T, TBX, TBY, NT, false>(a, s, Vs, gx0, ly0, seq);
   else
-    tb_body<T, TBX, TBY, NT, true>(a, s, Vs, gx0, ly0, skip, seq);
+    tb_body<T, TBX, TBY, NT, true>(a, s, Vs, gx0, ly0, seq);
 }
 
 // ---------------------------------------------------------------------------
@@ -288,6 +287,7 @@ __global__ void __launch_bounds__(NT, 1)
   const unsigned bar_a = smem_u32(bar);
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
+  if (skip) return;  // block-uniform: an earlier event failed, V stays where it stopped
   const long long rows = s.rows, w = s.w;
   int px[R], py[R];
 #pragma unroll
@@ -408,7 +408,7 @@ __global__ void __launch_bounds__(NT, 1)
           acc += cf[r][6] * sp[VX - 1];
           acc += cf[r][7] * sp[VX];
           acc += cf[r][8] * sp[VX + 1];
-          o = skip ? v0 : v0 - cf[r][9] * acc;
+          o = v0 - cf[r][9] * acc;
         } else {
           const double vsw = sp[-VX - 1], vss = sp[-VX], vse = sp[-VX + 1], vw = sp[-1], ve = sp[1];
           const double vnw = sp[VX - 1], vn = sp[VX], vne = sp[VX + 1];
@@ -423,14 +423,15 @@ __global__ void __launch_bounds__(NT, 1)
           tmp = acc + cf[r][6] * vnw; acc = (hn && hw) ? tmp : acc;
           tmp = acc + cf[r][7] * vn;  acc = hn ? tmp : acc;
           tmp = acc + cf[r][8] * vne; acc = (hn && he) ? tmp : acc;
-          o = skip ? v0 : v0 - cf[r][9] * acc;
+          o = v0 - cf[r][9] * acc;
         }
         out[r] = o;
         if (q + 1 < T && act) dst[vi[r]] = o;
-        if (act && threadIdx.x + r * NT < TBX * TBY && !skip && !isfinite(o)) {
+        if (act && threadIdx.x + r * NT < TBX * TBY && !isfinite(o)) {
           const long long x = gx0 + px[r], yl = ly0 + py[r];
           record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
-                                    (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2);
+                                    (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2,
+                         T, a.vin, a.vout);
         }
       }
       if (q + 1 < T) {
@@ -451,12 +452,9 @@ template <int T>
 static cudaError_t launch_tbm_t(const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm, int num_sms,
                                 cudaStream_t st) {
   using G = TbmGeom<T, 64, 16, 512>;
-  static bool set = false;
-  if (!set) {
-    cudaFuncSetAttribute(diffuse_stencil2d_tbm<T, 64, 16, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(G::smem));
-    set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  const cudaError_t e = ensure_dyn_smem(diffuse_stencil2d_tbm<T, 64, 16, 512>, static_cast<int>(G::smem), attr_done);
+  if (e != cudaSuccess) return e;
   const int tiles_x = static_cast<int>((s.w + 63) / 64);
   const int n_tiles = tiles_x * static_cast<int>((s.rows + 15) / 16);
   diffuse_stencil2d_tbm<T, 64, 16, 512><<<std::min(num_sms, n_tiles), 512, G::smem, st>>>(a, s, tm, tiles_x, n_tiles);
@@ -545,6 +543,7 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
   __shared__ double ring[4][PL];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
+  if (skip) return;  // block-uniform: an earlier event failed, V stays where it stopped
   const int tx = threadIdx.x % S3_TX, tz = threadIdx.x / S3_TX;
   const int x0 = blockIdx.x * S3_TX, z0 = blockIdx.y * S3_TZ;
   const int ix = x0 + tx, iz = z0 + tz;
@@ -604,9 +603,7 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
       const double vi = p0[c0];
       const long long gy = s.row_begin + yl;
       const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
-      if (skip) {
-        a.vout[i] = vi;
-      } else {
+      {
         double out;
         const double* pl[3] = {pm, p0, pp};
         if (xz_interior && by == 1) {
@@ -642,7 +639,8 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
         }
         a.vout[i] = out;
         if (!isfinite(out))
-          record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2);
+          record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2, 1,
+                         a.vin, a.vout);
       }
     }
     if (yl + 1 < ye) {
@@ -668,17 +666,15 @@ __global__ void __launch_bounds__(256) diffuse_csr(DiffArgs a, CsrDev m) {
   const bool skip = earlier_failure(a.err, seq);
   for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < a.n;
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (skip) return;  // an earlier event failed: V stays where it stopped
     const long long i = o + a.halo;
-    if (skip) {
-      a.vout[i] = a.vin[i];
-      continue;
-    }
     double acc = 0.0;
     const long long p1 = m.row_ptr[o + 1];
     for (long long p = m.row_ptr[o]; p < p1; ++p) acc += m.val[p] * a.vin[m.col[p]];
     const double out = a.vin[i] - m.cm[o] * acc;
     a.vout[i] = out;
-    if (!isfinite(out)) record_failure(a.err, static_cast<unsigned long long>(o + a.node_offset) << 22, seq, 2);
+    if (!isfinite(out))
+      record_failure(a.err, static_cast<unsigned long long>(o + a.node_offset) << 22, seq, 2, 1, a.vin, a.vout);
   }
 }
 

@@ -3,9 +3,27 @@
 
 #include <cuda.h>
 
+#include <atomic>
+#include <cstdint>
+
 #include "common.cuh"
 
 namespace cwg {
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device property of a
+// kernel: set it once per (kernel, device) -- `done` is the kernel's device
+// bitmask -- and report the CUDA status instead of dropping it.
+template <class K>
+inline cudaError_t ensure_dyn_smem(K* kernel, int bytes, std::atomic<uint64_t>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+  return e;
+}
 
 cudaError_t launch_react_exact(int kind, const ReactArgs& a, int grid, cudaStream_t st);
 int react_exact_threads(int kind);

@@ -126,7 +126,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         const unsigned long long key = (static_cast<unsigned long long>(node + a.node_offset) << 22) |
                                        (static_cast<unsigned long long>(k) << 11) |
                                        static_cast<unsigned long long>(j - 1);
-        record_failure(a.err, key, seq, 1);
+        record_failure(a.err, key, seq, 1, 1, a.v, a.v);
       }
       if (bad || j == k) {
         a.v[node] = v;
@@ -149,17 +149,19 @@ template <class M>
 __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(ReactArgs a) {
   extern __shared__ __align__(16) unsigned shist[];
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 16 + 15] = gtimer();  // block start
-  {
-    const long long seq = (*a.clock + a.step_off) * a.evs + a.ev;
-    if (earlier_failure(a.err, seq)) return;  // uniform across the grid
+  // A strictly earlier event failed: skip the work (uniform across the grid,
+  // common.cuh earlier_failure) but still arrive on `done` below, so the
+  // self-resetting work counter is reset by the last block either way.
+  const bool skip = earlier_failure(a.err, (*a.clock + a.step_off) * a.evs + a.ev);
+  if (!skip) {
+    for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x) shist[i] = 0u;
+    if constexpr (requires { M::block_init(); }) M::block_init();  // e.g. the exp table (fastmath.cuh)
+    __syncthreads();
+    react_body<M>(a, shist);
+    __syncthreads();
+    for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x)
+      if (shist[i]) atomicAdd(a.khist + i, static_cast<unsigned long long>(shist[i]));
   }
-  for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x) shist[i] = 0u;
-  if constexpr (requires { M::block_init(); }) M::block_init();  // e.g. the exp table (fastmath.cuh)
-  __syncthreads();
-  react_body<M>(a, shist);
-  __syncthreads();
-  for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x)
-    if (shist[i]) atomicAdd(a.khist + i, static_cast<unsigned long long>(shist[i]));
   if (a.trace && threadIdx.x == 0) a.trace[blockIdx.x * 16] = gtimer();  // block's reaction done
   if (threadIdx.x == 0) {
     // acq_rel: this block's claims happen before its arrival; the last block

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "fastmath.cuh"
+#include "launch.h"
 #include "react.cuh"
 
 namespace cwg {
@@ -576,11 +577,9 @@ template <class M>
 static cudaError_t launch_react_t(const ReactArgs& a, int grid, cudaStream_t st) {
   const size_t smem = smem_bytes<M>(a.khist_len);
   if (smem > 48 * 1024) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(react_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    const cudaError_t e = ensure_dyn_smem(react_kernel<M>, 200 * 1024, attr_done);
+    if (e != cudaSuccess) return e;
   }
   react_kernel<M><<<grid, M::kThreads, smem, st>>>(a);
   return cudaGetLastError();

@@ -422,3 +422,9 @@ extern "C" double cwg_struct3d_tables(const cwg_struct3d* s, double* coef, doubl
       }
   return std::isfinite(min_ratio) ? 0.9 * min_ratio : -1.0;
 }
+
+extern "C" void cwg_uniform_mt64(uint64_t seed, int64_t n, double lo, double hi, double* out) {
+  std::mt19937_64 gen(seed);
+  const double w = hi - lo;
+  for (int64_t i = 0; i < n; ++i) out[i] = lo + w * (static_cast<double>(gen() >> 11) * 0x1.0p-53);
+}

@@ -14,7 +14,16 @@ from typing import List, Optional
 
 import numpy as np
 
+from . import _lib as L
 from . import api
+
+
+def uniform_mt64(seed: int, n: int, lo: float, hi: float) -> np.ndarray:
+    """n seeded uniform draws in [lo, hi) from std::mt19937_64(seed) (the reference's RNG, mesh.cpp:112):
+    lo + (hi - lo) * ((x >> 11) * 2^-53) (cwgpu_setup.h cwg_uniform_mt64)."""
+    out = np.zeros(int(n))
+    L.lib().cwg_uniform_mt64(int(seed), int(n), float(lo), float(hi), L.dp(out))
+    return out
 
 
 @dataclass
@@ -82,8 +91,8 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
     """Pathological sheet (EXTENSION; parity pinned to the C oracle only).
 
     Central scar (r = 1 cm): elements with D = 0 and passive nodes; border
-    zone (1-1.5 cm): D x 0.5 and per-node GKr x U(0.8, 1.2) drawn with
-    numpy's PCG64(seed). S1: left edge x <= 0 at t = 0 (2x the line
+    zone (1-1.5 cm): D x 0.5 and per-node GKr x U(0.8, 1.2) drawn from
+    std::mt19937_64(seed) in ascending node order (uniform_mt64). S1: left edge x <= 0 at t = 0 (2x the line
     threshold, as C1); S2: quadrant [0, size/2]^2 at t = 300 ms with
     amplitude_s2 = 80 mV/ms -- a whole region has no diffusive drain, and at
     the S1 amplitude its corner node diverges under forward Euler (in the
@@ -99,10 +108,9 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
     sh = api.Sheet(size, size, h, 0.0, d0_myocyte=0.001, rho=1.0, elem_scale=scale)
     rn = np.hypot(sh.coords[:, 0] - c, sh.coords[:, 1] - c)
     model_of_node = np.where(rn < 1.0 - 1e-9, 1, 0).astype(np.uint8)  # strictly inside the scar: passive
-    rng = np.random.Generator(np.random.PCG64(seed))
     gkr = np.ones(sh.n)
     bz = (rn >= 1.0) & (rn <= 1.5)
-    gkr[bz] = rng.uniform(0.8, 1.2, int(bz.sum()))
+    gkr[bz] = uniform_mt64(seed, int(bz.sum()), 0.8, 1.2)  # border-zone nodes in ascending index
     s1 = sh.select("x_le", value=0.0)
     s2 = sh.select("rectangle", x0=0.0, x1=c, y0=0.0, y1=c)
     cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
@@ -112,17 +120,23 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
                    notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)")
 
 
+def site_centers(lx, ly, n_sites, seed):
+    """Endocardial stimulus sites of config 5: 2 n_sites draws of std::mt19937_64(seed), site k at
+    (lx * u[2k], ly * u[2k+1])."""
+    u = uniform_mt64(seed, 2 * n_sites, 0.0, 1.0)
+    return [(lx * u[2 * k], ly * u[2 * k + 1]) for k in range(n_sites)]
+
+
 def slab(lx, ly, lz, h, model="ohara2011-epi", t_end=10.0, k0_down=3, amplitude=150.0, stim="face", seed=2011,
          n_sites=16, site_radius=0.1, d_long=0.0012, rho=0.25) -> Problem:
     """3D slab (EXTENSION; oracle-pinned). Fibres rotate +60 -> -60 deg from endocardium (z = 0) to
     epicardium, D_l:D_t = 4:1 (rho 0.25), D_l = 0.0012 cm^2/ms (as C2). Stimulus on z = 0: the whole
-    face ("face", config 4) or n_sites seeded random discs ("sites", config 5; numpy PCG64(seed))."""
+    face ("face", config 4) or n_sites seeded random discs ("sites", config 5; site_centers)."""
     sl = api.Slab3D(lx, ly, lz, h, d_long=d_long, rho=rho)
     if stim == "face":
         nodes = sl.face_z0()
     else:
-        rng = np.random.Generator(np.random.PCG64(seed))
-        centers = list(zip(rng.uniform(0.0, lx, n_sites), rng.uniform(0.0, ly, n_sites)))
+        centers = site_centers(lx, ly, n_sites, seed)
         nodes = sl.discs_z0(centers, site_radius)
     cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
     probes = [sl.nearest(lx / 2, ly / 2, 0.0), sl.nearest(lx / 2, ly / 2, lz), sl.nearest(lx, ly, lz / 2)]
@@ -138,3 +152,10 @@ def c4(t_end=500.0, **kw) -> Problem:
 def c5(t_end=5.0, **kw) -> Problem:
     """BASELINE configs[4]: 10x10x2 cm, h = 0.01 (1001x1001x201 = 201M nodes), 16 random endocardial sites."""
     return slab(10.0, 10.0, 2.0, 0.01, t_end=t_end, stim="sites", **kw)
+
+
+def c5_subslab(ly=0.2, t_end=5.0, n_sites=16, **kw) -> Problem:
+    """A full-cross-section y-sub-slab of config 5 for parity at BASELINE resolution: 10 x ly x 2 cm at
+    h = 0.01 (1001 x (ly/h + 1) x 201 nodes; ly = 0.2 -> 4.2M nodes), same fibres, conductivities and
+    stimulus kind (n_sites seeded endocardial discs over its own face)."""
+    return slab(10.0, ly, 2.0, 0.01, t_end=t_end, stim="sites", n_sites=n_sites, **kw)
