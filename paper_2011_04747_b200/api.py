@@ -780,8 +780,12 @@ def _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog
 
 
 def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeConfig, device=0,
-                   integrator: StrangIntegrator = None) -> SimulationResult:
-    """run_simulation (splitting.cpp:219-294) on the GPU; raises InstabilityError like the reference."""
+                   integrator: StrangIntegrator = None, final_state_out: NodeStateArray = None) -> SimulationResult:
+    """run_simulation (splitting.cpp:219-294) on the GPU; raises InstabilityError like the reference.
+
+    The reference takes `state` by value and moves it into result.final_state; here the caller's arrays
+    are left untouched and the final state is downloaded into fresh arrays -- or into `final_state_out`
+    (e.g. pinned host buffers a caller reuses across runs), which is then returned as final_state."""
     import time
     t0 = time.perf_counter()
     integ = integrator or StrangIntegrator(setup, cfg, model_of_node=state.model_of_node, device=device)
@@ -796,7 +800,13 @@ def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeCon
         integ.run_sync()
     else:
         _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog, t0)
-    final = state.copy()
+    if final_state_out is not None:
+        final = final_state_out
+    elif integ.world > 1:
+        final = state.copy()  # this rank downloads its own y-slab only
+    else:  # every element is overwritten by the download: no copy of the input
+        final = NodeStateArray(state.n_nodes, state.stride, np.empty_like(state.v), np.empty_like(state.s),
+                               np.empty_like(state.last_dvdt), state.model_of_node.copy())
     integ.download(final)
     t, v = integ.traces()
     lat, apd = integ.maps()

@@ -9,6 +9,9 @@ namespace cwg {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr unsigned long long kNoError = ~0ull;
 constexpr long long kNoSeq = 0x7fffffffffffffffll;  // ErrRec::seq before any failure
+// doubles of slack after every V buffer: the 3D diffusion kernel's 16-byte
+// aligned row copies may run up to 2 nodes past a row (diffuse.cu S3R_COPY)
+constexpr long long kVPad = 128;
 
 // Error record, one per context. key = node << 22 | k << 11 | j (reaction) or
 // node << 22 (diffusion); atomicMin gives the reference's "lowest node"

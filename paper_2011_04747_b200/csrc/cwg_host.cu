@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
+#include <chrono>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -914,7 +915,22 @@ void configure_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int
   c->G = G <= 200 ? G : 0;
 }
 
+// CWG_TRACE_CREATE=1: per-phase wall times of cwg_create on stderr (fixed-cost analysis of the e2e path)
+struct PhaseTrace {
+  bool on = getenv("CWG_TRACE_CREATE") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), last = t0;
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[cwg_create] %-22s %8.3f ms (total %8.3f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
+
 void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
+  PhaseTrace tr;
   validation(p_in != nullptr, "integrator: empty problem");
   cwg_problem pc = *p_in;
   if (pc.op_kind == CWG_OP_AUTO) infer_grid(&pc);
@@ -929,10 +945,11 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
 
   c->device = p->device;
   CUDA_TRY(cudaSetDevice(c->device));
-  cudaDeviceProp prop{};
-  CUDA_TRY(cudaGetDeviceProperties(&prop, c->device));
-  if (prop.major < 10) throw Fail{CWG_ECUDA, "cwgpu needs an sm_100 (Blackwell) device"};
-  c->num_sms = prop.multiProcessorCount;
+  // two attribute queries (cudaGetDeviceProperties fills ~100 fields and costs milliseconds per context)
+  int major = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device));
+  if (major < 10) throw Fail{CWG_ECUDA, "cwgpu needs an sm_100 (Blackwell) device"};
+  CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device));
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
@@ -948,6 +965,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->stride = std::max(c->stride, state_count(c->model_kind[m]));
   }
   configure_scheme(c, p->scheme, p->dt_ms, p->t_end_ms, p->k0_up, p->k0_down, p->strict_substeps);
+  tr.mark("device+scheme");
 
   // ---- partition and operator layout
   std::vector<double> s3_coef, s3_mass;
@@ -1014,17 +1032,21 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->node_offset = 0;
   }
   c->n_alloc = c->n_own + 2 * c->halo;
+  tr.mark("partition");
 
   // ---- device state (SoA, pitch padded to 32 nodes = 256 B)
   c->pitch = (c->n_alloc + 31) / 32 * 32;
-  c->d_v[0] = dev_alloc<double>(c->n_alloc);
-  c->d_v[1] = dev_alloc<double>(c->n_alloc);
-  CUDA_TRY(cudaMemset(c->d_v[0], 0, c->n_alloc * sizeof(double)));
-  CUDA_TRY(cudaMemset(c->d_v[1], 0, c->n_alloc * sizeof(double)));
+  // (+ kVPad: slack for the 3D kernel's aligned row copies; the halo rows /
+  // planes stay zero unless a neighbour rank writes them)
+  c->d_v[0] = dev_alloc<double>(c->n_alloc + kVPad);
+  c->d_v[1] = dev_alloc<double>(c->n_alloc + kVPad);
+  CUDA_TRY(cudaMemset(c->d_v[0], 0, (c->n_alloc + kVPad) * sizeof(double)));
+  CUDA_TRY(cudaMemset(c->d_v[1], 0, (c->n_alloc + kVPad) * sizeof(double)));
   c->d_S = dev_alloc<double>(static_cast<size_t>(c->pitch) * c->stride);
   c->d_last = dev_alloc<double>(c->n_alloc);
   CUDA_TRY(cudaMemset(c->d_S, 0, static_cast<size_t>(c->pitch) * c->stride * sizeof(double)));
   CUDA_TRY(cudaMemset(c->d_last, 0, c->n_alloc * sizeof(double)));
+  tr.mark("state alloc");
 
   // ---- operator upload
   if (kind == CWG_OP_STRUCT3D) {
@@ -1072,6 +1094,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->d_val = upload(p->val + p0, static_cast<size_t>(p1 - p0));
   }
 
+  tr.mark("before models: per-model node bins over owned nodes");
   // ---- models: per-model node bins over owned nodes (local indices)
   validation(p->model_of_node != nullptr, "integrator: model_of_node missing");
   validation(c->n_alloc < (1ll << 31), "integrator: more than 2^31 local nodes per device (use more ranks)");
@@ -1111,6 +1134,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     c->d_gkr = upload(g.data(), g.size());
   }
 
+  tr.mark("before stimulus");
   // ---- stimulus (ProtocolIndex, flattened to the local slab)
   if (p->n_stim > 0) {
     validation(p->stim_node_ptr && p->stim_ids && p->stim_t_start && p->stim_duration && p->stim_amplitude &&
@@ -1137,6 +1161,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     }
   }
 
+  tr.mark("before bookkeeping");
   // ---- bookkeeping
   c->d_err = dev_alloc<ErrRec>(1);
   c->d_clock = dev_alloc<long long>(1);
@@ -1147,6 +1172,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->clock_at = 0;
   CUDA_TRY(cudaMemset(c->d_khist, 0, c->khist_len * sizeof(unsigned long long)));
 
+  tr.mark("before recording");
   // ---- recording
   c->lat_threshold = p->lat_threshold_mv;
   c->n_probes = p->n_probes;
@@ -1180,6 +1206,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     NCCL_TRY(g_nccl.init(&c->comm, c->world, id, c->rank));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  tr.mark("recording+comm");
 }
 
 thread_local std::string g_last_error;

@@ -657,6 +657,316 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
 }
 
 // ---------------------------------------------------------------------------
+// Structured 3D slab, register-blocked (default). The row sum is 27 DMUL +
+// 27 DADD in a fixed order (bit-exactness: no FMA, no reassociation), so at
+// 16 B of V traffic per node-substep the kernel is FP64-pipe bound unless
+// every V value and coefficient it multiplies is already in a register:
+//   * a thread owns two x-adjacent nodes (x, x+1) of one z row and marches
+//     over y; both have the same node class (x-interior, by = 1, iz), whose
+//     27 coefficients + dt/m stay in registers for the whole march (reloaded
+//     only on the slab's first / last global y plane);
+//   * the 3 x 3 x 4 window of V (planes y-1, y, y+1; rows z-1..z+1; columns
+//     x-1..x+2) lives in registers; a plane step brings in the 12 values of
+//     plane y+1 with 2-3 shared-memory loads per row (4.5-6 per node instead
+//     of 27 loads + 27 coefficient reads);
+//   * plane rows arrive in shared memory by 1D bulk copies (cp.async.bulk,
+//     the TMA engine: one instruction per 66-node row, no per-element
+//     address math), NS - 2 planes ahead of use, through a full/empty
+//     mbarrier ring -- no block-wide barrier: a warp waits only for the rows
+//     it reads and the slot it refills. The V rows are not 16-byte aligned
+//     (odd nx+1), so each copy starts at the aligned node at or below x0 - 1
+//     and moves 68 nodes; the row's shift (0/1) is known from the index
+//     parity, and the window read picks the matching load pattern;
+//   * absent neighbours (z faces, y faces) meet a zero coefficient and a
+//     zero V (rows outside the slab in z are zeroed once; the halo planes
+//     beyond the global y faces are zero-initialised memory that nothing
+//     writes): 0 * 0 adds +0, which leaves the sum (never -0: it starts at
+//     +0) unchanged -- the same bits as skipping the term like fem.cpp;
+//   * the two x faces (x = 0, x = nx; other classes) are rows of their own:
+//     extra blocks of the same grid compute them one thread per node with
+//     the generic class lookup.
+// Warp w of a block owns row z0 + w; lane l owns x = xb + 2l, xb + 2l + 1.
+// ---------------------------------------------------------------------------
+constexpr int S3R_NS = 6;     // plane stages in the ring (lead NS - 2 planes)
+constexpr int S3R_RS = 72;    // doubles per staged row (a 68-node copy + padding)
+constexpr int S3R_COPY = 68;  // nodes per row copy (544 B, a multiple of 16)
+
+template <int W>
+struct S3R {
+  static constexpr int NT = 32 * W;
+  static constexpr int ROWS = W + 2;
+  static constexpr int STAGE = ROWS * S3R_RS;  // doubles per plane stage
+  static constexpr size_t smem = static_cast<size_t>(S3R_NS) * STAGE * sizeof(double) + 2 * S3R_NS * 8;
+};
+
+// Generic row (any class, presence tests): the x-face nodes and tiny slabs.
+__device__ __forceinline__ void s3_generic_node(const DiffArgs& a, const Struct3D& s, int ix, int iz, long long yl,
+                                                long long seq) {
+  const int nx1 = static_cast<int>(s.nx1), nz1 = static_cast<int>(s.nz1);
+  const int nx = nx1 - 1, nz = nz1 - 1;
+  const long long gy = s.row_begin + yl;
+  const int bx = ix == 0 ? 0 : (ix == nx ? 2 : 1);
+  const int by = gy == 0 ? 0 : (gy == s.ny1 - 1 ? 2 : 1);
+  const long long cls = (by * 3 + bx) * static_cast<long long>(nz1) + iz;
+  const double* cf = s.coef + cls * 27;
+  const long long i = (yl + 1) * s.plane + static_cast<long long>(iz) * nx1 + ix;
+  double acc = 0.0;
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+    if ((dy < 0 && by == 0) || (dy > 0 && by == 2)) continue;
+#pragma unroll
+    for (int dz = -1; dz <= 1; ++dz) {
+      if ((dz < 0 && iz == 0) || (dz > 0 && iz == nz)) continue;
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        if ((dx < 0 && bx == 0) || (dx > 0 && bx == 2)) continue;
+        acc += __ldg(cf + (dy + 1) * 9 + (dz + 1) * 3 + (dx + 1)) * a.vin[i + dy * s.plane + dz * nx1 + dx];
+      }
+    }
+  }
+  const double out = a.vin[i] - __ldg(s.cm + cls) * acc;
+  a.vout[i] = out;
+  if (!isfinite(out))
+    record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2, 1,
+                   a.vin, a.vout);
+}
+
+// One plane step of a thread's node pair: window planes (m, o, p) = (y-1, y,
+// y+1), each [3 rows z-1..z+1][4 cols x-1..x+2].
+__device__ __forceinline__ void s3r_pair(const double (&m)[12], const double (&o)[12], const double (&p)[12],
+                                         const double (&cf)[27], double cm, double& outA, double& outB) {
+  const double* pl[3] = {m, o, p};
+  double accA = 0.0, accB = 0.0;
+#pragma unroll
+  for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz)
+#pragma unroll
+      for (int dx = 0; dx < 3; ++dx) {
+        const double c = cf[dy * 9 + dz * 3 + dx];
+        accA += c * pl[dy][dz * 4 + dx];
+        accB += c * pl[dy][dz * 4 + dx + 1];
+      }
+  outA = o[4 + 1] - cm * accA;
+  outB = o[4 + 2] - cm * accB;
+}
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+template <int W>
+__global__ void __launch_bounds__(32 * W, 2)
+    diffuse_struct3d_rb(DiffArgs a, Struct3D s, int tiles_x, int tiles_z, int n_items, int ychunk,
+                        long long n_edge) {
+  using G = S3R<W>;
+  extern __shared__ __align__(128) double s3r_smem[];
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  if (earlier_failure(a.err, seq)) return;  // block-uniform: an earlier event failed, V stays where it stopped
+  const int nx1 = static_cast<int>(s.nx1), nz1 = static_cast<int>(s.nz1);
+  const int nx = nx1 - 1;
+  if (static_cast<int>(blockIdx.x) >= n_items) {
+    // x-face rows (x = 0 and x = nx), one thread per node
+    const long long per = static_cast<long long>(nz1) * s.planes;
+    for (long long e = (blockIdx.x - n_items) * static_cast<long long>(G::NT) + threadIdx.x; e < n_edge;
+         e += static_cast<long long>(gridDim.x - n_items) * G::NT) {
+      const int side = static_cast<int>(e / per);
+      const long long r = e - side * per;
+      const long long yl = r / nz1;
+      const int iz = static_cast<int>(r - yl * nz1);
+      s3_generic_node(a, s, side == 0 ? 0 : nx, iz, yl, seq);
+    }
+    return;
+  }
+  const int item = blockIdx.x;
+  const int tile = item % (tiles_x * tiles_z), ych = item / (tiles_x * tiles_z);
+  const int xb = 1 + (tile % tiles_x) * 64;  // first node of the tile (x-interior rows start at x = 1)
+  const int z0 = (tile / tiles_x) * W;
+  const int planes = static_cast<int>(s.planes);
+  const int yb = ych * ychunk;
+  const int ye = yb + ychunk < planes ? yb + ychunk : planes;
+  if (ye <= yb) return;  // an empty trailing chunk (block-uniform)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int xA = xb + 2 * lane, z = z0 + w;
+  const bool okA = xA <= nx - 1 && z < nz1, okB = xA + 1 <= nx - 1 && z < nz1;
+  const int zc = z < nz1 ? z : nz1 - 1;  // clamped row for the coefficient reads of idle threads
+  const long long plane = s.plane;
+  const int gy0 = static_cast<int>(s.row_begin), gny = static_cast<int>(s.ny1);
+  const unsigned long long* bars = reinterpret_cast<const unsigned long long*>(s3r_smem + S3R_NS * G::STAGE);
+  const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
+  const unsigned empty0 = full0 + 8 * S3R_NS;
+  const unsigned smem0 = static_cast<unsigned>(__cvta_generic_to_shared(s3r_smem));
+
+  // rows of the stage this warp copies: its own row (stage row w + 1) and, for
+  // the first / last warp, the halo row below / above the tile; rows outside
+  // the slab in z are never copied (zeroed once below)
+  const int rA = w + 1, rB = w == 0 ? 0 : (w == W - 1 ? W + 1 : -1);
+  const bool vA = z0 - 1 + rA < nz1;                           // z0 - 1 + rA = z >= 0 always
+  const bool vB = rB >= 0 && z0 - 1 + rB >= 0 && z0 - 1 + rB < nz1;
+  const unsigned bytes_w = (vA ? S3R_COPY * 8u : 0u) + (vB ? S3R_COPY * 8u : 0u);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < S3R_NS; ++k) {
+      mbar_init(full0 + 8 * k, W);   // one arrival (with its bytes) per warp
+      mbar_init(empty0 + 8 * k, W);  // one arrival per warp once it has read the slot
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int t = threadIdx.x; t < S3R_NS * G::ROWS * S3R_RS; t += G::NT) {
+    const int r = (t / S3R_RS) % G::ROWS, zz = z0 - 1 + r;
+    if (zz < 0 || zz >= nz1) s3r_smem[t] = 0.0;
+  }
+  __syncthreads();
+
+  // plane P_k = yb - 1 + k -> slot k % NS; lane 0 of every warp arms the full
+  // barrier with its bytes and copies its rows (after the slot's previous
+  // plane was read by every warp)
+  auto issue = [&](int k) {
+    if (lane != 0) return;
+    const int slot = k % S3R_NS;
+    if (k >= S3R_NS) {
+      const unsigned par = static_cast<unsigned>((k / S3R_NS - 1) & 1);
+      mbar_wait(empty0 + 8 * slot, par);
+    }
+    mbar_arrive_tx(full0 + 8 * slot, bytes_w);
+    const long long yl = yb - 1 + k;
+    const long long pbase = (yl + 1) * plane + xb - 1;
+    auto copy_row = [&](int r) {
+      const long long idx = pbase + static_cast<long long>(z0 - 1 + r) * nx1;
+      const unsigned dst = smem0 + static_cast<unsigned>((slot * G::STAGE + r * S3R_RS) * 8);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+          "l"(a.vin + (idx & ~1ll)), "r"(S3R_COPY * 8), "r"(full0 + 8 * slot)
+          : "memory");
+    };
+    if (vA) copy_row(rA);
+    if (vB) copy_row(rB);
+  };
+  // this warp's 12 window values of plane P_k; row r's first copied node is
+  // x0 - 1 - sh with sh the parity of the row start's index
+  // parity of row w + dz's first node index in plane P_0; P_k flips it when k * plane is odd
+  int sh0 = 0;
+#pragma unroll
+  for (int dz = 0; dz < 3; ++dz)
+    sh0 |= static_cast<int>((static_cast<long long>(yb) * plane + xb - 1 + static_cast<long long>(z0 - 1 + w + dz) * nx1) &
+                            1) << dz;
+  const int podd = static_cast<int>(plane & 1);
+  auto window = [&](int k, double (&wv)[12]) {
+    const int slot = k % S3R_NS;
+    mbar_wait(full0 + 8 * slot, static_cast<unsigned>((k / S3R_NS) & 1));
+    const int shk = sh0 ^ (((k & podd) != 0) ? 7 : 0);
+#pragma unroll
+    for (int dz = 0; dz < 3; ++dz) {
+      const int r = w + dz;
+      const int sh = (shk >> dz) & 1;
+      const double* rp = s3r_smem + slot * G::STAGE + r * S3R_RS + 2 * lane;  // col c <-> node x0 - 1 - sh + c
+      if (sh) {  // x-1 at col 2l + 1
+        const double2 pr = *reinterpret_cast<const double2*>(rp + 2);
+        wv[dz * 4 + 0] = rp[1];
+        wv[dz * 4 + 1] = pr.x;
+        wv[dz * 4 + 2] = pr.y;
+        wv[dz * 4 + 3] = rp[4];
+      } else {  // x-1 at col 2l
+        const double2 p0 = *reinterpret_cast<const double2*>(rp);
+        const double2 p1 = *reinterpret_cast<const double2*>(rp + 2);
+        wv[dz * 4 + 0] = p0.x;
+        wv[dz * 4 + 1] = p0.y;
+        wv[dz * 4 + 2] = p1.x;
+        wv[dz * 4 + 3] = p1.y;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * slot);
+  };
+  auto load_coef = [&](int by, double (&cf)[27], double& cm) {
+    const long long cls = (by * 3 + 1) * static_cast<long long>(nz1) + zc;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) cf[q] = __ldg(s.coef + cls * 27 + q);
+    cm = __ldg(s.cm + cls);
+  };
+
+  const int n = ye - yb;
+  const int last_k = (ye < planes ? ye : planes) - (yb - 1);  // planes P_0 .. P_last_k are needed
+  double cf[27], cm;
+  load_coef(1, cf, cm);
+  for (int k = 0; k < S3R_NS && k <= last_k; ++k) issue(k);
+  double P0[12], P1[12], P2[12];
+  window(0, P0);
+  window(1, P1);
+  double* outp = a.vout + static_cast<long long>(yb + 1) * plane + static_cast<long long>(zc) * nx1 + xA;
+  const unsigned long long key0 =
+      static_cast<unsigned long long>(static_cast<long long>(yb) * plane + static_cast<long long>(zc) * nx1 + xA +
+                                      s.row_begin * plane);
+  // plane step i: output plane y = yb + i from (m, o, p); p <- P_{i+2}
+  auto step = [&](int i, double (&m)[12], double (&o)[12], double (&p)[12]) {
+    window(i + 2, p);
+    if (i + S3R_NS <= last_k) issue(i + S3R_NS);  // into the slot of P_i (read by every warp at step i-2)
+    const int gy = gy0 + yb + i;
+    const bool yface = gy == 0 || gy == gny - 1;
+    if (yface) load_coef(gy == 0 ? 0 : 2, cf, cm);
+    double oA, oB;
+    s3r_pair(m, o, p, cf, cm, oA, oB);
+    if (yface) load_coef(1, cf, cm);
+    if (okA) outp[0] = oA;
+    if (okB) outp[1] = oB;
+    if ((okA && !isfinite(oA)) || (okB && !isfinite(oB))) {
+      const unsigned long long k = key0 + static_cast<unsigned long long>(i) * plane;
+      if (okA && !isfinite(oA)) record_failure(a.err, k << 22, seq, 2, 1, a.vin, a.vout);
+      if (okB && !isfinite(oB)) record_failure(a.err, (k + 1) << 22, seq, 2, 1, a.vin, a.vout);
+    }
+    outp += plane;
+  };
+  int i = 0;
+  for (; i + 3 <= n; i += 3) {
+    step(i, P0, P1, P2);
+    step(i + 1, P1, P2, P0);
+    step(i + 2, P2, P0, P1);
+  }
+  if (i < n) step(i, P0, P1, P2);
+  if (i + 1 < n) step(i + 1, P1, P2, P0);
+  // every copy this block issued has been waited for (window of P_{n+1} = the last issued plane)
+}
+
+template <int W>
+static cudaError_t launch_s3r(const DiffArgs& a, const Struct3D& s, int num_sms, cudaStream_t st) {
+  using G = S3R<W>;
+  static std::atomic<uint64_t> attr_done{0};
+  cudaError_t e = ensure_dyn_smem(diffuse_struct3d_rb<W>, static_cast<int>(G::smem), attr_done);
+  if (e != cudaSuccess) return e;
+  const long long nxi = s.nx1 - 2;  // x-interior nodes 1 .. nx-1
+  const int tiles_x = nxi > 0 ? static_cast<int>((nxi + 63) / 64) : 0;
+  const int tiles_z = static_cast<int>((s.nz1 + W - 1) / W);
+  const long long tiles = static_cast<long long>(tiles_x) * tiles_z;
+  // y chunks: whole waves of 2 blocks per SM, chunks of >= 8 planes
+  const long long slots = 2ll * num_sms;
+  int nch = 1;
+  double best = 1e30;
+  for (int c = 1; c <= 64; ++c) {
+    if (c > 1 && (s.planes + c - 1) / c < 8) break;
+    const long long items = tiles * c;
+    const double waves = static_cast<double>((items + slots - 1) / slots);
+    const double cost = waves * static_cast<double>((s.planes + c - 1) / c) + 3.0 * waves;  // + pipeline fill
+    if (cost < best - 1e-9) {
+      best = cost;
+      nch = c;
+    }
+  }
+  const int ychunk = static_cast<int>((s.planes + nch - 1) / nch);
+  const int n_items = static_cast<int>(tiles * nch);
+  const long long n_edge = 2ll * s.nz1 * s.planes;
+  const int edge_blocks = static_cast<int>(std::min<long long>((n_edge + G::NT - 1) / G::NT, 2ll * num_sms));
+  if (n_items + edge_blocks == 0) return cudaSuccess;
+  diffuse_struct3d_rb<W><<<n_items + edge_blocks, G::NT, G::smem, st>>>(a, s, tiles_x, tiles_z, n_items, ychunk,
+                                                                         n_edge);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
 // Generic CSR (fem.cpp:201-206), one thread per row, ascending columns.
 // cols are local indices into vin; row i (owned) lives at vin[halo + i].
 // ---------------------------------------------------------------------------
@@ -840,7 +1150,19 @@ cudaError_t launch_diffuse_stencil2d(const DiffArgs& a, const Stencil2D& s, int 
 // [4, 16] that still gives >= 4 waves of resident blocks (C4: 4, C5: 16;
 // measured C4 0.140 / 0.153 / 0.163 ms per step at 4 / 8 / 16, C5 flat).
 // CWG_S3_YCHUNK overrides for experiments.
-cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s_in, int num_sms, cudaStream_t st) {
+static cudaError_t launch_diffuse_struct3d_ring(const DiffArgs& a, const Struct3D& s_in, int num_sms, cudaStream_t st);
+
+// Default: the register-blocked kernel; CWG_S3_KERNEL=0 selects the shared-memory ring kernel (A/B runs).
+cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int num_sms, cudaStream_t st) {
+  static const int which = [] {
+    const char* e = getenv("CWG_S3_KERNEL");
+    return e ? atoi(e) : 1;
+  }();
+  if (which == 0 || s.nx1 < 2 || s.nz1 < 2) return launch_diffuse_struct3d_ring(a, s, num_sms, st);
+  return launch_s3r<6>(a, s, num_sms, st);
+}
+
+static cudaError_t launch_diffuse_struct3d_ring(const DiffArgs& a, const Struct3D& s_in, int num_sms, cudaStream_t st) {
   static int capacity = 0;
   if (capacity == 0) {
     int per_sm = 0;

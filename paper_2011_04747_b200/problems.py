@@ -87,16 +87,26 @@ def c2(model="ohara2011-epi", t_end=500.0, k0_down=3, amplitude=C2_AMPLITUDE, ra
     return Problem("C2", sh, [model], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, amplitude, None)], cfg, probes)
 
 
-def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size=5.0, amplitude_s2=80.0) -> Problem:
+# C3 stimuli by the reference's rule, 2 x diastolic_threshold (stimulus.cpp:115-157) of each stimulus on the
+# C3 grid (tools/threshold_c3.py, searched on the device, window 200 ms; profiles/r02_thresholds.txt):
+#   S1: left-edge strip x <= 0.05 cm: 46.0 mV/ms at h = 0.005 and at h = 0.01 -> 92 mV/ms (a single node
+#       line at h = 0.005 does not propagate even at the search's 1000 mV/ms cap: too thin a source);
+#   S2: quadrant [0, 2.5]^2 cm: 35.0 mV/ms (h = 0.01) -> 70 mV/ms.
+C3_S1_AMPLITUDE = 92.0
+C3_S1_STRIP = 0.05
+C3_S2_AMPLITUDE = 70.0
+
+
+def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C3_S1_AMPLITUDE, h=0.005, size=5.0,
+       amplitude_s2=C3_S2_AMPLITUDE) -> Problem:
     """Pathological sheet (EXTENSION; parity pinned to the C oracle only).
 
     Central scar (r = 1 cm): elements with D = 0 and passive nodes; border
     zone (1-1.5 cm): D x 0.5 and per-node GKr x U(0.8, 1.2) drawn from
-    std::mt19937_64(seed) in ascending node order (uniform_mt64). S1: left edge x <= 0 at t = 0 (2x the line
-    threshold, as C1); S2: quadrant [0, size/2]^2 at t = 300 ms with
-    amplitude_s2 = 80 mV/ms -- a whole region has no diffusive drain, and at
-    the S1 amplitude its corner node diverges under forward Euler (in the
-    oracle as on the GPU: node 0, t = 300.36 ms).
+    std::mt19937_64(seed) in ascending node order (uniform_mt64). S1: left-
+    edge strip x <= 0.05 cm at t = 0; S2: quadrant [0, size/2]^2 at t = 300
+    ms (cross-field to the S1 wave); both 1 ms at 2 x their diastolic
+    threshold on this grid (constants above).
     """
     nx = int(round(size / h))
     c = size / 2.0
@@ -111,7 +121,7 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C1_AMPLITUDE, h=0.005, size
     gkr = np.ones(sh.n)
     bz = (rn >= 1.0) & (rn <= 1.5)
     gkr[bz] = uniform_mt64(seed, int(bz.sum()), 0.8, 1.2)  # border-zone nodes in ascending index
-    s1 = sh.select("x_le", value=0.0)
+    s1 = sh.select("x_le", value=C3_S1_STRIP)
     s2 = sh.select("rectangle", x0=0.0, x1=c, y0=0.0, y1=c)
     cfg = api.SchemeConfig(scheme=api.Scheme.DAETI, dt_ms=0.1, t_end_ms=t_end, k0_up=5, k0_down=k0_down)
     probes = [sh.nearest(0.5, c), sh.nearest(c, 0.5), sh.nearest(size - 0.5, c)]

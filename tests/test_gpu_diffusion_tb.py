@@ -115,3 +115,70 @@ def test_set_scheme_refreshes_fused_coefficients():
     assert np.array_equal(r.final_state.v, fresh.final_state.v)
     o = oracle_run(p, dt=0.2, t_end=3.0)
     assert np.array_equal(fresh.final_state.v, o["v"])
+
+
+@pytest.mark.parametrize("where", ["interior", "tile_corner", "edge"])
+def test_state_after_fused_failure_matches_oracle(where):
+    """After an InstabilityError the state is where the reference leaves it: V = the failing sub-step's
+    output (splitting.cpp:162-166 swap, then throw), not the end of the fused launch. StrangIntegrator
+    .advance downloads the state on an instability; the oracle's Integrator holds its state at the throw."""
+    import orapy
+    import paper_2011_04747_b200 as cw
+    from helpers import csr_of
+    p = _problem(1.3, 0.7, 0.4, t_end=3.0)
+    w = p.sheet.nx1
+    x, y = {"interior": (40, 30), "tile_corner": (63, 16), "edge": (0, 55)}[where]
+    node = y * w + x
+    n_steps = 10
+    st = p.initial_state()
+    st.v[node] = np.nan
+    integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=p.model_of_node)
+    try:
+        with pytest.raises(cw.InstabilityError):
+            integ.advance(st, 0.0, 0, n_steps)
+    finally:
+        integ.close()
+    it = orapy.Integrator(csr_of(p), p.sheet.op.dt_s, p.models, p.model_of_node, p.stimuli, dt=0.3,
+                          k0_up=p.cfg.k0_up, k0_down=p.cfg.k0_down)
+    it.v[node] = np.nan
+    with pytest.raises(orapy.OracleInstability):
+        it.advance(0.0, 0, n_steps)
+    assert np.array_equal(st.v, it.v, equal_nan=True)
+    assert np.array_equal(np.asarray(st.s).reshape(p.n, -1), it.s)
+
+
+def test_state_after_reaction_failure_matches_oracle():
+    """The C1 abort fixture (ORd-epi, paper k0, 592 mV/ms: InstabilityError at node 16, t = 2.04 ms): the
+    reaction pass finishes every node and the diffusion that would follow is skipped, so the downloaded V
+    equals the oracle's at the throw (tolerance parity for ORd; the failing node non-finite in both)."""
+    import orapy
+    import paper_2011_04747_b200 as cw
+    from helpers import csr_of
+    from paper_2011_04747_b200 import problems
+    p = problems.c1(t_end=4.0, k0_down=1)
+    n_steps = 40
+    st = p.initial_state()
+    integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=p.model_of_node)
+    it = orapy.Integrator(csr_of(p), p.sheet.op.dt_s, p.models, p.model_of_node, p.stimuli, dt=0.1,
+                          k0_up=p.cfg.k0_up, k0_down=p.cfg.k0_down)
+    try:
+        for step in range(n_steps):
+            try:
+                integ.advance(st, step * 0.1, step, n_steps)
+            except cw.InstabilityError as e:
+                with pytest.raises(orapy.OracleInstability) as eo:
+                    it.advance(step * 0.1, step, n_steps)
+                assert e.node_index == eo.value.node == 16
+                break
+            it.advance(step * 0.1, step, n_steps)
+        else:
+            pytest.fail("no instability")
+    finally:
+        integ.close()
+    fin_g, fin_o = np.isfinite(st.v), np.isfinite(it.v)
+    assert np.array_equal(fin_g, fin_o)
+    # paper k0 at dt 0.1 runs ORd forward Euler past its stability limit (SURVEY.md s0), which amplifies
+    # rounding differences by orders of magnitude in the aborting step (measured ~2e-4 mV next to the
+    # diverging node, ~1e-7 mV elsewhere); a wrongly restored state (one diffusion sub-step more or less)
+    # moves V near the stimulated edge by whole mV.
+    assert np.max(np.abs(st.v[fin_g] - it.v[fin_o])) <= 1e-3

@@ -12,6 +12,7 @@ rep = sys.argv[1]
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 d = dict(zip(rows[0], rows[2]))
+units = dict(zip(rows[0], rows[1]))  # ncu's units row (e.g. "Mbyte", "usecond", "%"): printed with every value
 print(f"kernel: {d.get('Kernel Name')}")
 for k in ["gpu__time_duration.sum", "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
           "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
@@ -21,7 +22,8 @@ for k in ["gpu__time_duration.sum", "launch__registers_per_thread", "launch__blo
           "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_active",
           "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed"]:
     if k in d:
-        print(f"  {k} = {d[k]}")
+        u = units.get(k, "")
+        print(f"  {k} = {d[k]}{' ' + u if u else ''}")
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))

@@ -17,8 +17,10 @@ import paper_2011_04747_b200 as cw  # noqa: E402
 h = float(sys.argv[1]) if len(sys.argv) > 1 else 0.005
 sh = cw.Sheet(5.0, 5.0, h, 0.0, d0_myocyte=0.001, rho=1.0)
 opts = cw.ThresholdOptions(window_ms=200.0)
-for name, nodes in (("S1 strip x<=0.05", sh.select("x_le", value=0.05)),
-                    ("S2 quadrant [0,2.5]^2", sh.select("rectangle", x0=0.0, x1=2.5, y0=0.0, y1=2.5))):
+which = sys.argv[2:] or ["S1", "S2"]
+cases = {"S1": ("S1 strip x<=0.05", lambda: sh.select("x_le", value=0.05)),
+         "S2": ("S2 quadrant [0,2.5]^2", lambda: sh.select("rectangle", x0=0.0, x1=2.5, y0=0.0, y1=2.5))}
+for name, nodes in ((cases[k][0], cases[k][1]()) for k in which):
     t0 = time.perf_counter()
     thr, probe = cw.diastolic_threshold(sh, cw.make_model("ohara2011-epi"), nodes, opts, return_probe=True)
     print(f"h={h} {name}: threshold {thr} mV/ms (2x = {2 * thr}), probe node {probe}, "
