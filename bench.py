@@ -61,7 +61,8 @@ DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt
 C1_AMPLITUDE = 592.0   # 2 x the reference's diastolic threshold on the C1 line (296 mV/ms)
 C2_AMPLITUDE = 100.0
 C2_RADIUS = 0.15
-SLAB_AMPLITUDE = 150.0  # C4/C5 endocardial stimulus, 1 ms
+SLAB_AMPLITUDE = 150.0  # C4 endocardial face stimulus, 1 ms
+C5_AMPLITUDE, C5_SITE_RADIUS = 450.0, 0.2  # C5 endocardial sites (problems.py C5_*)
 
 
 def host_cpu():
@@ -181,8 +182,10 @@ def build_problem(config, world, rank, scaling="strong"):
         # weak scaling: the slab grows in y with the number of ranks (same y extent per GPU)
         if config == "c4":
             return problems.slab(5.0, 5.0 * world, 1.0, 0.02, t_end=500.0)
-        return problems.slab(10.0, 10.0 * world, 2.0, 0.01, t_end=5.0 if world == 1 else 5.0, stim="sites",
-                             n_sites=16 * world)
+        if world == 1:
+            return problems.c5()
+        return problems.slab(10.0, 10.0 * world, 2.0, 0.01, t_end=5.0, stim="sites", n_sites=16 * world,
+                             amplitude=problems.C5_AMPLITUDE, site_radius=problems.C5_SITE_RADIUS)
     raise SystemExit(f"unknown config {config}")
 
 
@@ -222,10 +225,14 @@ def oracle_slab(config):
         x, y = ix * op.h, iy * op.h
         sel = np.zeros(ix.shape, bool)
         for k in range(16):
-            sel |= np.sqrt((x - 10.0 * u[2 * k]) ** 2 + (y - 10.0 * u[2 * k + 1]) ** 2) <= 0.1 + 1e-9
+            sel |= np.sqrt((x - 10.0 * u[2 * k]) ** 2 + (y - 10.0 * u[2 * k + 1]) ** 2) <= C5_SITE_RADIUS + 1e-9
         nodes = np.sort(op.index(ix[sel], iy[sel], 0))
         t_end = 5.0
     return op, nodes, t_end
+
+
+def slab_amplitude(config):
+    return SLAB_AMPLITUDE if config == "c4" else C5_AMPLITUDE
 
 
 def cpu_reference_steps(config, steps, warmup, budget_s, threads):
@@ -237,7 +244,8 @@ def cpu_reference_steps(config, steps, warmup, budget_s, threads):
         import orapy
         op, nodes, t_end = oracle_slab(config)
         it = orapy.Integrator(op, op.dt_s, ["ohara2011-epi"], np.zeros(op.n, np.uint8),
-                              [(nodes, 0.0, 1.0, SLAB_AMPLITUDE, None)], scheme="DAETI", dt=0.1, k0_up=5, k0_down=3)
+                              [(nodes, 0.0, 1.0, slab_amplitude(config), None)], scheme="DAETI", dt=0.1, k0_up=5,
+                              k0_down=3)
         n_total = int(round(t_end / 0.1))
         for st in range(warmup):
             it.advance(st * 0.1, st, n_total)

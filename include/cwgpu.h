@@ -233,6 +233,13 @@ int cwg_get_traces(cwg_ctx* ctx, double* t_ms, double* v /* [probe][sample] */);
 /* SimulationResult lat_map / apd90_map = ActivationDetector::lat / apd90
  * (postprocess.hpp:45-46, postprocess.cpp:68-90); this rank's slab */
 int cwg_get_maps(cwg_ctx* ctx, double* lat, uint8_t* lat_valid, double* apd90, uint8_t* apd_valid);
+/* The global SimulationResult::final_state (AoS, any stride >= the model
+ * list's) and lat_map / apd90_map (splitting.cpp:286-293) on EVERY rank of a
+ * y-slab run: each rank's owned slab is broadcast to all ranks over NCCL
+ * (world > 1); world == 1: the plain download. Arrays are global-size;
+ * any pointer may be NULL. Collective for world > 1 (call on all ranks). */
+int cwg_gather_result(cwg_ctx* ctx, double* v, double* s_aos, int stride, double* last_dvdt, double* lat,
+                      uint8_t* lat_valid, double* apd90, uint8_t* apd_valid);
 /* reaction / diffusion / recording device time (ms, CUDA events) of the last
  * cwg_advance calls (TimingBreakdown, splitting.hpp:57-62) */
 int cwg_get_timing(cwg_ctx* ctx, double* reaction_ms, double* diffusion_ms, double* recording_ms);

@@ -711,6 +711,16 @@ class StrangIntegrator:
         _check(L.lib().cwg_get_traces(self._h, L.dp(t), L.dp(v)))
         return t, v[: npb * ns].reshape(npb, ns)
 
+    def gather(self, state: NodeStateArray):
+        """The global final state and LAT/APD maps on every rank (cwg_gather_result; collective for world > 1):
+        returns (lat_map, apd90_map) and fills `state` (global arrays)."""
+        n = self.n
+        lat, apd = np.zeros(n), np.zeros(n)
+        lv, av = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        _check(L.lib().cwg_gather_result(self._h, L.dp(state.v), L.dp(state.s), state.stride, L.dp(state.last_dvdt),
+                                         L.dp(lat), lv.ctypes.data_as(L._u8p), L.dp(apd), av.ctypes.data_as(L._u8p)))
+        return ScalarMap(lat, lv.astype(bool)), ScalarMap(apd, av.astype(bool))
+
     def maps(self):
         n = self.info.n_local
         lat, apd = np.zeros(n), np.zeros(n)
@@ -802,14 +812,15 @@ def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeCon
         _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog, t0)
     if final_state_out is not None:
         final = final_state_out
-    elif integ.world > 1:
-        final = state.copy()  # this rank downloads its own y-slab only
-    else:  # every element is overwritten by the download: no copy of the input
+    else:  # every element is overwritten (all ranks' slabs gathered for world > 1): no copy of the input
         final = NodeStateArray(state.n_nodes, state.stride, np.empty_like(state.v), np.empty_like(state.s),
                                np.empty_like(state.last_dvdt), state.model_of_node.copy())
-    integ.download(final)
     t, v = integ.traces()
-    lat, apd = integ.maps()
+    if integ.world > 1:  # one global SimulationResult on every rank (splitting.cpp:286-293)
+        lat, apd = integ.gather(final)
+    else:
+        integ.download(final)
+        lat, apd = integ.maps()
     traces = [Trace(pr.node, pr.name, t.copy(), v[q].copy()) for q, pr in enumerate(setup.probes)]
     tb = TimingBreakdown(total_ms=(time.perf_counter() - t0) * 1e3)
     return SimulationResult(traces, lat, apd, tb, integ.k_histogram(), integ.dt_effective(), setup.op.dt_s,

@@ -131,6 +131,7 @@ struct Nccl {
   decltype(&ncclGroupStart) gstart = nullptr;
   decltype(&ncclGroupEnd) gend = nullptr;
   decltype(&ncclAllReduce) allreduce = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
   bool load() {
     if (h) return true;
@@ -146,7 +147,8 @@ struct Nccl {
     gend = reinterpret_cast<decltype(gend)>(dlsym(h, "ncclGroupEnd"));
     allreduce = reinterpret_cast<decltype(allreduce)>(dlsym(h, "ncclAllReduce"));
     errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
-    return init && destroy && send && recv && gstart && gend && allreduce && errstr;
+    bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
+    return init && destroy && send && recv && gstart && gend && allreduce && errstr && bcast;
   }
 };
 Nccl g_nccl;
@@ -1862,6 +1864,101 @@ int cwg_get_maps(cwg_ctx* c, double* lat, uint8_t* lat_valid, double* apd, uint8
       if (apd) apd[i] = av[i] ? A[i] : std::nan("");
       if (apd_valid) apd_valid[i] = av[i];
     }
+  });
+}
+
+// The whole result on every rank (run_simulation returns one SimulationResult,
+// splitting.cpp:286-293): each rank stages its owned y-slab in a global-size
+// device buffer and the ranks broadcast their slabs to each other (one NCCL
+// group of in-place ncclBroadcast per array; slab r = cwg_slab_plan rows).
+// world == 1 or loopback contexts: this context's own rows only (the
+// loopback tests assemble the slabs themselves). Any output may be null.
+int cwg_gather_result(cwg_ctx* c, double* v, double* s_aos, int stride, double* last, double* lat,
+                      uint8_t* lat_valid, double* apd, uint8_t* apd_valid) {
+  return guarded(nullptr, [&] {
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const bool multi = c->world > 1 && !c->loopback;
+    if (!multi) {
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      if (v || s_aos || last) {
+        const int rc = cwg_download_state(c, v, s_aos, stride, last);
+        if (rc != CWG_OK) throw Fail{rc, g_last_error};
+      }
+      std::vector<double> L(static_cast<size_t>(c->n_global)), A(static_cast<size_t>(c->n_global));
+      std::vector<uint8_t> lv(static_cast<size_t>(c->n_global)), av(static_cast<size_t>(c->n_global));
+      const int rc = cwg_get_maps(c, L.data() + c->own_global0, lv.data() + c->own_global0, A.data() + c->own_global0,
+                                  av.data() + c->own_global0);
+      if (rc != CWG_OK) throw Fail{rc, g_last_error};
+      for (long long i = c->own_global0; i < c->own_global0 + c->n_own; ++i) {
+        if (lat) lat[i] = L[static_cast<size_t>(i)];
+        if (lat_valid) lat_valid[i] = lv[static_cast<size_t>(i)];
+        if (apd) apd[i] = A[static_cast<size_t>(i)];
+        if (apd_valid) apd_valid[i] = av[static_cast<size_t>(i)];
+      }
+      return;
+    }
+    validation(!s_aos || stride >= c->stride, "state: stride smaller than the largest model state count");
+    const long long N = c->n_global;
+    std::vector<std::pair<long long, long long>> slab(static_cast<size_t>(c->world));  // (first node, count)
+    for (int r = 0; r < c->world; ++r) {
+      int64_t rb = 0, re = 0;
+      cwg_slab_plan(c->ny1, c->world, r, &rb, &re);
+      slab[static_cast<size_t>(r)] = {rb * c->w, (re - rb) * c->w};
+    }
+    DevScope scope;
+    auto bcast_all = [&](void* buf, size_t elem, ncclDataType_t type, long long per_node) {
+      NCCL_TRY(g_nccl.gstart());
+      for (int r = 0; r < c->world; ++r) {
+        char* p = static_cast<char*>(buf) + static_cast<size_t>(slab[static_cast<size_t>(r)].first * per_node) * elem;
+        NCCL_TRY(g_nccl.bcast(p, p, static_cast<size_t>(slab[static_cast<size_t>(r)].second * per_node), type, r,
+                              c->comm, c->stream));
+      }
+      NCCL_TRY(g_nccl.gend());
+    };
+    auto gather_d = [&](const double* own, double* host) {
+      double* d = scope.keep(dev_alloc<double>(static_cast<size_t>(N)));
+      CUDA_TRY(cudaMemcpyAsync(d + c->own_global0, own, c->n_own * sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->stream));
+      bcast_all(d, sizeof(double), ncclDouble, 1);
+      CUDA_TRY(cudaMemcpyAsync(host, d, N * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+    };
+    auto gather_u8 = [&](const unsigned char* own, uint8_t* host) {
+      unsigned char* d = scope.keep(dev_alloc<unsigned char>(static_cast<size_t>(N)));
+      CUDA_TRY(cudaMemcpyAsync(d + c->own_global0, own, c->n_own, cudaMemcpyDeviceToDevice, c->stream));
+      bcast_all(d, 1, ncclUint8, 1);
+      CUDA_TRY(cudaMemcpyAsync(host, d, N, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+    };
+    if (v) gather_d(c->d_v[c->cur] + c->halo, v);
+    if (last) gather_d(c->d_last + c->halo, last);
+    if (s_aos) {
+      double* d = scope.keep(dev_alloc<double>(static_cast<size_t>(N) * stride));
+      CUDA_TRY(launch_soa_to_aos(c->d_S, c->pitch, c->halo, c->stride, c->n_own, d + c->own_global0 * stride, stride,
+                                 c->stream));
+      bcast_all(d, sizeof(double), ncclDouble, stride);
+      CUDA_TRY(cudaMemcpyAsync(s_aos, d, static_cast<size_t>(N) * stride * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<uint8_t> lv(static_cast<size_t>(N)), av(static_cast<size_t>(N));
+    if (lat || lat_valid || apd || apd_valid) {
+      gather_u8(c->det.has_lat, lv.data());
+      gather_u8(c->det.has_apd, av.data());
+    }
+    if (lat) {
+      gather_d(c->det.lat, lat);
+      for (long long i = 0; i < N; ++i)
+        if (!lv[static_cast<size_t>(i)]) lat[i] = std::nan("");
+    }
+    if (apd) {
+      gather_d(c->det.apd, apd);
+      for (long long i = 0; i < N; ++i)
+        if (!av[static_cast<size_t>(i)]) apd[i] = std::nan("");
+    }
+    if (lat_valid) std::memcpy(lat_valid, lv.data(), static_cast<size_t>(N));
+    if (apd_valid) std::memcpy(apd_valid, av.data(), static_cast<size_t>(N));
   });
 }
 

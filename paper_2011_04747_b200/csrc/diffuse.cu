@@ -659,44 +659,46 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
 // ---------------------------------------------------------------------------
 // Structured 3D slab, register-blocked (default). The row sum is 27 DMUL +
 // 27 DADD in a fixed order (bit-exactness: no FMA, no reassociation), so at
-// 16 B of V traffic per node-substep the kernel is FP64-pipe bound unless
-// every V value and coefficient it multiplies is already in a register:
-//   * a thread owns two x-adjacent nodes (x, x+1) of one z row and marches
-//     over y; both have the same node class (x-interior, by = 1, iz), whose
-//     27 coefficients + dt/m stay in registers for the whole march (reloaded
-//     only on the slab's first / last global y plane);
-//   * the 3 x 3 x 4 window of V (planes y-1, y, y+1; rows z-1..z+1; columns
-//     x-1..x+2) lives in registers; a plane step brings in the 12 values of
-//     plane y+1 with 2-3 shared-memory loads per row (4.5-6 per node instead
-//     of 27 loads + 27 coefficient reads);
+// 16 B of V traffic per node-substep the kernel is FP64-pipe bound unless the
+// V values it multiplies are already in registers and the instructions that
+// are not FP64 are few per node:
+//   * a thread owns four x-adjacent nodes (x .. x+3) of one z row and marches
+//     over y. All four have the same node class (x-interior, by, iz): the
+//     warp-uniform 27 coefficients + dt/m of its row are read from shared
+//     memory as broadcasts, each feeding four DMULs, and the four
+//     accumulation chains (8-cycle DADD latency, measured) interleave;
+//   * the 3 x 3 x 6 window of V (planes y-1, y, y+1; rows z-1..z+1; columns
+//     x-1..x+4) lives in registers; a plane step brings in the 18 values of
+//     plane y+1 with 3-4 shared-memory loads per row (~2.5 per node);
 //   * plane rows arrive in shared memory by 1D bulk copies (cp.async.bulk,
-//     the TMA engine: one instruction per 66-node row, no per-element
-//     address math), NS - 2 planes ahead of use, through a full/empty
-//     mbarrier ring -- no block-wide barrier: a warp waits only for the rows
-//     it reads and the slot it refills. The V rows are not 16-byte aligned
-//     (odd nx+1), so each copy starts at the aligned node at or below x0 - 1
-//     and moves 68 nodes; the row's shift (0/1) is known from the index
-//     parity, and the window read picks the matching load pattern;
+//     the TMA engine: one instruction per 130-node row), NS - 2 planes ahead
+//     of use, through a full/empty mbarrier ring -- no block-wide barrier: a
+//     warp waits only for the rows it reads and the slot it refills. V rows
+//     are not 16-byte aligned (odd nx+1), so each copy starts at the aligned
+//     node at or below x0 - 1 and moves 132 nodes; the row's shift (0/1) is
+//     the parity of its first index, and the window read picks its pattern;
 //   * absent neighbours (z faces, y faces) meet a zero coefficient and a
 //     zero V (rows outside the slab in z are zeroed once; the halo planes
-//     beyond the global y faces are zero-initialised memory that nothing
-//     writes): 0 * 0 adds +0, which leaves the sum (never -0: it starts at
-//     +0) unchanged -- the same bits as skipping the term like fem.cpp;
+//     beyond the global y faces are zero-initialised memory nothing writes):
+//     0 * 0 adds +0, which leaves the sum (never -0: it starts at +0)
+//     unchanged -- the same bits as skipping the term like fem.cpp;
 //   * the two x faces (x = 0, x = nx; other classes) are rows of their own:
 //     extra blocks of the same grid compute them one thread per node with
 //     the generic class lookup.
-// Warp w of a block owns row z0 + w; lane l owns x = xb + 2l, xb + 2l + 1.
+// Warp w of a block owns row z0 + w; lane l owns x = xb + 4l .. xb + 4l + 3.
 // ---------------------------------------------------------------------------
-constexpr int S3R_NS = 6;     // plane stages in the ring (lead NS - 2 planes)
-constexpr int S3R_RS = 72;    // doubles per staged row (a 68-node copy + padding)
-constexpr int S3R_COPY = 68;  // nodes per row copy (544 B, a multiple of 16)
+constexpr int S3R_NS = 6;      // plane stages in the ring (lead NS - 2 planes)
+constexpr int S3R_TX = 128;    // nodes per tile row (32 lanes x 4)
+constexpr int S3R_COPY = 132;  // nodes per row copy (1056 B, a multiple of 16): x0 - 1 - sh .. x0 + 130 - sh
+constexpr int S3R_RS = 136;    // doubles per staged row
 
 template <int W>
 struct S3R {
   static constexpr int NT = 32 * W;
   static constexpr int ROWS = W + 2;
   static constexpr int STAGE = ROWS * S3R_RS;  // doubles per plane stage
-  static constexpr size_t smem = static_cast<size_t>(S3R_NS) * STAGE * sizeof(double) + 2 * S3R_NS * 8;
+  static constexpr int CF = 3 * W * 28;        // coefficient tables: [by][w][27 + dt/m]
+  static constexpr size_t smem = (static_cast<size_t>(S3R_NS) * STAGE + CF) * sizeof(double) + 2 * S3R_NS * 8;
 };
 
 // Generic row (any class, presence tests): the x-face nodes and tiny slabs.
@@ -731,12 +733,13 @@ __device__ __forceinline__ void s3_generic_node(const DiffArgs& a, const Struct3
                    a.vin, a.vout);
 }
 
-// One plane step of a thread's node pair: window planes (m, o, p) = (y-1, y,
-// y+1), each [3 rows z-1..z+1][4 cols x-1..x+2].
-__device__ __forceinline__ void s3r_pair(const double (&m)[12], const double (&o)[12], const double (&p)[12],
-                                         const double (&cf)[27], double cm, double& outA, double& outB) {
+// One plane step of a thread's four nodes: window planes (m, o, p) = (y-1, y,
+// y+1), each [3 rows z-1..z+1][6 cols x-1..x+4]; cf = the row's 27
+// coefficients and dt/m in shared memory (warp-uniform broadcasts).
+__device__ __forceinline__ void s3r_quad(const double (&m)[18], const double (&o)[18], const double (&p)[18],
+                                         const double* cf, double (&out)[4]) {
   const double* pl[3] = {m, o, p};
-  double accA = 0.0, accB = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
@@ -744,11 +747,12 @@ __device__ __forceinline__ void s3r_pair(const double (&m)[12], const double (&o
 #pragma unroll
       for (int dx = 0; dx < 3; ++dx) {
         const double c = cf[dy * 9 + dz * 3 + dx];
-        accA += c * pl[dy][dz * 4 + dx];
-        accB += c * pl[dy][dz * 4 + dx + 1];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j] += c * pl[dy][dz * 6 + dx + j];
       }
-  outA = o[4 + 1] - cm * accA;
-  outB = o[4 + 2] - cm * accB;
+  const double cm = cf[27];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out[j] = o[6 + 1 + j] - cm * acc[j];
 }
 
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
@@ -786,19 +790,20 @@ __global__ void __launch_bounds__(32 * W, 2)
   }
   const int item = blockIdx.x;
   const int tile = item % (tiles_x * tiles_z), ych = item / (tiles_x * tiles_z);
-  const int xb = 1 + (tile % tiles_x) * 64;  // first node of the tile (x-interior rows start at x = 1)
+  const int xb = 1 + (tile % tiles_x) * S3R_TX;  // first node of the tile (x-interior rows start at x = 1)
   const int z0 = (tile / tiles_x) * W;
   const int planes = static_cast<int>(s.planes);
   const int yb = ych * ychunk;
   const int ye = yb + ychunk < planes ? yb + ychunk : planes;
   if (ye <= yb) return;  // an empty trailing chunk (block-uniform)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int xA = xb + 2 * lane, z = z0 + w;
-  const bool okA = xA <= nx - 1 && z < nz1, okB = xA + 1 <= nx - 1 && z < nz1;
+  const int x0 = xb + 4 * lane, z = z0 + w;
   const int zc = z < nz1 ? z : nz1 - 1;  // clamped row for the coefficient reads of idle threads
+  const int nvalid = z < nz1 ? max(0, min(4, nx - x0)) : 0;  // nodes x0 .. x0+3 that are x-interior (<= nx - 1)
   const long long plane = s.plane;
   const int gy0 = static_cast<int>(s.row_begin), gny = static_cast<int>(s.ny1);
-  const unsigned long long* bars = reinterpret_cast<const unsigned long long*>(s3r_smem + S3R_NS * G::STAGE);
+  double* cft = s3r_smem + S3R_NS * G::STAGE;  // [by][w][28]
+  const unsigned long long* bars = reinterpret_cast<const unsigned long long*>(cft + G::CF);
   const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(bars));
   const unsigned empty0 = full0 + 8 * S3R_NS;
   const unsigned smem0 = static_cast<unsigned>(__cvta_generic_to_shared(s3r_smem));
@@ -807,7 +812,7 @@ __global__ void __launch_bounds__(32 * W, 2)
   // the first / last warp, the halo row below / above the tile; rows outside
   // the slab in z are never copied (zeroed once below)
   const int rA = w + 1, rB = w == 0 ? 0 : (w == W - 1 ? W + 1 : -1);
-  const bool vA = z0 - 1 + rA < nz1;                           // z0 - 1 + rA = z >= 0 always
+  const bool vA = z0 - 1 + rA < nz1;  // z0 - 1 + rA = z >= 0 always
   const bool vB = rB >= 0 && z0 - 1 + rB >= 0 && z0 - 1 + rB < nz1;
   const unsigned bytes_w = (vA ? S3R_COPY * 8u : 0u) + (vB ? S3R_COPY * 8u : 0u);
   if (threadIdx.x == 0) {
@@ -821,21 +826,22 @@ __global__ void __launch_bounds__(32 * W, 2)
     const int r = (t / S3R_RS) % G::ROWS, zz = z0 - 1 + r;
     if (zz < 0 || zz >= nz1) s3r_smem[t] = 0.0;
   }
+  for (int t = threadIdx.x; t < G::CF; t += G::NT) {  // the block's coefficient rows for by = 0, 1, 2
+    const int by = t / (W * 28), ww = (t / 28) % W, q = t % 28;
+    const int zz = min(z0 + ww, nz1 - 1);
+    const long long cls = (by * 3 + 1) * static_cast<long long>(nz1) + zz;
+    cft[t] = q < 27 ? __ldg(s.coef + cls * 27 + q) : __ldg(s.cm + cls);
+  }
   __syncthreads();
 
   // plane P_k = yb - 1 + k -> slot k % NS; lane 0 of every warp arms the full
   // barrier with its bytes and copies its rows (after the slot's previous
   // plane was read by every warp)
-  auto issue = [&](int k) {
+  auto issue = [&](int k, int slot, unsigned empty_par, bool wait_empty) {
     if (lane != 0) return;
-    const int slot = k % S3R_NS;
-    if (k >= S3R_NS) {
-      const unsigned par = static_cast<unsigned>((k / S3R_NS - 1) & 1);
-      mbar_wait(empty0 + 8 * slot, par);
-    }
+    if (wait_empty) mbar_wait(empty0 + 8 * slot, empty_par);
     mbar_arrive_tx(full0 + 8 * slot, bytes_w);
-    const long long yl = yb - 1 + k;
-    const long long pbase = (yl + 1) * plane + xb - 1;
+    const long long pbase = static_cast<long long>(yb + k) * plane + xb - 1;  // (yl + 1) * plane, yl = yb - 1 + k
     auto copy_row = [&](int r) {
       const long long idx = pbase + static_cast<long long>(z0 - 1 + r) * nx1;
       const unsigned dst = smem0 + static_cast<unsigned>((slot * G::STAGE + r * S3R_RS) * 8);
@@ -847,77 +853,104 @@ __global__ void __launch_bounds__(32 * W, 2)
     if (vA) copy_row(rA);
     if (vB) copy_row(rB);
   };
-  // this warp's 12 window values of plane P_k; row r's first copied node is
-  // x0 - 1 - sh with sh the parity of the row start's index
   // parity of row w + dz's first node index in plane P_0; P_k flips it when k * plane is odd
   int sh0 = 0;
 #pragma unroll
   for (int dz = 0; dz < 3; ++dz)
     sh0 |= static_cast<int>((static_cast<long long>(yb) * plane + xb - 1 + static_cast<long long>(z0 - 1 + w + dz) * nx1) &
                             1) << dz;
-  const int podd = static_cast<int>(plane & 1);
-  auto window = [&](int k, double (&wv)[12]) {
-    const int slot = k % S3R_NS;
-    mbar_wait(full0 + 8 * slot, static_cast<unsigned>((k / S3R_NS) & 1));
-    const int shk = sh0 ^ (((k & podd) != 0) ? 7 : 0);
+  const int pflip = (plane & 1) ? 7 : 0;
+  // this warp's 18 window values of plane P_k (in `slot`); row r's first
+  // copied node is x0 - 1 - sh with sh the parity of the row start's index
+  auto window = [&](int k, int slot, unsigned full_par, double (&wv)[18]) {
+    mbar_wait(full0 + 8 * slot, full_par);
+    const int shk = sh0 ^ ((k & 1) ? pflip : 0);
 #pragma unroll
     for (int dz = 0; dz < 3; ++dz) {
-      const int r = w + dz;
-      const int sh = (shk >> dz) & 1;
-      const double* rp = s3r_smem + slot * G::STAGE + r * S3R_RS + 2 * lane;  // col c <-> node x0 - 1 - sh + c
-      if (sh) {  // x-1 at col 2l + 1
-        const double2 pr = *reinterpret_cast<const double2*>(rp + 2);
-        wv[dz * 4 + 0] = rp[1];
-        wv[dz * 4 + 1] = pr.x;
-        wv[dz * 4 + 2] = pr.y;
-        wv[dz * 4 + 3] = rp[4];
-      } else {  // x-1 at col 2l
-        const double2 p0 = *reinterpret_cast<const double2*>(rp);
-        const double2 p1 = *reinterpret_cast<const double2*>(rp + 2);
-        wv[dz * 4 + 0] = p0.x;
-        wv[dz * 4 + 1] = p0.y;
-        wv[dz * 4 + 2] = p1.x;
-        wv[dz * 4 + 3] = p1.y;
+      const double* rp = s3r_smem + slot * G::STAGE + (w + dz) * S3R_RS + 4 * lane;  // col c <-> x0 - 1 - sh + c
+      if ((shk >> dz) & 1) {  // x-1 at col 4l + 1
+        const double2 q0 = *reinterpret_cast<const double2*>(rp + 2);
+        const double2 q1 = *reinterpret_cast<const double2*>(rp + 4);
+        wv[dz * 6 + 0] = rp[1];
+        wv[dz * 6 + 1] = q0.x;
+        wv[dz * 6 + 2] = q0.y;
+        wv[dz * 6 + 3] = q1.x;
+        wv[dz * 6 + 4] = q1.y;
+        wv[dz * 6 + 5] = rp[6];
+      } else {  // x-1 at col 4l
+        const double2 q0 = *reinterpret_cast<const double2*>(rp);
+        const double2 q1 = *reinterpret_cast<const double2*>(rp + 2);
+        const double2 q2 = *reinterpret_cast<const double2*>(rp + 4);
+        wv[dz * 6 + 0] = q0.x;
+        wv[dz * 6 + 1] = q0.y;
+        wv[dz * 6 + 2] = q1.x;
+        wv[dz * 6 + 3] = q1.y;
+        wv[dz * 6 + 4] = q2.x;
+        wv[dz * 6 + 5] = q2.y;
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * slot);
   };
-  auto load_coef = [&](int by, double (&cf)[27], double& cm) {
-    const long long cls = (by * 3 + 1) * static_cast<long long>(nz1) + zc;
-#pragma unroll
-    for (int q = 0; q < 27; ++q) cf[q] = __ldg(s.coef + cls * 27 + q);
-    cm = __ldg(s.cm + cls);
-  };
 
   const int n = ye - yb;
-  const int last_k = (ye < planes ? ye : planes) - (yb - 1);  // planes P_0 .. P_last_k are needed
-  double cf[27], cm;
-  load_coef(1, cf, cm);
-  for (int k = 0; k < S3R_NS && k <= last_k; ++k) issue(k);
-  double P0[12], P1[12], P2[12];
-  window(0, P0);
-  window(1, P1);
-  double* outp = a.vout + static_cast<long long>(yb + 1) * plane + static_cast<long long>(zc) * nx1 + xA;
+  const int last_k = ye - (yb - 1);  // planes P_0 .. P_{n+1} are needed (P_{n+1} = plane ye <= planes)
+  // ring bookkeeping by counters (no divisions): slot and phase of the next plane to read / to issue
+  int rd_slot = 0, wr_slot = 0;
+  unsigned rd_par = 0, wr_par = 0;
+  for (int k = 0; k < S3R_NS && k <= last_k; ++k) {
+    issue(k, wr_slot, 0, false);
+    if (++wr_slot == S3R_NS) {
+      wr_slot = 0;
+      wr_par ^= 1;
+    }
+  }
+  double P0[18], P1[18], P2[18];
+  auto read_next = [&](int k, double (&wv)[18]) {
+    window(k, rd_slot, rd_par, wv);
+    if (++rd_slot == S3R_NS) {
+      rd_slot = 0;
+      rd_par ^= 1;
+    }
+  };
+  read_next(0, P0);
+  read_next(1, P1);
+  double* outp = a.vout + static_cast<long long>(yb + 1) * plane + static_cast<long long>(zc) * nx1 + x0;
   const unsigned long long key0 =
-      static_cast<unsigned long long>(static_cast<long long>(yb) * plane + static_cast<long long>(zc) * nx1 + xA +
+      static_cast<unsigned long long>(static_cast<long long>(yb) * plane + static_cast<long long>(zc) * nx1 + x0 +
                                       s.row_begin * plane);
+  const double* cfw = cft + w * 28;
   // plane step i: output plane y = yb + i from (m, o, p); p <- P_{i+2}
-  auto step = [&](int i, double (&m)[12], double (&o)[12], double (&p)[12]) {
-    window(i + 2, p);
-    if (i + S3R_NS <= last_k) issue(i + S3R_NS);  // into the slot of P_i (read by every warp at step i-2)
+  auto step = [&](int i, double (&m)[18], double (&o)[18], double (&p)[18]) {
+    read_next(i + 2, p);
+    if (i + S3R_NS <= last_k) {  // into the slot of P_i (read by every warp at step i-2)
+      issue(i + S3R_NS, wr_slot, wr_par ^ 1u, true);
+      if (++wr_slot == S3R_NS) {
+        wr_slot = 0;
+        wr_par ^= 1;
+      }
+    }
     const int gy = gy0 + yb + i;
-    const bool yface = gy == 0 || gy == gny - 1;
-    if (yface) load_coef(gy == 0 ? 0 : 2, cf, cm);
-    double oA, oB;
-    s3r_pair(m, o, p, cf, cm, oA, oB);
-    if (yface) load_coef(1, cf, cm);
-    if (okA) outp[0] = oA;
-    if (okB) outp[1] = oB;
-    if ((okA && !isfinite(oA)) || (okB && !isfinite(oB))) {
+    const int by = gy == 0 ? 0 : (gy == gny - 1 ? 2 : 1);
+    double out[4];
+    s3r_quad(m, o, p, cfw + by * (W * 28), out);
+    if (nvalid == 4) {
+      outp[0] = out[0];
+      outp[1] = out[1];
+      outp[2] = out[2];
+      outp[3] = out[3];
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nvalid) outp[j] = out[j];
+    }
+    // one check for the four (a non-finite output makes the sum non-finite; a finite overflow of the sum
+    // only sends the thread to the exact per-node test)
+    if (!isfinite((out[0] + out[1]) + (out[2] + out[3]))) {
       const unsigned long long k = key0 + static_cast<unsigned long long>(i) * plane;
-      if (okA && !isfinite(oA)) record_failure(a.err, k << 22, seq, 2, 1, a.vin, a.vout);
-      if (okB && !isfinite(oB)) record_failure(a.err, (k + 1) << 22, seq, 2, 1, a.vin, a.vout);
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nvalid && !isfinite(out[j])) record_failure(a.err, (k + j) << 22, seq, 2, 1, a.vin, a.vout);
     }
     outp += plane;
   };
@@ -929,7 +962,7 @@ __global__ void __launch_bounds__(32 * W, 2)
   }
   if (i < n) step(i, P0, P1, P2);
   if (i + 1 < n) step(i + 1, P1, P2, P0);
-  // every copy this block issued has been waited for (window of P_{n+1} = the last issued plane)
+  // every copy this block issued has been waited for (P_{n+1}, the last issued plane, was read at step n-1)
 }
 
 template <int W>
@@ -939,7 +972,7 @@ static cudaError_t launch_s3r(const DiffArgs& a, const Struct3D& s, int num_sms,
   cudaError_t e = ensure_dyn_smem(diffuse_struct3d_rb<W>, static_cast<int>(G::smem), attr_done);
   if (e != cudaSuccess) return e;
   const long long nxi = s.nx1 - 2;  // x-interior nodes 1 .. nx-1
-  const int tiles_x = nxi > 0 ? static_cast<int>((nxi + 63) / 64) : 0;
+  const int tiles_x = nxi > 0 ? static_cast<int>((nxi + S3R_TX - 1) / S3R_TX) : 0;
   const int tiles_z = static_cast<int>((s.nz1 + W - 1) / W);
   const long long tiles = static_cast<long long>(tiles_x) * tiles_z;
   // y chunks: whole waves of 2 blocks per SM, chunks of >= 8 planes

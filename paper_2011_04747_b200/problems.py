@@ -37,6 +37,9 @@ class Problem:
     probes: List[int] = field(default_factory=list)
     gkr_scale: Optional[np.ndarray] = None
     notes: str = ""
+    # (model id, cycle length ms, beats, amplitude mV/ms, duration ms): that model's nodes start from
+    # pace_to_steady_state (ionic.cpp:122-167) instead of the rest state (computed on the device)
+    pacing: Optional[tuple] = None
 
     @property
     def n(self):
@@ -49,8 +52,18 @@ class Problem:
                                    probes=[api.Probe(int(p), f"p{q}") for q, p in enumerate(self.probes)],
                                    gkr_scale=self.gkr_scale)
 
-    def initial_state(self) -> api.NodeStateArray:
-        return api.make_initial_state(self.n, [api.make_model(m) for m in self.models], self.model_of_node)
+    def initial_state(self, paced_state=None) -> api.NodeStateArray:
+        """make_initial_state; with `pacing`, the paced model's nodes start from its paced state
+        (`paced_state` if given, e.g. a fixture's, else pace_to_steady_state on the device)."""
+        models = [api.make_model(m) for m in self.models]
+        per_model = None
+        if self.pacing is not None:
+            mid, cl, beats, amp, dur = self.pacing
+            if paced_state is None:
+                paced_state = api.pace_to_steady_state(models[mid], cl, beats, amp, dur).state
+            per_model = [None] * len(models)
+            per_model[mid] = np.asarray(paced_state, np.float64)
+        return api.make_initial_state(self.n, models, self.model_of_node, initial_per_model=per_model)
 
 
 # C1: 1x1 cm, h = 0.01, D = 0.001 isotropic; ORd-epi; left-edge line x <= 0 for
@@ -95,6 +108,12 @@ def c2(model="ohara2011-epi", t_end=500.0, k0_down=3, amplitude=C2_AMPLITUDE, ra
 C3_S1_AMPLITUDE = 92.0
 C3_S1_STRIP = 0.05
 C3_S2_AMPLITUDE = 70.0
+# C3 tissue state: ORd-epi paced to steady state at a 600 ms cycle (20 beats, 70 mV/ms = 2 x the no-drain
+# threshold, 1 ms; APD90 ~227 ms). From the rest state (APD90 ~290 ms on the first beat) or paced at 1 Hz
+# (APD90 ~242 ms) the S2 at 300 ms finds the S1-activated tissue still refractory and no re-entry follows;
+# at 500-600 ms cycles the S2 wave re-enters around the scar (tools/c3_reentry.py,
+# profiles/r02_c3_reentry.txt).
+C3_PACING = (0, 600.0, 20, 70.0, 1.0)
 
 
 def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C3_S1_AMPLITUDE, h=0.005, size=5.0,
@@ -127,7 +146,7 @@ def c3(t_end=1000.0, k0_down=3, seed=2011, amplitude=C3_S1_AMPLITUDE, h=0.005, s
     probes = [sh.nearest(0.5, c), sh.nearest(c, 0.5), sh.nearest(size - 0.5, c)]
     return Problem("C3", sh, ["ohara2011-epi", "passive"], model_of_node,
                    [(s1, 0.0, 1.0, amplitude, None), (s2, 300.0, 1.0, amplitude_s2, None)], cfg, probes, gkr,
-                   notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)")
+                   notes="extension: scar/passive/GKr jitter (parity unpinned by the reference)", pacing=C3_PACING)
 
 
 def site_centers(lx, ly, n_sites, seed):
@@ -159,8 +178,19 @@ def c4(t_end=500.0, **kw) -> Problem:
     return slab(5.0, 5.0, 1.0, 0.02, t_end=t_end, **kw)
 
 
+# C5 endocardial sites: discs of radius 0.2 cm at 450 mV/ms for 1 ms. A site's threshold (the reference's
+# bisection rule applied in 3D, tools/threshold_c5_site.py: a node >= 0.5 cm away activates within 30 ms)
+# lies in (360, 400] mV/ms; 2x that drives the ORd forward-Euler reaction past its stability limit under DAETI
+# at dt 0.1 ms (512 mV/ms aborts at t = 0.99 ms), so the largest tested amplitude below it that propagates is
+# used. Radius-0.1 cm sites do not propagate at any amplitude below the abort (profiles/r02_c5_sites.txt).
+C5_SITE_RADIUS = 0.2
+C5_AMPLITUDE = 450.0
+
+
 def c5(t_end=5.0, **kw) -> Problem:
     """BASELINE configs[4]: 10x10x2 cm, h = 0.01 (1001x1001x201 = 201M nodes), 16 random endocardial sites."""
+    kw.setdefault("amplitude", C5_AMPLITUDE)
+    kw.setdefault("site_radius", C5_SITE_RADIUS)
     return slab(10.0, 10.0, 2.0, 0.01, t_end=t_end, stim="sites", **kw)
 
 
@@ -168,4 +198,6 @@ def c5_subslab(ly=0.2, t_end=5.0, n_sites=16, **kw) -> Problem:
     """A full-cross-section y-sub-slab of config 5 for parity at BASELINE resolution: 10 x ly x 2 cm at
     h = 0.01 (1001 x (ly/h + 1) x 201 nodes; ly = 0.2 -> 4.2M nodes), same fibres, conductivities and
     stimulus kind (n_sites seeded endocardial discs over its own face)."""
+    kw.setdefault("amplitude", C5_AMPLITUDE)
+    kw.setdefault("site_radius", C5_SITE_RADIUS)
     return slab(10.0, ly, 2.0, 0.01, t_end=t_end, stim="sites", n_sites=n_sites, **kw)

@@ -81,11 +81,17 @@ def make(name):
     prob = problem(name)
     cfg = prob.cfg
     op, dt_s = oracle_op(prob)
+    init, paced = None, None
+    if prob.pacing is not None:  # the paced model's state from the oracle's pace_to_steady_state (ionic.cpp:122-167)
+        mid, cl, beats, amp, dur = prob.pacing
+        paced, _, _ = orapy.pace(prob.models[mid], cl, beats, amp, dur)
+        st = prob.initial_state(paced_state=paced)
+        init = (st.v, st.s.reshape(prob.n, -1), st.last_dvdt)
     t0 = time.time()
     r = orapy.run_simulation(op, dt_s, prob.models, prob.model_of_node, prob.stimuli, scheme=cfg.scheme.name,
                              dt=cfg.dt_ms, t_end=cfg.t_end_ms, k0_up=cfg.k0_up, k0_down=cfg.k0_down,
                              record_interval=cfg.record_interval_ms, probes=prob.probes,
-                             gkr_scale=prob.gkr_scale)
+                             gkr_scale=prob.gkr_scale, init=init)
     wall = time.time() - t0
     idx = sampled(prob)
     out = dict(
@@ -100,6 +106,7 @@ def make(name):
         apd_valid=r["apd_valid"][idx], k_histogram=r["k_histogram"], trace_t=r["trace_t"], traces=r["traces"],
         v_mean=np.array(float(np.mean(r["v"]))), v_max=np.array(float(np.max(r["v"]))),
         activated=np.array(int(np.sum(r["lat_valid"]))), oracle_wall_s=np.array(wall),
+        paced_state=np.asarray(paced if paced is not None else [], np.float64),
         oracle_threads=np.array(os.cpu_count()))
     path = os.path.join(HERE, f"scale_{name}.npz")
     np.savez_compressed(path, **out)

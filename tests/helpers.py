@@ -11,9 +11,19 @@ def csr_of(problem):
     return (op.row_ptr, op.col, op.val, op.lumped_mass)
 
 
+def paced_state(problem):
+    """A problem with `pacing` starts its paced model from pace_to_steady_state: both the GPU run and the
+    oracle run start from the ORACLE's paced state (ionic.cpp:122-167 restated), so they see the same input."""
+    if problem.pacing is None:
+        return None
+    import orapy
+    mid, cl, beats, amp, dur = problem.pacing
+    return orapy.pace(problem.models[mid], cl, beats, amp, dur)[0]
+
+
 def gpu_run(problem, device=0):
     import paper_2011_04747_b200 as cw
-    st = problem.initial_state()
+    st = problem.initial_state(paced_state=paced_state(problem))
     return cw.run_simulation(st, problem.setup(), problem.cfg, device=device)
 
 
@@ -23,6 +33,9 @@ def oracle_run(problem, **over):
     kw = dict(scheme=cfg.scheme.name, dt=cfg.dt_ms, t_end=cfg.t_end_ms, k0_up=cfg.k0_up, k0_down=cfg.k0_down,
               strict=cfg.strict_substeps, record_interval=cfg.record_interval_ms, probes=problem.probes,
               gkr_scale=problem.gkr_scale)
+    if problem.pacing is not None and "init" not in over:
+        st = problem.initial_state(paced_state=paced_state(problem))
+        kw["init"] = (st.v, st.s.reshape(problem.n, -1), st.last_dvdt)
     kw.update(over)
     return orapy.run_simulation(csr_of(problem), problem.sheet.op.dt_s, problem.models, problem.model_of_node,
                                 problem.stimuli, **kw)

@@ -20,6 +20,7 @@ def test_constants_match_problems():
     assert bench.C2_RADIUS == problems.C2_RADIUS
     p = problems.c4(t_end=1.0)
     assert p.stimuli[0][3] == bench.SLAB_AMPLITUDE
+    assert (bench.C5_AMPLITUDE, bench.C5_SITE_RADIUS) == (problems.C5_AMPLITUDE, problems.C5_SITE_RADIUS)
 
 
 def test_oracle_c4_matches_product_c4():
@@ -41,7 +42,7 @@ def test_oracle_c5_sites_match_product():
     centers = problems.site_centers(10.0, 10.0, 16, 2011)
     sub = problems.slab(10.0, 0.2, 2.0, 0.01, stim="face")  # geometry of the sampled sub-slab
     assert sub.n == op.n
-    want = sub.sheet.discs_z0(centers, 0.1)
+    want = sub.sheet.discs_z0(centers, problems.C5_SITE_RADIUS)
     assert np.array_equal(want, nodes)
 
 

@@ -40,6 +40,13 @@ def propagates(amp):
     return ok
 
 
+if len(sys.argv) > 3 and "," in sys.argv[3]:  # probe mode: just test the listed amplitudes
+    for amp in (float(a) for a in sys.argv[3].split(",")):
+        try:
+            propagates(amp)
+        except cw.InstabilityError:
+            pass
+    raise SystemExit(0)
 lo, hi = 0.0, float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
 while not propagates(hi):
     lo, hi = hi, hi * 2.0
