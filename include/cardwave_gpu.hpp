@@ -13,6 +13,21 @@
 // std::runtime_error. There is no CPU fallback: a model the device path does
 // not implement (CellModel::name() outside the registry) is a ValidationError.
 //
+// Multi-GPU (one process per GPU, y-slabs, NCCL halo exchange): pass a
+// gpu::Placement{device, rank, world, nccl_id}; every rank constructs the
+// integrator with the full problem and run_simulation returns the global
+// SimulationResult on every rank (cwg_gather_result).
+//
+// State residency (StrangIntegrator::advance): by default every advance()
+// uploads and downloads the whole NodeStateArray, exactly the reference's
+// in-place semantics (splitting.cpp:171-181) for any caller. A caller that
+// steps one state object through many advance() calls and reads only V
+// between them can call set_state_residency(true): the state then stays on
+// the device, is uploaded only when advance() sees other buffers (or after
+// mark_state_modified()), V and last_dvdt come back every step (8 + 8 B per
+// node instead of 344 for ORd), and the cell states on sync_state() or on
+// an InstabilityError.
+//
 // ProtocolIndex exposes no accessors (stimulus.hpp:35-50), so the shim reads
 // its two members through a layout mirror, guarded by static_asserts; a
 // maintainer who prefers can instead add `entries()`/`node_entries()`
@@ -40,6 +55,15 @@
 #include "cwgpu.h"
 
 namespace cardwave::gpu {
+
+/// Device placement of an integrator: one GPU (default), or rank `rank` of a
+/// `world`-rank y-slab run whose ranks share one NCCL unique id (128 bytes).
+struct Placement {
+  int device = 0;
+  int rank = 0;
+  int world = 1;
+  const unsigned char* nccl_id = nullptr;
+};
 
 namespace detail {
 
@@ -113,7 +137,8 @@ inline int model_kind(const CellModel& m) {
 // the state (the reference ctor sees only setup + cfg).
 class Context {
  public:
-  Context(const SimulationSetup& setup, const SchemeConfig& cfg, int device) : setup_(setup), cfg_(cfg), device_(device) {
+  Context(const SimulationSetup& setup, const SchemeConfig& cfg, const Placement& pl)
+      : setup_(setup), cfg_(cfg), device_(pl.device), place_(pl) {
     cfg.validate();
     if (setup.op == nullptr) throw ValidationError("integrator: missing assembled operator");
     if (setup.models.empty()) throw ValidationError("integrator: no cell models");
@@ -169,7 +194,9 @@ class Context {
     p.strict_substeps = cfg_.strict_substeps ? 1 : 0;
     p.record_interval_ms = cfg_.record_interval_ms;
     p.device = device_;
-    p.world = 1;
+    p.rank = place_.rank;
+    p.world = place_.world;
+    p.nccl_id = place_.nccl_id;
     cwg_error e{};
     check(cwg_create(&p, &ctx_, &e), e);
     return ctx_;
@@ -178,6 +205,7 @@ class Context {
   const SimulationSetup& setup_;
   const SchemeConfig& cfg_;
   int device_;
+  Placement place_;
   std::vector<int> kinds_;
   double dt_eff_ = 0.0;
   DiffusionPlan plan_;
@@ -195,17 +223,42 @@ class Context {
 class StrangIntegrator {
  public:
   StrangIntegrator(const SimulationSetup& setup, const SchemeConfig& cfg, int device = 0)
-      : c_(std::make_unique<detail::Context>(setup, cfg, device)) {}
+      : StrangIntegrator(setup, cfg, Placement{device, 0, 1, nullptr}) {}
+  StrangIntegrator(const SimulationSetup& setup, const SchemeConfig& cfg, const Placement& pl)
+      : c_(std::make_unique<detail::Context>(setup, cfg, pl)) {}
 
   /// One outer step; mutates `state` in place like splitting.cpp:171-181.
   void advance(NodeStateArray& state, double t_ms, std::int64_t step_index, std::int64_t n_steps) {
     cwg_ctx* ctx = c_->get(state);
-    detail::check(cwg_upload_state(ctx, state.v.data(), state.s.data(), state.stride, state.last_dvdt.data()));
+    const bool same = resident_ && !dirty_ && state.v.data() == synced_v_ && state.s.data() == synced_s_ &&
+                      state.last_dvdt.data() == synced_last_;
+    if (!same)
+      detail::check(cwg_upload_state(ctx, state.v.data(), state.s.data(), state.stride, state.last_dvdt.data()));
     cwg_error e{};
     const int rc = cwg_advance(ctx, t_ms, step_index, n_steps, &e);
-    detail::check(cwg_download_state(ctx, state.v.data(), state.s.data(), state.stride, state.last_dvdt.data()));
+    const bool full = !resident_ || rc != CWG_OK;
+    detail::check(cwg_download_state(ctx, state.v.data(), full ? state.s.data() : nullptr, state.stride,
+                                     state.last_dvdt.data()));
+    synced_v_ = state.v.data();
+    synced_s_ = state.s.data();
+    synced_last_ = state.last_dvdt.data();
+    dirty_ = false;
     refresh();
     detail::check(rc, e);
+  }
+
+  /// Opt-in device residency of the state across advance() calls (see the header comment).
+  void set_state_residency(bool on) {
+    resident_ = on;
+    dirty_ = true;
+  }
+  /// The caller changed the state's values in place: the next advance() uploads it.
+  void mark_state_modified() { dirty_ = true; }
+  /// Bring the cell states (and V, last_dvdt) of a resident run back to `state`.
+  void sync_state(NodeStateArray& state) {
+    if (!c_->ctx_) return;
+    detail::check(cwg_download_state(c_->ctx_, state.v.data(), state.s.data(), state.stride,
+                                     state.last_dvdt.data()));
   }
 
   double dt_effective() const { return c_->dt_eff_; }
@@ -220,17 +273,20 @@ class StrangIntegrator {
     cwg_get_khist(c_->ctx_, c_->khist_.data(), static_cast<int>(c_->khist_.size()));
     cwg_get_timing(c_->ctx_, &c_->timing_.reaction_ms, &c_->timing_.diffusion_ms, &c_->timing_.recording_ms);
   }
+  int world() const { return c_->place_.world; }
 
  private:
   std::unique_ptr<detail::Context> c_;
+  bool resident_ = false, dirty_ = true;
+  const double *synced_v_ = nullptr, *synced_s_ = nullptr, *synced_last_ = nullptr;
 };
 
 /// Drop-in for cardwave::run_simulation (splitting.cpp:219-294): device-resident
 /// state, CUDA-graph replay between record points, callbacks at their cadence.
 inline SimulationResult run_simulation(NodeStateArray state, const SimulationSetup& setup,
-                                       const SchemeConfig& cfg) {
+                                       const SchemeConfig& cfg, const Placement& place = Placement{}) {
   const auto t_run0 = std::chrono::steady_clock::now();
-  StrangIntegrator integ(setup, cfg);
+  StrangIntegrator integ(setup, cfg, place);
   cwg_ctx* ctx = integ.handle(state);
   cwg_info info{};
   cwg_get_info(ctx, &info);
@@ -318,10 +374,11 @@ inline SimulationResult run_simulation(NodeStateArray state, const SimulationSet
   r.lat_map.value.resize(n);
   r.apd90_map.value.resize(n);
   std::vector<std::uint8_t> lv(n), av(n);
-  detail::check(cwg_get_maps(ctx, r.lat_map.value.data(), lv.data(), r.apd90_map.value.data(), av.data()));
+  // the global maps and final state on every rank (world == 1: the plain download)
+  detail::check(cwg_gather_result(ctx, state.v.data(), state.s.data(), state.stride, state.last_dvdt.data(),
+                                  r.lat_map.value.data(), lv.data(), r.apd90_map.value.data(), av.data()));
   r.lat_map.valid.assign(lv.begin(), lv.end());
   r.apd90_map.valid.assign(av.begin(), av.end());
-  detail::check(cwg_download_state(ctx, state.v.data(), state.s.data(), state.stride, state.last_dvdt.data()));
   integ.refresh();
   r.k_histogram = integ.k_histogram();
   r.timing = integ.timing();

@@ -240,6 +240,10 @@ int cwg_get_maps(cwg_ctx* ctx, double* lat, uint8_t* lat_valid, double* apd90, u
  * any pointer may be NULL. Collective for world > 1 (call on all ranks). */
 int cwg_gather_result(cwg_ctx* ctx, double* v, double* s_aos, int stride, double* last_dvdt, double* lat,
                       uint8_t* lat_valid, double* apd90, uint8_t* apd_valid);
+/* No reference counterpart (runtime): return the device blocks cached by
+ * destroyed contexts to CUDA (contexts reuse them for allocations of the
+ * same size; at most 32 GiB is kept; CWG_POOL=0 disables caching). */
+void cwg_trim_pool(void);
 /* reaction / diffusion / recording device time (ms, CUDA events) of the last
  * cwg_advance calls (TimingBreakdown, splitting.hpp:57-62) */
 int cwg_get_timing(cwg_ctx* ctx, double* reaction_ms, double* diffusion_ms, double* recording_ms);

@@ -1,6 +1,7 @@
 // TEST INFRASTRUCTURE: the C++ drop-in (include/cardwave_gpu.hpp) side by side
 // with the unmodified reference, on the same reference-built problem.
 //   shim_parity ap|ord|abort|diffusion   -> one JSON line; exit 0 on parity
+//   shim_parity advance|resident          -> StrangIntegrator::advance step by step (resident: device-resident state)
 //   shim_parity c2 [t_end_ms]            -> the bench workload (BASELINE configs[1]) end to end
 //   shim_parity c1 [t_end_ms]            -> BASELINE configs[0] (ORd-epi, C1 line at 592 mV/ms), default 400 ms
 // Built by oracle/Makefile (target `shim`) into oracle/_ref/shim_parity,
@@ -69,6 +70,33 @@ int main(int argc, char** argv) {
   if (mode == "c1") cfg.t_end_ms = argc > 2 ? std::atof(argv[2]) : 400.0;
   cfg.k0_down = mode == "abort" ? 1 : (ap ? 1 : 3);
   NodeStateArray s0 = make_initial_state(mesh, models, {0});
+  if (mode == "advance" || mode == "resident") {
+    // StrangIntegrator::advance step by step (oracles::reference_solution-style callers): the reference
+    // and the drop-in side by side, V compared after every step (ORd, C1 line, k0_down = 3, 20 ms);
+    // "resident": the drop-in keeps the state on the device (set_state_residency), the cell states come
+    // back at the end through sync_state()
+    cfg.t_end_ms = 20.0;
+    StrangIntegrator ref(setup, cfg);
+    gpu::StrangIntegrator dev(setup, cfg);
+    if (mode == "resident") dev.set_state_residency(true);
+    NodeStateArray sa = s0, sb = s0;
+    const std::int64_t n_steps = static_cast<std::int64_t>(std::ceil(cfg.t_end_ms / cfg.dt_ms - 1e-9));
+    double dv = 0.0;
+    for (std::int64_t k = 0; k < n_steps; ++k) {
+      ref.advance(sa, k * cfg.dt_ms, k, n_steps);
+      dev.advance(sb, k * cfg.dt_ms, k, n_steps);
+      for (std::size_t i = 0; i < sa.v.size(); ++i) dv = std::max(dv, std::abs(sa.v[i] - sb.v[i]));
+    }
+    if (mode == "resident") dev.sync_state(sb);
+    double ds = 0.0;
+    for (std::size_t i = 0; i < sa.s.size(); ++i) ds = std::max(ds, std::abs(sa.s[i] - sb.s[i]) / (1.0 + std::abs(sa.s[i])));
+    const bool kh = ref.k_histogram() == dev.k_histogram();
+    const bool pass = dv <= 1e-6 && ds <= 1e-9 && kh;
+    std::printf("{\"mode\":\"%s\",\"steps\":%lld,\"max_dV_mV\":%.3e,\"max_rel_dstate\":%.3e,\"khist_equal\":%s,"
+                "\"pass\":%s}\n",
+                mode.c_str(), static_cast<long long>(n_steps), dv, ds, kh ? "true" : "false", pass ? "true" : "false");
+    return pass ? 0 : 1;
+  }
   // snapshots (asynchronous in the drop-in) and progress callbacks
   std::vector<std::pair<double, std::vector<double>>> snaps[2];
   int which = 0;

@@ -79,6 +79,7 @@ _SIGS = {
     "cwg_get_khist": (C.c_int, [C.c_void_p, _lp, C.c_int]),
     "cwg_get_traces": (C.c_int, [C.c_void_p, _dp, _dp]),
     "cwg_get_maps": (C.c_int, [C.c_void_p, _dp, _u8p, _dp, _u8p]),
+    "cwg_trim_pool": (None, []),
     "cwg_gather_result": (C.c_int, [C.c_void_p, _dp, _dp, C.c_int, _dp, _dp, _u8p, _dp, _u8p]),
     "cwg_get_timing": (C.c_int, [C.c_void_p, _dp, _dp, _dp]),
     "cwg_launch_count": (C.c_int64, [C.c_void_p]),

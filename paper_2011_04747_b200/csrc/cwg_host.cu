@@ -12,6 +12,9 @@
 #include <cmath>
 #include <cstdio>
 #include <chrono>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -159,17 +162,97 @@ Nccl g_nccl;
     if (_r != ncclSuccess) throw Fail{CWG_ECUDA, std::string("NCCL error: ") + g_nccl.errstr(_r)};    \
   } while (0)
 
+// Caching device allocator. A run_simulation-style caller builds a context
+// per run (the reference's run_simulation constructs its StrangIntegrator);
+// at C4 that is ~1.5 GB in a dozen cudaMallocs, 20-60 ms per context
+// (tools/e2e_phases.py). Freed blocks are kept per (device, rounded size) and
+// handed to the next allocation of that size; cwg_trim_pool() returns them.
+// Contexts synchronise their streams before freeing (ctx_free), since
+// reusing a block skips cudaFree's implicit device synchronisation.
+// CWG_POOL=0 disables caching.
+struct DevPool {
+  std::mutex mu;
+  std::multimap<std::pair<int, size_t>, void*> free_blocks;
+  std::unordered_map<void*, std::pair<int, size_t>> live;
+  size_t cached = 0;
+  static constexpr size_t kCap = 32ull << 30;  // at most 32 GiB kept
+  bool on = [] {
+    const char* e = getenv("CWG_POOL");
+    return !(e && e[0] == '0');
+  }();
+  static size_t round(size_t b) {
+    return b >= (1u << 20) ? (b + (2u << 20) - 1) / (2u << 20) * (2u << 20) : (b + 255) / 256 * 256;
+  }
+  void* get(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const size_t rb = round(bytes);
+    {
+      std::lock_guard<std::mutex> g(mu);
+      auto it = free_blocks.find({dev, rb});
+      if (it != free_blocks.end()) {
+        void* p = it->second;
+        free_blocks.erase(it);
+        cached -= rb;
+        live[p] = {dev, rb};
+        return p;
+      }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, rb);
+    if (e != cudaSuccess && cached > 0) {  // device full: release the cache and retry once
+      cudaGetLastError();
+      trim();
+      e = cudaMalloc(&p, rb);
+    }
+    CUDA_TRY(e);
+    std::lock_guard<std::mutex> g(mu);
+    live[p] = {dev, rb};
+    return p;
+  }
+  void put(void* p) {
+    std::unique_lock<std::mutex> g(mu);
+    auto it = live.find(p);
+    if (it == live.end()) {  // not ours (never happens) -- plain free
+      g.unlock();
+      cudaFree(p);
+      return;
+    }
+    const auto key = it->second;
+    live.erase(it);
+    if (on && cached + key.second <= kCap) {
+      free_blocks.insert({key, p});
+      cached += key.second;
+      return;
+    }
+    g.unlock();
+    cudaFree(p);
+  }
+  void trim() {
+    std::vector<void*> v;
+    {
+      std::lock_guard<std::mutex> g(mu);
+      for (auto& kv : free_blocks) v.push_back(kv.second);
+      free_blocks.clear();
+      cached = 0;
+    }
+    for (void* p : v) cudaFree(p);
+  }
+};
+DevPool& dev_pool() {
+  static DevPool* pool = new DevPool();  // never destroyed: no cudaFree after the driver shuts down
+  return *pool;
+}
+
 template <class T>
 T* dev_alloc(size_t count) {
-  void* p = nullptr;
   if (count == 0) count = 1;
-  CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
-  return static_cast<T*>(p);
+  return static_cast<T*>(dev_pool().get(count * sizeof(T)));
 }
 
 template <class T>
 void dev_free(T*& p) {
-  if (p) cudaFree(p);
+  if (p) dev_pool().put(p);
   p = nullptr;
 }
 
@@ -183,6 +266,8 @@ struct Bin {
   long long first = 0, count = 0;
   int grid = 1;
   unsigned* d_counter = nullptr;  // [0] counter, [1] done
+  unsigned* d_counter_b = nullptr;  // boundary-first split (y-slab runs): [0..1] lower rows, [2..3] upper rows
+  int variant_b = 0, grid_b = 1;   // launch shape of the edge-row ranges
 };
 
 struct cwg_ctx {
@@ -270,6 +355,14 @@ struct cwg_ctx {
   long long restored_seq = -1;  // failure whose state restore_failed_state already put in place
 
   // multi-GPU
+  // boundary-first reaction (world > 1, dense model bins): the split_rows owned
+  // rows/planes at each slab edge -- what the neighbours' first diffusion
+  // launch needs -- run as launches of their own (on `side` under NCCL, so the
+  // halo exchange overlaps the interior reaction on the solver stream)
+  bool split = false;
+  long long split_rows = 0;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ncclComm_t comm = nullptr;
   bool loopback = false;  // world > 1 without NCCL: halos copied by cwg_loopback_steps (testing hook)
 
@@ -309,12 +402,20 @@ namespace {
 void ctx_free(cwg_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  // pooled blocks may be handed out again at once: no kernel of this context may still use them
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->snap_stream) cudaStreamSynchronize(c->snap_stream);
   for (auto& gx : c->graph_p)
     if (gx) cudaGraphExecDestroy(gx);
   for (auto& b : c->bins) {
     dev_free(b.d_list);
     dev_free(b.d_counter);
+    dev_free(b.d_counter_b);
   }
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   dev_free(c->d_v[0]);
   dev_free(c->d_v[1]);
   dev_free(c->d_S);
@@ -383,7 +484,7 @@ struct DevScope {
   }
   ~DevScope() {
     for (void* p : ptrs)
-      if (p) cudaFree(p);
+      if (p) dev_pool().put(p);
   }
 };
 
@@ -415,17 +516,18 @@ HaloPlan halo_plan(const cwg_ctx* c, double* buf, int rows) {
   return h;
 }
 
-void halo_exchange(cwg_ctx* c, double* buf, int rows) {
+void halo_exchange(cwg_ctx* c, double* buf, int rows, cudaStream_t st = nullptr) {
   if (c->world <= 1 || c->loopback) return;
+  if (!st) st = c->stream;
   const HaloPlan h = halo_plan(c, buf, rows);
   NCCL_TRY(g_nccl.gstart());
   if (h.lo) {
-    NCCL_TRY(g_nccl.send(h.send_lo, h.n, ncclDouble, c->rank - 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(h.recv_lo, h.n, ncclDouble, c->rank - 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.send(h.send_lo, h.n, ncclDouble, c->rank - 1, c->comm, st));
+    NCCL_TRY(g_nccl.recv(h.recv_lo, h.n, ncclDouble, c->rank - 1, c->comm, st));
   }
   if (h.hi) {
-    NCCL_TRY(g_nccl.send(h.send_hi, h.n, ncclDouble, c->rank + 1, c->comm, c->stream));
-    NCCL_TRY(g_nccl.recv(h.recv_hi, h.n, ncclDouble, c->rank + 1, c->comm, c->stream));
+    NCCL_TRY(g_nccl.send(h.send_hi, h.n, ncclDouble, c->rank + 1, c->comm, st));
+    NCCL_TRY(g_nccl.recv(h.recv_hi, h.n, ncclDouble, c->rank + 1, c->comm, st));
   }
   NCCL_TRY(g_nccl.gend());
 }
@@ -541,7 +643,7 @@ void launch_diffusion_group(cwg_ctx* c, int T, const double* vin, double* vout, 
   ++c->launches;
 }
 
-void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
+void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0, bool first_exchanged = false) {
   // ceil(count / fuse) launches with balanced group sizes; every launch flips
   // the V double buffer (graphs are kept per starting parity)
   const std::vector<int> groups = diffusion_groups(c, count);
@@ -549,7 +651,7 @@ void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0) {
     const int T = groups[static_cast<size_t>(gi)];
     double* vin = c->d_v[c->cur];
     double* vout = c->d_v[c->cur ^ 1];
-    halo_exchange(c, vin, T);
+    if (!(gi == 0 && first_exchanged)) halo_exchange(c, vin, T);
     // threshold probe runs: no NaN scan after diffusion (stimulus.cpp:106) -> unchecked launch
     launch_diffusion_group(c, T, vin, vout, c->fixed_step ? nullptr : c->d_err, step_off, ev0 + q);
     c->cur ^= 1;
@@ -620,9 +722,35 @@ ReactArgs react_args(const cwg_ctx* c, const Bin& b, long long step_off, int ev,
   return a;
 }
 
-void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double t_fixed) {
+// One reaction launch of bin b over the dense local range [first, first + count)
+// with its own self-resetting counter pair (concurrent launches never share one).
+void launch_bin_range(cwg_ctx* c, const Bin& b, long long first, long long count, unsigned* counter, int variant,
+                      int grid, cudaStream_t st, long long step_off, int ev, bool use_t, double t_fixed) {
+  if (count <= 0) return;
+  ReactArgs a = react_args(c, b, step_off, ev, use_t, t_fixed);
+  a.first = first;
+  a.count = count;
+  a.counter = counter;
+  a.done = counter + 1;
+  cudaError_t e = is_ord(b.kind) ? launch_react_ord(b.kind, variant, a, grid, st)
+                                 : launch_react_exact(b.kind, a, grid, st);
+  CUDA_TRY(e);
+  ++c->launches;
+}
+
+// bst: stream of the boundary-first launches (split runs; default the solver stream)
+void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double t_fixed, cudaStream_t bst = nullptr) {
   for (auto& b : c->bins) {
     if (b.count == 0) continue;
+    if (c->split && !b.d_list) {  // edge rows first, then the interior (node-local: same bits in any order)
+      const long long e = c->split_rows * c->w, lo = c->halo, hi = c->halo + c->n_own;
+      const cudaStream_t es = bst ? bst : c->stream;
+      launch_bin_range(c, b, lo, e, b.d_counter_b, b.variant_b, b.grid_b, es, step_off, ev, use_t, t_fixed);
+      launch_bin_range(c, b, hi - e, e, b.d_counter_b + 2, b.variant_b, b.grid_b, es, step_off, ev, use_t, t_fixed);
+      launch_bin_range(c, b, lo + e, c->n_own - 2 * e, b.d_counter, b.variant, b.grid, c->stream, step_off, ev, use_t,
+                       t_fixed);
+      continue;
+    }
     ReactArgs a = react_args(c, b, step_off, ev, use_t, t_fixed);
     if (getenv("CWG_REACT_TRACE") && b.grid <= 4096) {
       if (!g_react_trace) CUDA_TRY(cudaMalloc(&g_react_trace, 16 * 4096 * sizeof(unsigned long long)));
@@ -637,7 +765,20 @@ void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double
 }
 
 // Reaction then the step's merged diffusion sub-steps (steps A and B/III).
+// NCCL y-slab runs overlap the first halo exchange with the reaction: the slab
+// edge rows react first on the side stream, their exchange follows there while
+// the interior reacts on the solver stream, and the diffusion joins both.
 void enqueue_react_then_diffuse(cwg_ctx* c, long long step_off, int count, bool use_t, double t_fixed) {
+  if (c->split && c->side && !c->loopback) {
+    CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
+    CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+    enqueue_reaction(c, step_off, c->l, use_t, t_fixed, c->side);
+    halo_exchange(c, c->d_v[c->cur], diffusion_groups(c, count).front(), c->side);
+    CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+    CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    enqueue_diffusion(c, count, step_off, c->l + 1, true);
+    return;
+  }
   enqueue_reaction(c, step_off, c->l, use_t, t_fixed);
   enqueue_diffusion(c, count, step_off, c->l + 1);
 }
@@ -1103,7 +1244,8 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   std::vector<long long> per_model(static_cast<size_t>(p->n_models), 0);
   for (long long o = 0; o < c->n_own; ++o) {
     const int m = p->model_of_node[c->own_global0 + o];
-    validation(m < p->n_models, "initial state: node " + std::to_string(c->own_global0 + o) + " has no model");
+    if (m >= p->n_models)  // (message built only on failure: this loop runs over every node)
+      validation(false, "initial state: node " + std::to_string(c->own_global0 + o) + " has no model");
     ++per_model[static_cast<size_t>(m)];
   }
   for (int m = 0; m < p->n_models; ++m) {
@@ -1129,6 +1271,30 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     b.d_counter = dev_alloc<unsigned>(2);
     CUDA_TRY(cudaMemset(b.d_counter, 0, 2 * sizeof(unsigned)));
     c->bins.push_back(b);
+  }
+  // boundary-first split of the reaction (y-slab runs): the rows a neighbour's
+  // first fused diffusion launch reads (hrows_v, >= its fused depth)
+  c->split_rows = c->hrows_v;
+  c->split = c->world > 1 && c->op_kind != CWG_OP_CSR && c->n_own >= 4 * c->split_rows * c->w &&
+             getenv("CWG_SPLIT") == nullptr;
+  if (c->split) {
+    for (auto& b : c->bins)
+      if (!b.d_list && b.count > 0) {
+        b.d_counter_b = dev_alloc<unsigned>(4);
+        CUDA_TRY(cudaMemset(b.d_counter_b, 0, 4 * sizeof(unsigned)));
+        const long long e = c->split_rows * c->w;
+        b.variant_b = choose_ord_variant(e, c->num_sms);
+        const int threads = is_ord(b.kind) ? react_ord_threads(b.variant_b) : react_exact_threads(b.kind);
+        const int occ = std::max(1, is_ord(b.kind) ? react_ord_occupancy(b.kind, b.variant_b)
+                                                   : react_exact_occupancy(b.kind));
+        b.grid_b = static_cast<int>(std::max<long long>(
+            1, std::min<long long>((e + threads - 1) / threads, static_cast<long long>(occ) * c->num_sms)));
+      }
+    if (!c->loopback) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
   }
   if (p->gkr_scale) {
     std::vector<double> g(static_cast<size_t>(c->n_alloc), 1.0);
@@ -1242,8 +1408,10 @@ void reset_error(cwg_ctx* c) {
   CUDA_TRY(cudaMemcpyAsync(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice, c->stream));
   // the reaction bins' work/done counters reset themselves at the end of
   // every launch; zero them here too so no earlier launch can leave them stale
-  for (const auto& b : c->bins)
+  for (const auto& b : c->bins) {
     if (b.d_counter) CUDA_TRY(cudaMemsetAsync(b.d_counter, 0, 2 * sizeof(unsigned), c->stream));
+    if (b.d_counter_b) CUDA_TRY(cudaMemsetAsync(b.d_counter_b, 0, 4 * sizeof(unsigned), c->stream));
+  }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
 }
 
@@ -1851,18 +2019,28 @@ int cwg_get_maps(cwg_ctx* c, double* lat, uint8_t* lat_valid, double* apd, uint8
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    // straight into the caller's arrays (no host temporaries), then NaN where a map has no value
     const size_t n = static_cast<size_t>(c->n_own);
-    std::vector<double> L(n), A(n);
-    std::vector<unsigned char> lv(n), av(n);
-    CUDA_TRY(cudaMemcpy(L.data(), c->det.lat, n * sizeof(double), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(A.data(), c->det.apd, n * sizeof(double), cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(lv.data(), c->det.has_lat, n, cudaMemcpyDeviceToHost));
-    CUDA_TRY(cudaMemcpy(av.data(), c->det.has_apd, n, cudaMemcpyDeviceToHost));
+    std::vector<unsigned char> lv_tmp, av_tmp;
+    unsigned char* lv = lat_valid;
+    unsigned char* av = apd_valid;
+    if (!lv && lat) {
+      lv_tmp.resize(n);
+      lv = lv_tmp.data();
+    }
+    if (!av && apd) {
+      av_tmp.resize(n);
+      av = av_tmp.data();
+    }
+    if (lat) CUDA_TRY(cudaMemcpyAsync(lat, c->det.lat, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (apd) CUDA_TRY(cudaMemcpyAsync(apd, c->det.apd, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (lv) CUDA_TRY(cudaMemcpyAsync(lv, c->det.has_lat, n, cudaMemcpyDeviceToHost, c->stream));
+    if (av) CUDA_TRY(cudaMemcpyAsync(av, c->det.has_apd, n, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const double nan = std::nan("");
     for (size_t i = 0; i < n; ++i) {
-      if (lat) lat[i] = lv[i] ? L[i] : std::nan("");
-      if (lat_valid) lat_valid[i] = lv[i];
-      if (apd) apd[i] = av[i] ? A[i] : std::nan("");
-      if (apd_valid) apd_valid[i] = av[i];
+      if (lat && !lv[i]) lat[i] = nan;
+      if (apd && !av[i]) apd[i] = nan;
     }
   });
 }
@@ -1961,6 +2139,8 @@ int cwg_gather_result(cwg_ctx* c, double* v, double* s_aos, int stride, double* 
     if (apd_valid) std::memcpy(apd_valid, av.data(), static_cast<size_t>(N));
   });
 }
+
+void cwg_trim_pool(void) { dev_pool().trim(); }
 
 int cwg_get_timing(cwg_ctx* c, double* r, double* d, double* rec) {
   *r = c->t_react;

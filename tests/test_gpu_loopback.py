@@ -127,3 +127,58 @@ def test_loopback_c2_single_substep_launches():
     out, kh = _loopback(p, 2)
     ref = _single(p)
     assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
+
+
+def _loopback_full(p, world):
+    """Loopback run that also assembles the global traces (each probe recorded by its owning rank) and the
+    LAT/APD maps (each rank's y-slab rows) like cwg_gather_result does over NCCL."""
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import _lib as L
+    setup = p.setup()
+    integs = [cw.StrangIntegrator(setup, p.cfg, model_of_node=p.model_of_node, rank=r, world=world)
+              for r in range(world)]
+    try:
+        st = p.initial_state()
+        for it in integs:
+            it.upload(st)
+            it.run_begin()
+        n = integs[0].info.n_steps
+        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
+        rc = L.lib().cwg_loopback_steps(hs, world, 0, n)
+        assert rc == 0, L.lib().cwg_last_error().decode()
+        out = p.initial_state()
+        lat, lv = np.zeros(p.n), np.zeros(p.n, bool)
+        apd, av = np.zeros(p.n), np.zeros(p.n, bool)
+        traces = None
+        plane = p.n // p.sheet.op.ny1
+        for r, it in enumerate(integs):
+            it.download(out)
+            rb, re = cw.slab_plan(p.sheet.op.ny1, world, r)
+            lm, am = it.maps()
+            lat[rb * plane:re * plane], lv[rb * plane:re * plane] = lm.value, lm.valid
+            apd[rb * plane:re * plane], av[rb * plane:re * plane] = am.value, am.valid
+            _, tv = it.traces()
+            traces = tv if traces is None else traces + tv  # a probe's non-owning ranks record 0
+        kh = sum(it.k_histogram() for it in integs)
+        return out, kh, traces, (lat, lv), (apd, av)
+    finally:
+        for it in integs:
+            it.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_c4_geometry_traces_and_maps(world):
+    """BASELINE configs[3] at full size (251 x 251 x 51) split into 2 / 4 / 8 y-slabs: state, k-histogram,
+    probe traces and LAT/APD maps bit-identical to the single-context run (the multi-GPU analogue of the
+    reference's worker-count determinism)."""
+    from paper_2011_04747_b200 import problems
+    p = problems.c4(t_end=8.0)
+    out, kh, tr, (lat, lv), (apd, av) = _loopback_full(p, world)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v)
+    assert np.array_equal(out.s, ref.final_state.s)
+    assert np.array_equal(kh, ref.k_histogram)
+    assert np.array_equal(tr, np.array([t.v_mv for t in ref.traces]))
+    assert np.array_equal(lv, ref.lat_map.valid) and np.array_equal(lat[lv], ref.lat_map.value[lv])
+    assert np.array_equal(av, ref.apd90_map.valid) and np.array_equal(apd[av], ref.apd90_map.value[av])
+    assert lv.sum() > 0  # the endocardial wave has activated nodes within the window

@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 EXE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "shim_parity")
 
 
-@pytest.mark.parametrize("mode", ["diffusion", "ap", "ord", "abort", "c2"])
+@pytest.mark.parametrize("mode", ["diffusion", "ap", "ord", "abort", "c2", "advance", "resident"])
 def test_cpp_dropin_matches_reference(mode):
     if not os.path.exists(EXE):
         pytest.skip("shim_parity not built (needs /root/reference at build time)")
@@ -27,3 +27,5 @@ def test_cpp_dropin_matches_reference(mode):
         assert line["snapshots"][0] == line["snapshots"][1] == 5  # t = 0, 0.5, ..., 2.0
     elif mode in ("ap", "ord", "c2"):
         assert line["snapshots"][0] == line["snapshots"][1] > 1 and line["pass"]
+    elif mode in ("advance", "resident"):
+        assert line["steps"] == 200 and line["pass"]
