@@ -3,7 +3,7 @@
 Run under ncu so that every reaction launch is counted:
   ncu --metrics smsp__sass_thread_inst_executed_op_dfma_pred_on.sum,\
 smsp__sass_thread_inst_executed_op_dmul_pred_on.sum,smsp__sass_thread_inst_executed_op_dadd_pred_on.sum \
-      -k regex:react_kernel --csv --log-file gpurun_out/flops.csv python tools/flops_per_eval.py
+      -k regex:react_kernel --csv --log-file gpurun_out/flops.csv python tools/flops_per_eval.py [c2|c4] [steps]
 then: python tools/flops_per_eval.py --parse gpurun_out/flops.csv gpurun_out/evals.txt
 """
 import csv
@@ -13,10 +13,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def run(out="gpurun_out/evals.txt", steps=60):
+def run(out="gpurun_out/evals.txt", steps=60, config="c2"):
     import paper_2011_04747_b200 as cw
     from paper_2011_04747_b200 import problems, _lib as L
-    p = problems.c2(t_end=steps * 0.1)
+    p = {"c2": problems.c2, "c4": problems.c4}[config](t_end=steps * 0.1)
     integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=p.model_of_node)
     integ.upload(p.initial_state())
     integ.run_begin()
@@ -43,5 +43,5 @@ def parse(csv_path, evals_path):
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--parse":
         parse(sys.argv[2], sys.argv[3])
-    else:
-        run()
+    else:  # [config (c2 | c4)] [steps]
+        run(config=sys.argv[1] if len(sys.argv) > 1 else "c2", steps=int(sys.argv[2]) if len(sys.argv) > 2 else 60)
