@@ -436,7 +436,8 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             summ = json.load(f)
-        traffic = summ.get("react_dram_bytes_per_launch")
+        # DRAM bytes per reaction launch from the ncu capture of the same configuration (C4; other configs: none)
+        traffic = summ.get("react_c4", {}).get("dram_bytes_per_launch") if args.config == "c4" else None
         pipe = summ.get("fp64_pipe_active_pct_of_active", {})
         pipe_ncu = pipe.get("c2_latency_shape" if args.config in ("c1", "c2") else "c4_throughput_shape")
     except (OSError, ValueError):
@@ -481,8 +482,10 @@ def main():
                                   "sub-steps sequential, so the step's largest k sets the critical path; the "
                                   "event-timed phase includes ~10 us of launch/completion latency around a ~42 us "
                                   "kernel span (tools/react_trace.py, DESIGN.md 3.5)" if args.config in ("c1", "c2") else
-                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 56% of "
-                                  "active cycles on C4 (profiles/r01_react_c4_digest.txt)")},
+                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 55% of "
+                                  "active cycles on C4, 8-cycle FP64 latency with 3 warps per sub-partition "
+                                  "(profiles/r02_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
+                                  "read+write per launch (algorithmic 677 B x 3.2M nodes = 2.18 GB)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
                                        ("diffuse_stencil2d_tbm (TMA)" if tma_path else "diffuse_stencil2d_tb")
@@ -491,6 +494,14 @@ def main():
                                    "frac": diff_gbs / peaks["hbm_gbs"] if peaks.get("hbm_gbs") else None,
                                    "peak_source": peak_src, "bytes_per_node_substep": diff_bytes,
                                    "launches_per_step": launches_per_step,
+                                   # the bit-exact row sum is 28 DMUL + 28 DADD per node-substep (27-point 3D /
+                                   # 10 + 10 in 2D): against 16 B of V the 3D kernel is FP64-bound, so its FP64
+                                   # fraction is reported beside the HBM one
+                                   "fp64_ops_per_node_substep": 56 if is3d else 20,
+                                   "fp64_tflops": (56 if is3d else 20) * info.n_local * 2 * info.l * K
+                                                  / (diff_tot_ms / 1e3) / 1e12,
+                                   "fp64_frac": ((56 if is3d else 20) * info.n_local * 2 * info.l * K
+                                                 / (diff_tot_ms / 1e3) / 1e12 / fp64_peak) if fp64_peak > 0 else None,
                                    "note": "phase time includes probe/detector recording and the ~6 us that any "
                                            "kernel between two CUDA events costs here (DESIGN.md 3.5)"},
             "clocks": clocks.summary(), "gpu_launches": int(launches),
