@@ -49,10 +49,10 @@ UNIT = "node-updates/s"
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<epi>>
 # (2*DFMA + DMUL + DADD predicated-on lane ops / evaluations), counted by ncu
-# over every reaction launch of a 60-step C2 run (tools/flops_per_eval.py;
-# profiles/r01_flops_per_eval_c2.txt): 1054.3 DFMA + 442.6 DMUL + 299.3 DADD.
-# Updated when the kernel changes.
-ORD_FP64_FLOPS_PER_EVAL = 2850.6
+# over every reaction launch of a 40-step C4 run (tools/flops_per_eval.py c4 40;
+# profiles/r02_flops_per_eval_c4.txt): 996.1 DFMA + 443.3 DMUL + 300.4 DADD
+# (C2: 2,734.6). Updated when the kernel changes.
+ORD_FP64_FLOPS_PER_EVAL = 2735.9
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 

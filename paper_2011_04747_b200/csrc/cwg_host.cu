@@ -768,18 +768,23 @@ void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double
 // NCCL y-slab runs overlap the first halo exchange with the reaction: the slab
 // edge rows react first on the side stream, their exchange follows there while
 // the interior reacts on the solver stream, and the diffusion joins both.
-void enqueue_react_then_diffuse(cwg_ctx* c, long long step_off, int count, bool use_t, double t_fixed) {
+// mid_event (bench phase timing, graph capture): recorded on the solver stream
+// once the reaction is enqueued there (the interior part, under the split).
+void enqueue_react_then_diffuse(cwg_ctx* c, long long step_off, int count, bool use_t, double t_fixed,
+                                cudaEvent_t mid_event = nullptr) {
   if (c->split && c->side && !c->loopback) {
     CUDA_TRY(cudaEventRecord(c->ev_fork, c->stream));
     CUDA_TRY(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
     enqueue_reaction(c, step_off, c->l, use_t, t_fixed, c->side);
     halo_exchange(c, c->d_v[c->cur], diffusion_groups(c, count).front(), c->side);
     CUDA_TRY(cudaEventRecord(c->ev_join, c->side));
+    if (mid_event) CUDA_TRY(cudaEventRecordWithFlags(mid_event, c->stream, cudaEventRecordExternal));
     CUDA_TRY(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     enqueue_diffusion(c, count, step_off, c->l + 1, true);
     return;
   }
   enqueue_reaction(c, step_off, c->l, use_t, t_fixed);
+  if (mid_event) CUDA_TRY(cudaEventRecordWithFlags(mid_event, c->stream, cudaEventRecordExternal));
   enqueue_diffusion(c, count, step_off, c->l + 1);
 }
 
@@ -873,10 +878,9 @@ StepGraph& step_graph(cwg_ctx* c, long long step, StepGraph* cache, bool events 
   CUDA_TRY(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
     if (events) CUDA_TRY(cudaEventRecordWithFlags(tmp[0], c->stream, cudaEventRecordExternal));
-    enqueue_reaction(c, 0, c->l, false, 0.0);
-    if (events) CUDA_TRY(cudaEventRecordWithFlags(tmp[1], c->stream, cudaEventRecordExternal));
+    // the production step (boundary-first reaction + overlapped exchange under a y-slab split)
+    enqueue_react_then_diffuse(c, 0, 2 * c->l, false, 0.0, events ? tmp[1] : nullptr);
     const long long base = step;
-    enqueue_diffusion(c, 2 * c->l, 0, c->l + 1);
     if (flags & 1) {
       CUDA_TRY(launch_record_probes(c->d_v[c->cur], c->d_probe_loc, c->n_probes, c->d_traces, c->d_clock, 1, c->spr,
                                     c->stream));
