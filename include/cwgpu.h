@@ -174,6 +174,12 @@ int cwg_set_scheme(cwg_ctx* ctx, int scheme, double dt_ms, double t_end_ms, int 
  * would. Everything but the transport (slab kernels, offsets, failure keys,
  * recording) runs as on N GPUs. Call cwg_run_begin on each rank first. */
 int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t count);
+/* No reference counterpart (testing hook of the peer-memory transport): link
+ * loopback rank contexts the way NCCL ranks are linked over IPC at creation
+ * (PeerLink: each diffusion launch stores the neighbours' halo rows into their
+ * V buffers and paces itself on launch counters). cwg_loopback_steps then runs
+ * the peer-memory data path instead of copying halos. */
+int cwg_loopback_link(cwg_ctx* const* ranks, int world);
 
 /* Asynchronous V snapshot for on_snapshot (splitting.cpp:267-277): enqueue,
  * after the steps issued so far, a device-side copy of V and of the failure

@@ -95,6 +95,7 @@ _SIGS = {
     "cwg_set_scheme": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
                                  C.POINTER(cwg_error)]),
     "cwg_loopback_steps": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int64, C.c_int64]),
+    "cwg_loopback_link": (C.c_int, [C.POINTER(C.c_void_p), C.c_int]),
     "cwg_snapshot_begin": (C.c_int, [C.c_void_p, _dp]),
     "cwg_snapshot_wait": (C.c_int, [C.c_void_p, C.POINTER(cwg_error)]),
     "cwg_host_register": (C.c_int, [C.c_void_p, C.c_size_t]),

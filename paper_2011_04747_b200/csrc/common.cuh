@@ -102,6 +102,78 @@ struct ReactArgs {
   int preclaim;         // claim a finishing lane's next node one trip ahead (react.cuh)
 };
 
+// Peer-memory halo link of a y-slab rank (multi-GPU without NCCL on the data
+// path): a diffusion launch stores the rows/planes its neighbours need straight
+// into their V buffers over NVLink (IPC-mapped), and the ranks pace each other
+// with launch counters: every halo-writing launch first waits until both
+// neighbours completed as many such launches as this rank (their data for it
+// is in place and they no longer read the buffers it is about to write), and
+// its last block publishes the new count into the neighbours' memory
+// (release/acquire at system scope). Loopback contexts on one device link the
+// same way (cwg_loopback_link), which is how the data path is tested.
+struct PeerLink {
+  int on = 0;
+  long long w = 0;     // nodes per row / plane
+  long long rows = 0;  // owned rows / planes
+  // this rank's owned row r (0-based) -> lo_dst[p][r*w + x] (neighbour rank-1's upper halo rows) for
+  // rows r < H; row rows-j -> hi_dst[p][-j*w + x] (rank+1's lower halo) for j <= H; p = buffer parity
+  double* lo_dst[2] = {nullptr, nullptr};
+  double* hi_dst[2] = {nullptr, nullptr};
+  unsigned long long* wait_lo = nullptr;  // local: launches completed by rank-1 (written by it)
+  unsigned long long* wait_hi = nullptr;  // local: launches completed by rank+1
+  unsigned long long* post_lo = nullptr;  // remote: rank-1's wait_hi
+  unsigned long long* post_hi = nullptr;  // remote: rank+1's wait_lo
+  unsigned long long* count = nullptr;    // local: halo-writing launches this rank completed
+  unsigned* blocks_done = nullptr;        // local: block arrivals of the running launch
+  long long lim = 1;                      // halo rows a neighbour keeps (2D: hrows_v; 3D: one plane)
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Block entry of a halo-writing launch: wait for the neighbours (bounded; a
+// neighbour that never arrives traps instead of hanging the device).
+__device__ __forceinline__ void peer_wait(const PeerLink& pl) {
+  if (!pl.on) return;
+  if (threadIdx.x == 0) {
+    const unsigned long long need = *reinterpret_cast<volatile unsigned long long*>(pl.count);
+    for (long long it = 0;; ++it) {
+      const bool lo = !pl.wait_lo || ld_acquire_sys(pl.wait_lo) >= need;
+      const bool hi = !pl.wait_hi || ld_acquire_sys(pl.wait_hi) >= need;
+      if (lo && hi) break;
+      if (it > (1ll << 28)) __trap();  // minutes: a rank is gone (trap instead of hanging the device)
+      __nanosleep(64);
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");  // the peers' stores before our bulk copies
+  }
+  __syncthreads();
+}
+
+// Block exit: after this block's peer stores; the last block publishes the count.
+__device__ __forceinline__ void peer_post(const PeerLink& pl) {
+  if (!pl.on) return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(pl.blocks_done) : "memory");
+    if (prev == gridDim.x * gridDim.y * gridDim.z - 1) {  // (the fused 2D kernel has a 2D grid)
+      *pl.blocks_done = 0u;
+      const unsigned long long n = *pl.count + 1;
+      *pl.count = n;
+      __threadfence_system();
+      if (pl.post_lo) st_release_sys(pl.post_lo, n);
+      if (pl.post_hi) st_release_sys(pl.post_hi, n);
+    }
+  }
+}
+
 struct DiffArgs {
   const double* vin;
   double* vout;
@@ -114,7 +186,18 @@ struct DiffArgs {
   long long evs;
   int ev;
   long long node_offset;
+  PeerLink pl;      // peer-memory halo stores (multi-GPU P2P transport), off by default
+  int out_par = 0;  // parity (index in the context's V pair) of vout
 };
+
+// this rank's output value of owned row `r`, column offset `xo` (within the row / plane) to the
+// neighbours that keep it as a halo row: rows r < lim go down, rows r >= rows - lim go up
+__device__ __forceinline__ void peer_store(const DiffArgs& a, long long r, long long xo, double val) {
+  const PeerLink& pl = a.pl;
+  if (!pl.on) return;
+  if (r < pl.lim && pl.lo_dst[a.out_par]) pl.lo_dst[a.out_par][r * pl.w + xo] = val;
+  if (r >= pl.rows - pl.lim && pl.hi_dst[a.out_par]) pl.hi_dst[a.out_par][(r - pl.rows) * pl.w + xo] = val;
+}
 
 __device__ __forceinline__ long long cur_seq(const long long* clock, long long step_off, long long evs,
                                              int ev) {

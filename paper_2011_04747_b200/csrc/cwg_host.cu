@@ -135,6 +135,7 @@ struct Nccl {
   decltype(&ncclGroupEnd) gend = nullptr;
   decltype(&ncclAllReduce) allreduce = nullptr;
   decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclAllGather) allgather = nullptr;
   decltype(&ncclGetErrorString) errstr = nullptr;
   bool load() {
     if (h) return true;
@@ -151,7 +152,8 @@ struct Nccl {
     allreduce = reinterpret_cast<decltype(allreduce)>(dlsym(h, "ncclAllReduce"));
     errstr = reinterpret_cast<decltype(errstr)>(dlsym(h, "ncclGetErrorString"));
     bcast = reinterpret_cast<decltype(bcast)>(dlsym(h, "ncclBroadcast"));
-    return init && destroy && send && recv && gstart && gend && allreduce && errstr && bcast;
+    allgather = reinterpret_cast<decltype(allgather)>(dlsym(h, "ncclAllGather"));
+    return init && destroy && send && recv && gstart && gend && allreduce && errstr && bcast && allgather;
   }
 };
 Nccl g_nccl;
@@ -361,6 +363,13 @@ struct cwg_ctx {
   // halo exchange overlaps the interior reaction on the solver stream)
   bool split = false;
   long long split_rows = 0;
+  // peer-memory halo transport (default for NCCL y-slab runs whose neighbours are peer-accessible, and for
+  // linked loopback contexts): diffusion launches store the neighbours' halo rows themselves (PeerLink)
+  bool p2p = false;
+  bool halo_fresh = false;  // the last enqueued V writer already pushed the current halos (capture-time state)
+  PeerLink pl;
+  unsigned long long* d_flags = nullptr;  // [0] wait_lo, [1] wait_hi, [2] count, [3] blocks_done
+  std::vector<void*> ipc_opened;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ncclComm_t comm = nullptr;
@@ -412,6 +421,9 @@ void ctx_free(cwg_ctx* c) {
     dev_free(b.d_counter);
     dev_free(b.d_counter_b);
   }
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  c->ipc_opened.clear();
+  dev_free(c->d_flags);
   if (c->side) cudaStreamSynchronize(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
@@ -516,7 +528,14 @@ HaloPlan halo_plan(const cwg_ctx* c, double* buf, int rows) {
   return h;
 }
 
+cudaError_t push_halo_now(cwg_ctx* c, const double* buf, cudaStream_t st);
+
 void halo_exchange(cwg_ctx* c, double* buf, int rows, cudaStream_t st = nullptr) {
+  if (c->p2p) {  // peer-memory transport: only a V writer that did not push its halos needs a push
+    if (!c->halo_fresh) CUDA_TRY(push_halo_now(c, buf, st ? st : c->stream));
+    c->halo_fresh = true;
+    return;
+  }
   if (c->world <= 1 || c->loopback) return;
   if (!st) st = c->stream;
   const HaloPlan h = halo_plan(c, buf, rows);
@@ -624,6 +643,10 @@ void launch_diffusion_group(cwg_ctx* c, int T, const double* vin, double* vout, 
   a.evs = c->evs;
   a.ev = ev;
   a.node_offset = c->own_global0;
+  if (c->p2p && err) {  // (the unchecked replay of restore_failed_state never runs on linked ranks)
+    a.pl = c->pl;
+    a.out_par = vout == c->d_v[1] ? 1 : 0;
+  }
   if (c->op_kind == CWG_OP_STENCIL2D) {
     Stencil2D s{c->d_coef, c->n_coef, c->d_cm, c->w, c->row_end - c->row_begin, c->row_begin, c->ny1,
                 c->hrows_v, c->hrows_c};
@@ -641,6 +664,18 @@ void launch_diffusion_group(cwg_ctx* c, int T, const double* vin, double* vout, 
     CUDA_TRY(launch_diffuse_csr(a, m, c->num_sms * 16, c->stream));
   }
   ++c->launches;
+  if (a.pl.on) c->halo_fresh = true;  // this launch stored the neighbours' halo rows of vout
+}
+
+// P2P: push this rank's edge rows of `buf` (one of the context's V pair) into the neighbours' halos
+cudaError_t push_halo_now(cwg_ctx* c, const double* buf, cudaStream_t st) {
+  DiffArgs a{};
+  a.vin = buf;
+  a.halo = c->halo;
+  a.pl = c->pl;
+  a.out_par = buf == c->d_v[1] ? 1 : 0;
+  ++c->launches;
+  return launch_push_halo(a, st);
 }
 
 void enqueue_diffusion(cwg_ctx* c, int count, long long step_off, int ev0, bool first_exchanged = false) {
@@ -740,6 +775,7 @@ void launch_bin_range(cwg_ctx* c, const Bin& b, long long first, long long count
 
 // bst: stream of the boundary-first launches (split runs; default the solver stream)
 void enqueue_reaction(cwg_ctx* c, long long step_off, int ev, bool use_t, double t_fixed, cudaStream_t bst = nullptr) {
+  c->halo_fresh = false;  // V changes in place: the neighbours' copies of the edge rows are stale
   for (auto& b : c->bins) {
     if (b.count == 0) continue;
     if (c->split && !b.d_list) {  // edge rows first, then the interior (node-local: same bits in any order)
@@ -1062,6 +1098,114 @@ void configure_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int
   c->G = G <= 200 ? G : 0;
 }
 
+// ------------------------------------------------------------------ peer-memory halo link
+bool p2p_eligible(const cwg_ctx* c) {
+  if (c->world <= 1) return false;
+  if (const char* e = getenv("CWG_P2P"))
+    if (e[0] == '0') return false;
+  if (c->op_kind == CWG_OP_CSR) return false;
+  return c->row_end - c->row_begin >= 2 * c->hrows_v;  // the edge rows of the two sides do not overlap
+}
+
+// Fill c->pl from the neighbours' buffers (loopback: other contexts' pointers; NCCL ranks: IPC-mapped).
+void set_peer_link(cwg_ctx* c, double* const lo_v[2], long long lo_halo, long long lo_own, unsigned long long* lo_flags,
+                   double* const hi_v[2], long long hi_halo, unsigned long long* hi_flags) {
+  PeerLink& pl = c->pl;
+  pl.on = 1;
+  pl.w = c->w;
+  pl.rows = c->row_end - c->row_begin;
+  pl.lim = c->op_kind == CWG_OP_STRUCT3D ? 1 : c->hrows_v;
+  for (int p = 0; p < 2; ++p) {
+    pl.lo_dst[p] = lo_v[p] ? lo_v[p] + lo_halo + lo_own : nullptr;  // rank-1's upper halo rows
+    pl.hi_dst[p] = hi_v[p] ? hi_v[p] + hi_halo : nullptr;           // rank+1's first owned node
+  }
+  pl.wait_lo = lo_flags ? c->d_flags + 0 : nullptr;
+  pl.wait_hi = hi_flags ? c->d_flags + 1 : nullptr;
+  pl.post_lo = lo_flags ? lo_flags + 1 : nullptr;
+  pl.post_hi = hi_flags ? hi_flags + 0 : nullptr;
+  pl.count = c->d_flags + 2;
+  pl.blocks_done = reinterpret_cast<unsigned*>(c->d_flags + 3);
+  c->p2p = true;
+  c->split = false;  // the halo goes out with the launches themselves
+}
+
+void alloc_flags(cwg_ctx* c) {
+  if (c->d_flags) return;
+  c->d_flags = dev_alloc<unsigned long long>(4);
+  CUDA_TRY(cudaMemset(c->d_flags, 0, 4 * sizeof(unsigned long long)));
+}
+
+// NCCL ranks: exchange IPC handles of both V buffers and the flag words with an
+// allgather, map the two neighbours'. All ranks agree (allreduce min) or all
+// keep the NCCL transport.
+struct P2PInfo {
+  cudaIpcMemHandle_t hv[2], hf;
+  long long halo, n_own;
+  int ok, pad;
+};
+
+void setup_p2p_nccl(cwg_ctx* c) {
+  if (!p2p_eligible(c) || c->loopback || !c->comm) return;
+  alloc_flags(c);
+  P2PInfo mine{};
+  mine.ok = 1;
+  if (cudaIpcGetMemHandle(&mine.hv[0], c->d_v[0]) != cudaSuccess ||
+      cudaIpcGetMemHandle(&mine.hv[1], c->d_v[1]) != cudaSuccess || cudaIpcGetMemHandle(&mine.hf, c->d_flags) != cudaSuccess) {
+    cudaGetLastError();
+    mine.ok = 0;
+  }
+  mine.halo = c->halo;
+  mine.n_own = c->n_own;
+  DevScope scope;
+  char* d_all = scope.keep(dev_alloc<char>(sizeof(P2PInfo) * c->world));
+  char* d_mine = scope.keep(dev_alloc<char>(sizeof(P2PInfo)));
+  CUDA_TRY(cudaMemcpy(d_mine, &mine, sizeof(P2PInfo), cudaMemcpyHostToDevice));
+  NCCL_TRY(g_nccl.allgather(d_mine, d_all, sizeof(P2PInfo), ncclChar, c->comm, c->stream));
+  std::vector<P2PInfo> all(static_cast<size_t>(c->world));
+  CUDA_TRY(cudaMemcpyAsync(all.data(), d_all, sizeof(P2PInfo) * c->world, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  double* lo_v[2] = {nullptr, nullptr};
+  double* hi_v[2] = {nullptr, nullptr};
+  unsigned long long *lo_f = nullptr, *hi_f = nullptr;
+  int ok = 1;
+  for (const auto& a : all) ok &= a.ok;
+  auto open = [&](const P2PInfo& nb, double** v, unsigned long long** f) {
+    void* p = nullptr;
+    for (int q = 0; q < 2 && ok; ++q) {
+      if (cudaIpcOpenMemHandle(&p, nb.hv[q], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = 0;
+        return;
+      }
+      c->ipc_opened.push_back(p);
+      v[q] = static_cast<double*>(p);
+    }
+    if (ok && cudaIpcOpenMemHandle(&p, nb.hf, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+      c->ipc_opened.push_back(p);
+      *f = static_cast<unsigned long long*>(p);
+    } else {
+      cudaGetLastError();
+      ok = 0;
+    }
+  };
+  if (ok && c->rank > 0) open(all[static_cast<size_t>(c->rank - 1)], lo_v, &lo_f);
+  if (ok && c->rank + 1 < c->world) open(all[static_cast<size_t>(c->rank + 1)], hi_v, &hi_f);
+  // every rank must take the same transport
+  int* d_ok = scope.keep(dev_alloc<int>(1));
+  CUDA_TRY(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_TRY(g_nccl.allreduce(d_ok, d_ok, 1, ncclInt, ncclMin, c->comm, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  if (!ok) {
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    c->ipc_opened.clear();
+    return;
+  }
+  const P2PInfo* lo = c->rank > 0 ? &all[static_cast<size_t>(c->rank - 1)] : nullptr;
+  const P2PInfo* hi = c->rank + 1 < c->world ? &all[static_cast<size_t>(c->rank + 1)] : nullptr;
+  set_peer_link(c, lo_v, lo ? lo->halo : 0, lo ? lo->n_own : 0, lo_f, hi_v, hi ? hi->halo : 0, hi_f);
+}
+
 // CWG_TRACE_CREATE=1: per-phase wall times of cwg_create on stderr (fixed-cost analysis of the e2e path)
 struct PhaseTrace {
   bool on = getenv("CWG_TRACE_CREATE") != nullptr;
@@ -1376,6 +1520,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     ncclUniqueId id;
     std::memcpy(&id, p->nccl_id, sizeof(id));
     NCCL_TRY(g_nccl.init(&c->comm, c->world, id, c->rank));
+    setup_p2p_nccl(c);
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   tr.mark("recording+comm");
@@ -1619,6 +1764,7 @@ int cwg_upload_state(cwg_ctx* c, const double* v, const double* s_aos, int strid
     validation(stride >= c->stride, "state: stride smaller than the largest model state count");
     CUDA_TRY(cudaSetDevice(c->device));
     c->cur = 0;
+    c->halo_fresh = false;
     const long long g0 = c->own_global0;
     CUDA_TRY(cudaMemcpyAsync(c->d_v[0] + c->halo, v + g0, c->n_own * sizeof(double), cudaMemcpyHostToDevice,
                              c->stream));
@@ -1640,6 +1786,7 @@ int cwg_init_rest_state(cwg_ctx* c) {
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     c->cur = 0;
+    c->halo_fresh = false;
     for (const auto& b : c->bins) {
       double rest[64] = {0};
       cwg_model_rest_state(b.kind, rest);
@@ -1705,6 +1852,27 @@ int cwg_set_scheme(cwg_ctx* c, int scheme, double dt_ms, double t_end_ms, int k0
   });
 }
 
+int cwg_loopback_link(cwg_ctx* const* ranks, int world) {
+  return guarded(nullptr, [&] {
+    validation(ranks && world >= 2, "loopback: need >= 2 rank contexts");
+    for (int r = 0; r < world; ++r) {
+      validation(ranks[r] && ranks[r]->loopback && ranks[r]->world == world && ranks[r]->rank == r,
+                 "loopback: contexts must be ranks 0..world-1 created with CWG_LOOPBACK=1");
+      validation(p2p_eligible(ranks[r]), "loopback: the peer-memory transport needs 2D stencil / 3D slabs");
+      CUDA_TRY(cudaSetDevice(ranks[r]->device));
+      alloc_flags(ranks[r]);
+    }
+    for (int r = 0; r < world; ++r) {
+      cwg_ctx* lo = r > 0 ? ranks[r - 1] : nullptr;
+      cwg_ctx* hi = r + 1 < world ? ranks[r + 1] : nullptr;
+      double* lo_v[2] = {lo ? lo->d_v[0] : nullptr, lo ? lo->d_v[1] : nullptr};
+      double* hi_v[2] = {hi ? hi->d_v[0] : nullptr, hi ? hi->d_v[1] : nullptr};
+      set_peer_link(ranks[r], lo_v, lo ? lo->halo : 0, lo ? lo->n_own : 0, lo ? lo->d_flags : nullptr, hi_v,
+                    hi ? hi->halo : 0, hi ? hi->d_flags : nullptr);
+    }
+  });
+}
+
 int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t count) {
   return guarded(nullptr, [&] {
     validation(ranks && world >= 2, "loopback: need >= 2 rank contexts");
@@ -1737,11 +1905,19 @@ int cwg_loopback_steps(cwg_ctx* const* ranks, int world, int64_t first, int64_t 
         }
       }
     };
+    // linked contexts (cwg_loopback_link): the launches store the halos themselves (peer-memory
+    // transport); a rank whose halos are stale after the reaction pushes them, all ranks before any launch
+    const bool linked = c0->p2p;
     auto diffuse_all = [&](int count, int ev0) {
       int q = 0;
       for (int T : diffusion_groups(c0, count)) {
-        exchange(T);
-        for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], T, 0, ev0 + q);
+        if (linked) {
+          for (int r = 0; r < world; ++r) halo_exchange(ranks[r], ranks[r]->d_v[ranks[r]->cur], T);
+          for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], T, 0, ev0 + q, true);
+        } else {
+          exchange(T);
+          for (int r = 0; r < world; ++r) enqueue_diffusion(ranks[r], T, 0, ev0 + q);
+        }
         q += T;
       }
     };
@@ -1894,6 +2070,7 @@ int cwg_run_begin(cwg_ctx* c) {
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     normalise_parity(c);
+    c->halo_fresh = false;
     reset_error(c);
     CUDA_TRY(cudaMemsetAsync(c->d_khist, 0, c->khist_len * sizeof(unsigned long long), c->stream));
     set_clock(c, 0);

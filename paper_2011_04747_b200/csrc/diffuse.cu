@@ -29,12 +29,14 @@ static inline int blocks_for(long long n, int t, int cap);
 __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s) {
   const long long nown = s.rows * s.w;
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  // an earlier event failed: leave V where it stopped (host: restore_failed_state); a peer-linked rank still
+  // takes part in the launch pacing so its neighbours do not wait for it
   const bool skip = earlier_failure(a.err, seq);
-  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown;
+  peer_wait(a.pl);
+  for (long long o = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; o < nown && !skip;
        o += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long i = o + s.hrows_v * s.w;  // local V index
     const long long oc = o + s.hrows_c * s.w;  // local coefficient index
-    if (skip) return;  // an earlier event failed: leave V where it stopped (host: restore_failed_state)
     const double vi = a.vin[i];
     const long long r = o / s.w, x = o - r * s.w;
     const long long gy = s.row_begin + r;
@@ -57,9 +59,11 @@ __global__ void __launch_bounds__(256) diffuse_stencil2d(DiffArgs a, Stencil2D s
     }
     const double out = vi - s.cm[oc] * acc;
     a.vout[i] = out;
+    peer_store(a, r, x, out);
     if (!isfinite(out))
       record_failure(a.err, static_cast<unsigned long long>(o + s.row_begin * s.w) << 22, seq, 2, 1, a.vin, a.vout);
   }
+  peer_post(a.pl);
 }
 
 // ---------------------------------------------------------------------------
@@ -197,7 +201,10 @@ __device__ __forceinline__ void tb_body(const DiffArgs& a, const Stencil2D& s, d
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r * NT >= TBX * TBY) break;
-        if (fl[r] & 32u) a.vout[(ly0 + py[r] + s.hrows_v) * w + gx0 + px[r]] = out[r];
+        if (fl[r] & 32u) {
+          a.vout[(ly0 + py[r] + s.hrows_v) * w + gx0 + px[r]] = out[r];
+          peer_store(a, ly0 + py[r], gx0 + px[r], out[r]);
+        }
       }
     }
   }
@@ -209,7 +216,11 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
   __shared__ double Vs[2][VY * VX];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
-  if (skip) return;  // block-uniform: an earlier event failed, V stays where it stopped
+  peer_wait(a.pl);
+  if (skip) {  // block-uniform: an earlier event failed, V stays where it stopped
+    peer_post(a.pl);
+    return;
+  }
   const long long gx0 = static_cast<long long>(blockIdx.x) * TBX, ly0 = static_cast<long long>(blockIdx.y) * TBY;
   const long long rows = s.rows, w = s.w;
   {
@@ -227,6 +238,7 @@ __global__ void __launch_bounds__(NT) diffuse_stencil2d_tb(DiffArgs a, Stencil2D
     tb_body<T, TBX, TBY, NT, false>(a, s, Vs, gx0, ly0, seq);
   else
     tb_body<T, TBX, TBY, NT, true>(a, s, Vs, gx0, ly0, seq);
+  peer_post(a.pl);
 }
 
 // ---------------------------------------------------------------------------
@@ -543,7 +555,11 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
   __shared__ double ring[4][PL];
   const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
   const bool skip = earlier_failure(a.err, seq);
-  if (skip) return;  // block-uniform: an earlier event failed, V stays where it stopped
+  peer_wait(a.pl);
+  if (skip) {  // block-uniform: an earlier event failed, V stays where it stopped
+    peer_post(a.pl);
+    return;
+  }
   const int tx = threadIdx.x % S3_TX, tz = threadIdx.x / S3_TX;
   const int x0 = blockIdx.x * S3_TX, z0 = blockIdx.y * S3_TZ;
   const int ix = x0 + tx, iz = z0 + tz;
@@ -638,6 +654,7 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
           out = vi - __ldg(s.cm + cls) * acc;
         }
         a.vout[i] = out;
+        peer_store(a, yl, static_cast<long long>(iz) * nx1 + ix, out);
         if (!isfinite(out))
           record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2, 1,
                          a.vin, a.vout);
@@ -654,6 +671,7 @@ __global__ void __launch_bounds__(S3_TX * S3_TZ, 6) diffuse_struct3d(DiffArgs a,
     pp = pw;
     pw = t;
   }
+  peer_post(a.pl);
 }
 
 // ---------------------------------------------------------------------------
@@ -728,6 +746,7 @@ __device__ __forceinline__ void s3_generic_node(const DiffArgs& a, const Struct3
   }
   const double out = a.vin[i] - __ldg(s.cm + cls) * acc;
   a.vout[i] = out;
+  peer_store(a, yl, static_cast<long long>(iz) * nx1 + ix, out);
   if (!isfinite(out))
     record_failure(a.err, static_cast<unsigned long long>(i - s.plane + s.row_begin * s.plane) << 22, seq, 2, 1,
                    a.vin, a.vout);
@@ -766,13 +785,25 @@ __device__ __forceinline__ void mbar_arrive_tx(unsigned bar, unsigned bytes) {
 }
 
 template <int W>
+__device__ __forceinline__ void struct3d_rb_body(const DiffArgs& a, const Struct3D& s, int tiles_x, int tiles_z,
+                                                 int n_items, int ychunk, long long n_edge, long long seq);
+
+template <int W>
 __global__ void __launch_bounds__(32 * W, 2)
     diffuse_struct3d_rb(DiffArgs a, Struct3D s, int tiles_x, int tiles_z, int n_items, int ychunk,
                         long long n_edge) {
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  peer_wait(a.pl);
+  // block-uniform: after an earlier failed event V stays where it stopped
+  if (!earlier_failure(a.err, seq)) struct3d_rb_body<W>(a, s, tiles_x, tiles_z, n_items, ychunk, n_edge, seq);
+  peer_post(a.pl);
+}
+
+template <int W>
+__device__ __forceinline__ void struct3d_rb_body(const DiffArgs& a, const Struct3D& s, int tiles_x, int tiles_z,
+                                                 int n_items, int ychunk, long long n_edge, long long seq) {
   using G = S3R<W>;
   extern __shared__ __align__(128) double s3r_smem[];
-  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
-  if (earlier_failure(a.err, seq)) return;  // block-uniform: an earlier event failed, V stays where it stopped
   const int nx1 = static_cast<int>(s.nx1), nz1 = static_cast<int>(s.nz1);
   const int nx = nx1 - 1;
   if (static_cast<int>(blockIdx.x) >= n_items) {
@@ -944,6 +975,11 @@ __global__ void __launch_bounds__(32 * W, 2)
       for (int j = 0; j < 4; ++j)
         if (j < nvalid) outp[j] = out[j];
     }
+    if (a.pl.on && (yb + i == 0 || yb + i == planes - 1)) {  // the slab's edge planes: also the neighbours' halos
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nvalid) peer_store(a, yb + i, static_cast<long long>(zc) * nx1 + x0 + j, out[j]);
+    }
     // one check for the four (a non-finite output makes the sum non-finite; a finite overflow of the sum
     // only sends the thread to the exact per-node test)
     if (!isfinite((out[0] + out[1]) + (out[2] + out[3]))) {
@@ -996,6 +1032,31 @@ static cudaError_t launch_s3r(const DiffArgs& a, const Struct3D& s, int num_sms,
   if (n_items + edge_blocks == 0) return cudaSuccess;
   diffuse_struct3d_rb<W><<<n_items + edge_blocks, G::NT, G::smem, st>>>(a, s, tiles_x, tiles_z, n_items, ychunk,
                                                                          n_edge);
+  return cudaGetLastError();
+}
+
+// Peer-memory halo push (multi-GPU P2P transport): after the reaction changed
+// V in place, this rank's edge rows/planes of V buffer `par` go into the
+// neighbours' halo rows (paced like a diffusion launch; no compute).
+__global__ void __launch_bounds__(256) push_halo(DiffArgs a) {
+  peer_wait(a.pl);
+  const PeerLink& pl = a.pl;
+  const long long per = pl.lim * pl.w;  // nodes per side
+  for (long long e = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; e < 2 * per;
+       e += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const bool up = e >= per;
+    const long long k = up ? e - per : e;
+    const long long r = up ? pl.rows - pl.lim + k / pl.w : k / pl.w, xo = k % pl.w;
+    const double val = a.vin[a.halo + r * pl.w + xo];
+    if (!up && pl.lo_dst[a.out_par]) pl.lo_dst[a.out_par][r * pl.w + xo] = val;
+    if (up && pl.hi_dst[a.out_par]) pl.hi_dst[a.out_par][(r - pl.rows) * pl.w + xo] = val;
+  }
+  peer_post(a.pl);
+}
+
+cudaError_t launch_push_halo(const DiffArgs& a, cudaStream_t st) {
+  const long long per = a.pl.lim * a.pl.w;
+  push_halo<<<blocks_for(2 * per, 256, 1024), 256, 0, st>>>(a);
   return cudaGetLastError();
 }
 

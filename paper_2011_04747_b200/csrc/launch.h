@@ -49,6 +49,7 @@ cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil
 cudaError_t launch_pad_planes(const double* src, long long src_pitch, int n_planes, long long w, long long rows,
                               double* dst, long long w_pad, int dst_plane0, cudaStream_t st);
 cudaError_t launch_diffuse_csr(const DiffArgs& a, const CsrDev& m, int max_blocks, cudaStream_t st);
+cudaError_t launch_push_halo(const DiffArgs& a, cudaStream_t st);
 cudaError_t launch_detector_init(const double* v, long long n, long long halo, const DetDev& d, cudaStream_t st);
 cudaError_t launch_detector_observe(const double* v, long long n, long long halo, const DetDev& d,
                                     const long long* clock, long long s_off, long long every, double dt,

@@ -29,7 +29,8 @@ def _need_cuda():
         os.environ["CWG_LOOPBACK"] = old
 
 
-def _loopback(p, world):
+def _loopback(p, world, link=False):
+    """link=True: the peer-memory transport (cwg_loopback_link) instead of the NCCL-equivalent copies."""
     import paper_2011_04747_b200 as cw
     from paper_2011_04747_b200 import _lib as L
     setup = p.setup()
@@ -37,11 +38,13 @@ def _loopback(p, world):
               for r in range(world)]
     try:
         st = p.initial_state()
+        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
+        if link:
+            assert L.lib().cwg_loopback_link(hs, world) == 0, L.lib().cwg_last_error().decode()
         for it in integs:
             it.upload(st)
             it.run_begin()
         n = integs[0].info.n_steps
-        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
         rc = L.lib().cwg_loopback_steps(hs, world, 0, n)
         assert rc == 0, L.lib().cwg_last_error().decode()
         out = p.initial_state()
@@ -129,7 +132,7 @@ def test_loopback_c2_single_substep_launches():
     assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
 
 
-def _loopback_full(p, world):
+def _loopback_full(p, world, link=False):
     """Loopback run that also assembles the global traces (each probe recorded by its owning rank) and the
     LAT/APD maps (each rank's y-slab rows) like cwg_gather_result does over NCCL."""
     import paper_2011_04747_b200 as cw
@@ -139,11 +142,13 @@ def _loopback_full(p, world):
               for r in range(world)]
     try:
         st = p.initial_state()
+        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
+        if link:
+            assert L.lib().cwg_loopback_link(hs, world) == 0, L.lib().cwg_last_error().decode()
         for it in integs:
             it.upload(st)
             it.run_begin()
         n = integs[0].info.n_steps
-        hs = (C.c_void_p * world)(*[it._h.value for it in integs])
         rc = L.lib().cwg_loopback_steps(hs, world, 0, n)
         assert rc == 0, L.lib().cwg_last_error().decode()
         out = p.initial_state()
@@ -182,3 +187,39 @@ def test_loopback_c4_geometry_traces_and_maps(world):
     assert np.array_equal(lv, ref.lat_map.valid) and np.array_equal(lat[lv], ref.lat_map.value[lv])
     assert np.array_equal(av, ref.apd90_map.valid) and np.array_equal(apd[av], ref.apd90_map.value[av])
     assert lv.sum() > 0  # the endocardial wave has activated nodes within the window
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_memory_transport_c4(world):
+    """The peer-memory (P2P) transport's data path on the full C4 grid: linked rank contexts store the
+    neighbours' halo planes from inside the diffusion kernel (and push them after the reaction), pacing on
+    launch counters -- bit-identical to one context."""
+    from paper_2011_04747_b200 import problems
+    p = problems.c4(t_end=6.0)
+    out, kh, tr, (lat, lv), (apd, av) = _loopback_full(p, world, link=True)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v)
+    assert np.array_equal(out.s, ref.final_state.s)
+    assert np.array_equal(kh, ref.k_histogram)
+    assert np.array_equal(tr, np.array([t.v_mv for t in ref.traces]))
+    assert np.array_equal(lv, ref.lat_map.valid) and np.array_equal(lat[lv], ref.lat_map.value[lv])
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_memory_transport_2d(world):
+    """2D: fused diffusion launches (T <= H halo rows) store H halo rows into the neighbours; ORd C2 sheet
+    (l = 1: the merged step is one fused launch of 2) and the thin-slab AP case (several launches per step)."""
+    from paper_2011_04747_b200 import problems
+    p = problems.c2(t_end=3.0)
+    out, kh = _loopback(p, world, link=True)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
+    import paper_2011_04747_b200 as cw
+    from paper_2011_04747_b200 import api
+    sh = cw.Sheet(1.0, 0.6, 0.02, 0.3, d0_myocyte=0.0017, rho=0.25)  # 31 rows: >= 2 H per rank
+    nodes = sh.select("x_le", value=0.05)
+    q = problems.Problem("thin", sh, ["aliev-panfilov"], np.zeros(sh.n, np.uint8), [(nodes, 0.0, 1.0, 100.0, None)],
+                         api.SchemeConfig(dt_ms=0.3, t_end_ms=6.0), [0])
+    out, kh = _loopback(q, world, link=True)
+    ref = _single(q)
+    assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
