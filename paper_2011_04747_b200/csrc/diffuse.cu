@@ -1248,11 +1248,8 @@ static cudaError_t launch_diffuse_struct3d_ring(const DiffArgs& a, const Struct3
 
 // Default: the register-blocked kernel; CWG_S3_KERNEL=0 selects the shared-memory ring kernel (A/B runs).
 cudaError_t launch_diffuse_struct3d(const DiffArgs& a, const Struct3D& s, int num_sms, cudaStream_t st) {
-  static const int which = [] {
-    const char* e = getenv("CWG_S3_KERNEL");
-    return e ? atoi(e) : 1;
-  }();
-  if (which == 0 || s.nx1 < 2 || s.nz1 < 2) return launch_diffuse_struct3d_ring(a, s, num_sms, st);
+  const char* e = getenv("CWG_S3_KERNEL");  // read per launch (graphs capture it once)
+  if ((e && atoi(e) == 0) || s.nx1 < 2 || s.nz1 < 2) return launch_diffuse_struct3d_ring(a, s, num_sms, st);
   return launch_s3r<6>(a, s, num_sms, st);
 }
 

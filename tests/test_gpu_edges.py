@@ -118,3 +118,25 @@ def test_record_interval_not_a_multiple_of_dt(cw):
     res, o = gpu_run(p), oracle_run(p)
     _exact(res, o)
     assert len(res.traces[0].v_mv) == len(o["traces"][0])
+
+
+def test_3d_kernels_agree():
+    """The register-blocked 3D diffusion kernel (default) and the round-1 shared-memory ring kernel
+    (CWG_S3_KERNEL=0) give the same bits on an ORd slab with every node class (faces, edges, corners)."""
+    import os
+    from paper_2011_04747_b200 import problems
+    from helpers import gpu_run
+    p = problems.slab(0.6, 0.5, 0.3, 0.02, t_end=3.0)
+    old = os.environ.get("CWG_S3_KERNEL")
+    try:
+        os.environ["CWG_S3_KERNEL"] = "0"
+        a = gpu_run(p)
+    finally:
+        if old is None:
+            os.environ.pop("CWG_S3_KERNEL", None)
+        else:
+            os.environ["CWG_S3_KERNEL"] = old
+    b = gpu_run(p)
+    assert np.array_equal(a.final_state.v, b.final_state.v)
+    assert np.array_equal(a.final_state.s, b.final_state.s)
+    assert np.array_equal(a.k_histogram, b.k_histogram)
