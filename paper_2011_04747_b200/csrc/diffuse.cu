@@ -460,6 +460,221 @@ __global__ void __launch_bounds__(NT, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// TMA-fed fused diffusion, register quads (default for large one-GPU sheets).
+// Same tiles, coefficient boxes (the tbm tensor maps), V prefetch and fused
+// depth as diffuse_stencil2d_tbm, but each thread owns a 2 x 2 quad of points
+// for all T sub-steps: its 40 coefficients live in registers (20 16-byte
+// shared loads per tile: quads start at even x, so a quad row's two points
+// are one aligned pair in every coefficient plane) and each sub-step streams
+// the quad's 4 x 4 V neighbourhood row by row with two 16-byte shared loads
+// per row -- 2 loads per point-sub-step instead of 9, and four independent
+// accumulation chains per thread. Each point's 9 terms are added in ascending
+// column order (row by row), exactly as diffuse_stencil2d. Absent neighbours
+// meet a zero coefficient (stored 0, or TMA's zero fill) and a zero or finite
+// V: 0 * v adds a signed zero, which never changes the sum (it starts at +0
+// and so is never -0) -- the bits of skipping the term, with no presence
+// tests. A quad computes while it touches the shrinking region; its points
+// beyond the region hold finite values no counting point reads. Non-finite
+// results of owned points set bits of a per-thread mask, resolved once per
+// tile into the same failure keys the per-sub-step check would record (the
+// minimum key is each point's first failing sub-step).
+// ---------------------------------------------------------------------------
+template <int T, int TBX, int TBY, int NT>
+struct TbqGeom {
+  using B = TbmGeom<T, TBX, TBY, NT>;                  // the coefficient box of the tbm tensor maps
+  static constexpr int PX0 = -(T - 1) - ((T - 1) & 1);  // first quad column: even, <= -(T-1)
+  static constexpr int QX = (TBX + T - PX0) / 2;        // quad columns covering PX0 .. TBX+T-2 (rounded up)
+  static constexpr int QY = (TBY + 2 * (T - 1)) / 2;    // quad rows covering -(T-1) .. TBY+T-2
+  static constexpr int VOFF = 1 - PX0;                  // V smem column of x: x + VOFF (x - 1 lands on an even column)
+  static constexpr int VX = (PX0 + 2 * QX + VOFF + 2) / 2 * 2;  // even pitch: 16-byte aligned rows
+  static constexpr int VY = TBY + 2 * T + 2;            // V smem row of y: y + T + 1
+  static constexpr int VXY = VX * VY;
+  static_assert(QX * QY <= NT && (TBY % 2) == 0 && VOFF % 2 == 1 && PX0 + 2 * QX - 1 >= TBX + T - 2, "quad geometry");
+  static_assert(PX0 >= -B::SX && PX0 + 2 * QX <= B::BXW - B::SX, "quads inside the coefficient box");
+  static constexpr size_t smem = (static_cast<size_t>(B::BOX) + 3ull * VXY) * sizeof(double) + 16;
+};
+
+template <int T, int TBX, int TBY, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    diffuse_stencil2d_tbq(DiffArgs a, Stencil2D s, const __grid_constant__ CUtensorMap tmap, int tiles_x, int n_tiles) {
+  using G = TbqGeom<T, TBX, TBY, NT>;
+  using B = typename G::B;
+  constexpr int VX = G::VX, VY = G::VY, VXY = G::VXY, QX = G::QX, QY = G::QY, VOFF = G::VOFF;
+  constexpr int BOX = B::BOX, BXW = B::BXW, SX = B::SX, CY = B::CY;
+  extern __shared__ __align__(128) double tbq_smem[];
+  double* cfs = tbq_smem;  // [10][CY][BXW]: the TMA box
+  double* vb0 = cfs + BOX;
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(vb0 + 3 * VXY);
+  const unsigned bar_a = smem_u32(bar);
+  const long long seq = cur_seq(a.clock, a.step_off, a.evs, a.ev);
+  if (earlier_failure(a.err, seq)) return;  // block-uniform: an earlier event failed, V stays where it stopped
+  const long long rows = s.rows, w = s.w;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const bool has_quad = t < QX * QY;
+  const int qx = G::PX0 + 2 * (t % QX), qy = 2 * (t / QX) - (T - 1);  // quad origin relative to the tile
+  // the quad takes part in sub-steps q <= qlast: it touches region(q) = the tile grown by T-1-q
+  const int dx = qx + 1 < 0 ? -(qx + 1) : (qx >= TBX ? qx - TBX + 1 : 0);
+  const int dy = qy + 1 < 0 ? -(qy + 1) : (qy >= TBY ? qy - TBY + 1 : 0);
+  const int qlast = has_quad ? T - 1 - (dx > dy ? dx : dy) : -1;
+  const int cfo = (qy + T - 1) * BXW + qx + SX;     // box offset of the quad's (x, y) point: even
+  const int wo = (qy - 1 + T + 1) * VX + qx - 1 + VOFF;  // V offset of the window's (x-1, y-1): even
+  auto issue_box = [&](int tile) {  // thread 0 only
+    const int gx0 = (tile % tiles_x) * TBX, ly0 = (tile / tiles_x) * TBY;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"(BOX * 8) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(cfs)),
+        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(ly0 - (T - 1)), "r"(0), "r"(bar_a)
+        : "memory");
+  };
+  // V rows ly0-T-1 .. ly0+TBY+T, columns gx0-VOFF .. gx0-VOFF+VX-1 (zero outside the sheet / local rows);
+  // one warp per row, lanes along it
+  auto fetch_v = [&](int tile, double* vdst) {
+    const long long gx0 = static_cast<long long>(tile % tiles_x) * TBX, ly0 = static_cast<long long>(tile / tiles_x) * TBY;
+    for (int cy = warp; cy < VY; cy += NT / 32) {
+      const long long yl = ly0 - T - 1 + cy, gy = s.row_begin + yl;
+      const bool row_in = gy >= 0 && gy < s.ny1 && yl >= -s.hrows_v && yl < rows + s.hrows_v;
+      const double* vrow = a.vin + (yl + s.hrows_v) * w + gx0 - VOFF;
+      double* drow = vdst + cy * VX;
+      for (int cx = lane; cx < VX; cx += 32) {
+        const long long x = gx0 - VOFF + cx;
+        if (row_in && x >= 0 && x < w)
+          cp_async8(drow + cx, vrow + cx);
+        else
+          drow[cx] = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (t == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // the second and third V frames start finite (quads read one point beyond the region they computed)
+  for (int e = t; e < 2 * VXY; e += NT) vb0[VXY + e] = 0.0;
+  __syncthreads();
+  int tile = blockIdx.x;
+  if (tile < n_tiles) {
+    if (t == 0) issue_box(tile);
+    fetch_v(tile, vb0);
+  }
+  int cur = 0;
+  unsigned parity = 0;
+  for (; tile < n_tiles; tile += gridDim.x) {
+    const long long gx0 = static_cast<long long>(tile % tiles_x) * TBX, ly0 = static_cast<long long>(tile / tiles_x) * TBY;
+    mbar_wait(bar_a, parity);
+    parity ^= 1u;
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // the quad's 4 x 10 coefficients (zero outside the local rows: those points never count)
+    double cf[4][10];
+    unsigned own = 0;  // bit k: point k lies in this tile and the sheet
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const long long yl = ly0 + qy + j;
+      const bool in = has_quad && yl >= -s.hrows_c && yl < rows + s.hrows_c;
+#pragma unroll
+      for (int c = 0; c < 10; ++c) {
+        double2 p = make_double2(0.0, 0.0);
+        if (in) p = *reinterpret_cast<const double2*>(cfs + c * BXW * CY + cfo + j * BXW);
+        cf[2 * j][c] = p.x;
+        cf[2 * j + 1][c] = p.y;
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int px = qx + i, py = qy + j;
+        if (has_quad && px >= 0 && px < TBX && py >= 0 && py < TBY && gx0 + px < w && yl < rows) own |= 1u << (2 * j + i);
+      }
+    }
+    __syncthreads();  // cfs and the spare V frame are free: start the next tile's copies
+    const int nxt = tile + static_cast<int>(gridDim.x);
+    double* vnext = vb0 + ((cur + 2) % 3) * VXY;
+    if (nxt < n_tiles) {
+      if (t == 0) issue_box(nxt);
+      fetch_v(nxt, vnext);
+    }
+    double* va = vb0 + cur * VXY;
+    double* vs = vb0 + ((cur + 1) % 3) * VXY;
+    double out[4] = {0.0, 0.0, 0.0, 0.0};
+    unsigned bad = 0;  // bit 4q + k: point k non-finite after sub-step q
+#pragma unroll
+    for (int q = 0; q < T; ++q) {
+      const double* src = (q & 1) ? vs : va;
+      double* dst = (q & 1) ? va : vs;
+      if (q <= qlast) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double v0[4];
+        // window rows y-1 .. y+2; quad row j (points k = 2j, 2j+1) takes rows y+j-1 .. y+j+1 in order
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const double* rp = src + wo + r * VX;
+          const double2 p0 = *reinterpret_cast<const double2*>(rp);
+          const double2 p1 = *reinterpret_cast<const double2*>(rp + 2);
+          const double wv[4] = {p0.x, p0.y, p1.x, p1.y};  // x-1, x, x+1, x+2
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int ry = r - j;  // this window row is quad row j's row ry-1 (ry = 0, 1, 2)
+            if (ry < 0 || ry > 2) continue;
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+              const int k = 2 * j + i;
+              acc[k] += cf[k][ry * 3 + 0] * wv[i];
+              acc[k] += cf[k][ry * 3 + 1] * wv[i + 1];
+              acc[k] += cf[k][ry * 3 + 2] * wv[i + 2];
+              if (ry == 1) v0[k] = wv[i + 1];
+            }
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          out[k] = v0[k] - cf[k][9] * acc[k];
+          bad |= (isfinite(out[k]) ? 0u : 1u) << (4 * q + k);
+        }
+        if (q + 1 < T) {
+          double* dp = dst + wo + VX + 1;  // (x, y)
+          dp[0] = out[0];
+          dp[1] = out[1];
+          dp[VX] = out[2];
+          dp[VX + 1] = out[3];
+        }
+      }
+      if (q + 1 < T) __syncthreads();
+    }
+    bad &= own * 0x11111111u;  // owned points only (own <= 0xF: the nibble replicated per sub-step)
+    if (bad) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const unsigned m = (bad >> k) & 0x11111111u;
+        if (!m) continue;
+        const unsigned q = static_cast<unsigned>(__ffs(static_cast<int>(m)) - 1) / 4;
+        const long long x = gx0 + qx + (k & 1), yl = ly0 + qy + (k >> 1);
+        record_failure(a.err, (static_cast<unsigned long long>(q) << 58) |
+                                  (static_cast<unsigned long long>(yl * w + x + s.row_begin * w) << 22), seq, 2, T,
+                       a.vin, a.vout);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (own >> k & 1u) a.vout[(ly0 + qy + (k >> 1) + s.hrows_v) * w + gx0 + qx + (k & 1)] = out[k];
+    cur = (cur + 2) % 3;
+  }
+}
+
+template <int T>
+static cudaError_t launch_tbq_t(const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm, int num_sms,
+                                cudaStream_t st) {
+  using G = TbqGeom<T, 64, 16, 512>;
+  static std::atomic<uint64_t> attr_done{0};
+  const cudaError_t e = ensure_dyn_smem(diffuse_stencil2d_tbq<T, 64, 16, 512>, static_cast<int>(G::smem), attr_done);
+  if (e != cudaSuccess) return e;
+  const int tiles_x = static_cast<int>((s.w + 63) / 64);
+  const int n_tiles = tiles_x * static_cast<int>((s.rows + 15) / 16);
+  diffuse_stencil2d_tbq<T, 64, 16, 512><<<std::min(num_sms, n_tiles), 512, G::smem, st>>>(a, s, tm, tiles_x, n_tiles);
+  return cudaGetLastError();
+}
+
 template <int T>
 static cudaError_t launch_tbm_t(const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm, int num_sms,
                                 cudaStream_t st) {
@@ -487,6 +702,17 @@ void tbm_box(int T, unsigned* cx, unsigned* cy, int* margin) {
 
 cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm,
                                          int num_sms, cudaStream_t st) {
+  const char* e = getenv("CWG_TBQ");  // register-quad kernel by default; CWG_TBQ=0: the slot kernel (A/B)
+  if (!(e && e[0] == '0')) {
+    switch (T) {
+      case 2: return launch_tbq_t<2>(a, s, tm, num_sms, st);
+      case 3: return launch_tbq_t<3>(a, s, tm, num_sms, st);
+      case 4: return launch_tbq_t<4>(a, s, tm, num_sms, st);
+      case 5: return launch_tbq_t<5>(a, s, tm, num_sms, st);
+      case 6: return launch_tbq_t<6>(a, s, tm, num_sms, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (T) {
     case 2: return launch_tbm_t<2>(a, s, tm, num_sms, st);
     case 3: return launch_tbm_t<3>(a, s, tm, num_sms, st);

@@ -67,16 +67,48 @@ def test_fused_equals_unfused():
         assert np.array_equal(a.final_state.s, r.final_state.s)
 
 
-@pytest.mark.parametrize("where", ["interior", "tile_corner", "edge"])
-def test_nonfinite_in_fused_substep_reports_like_oracle(where):
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    try:
+        os.environ.update(env)
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def test_tma_kernels_every_depth_bitwise():
+    """The one-GPU TMA path (801 x 401 sheet: 338 tiles of 64 x 16, ragged on both edges) at every fused
+    depth T = 2..6, through the register-quad kernel and the slot kernel (CWG_TBQ=0): bit-identical to
+    unfused sub-steps."""
+    p = _problem(8.0, 4.0, 0.7, t_end=3.0)
+    ref = _with_env({"CWG_DIFF_TB": "1"}, lambda: gpu_run(p))
+    for T in range(2, 7):
+        for tbq in ("1", "0"):
+            r = _with_env({"CWG_DIFF_TB": str(T), "CWG_TBQ": tbq}, lambda: gpu_run(p))
+            assert np.array_equal(ref.final_state.v, r.final_state.v), (T, tbq)
+            assert np.array_equal(ref.final_state.s, r.final_state.s), (T, tbq)
+
+
+SIZES = {"small": (1.3, 0.7), "tma": (8.0, 4.0)}  # 131 x 71: register-loading kernel; 801 x 401: TMA path
+WHERE = {"interior": lambda w: (40, 30), "tile_corner": lambda w: (63, 16), "edge": lambda w: (0, 55),
+         "right_edge": lambda w: (w - 1, 47)}
+
+
+@pytest.mark.parametrize("size", list(SIZES))
+@pytest.mark.parametrize("where", list(WHERE))
+def test_nonfinite_in_fused_substep_reports_like_oracle(where, size):
     """A NaN in the initial V: the first diffusion sub-step of step I spreads it;
     the reported node is the lowest non-finite one, t = 0 (as in the reference)."""
     import orapy
     import paper_2011_04747_b200 as cw
     from helpers import csr_of
-    p = _problem(1.3, 0.7, 0.4, t_end=3.0)
+    p = _problem(*SIZES[size], 0.4, t_end=3.0)
     w = p.sheet.nx1
-    x, y = {"interior": (40, 30), "tile_corner": (63, 16), "edge": (0, 55)}[where]
+    x, y = WHERE[where](w)
     node = y * w + x
     st = p.initial_state()
     st.v[node] = np.nan
@@ -117,17 +149,18 @@ def test_set_scheme_refreshes_fused_coefficients():
     assert np.array_equal(fresh.final_state.v, o["v"])
 
 
-@pytest.mark.parametrize("where", ["interior", "tile_corner", "edge"])
-def test_state_after_fused_failure_matches_oracle(where):
+@pytest.mark.parametrize("size", list(SIZES))
+@pytest.mark.parametrize("where", list(WHERE))
+def test_state_after_fused_failure_matches_oracle(where, size):
     """After an InstabilityError the state is where the reference leaves it: V = the failing sub-step's
     output (splitting.cpp:162-166 swap, then throw), not the end of the fused launch. StrangIntegrator
     .advance downloads the state on an instability; the oracle's Integrator holds its state at the throw."""
     import orapy
     import paper_2011_04747_b200 as cw
     from helpers import csr_of
-    p = _problem(1.3, 0.7, 0.4, t_end=3.0)
+    p = _problem(*SIZES[size], 0.4, t_end=3.0)
     w = p.sheet.nx1
-    x, y = {"interior": (40, 30), "tile_corner": (63, 16), "edge": (0, 55)}[where]
+    x, y = WHERE[where](w)
     node = y * w + x
     n_steps = 10
     st = p.initial_state()
