@@ -522,6 +522,8 @@ def main():
         # the result lands in pinned host buffers too (allocated once, outside the timed region)
         fin = st0.copy()
         fin.v, fin.s, fin.last_dvdt = pin(fin.v), pin(fin.s), pin(fin.last_dvdt)
+        pinned = lambda dt: torch.empty(prob.n, dtype=dt, pin_memory=True).numpy()
+        maps_out = tuple(cw.ScalarMap(pinned(torch.float64), pinned(torch.bool)) for _ in range(2))
         e2e_cfg = cw.SchemeConfig(scheme=prob.cfg.scheme, dt_ms=prob.cfg.dt_ms,
                                   t_end_ms=(args.warmup + K) * prob.cfg.dt_ms, k0_up=prob.cfg.k0_up,
                                   k0_down=prob.cfg.k0_down)
@@ -537,7 +539,8 @@ def main():
             e_integ = cw.StrangIntegrator(setup, e2e_cfg, model_of_node=prob.model_of_node, device=local, rank=rank,
                                           world=world, nccl_id=e_id)
             creates.append(time.perf_counter() - t0)
-            res = cw.run_simulation(st0, setup, e2e_cfg, device=local, integrator=e_integ, final_state_out=fin)
+            res = cw.run_simulation(st0, setup, e2e_cfg, device=local, integrator=e_integ, final_state_out=fin,
+                                  maps_out=maps_out)
             torch.cuda.synchronize()
             w_s = time.perf_counter() - t0
             if dist:
@@ -556,7 +559,7 @@ def main():
         line["e2e"] = {"value": e_val, "unit": UNIT, "h2d_bytes_per_step": h2d / n_steps_e,
                        "d2h_bytes_per_step": d2h / n_steps_e,
                        "call": "paper_2011_04747_b200.run_simulation (cwg_create + state upload from pinned host "
-                               "memory + all steps + traces/maps/final-state download into pinned host memory)",
+                               "memory + all steps + traces/LAT/APD maps/final-state download into pinned host memory)",
                        "steps": n_steps_e, "wall_s": e2e_s, "wall_s_all": walls,
                        "create_s_all": creates}
 

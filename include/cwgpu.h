@@ -59,7 +59,8 @@ enum {
   CWG_OP_AUTO = 0,      /* stencil-2D when the CSR is a regular-sheet 9-point operator, else CSR */
   CWG_OP_CSR = 1,       /* generic CSR row loop, ascending columns (fem.cpp:201-206) */
   CWG_OP_STENCIL2D = 2, /* per-node 9 coefficients taken verbatim from the CSR */
-  CWG_OP_STRUCT3D = 3   /* extension: structured 3D slab, per-layer tables (see cwg_problem.s3d) */
+  CWG_OP_STRUCT3D = 3,  /* extension: structured 3D slab, per-layer tables (see cwg_problem.s3d) */
+  CWG_OP_SHEET2D = 4    /* regular sheet assembled on the device (see cwg_problem.sheet2d) */
 };
 
 typedef struct cwg_ctx cwg_ctx;
@@ -84,6 +85,23 @@ typedef struct {
   double d_long, rho; /* D_l, D_t = rho * D_l */
   const double* fiber_angle_of_layer; /* nz element layers, radians */
 } cwg_struct3d;
+
+/* Regular sheet whose operator is assembled ON THE DEVICE (replaces the host
+ * path build_diffusion_field fem.cpp:21-51 -> assemble fem.cpp:112-176 ->
+ * gershgorin_step fem.cpp:178-192 for meshes made by build_regular_sheet,
+ * mesh.cpp:72-98): node (ix, iy) at (ix h, iy h) with index iy (nx+1) + ix,
+ * element (ex, ey) = ey nx + ex. Lumped mass and off-diagonal entries are
+ * bit-identical to the reference's; a diagonal entry sums its four element
+ * contributions in ascending element index and can differ from the
+ * reference's std::sort order by 1-2 ulp. */
+typedef struct {
+  int64_t nx, ny;             /* element counts */
+  double h;                   /* cm */
+  double fiber_angle;         /* radians, uniform (cos/sin taken on the host) */
+  double d0_myocyte, d0_fibrotic, rho;
+  const int32_t* node_tags;   /* [n] host, 1 = fibroblast (assign_fibrosis, mesh.cpp:100-122); NULL = none */
+  const double* elem_scale;   /* [nx ny] host, D multiplier (extension, 0 = scar); NULL = 1 */
+} cwg_sheet2d;
 
 /* Everything StrangIntegrator/run_simulation consume (splitting.hpp:83-94,
  * fem.hpp:23-32, ionic.hpp:39-55, stimulus.hpp:35-50), flattened. */
@@ -132,6 +150,9 @@ typedef struct {
   int device;     /* CUDA ordinal */
   int rank, world;                 /* y-slab decomposition; world = 1 for single GPU */
   const unsigned char* nccl_id;    /* 128-byte ncclUniqueId (world > 1) */
+
+  /* ---- appended (ABI: older callers that zero-initialise the struct are unaffected) */
+  const cwg_sheet2d* sheet2d; /* for CWG_OP_SHEET2D (row_ptr/col/val/lumped_mass/dt_s ignored) */
 } cwg_problem;
 
 /* StrangIntegrator ctor (splitting.cpp:74-93): validates, uploads the operator,
@@ -345,6 +366,15 @@ int cwg_model_kind_from_name(const char* name); /* -1 if unknown (make_model, io
 int cwg_reaction_substeps(double dvdt_prev, int scheme, int k0_up, int k0_down, int k_max); /* splitting.cpp:48-54 */
 int cwg_diffusion_substeps(double dt, double dt_s, int strict, int scheme, int* l, double* dt_ad); /* :56-67 */
 int cwg_k_max_for(double dt, int model_kind);                                                /* :69-72 */
+
+/* assemble (fem.cpp:112-176) + gershgorin_step (fem.cpp:178-192) of a
+ * regular sheet on `device` (see cwg_sheet2d). Outputs may be NULL; CSR in
+ * the reference's layout (ascending columns): row_ptr [n+1], col / val
+ * [cwg_sheet2d_nnz], lumped_mass [n], dt_s. Validation failures carry the
+ * reference's messages (first failing element / node, as its loops throw). */
+int64_t cwg_sheet2d_nnz(const cwg_sheet2d* g);
+int cwg_sheet2d_assemble(const cwg_sheet2d* g, int device, int64_t* row_ptr, int64_t* col, double* val,
+                         double* lumped_mass, double* dt_s, cwg_error* err);
 
 /* No reference counterpart (new: the reference is single-process OpenMP):
  * y-slab plan for world ranks over ny1 node rows,

@@ -43,6 +43,12 @@ int cwg_sheet_build(double lx_cm, double ly_cm, double h_cm, double fiber_angle_
                     double d0_myocyte, double d0_fibrotic, double rho, double fib_fraction,
                     uint64_t seed, const double* elem_scale, cwg_sheet** out, cwg_error* err);
 void cwg_sheet_free(cwg_sheet* s);
+/* build_regular_sheet + assign_fibrosis only (mesh.cpp:72-122): coordinates
+ * and tags for select / nearest, no host assembly -- the operator is then
+ * assembled on the device (cwg_sheet2d, CWG_OP_SHEET2D in cwgpu.h). The
+ * operator views below are empty (nnz 0, dt_s 0) for such a sheet. */
+int cwg_sheet_mesh(double lx_cm, double ly_cm, double h_cm, double fib_fraction, uint64_t seed, cwg_sheet** out,
+                   cwg_error* err);
 
 /* Mesh::node_count / element_count (mesh.hpp), AssembledOperator nnz /
  * rows / dt_s (fem.hpp:23-32), grid node counts of build_regular_sheet */

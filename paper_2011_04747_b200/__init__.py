@@ -12,7 +12,7 @@ _load_lib()
 from .api import (  # noqa: E402
     AssembledOperator, CellModel, DeviceError, DiffusionPlan, InstabilityError, IoError, NodeStateArray, Probe,
     Protocol, ProtocolIndex, Scheme, SchemeConfig, ScalarMap, Sheet, SimulationResult, Slab3D, SimulationSetup, Stimulus,
-    StrangIntegrator, ThresholdOptions, TimingBreakdown, Trace, ValidationError, build_sheet, diastolic_threshold, diffusion_substep, diffusion_substeps,
+    DeviceSheetOperator, StrangIntegrator, ThresholdOptions, TimingBreakdown, Trace, ValidationError, build_sheet, diastolic_threshold, diffusion_substep, diffusion_substeps,
     k_max_for, make_initial_state, make_model, pace_cells, pace_to_steady_state, PacingResult, reaction_substeps, registered_model_names, run_simulation,
     scheme_from_string, slab_plan,
 )

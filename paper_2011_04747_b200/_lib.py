@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("CWG_LIB_PATH") or os.path.join(HERE, "libcwgpu.so")  # override: experiments only
 
 CWG_OK, CWG_EVALIDATION, CWG_EINSTABILITY, CWG_EIO, CWG_ECUDA = 0, 2, 3, 4, 5
-OP_AUTO, OP_CSR, OP_STENCIL2D, OP_STRUCT3D = 0, 1, 2, 3
+OP_AUTO, OP_CSR, OP_STENCIL2D, OP_STRUCT3D, OP_SHEET2D = 0, 1, 2, 3, 4
 
 
 class cwg_error(C.Structure):
@@ -32,6 +32,12 @@ _i32p = C.POINTER(C.c_int32)
 _u8p = C.POINTER(C.c_uint8)
 
 
+class cwg_sheet2d(C.Structure):
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("h", C.c_double), ("fiber_angle", C.c_double),
+                ("d0_myocyte", C.c_double), ("d0_fibrotic", C.c_double), ("rho", C.c_double),
+                ("node_tags", _i32p), ("elem_scale", _dp)]
+
+
 class cwg_problem(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("row_ptr", _lp), ("col", _lp), ("val", _dp), ("lumped_mass", _dp), ("dt_s", C.c_double),
@@ -43,6 +49,7 @@ class cwg_problem(C.Structure):
         ("scheme", C.c_int), ("dt_ms", C.c_double), ("t_end_ms", C.c_double), ("k0_up", C.c_int), ("k0_down", C.c_int),
         ("strict_substeps", C.c_int), ("record_interval_ms", C.c_double),
         ("device", C.c_int), ("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.POINTER(C.c_ubyte)),
+        ("sheet2d", C.POINTER(cwg_sheet2d)),
     ]
 
 
@@ -110,11 +117,16 @@ _SIGS = {
     "cwg_diffusion_substeps": (C.c_int, [C.c_double, C.c_double, C.c_int, C.c_int, _ip, _dp]),
     "cwg_k_max_for": (C.c_int, [C.c_double, C.c_int]),
     "cwg_slab_plan": (C.c_int, [C.c_int64, C.c_int, C.c_int, _lp, _lp]),
+    "cwg_sheet2d_nnz": (C.c_int64, [C.POINTER(cwg_sheet2d)]),
+    "cwg_sheet2d_assemble": (C.c_int, [C.POINTER(cwg_sheet2d), C.c_int, _lp, _lp, _dp, _dp, _dp,
+                                       C.POINTER(cwg_error)]),
     # setup (cwgpu_setup.h)
     "cwg_sheet_build": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_uint64, _dp, C.POINTER(C.c_void_p),
                                   C.POINTER(cwg_error)]),
     "cwg_sheet_free": (None, [C.c_void_p]),
+    "cwg_sheet_mesh": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(C.c_void_p),
+                                 C.POINTER(cwg_error)]),
     "cwg_sheet_nodes": (C.c_int64, [C.c_void_p]),
     "cwg_sheet_elements": (C.c_int64, [C.c_void_p]),
     "cwg_sheet_nnz": (C.c_int64, [C.c_void_p]),

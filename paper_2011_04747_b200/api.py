@@ -301,11 +301,52 @@ class AssembledOperator:
         return 0.0
 
 
+class DeviceSheetOperator:
+    """The operator of a regular sheet assembled ON THE DEVICE (cwg_sheet2d / CWG_OP_SHEET2D):
+    build_diffusion_field (fem.cpp:21-51) + assemble (fem.cpp:112-176) + gershgorin_step (fem.cpp:178-192) without
+    the host triplet sort or a CSR upload. Acts as SimulationSetup.op. Lumped mass and off-diagonal entries equal
+    the reference's bit for bit; a diagonal entry can differ by 1-2 ulp (its four element contributions are summed
+    in ascending element order, the reference's in std::sort's tie order). `csr()` returns the assembled CSR."""
+
+    def __init__(self, nx, ny, h, fiber_angle_rad, d0_myocyte, d0_fibrotic, rho, tags=None, elem_scale=None,
+                 device=0):
+        self._tags = None if tags is None else np.ascontiguousarray(tags, np.int32)
+        self._es = None if elem_scale is None else np.ascontiguousarray(elem_scale, np.float64)
+        self.desc = L.cwg_sheet2d(nx, ny, h, fiber_angle_rad, d0_myocyte, d0_fibrotic, rho,
+                                  None if self._tags is None else self._tags.ctypes.data_as(L._i32p),
+                                  None if self._es is None else L.dp(self._es))
+        self.grid_nx1, self.grid_ny1 = nx + 1, ny + 1
+        self.n = self.grid_nx1 * self.grid_ny1
+        self.device = device
+        dts = C.c_double()
+        err = L.cwg_error()
+        _check(L.lib().cwg_sheet2d_assemble(C.byref(self.desc), device, None, None, None, None, C.byref(dts),
+                                            C.byref(err)), err)
+        self.dt_s = dts.value
+
+    def rows(self):
+        return self.n
+
+    def csr(self) -> AssembledOperator:
+        nnz = L.lib().cwg_sheet2d_nnz(C.byref(self.desc))
+        rp, col = np.zeros(self.n + 1, np.int64), np.zeros(nnz, np.int64)
+        val, mass = np.zeros(nnz), np.zeros(self.n)
+        dts = C.c_double()
+        err = L.cwg_error()
+        _check(L.lib().cwg_sheet2d_assemble(C.byref(self.desc), self.device, L.lp(rp), L.lp(col), L.dp(val),
+                                            L.dp(mass), C.byref(dts), C.byref(err)), err)
+        return AssembledOperator(rp, col, val, mass, dts.value, self.grid_nx1, self.grid_ny1)
+
+
 class Sheet:
-    """build_regular_sheet (+assign_fibrosis) + build_diffusion_field + assemble, on the host."""
+    """build_regular_sheet (+assign_fibrosis) + build_diffusion_field + assemble.
+
+    assembly="host" (default): the host restatement of the reference's assembly, CSR bit-identical to it.
+    assembly="device": only the mesh is built on the host (coordinates, fibrosis tags); the operator is
+    assembled on the GPU (DeviceSheetOperator) -- the path for large sheets."""
 
     def __init__(self, lx_cm, ly_cm, h_cm, fiber_angle_rad=0.0, d0_myocyte=0.0017, d0_fibrotic=0.00066, rho=0.25,
-                 fib_fraction=0.0, seed=0, elem_scale=None):
+                 fib_fraction=0.0, seed=0, elem_scale=None, assembly="host", device=0):
         lib = L.lib()
         h = C.c_void_p()
         err = L.cwg_error()
@@ -313,23 +354,32 @@ class Sheet:
         if elem_scale is not None:
             self._es = np.ascontiguousarray(elem_scale, np.float64)
             es = L.dp(self._es)
-        rc = lib.cwg_sheet_build(lx_cm, ly_cm, h_cm, fiber_angle_rad, d0_myocyte, d0_fibrotic, rho, fib_fraction, seed,
-                                 es, C.byref(h), C.byref(err))
+        if assembly == "host":
+            rc = lib.cwg_sheet_build(lx_cm, ly_cm, h_cm, fiber_angle_rad, d0_myocyte, d0_fibrotic, rho, fib_fraction,
+                                     seed, es, C.byref(h), C.byref(err))
+        elif assembly == "device":
+            rc = lib.cwg_sheet_mesh(lx_cm, ly_cm, h_cm, fib_fraction, seed, C.byref(h), C.byref(err))
+        else:
+            raise ValidationError(f"sheet: unknown assembly '{assembly}'")
         _check(rc, err)
         self._h = h
         n = lib.cwg_sheet_nodes(h)
-        nnz = lib.cwg_sheet_nnz(h)
         self.n = n
         self.nx1, self.ny1 = lib.cwg_sheet_nx1(h), lib.cwg_sheet_ny1(h)
         self.n_elements = lib.cwg_sheet_elements(h)
         as_np = np.ctypeslib.as_array
-        self.op = AssembledOperator(as_np(lib.cwg_sheet_row_ptr(h), (n + 1,)).copy(),
-                                    as_np(lib.cwg_sheet_col(h), (nnz,)).copy(),
-                                    as_np(lib.cwg_sheet_val(h), (nnz,)).copy(),
-                                    as_np(lib.cwg_sheet_mass(h), (n,)).copy(),
-                                    lib.cwg_sheet_dt_s(h), self.nx1, self.ny1)
         self.coords = as_np(lib.cwg_sheet_coords(h), (n, 2)).copy()
         self.tags = as_np(lib.cwg_sheet_tags(h), (n,)).copy()
+        if assembly == "host":
+            nnz = lib.cwg_sheet_nnz(h)
+            self.op = AssembledOperator(as_np(lib.cwg_sheet_row_ptr(h), (n + 1,)).copy(),
+                                        as_np(lib.cwg_sheet_col(h), (nnz,)).copy(),
+                                        as_np(lib.cwg_sheet_val(h), (nnz,)).copy(),
+                                        as_np(lib.cwg_sheet_mass(h), (n,)).copy(),
+                                        lib.cwg_sheet_dt_s(h), self.nx1, self.ny1)
+        else:
+            self.op = DeviceSheetOperator(self.nx1 - 1, self.ny1 - 1, h_cm, fiber_angle_rad, d0_myocyte, d0_fibrotic,
+                                          rho, self.tags if fib_fraction > 0.0 else None, elem_scale, device)
 
     def __del__(self):
         if getattr(self, "_h", None) and L._lib is not None:
@@ -567,6 +617,10 @@ class StrangIntegrator:
             keep["s3d"] = op.s3d
             p.op_kind = L.OP_STRUCT3D
             p.s3d = C.pointer(op.s3d)
+        elif isinstance(op, DeviceSheetOperator):
+            keep["sheet2d"] = op
+            p.op_kind = L.OP_SHEET2D
+            p.sheet2d = C.pointer(op.desc)
         else:
             keep["rp"] = np.ascontiguousarray(op.row_ptr, np.int64)
             keep["col"] = np.ascontiguousarray(op.col, np.int64)
@@ -711,23 +765,33 @@ class StrangIntegrator:
         _check(L.lib().cwg_get_traces(self._h, L.dp(t), L.dp(v)))
         return t, v[: npb * ns].reshape(npb, ns)
 
-    def gather(self, state: NodeStateArray):
+    @staticmethod
+    def _map_buffers(n, out):
+        """(lat, apd) ScalarMaps to fill: `out` (e.g. pinned host arrays reused across runs; value float64[n],
+        valid bool[n], written in place) or fresh arrays."""
+        if out is None:
+            out = (ScalarMap(np.empty(n), np.empty(n, bool)), ScalarMap(np.empty(n), np.empty(n, bool)))
+        for m in out:
+            if (m.value.dtype != np.float64 or m.valid.dtype != np.bool_ or m.value.shape != (n,)
+                    or m.valid.shape != (n,) or not m.value.flags.c_contiguous or not m.valid.flags.c_contiguous):
+                raise ValidationError("maps: output arrays must be contiguous float64[n] / bool[n]")
+        return out
+
+    def gather(self, state: NodeStateArray, maps_out=None):
         """The global final state and LAT/APD maps on every rank (cwg_gather_result; collective for world > 1):
         returns (lat_map, apd90_map) and fills `state` (global arrays)."""
-        n = self.n
-        lat, apd = np.zeros(n), np.zeros(n)
-        lv, av = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+        lat, apd = self._map_buffers(self.n, maps_out)
         _check(L.lib().cwg_gather_result(self._h, L.dp(state.v), L.dp(state.s), state.stride, L.dp(state.last_dvdt),
-                                         L.dp(lat), lv.ctypes.data_as(L._u8p), L.dp(apd), av.ctypes.data_as(L._u8p)))
-        return ScalarMap(lat, lv.astype(bool)), ScalarMap(apd, av.astype(bool))
+                                         L.dp(lat.value), lat.valid.ctypes.data_as(L._u8p), L.dp(apd.value),
+                                         apd.valid.ctypes.data_as(L._u8p)))
+        return lat, apd
 
-    def maps(self):
-        n = self.info.n_local
-        lat, apd = np.zeros(n), np.zeros(n)
-        lv, av = np.zeros(n, np.uint8), np.zeros(n, np.uint8)
-        _check(L.lib().cwg_get_maps(self._h, L.dp(lat), lv.ctypes.data_as(L._u8p), L.dp(apd),
-                                    av.ctypes.data_as(L._u8p)))
-        return ScalarMap(lat, lv.astype(bool)), ScalarMap(apd, av.astype(bool))
+    def maps(self, out=None):
+        """LAT / APD90 maps of the owned nodes (NaN where a map has no value); `out`: see _map_buffers."""
+        lat, apd = self._map_buffers(self.info.n_local, out)
+        _check(L.lib().cwg_get_maps(self._h, L.dp(lat.value), lat.valid.ctypes.data_as(L._u8p), L.dp(apd.value),
+                                    apd.valid.ctypes.data_as(L._u8p)))
+        return lat, apd
 
 
 def round_half_away(x: float) -> int:
@@ -790,12 +854,14 @@ def _run_with_callbacks(integ, state, setup, n_steps, dt, every_snap, every_prog
 
 
 def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeConfig, device=0,
-                   integrator: StrangIntegrator = None, final_state_out: NodeStateArray = None) -> SimulationResult:
+                   integrator: StrangIntegrator = None, final_state_out: NodeStateArray = None,
+                   maps_out=None) -> SimulationResult:
     """run_simulation (splitting.cpp:219-294) on the GPU; raises InstabilityError like the reference.
 
     The reference takes `state` by value and moves it into result.final_state; here the caller's arrays
     are left untouched and the final state is downloaded into fresh arrays -- or into `final_state_out`
-    (e.g. pinned host buffers a caller reuses across runs), which is then returned as final_state."""
+    (e.g. pinned host buffers a caller reuses across runs), which is then returned as final_state; likewise
+    `maps_out` = (lat_map, apd90_map) ScalarMaps receive the LAT / APD90 maps."""
     import time
     t0 = time.perf_counter()
     integ = integrator or StrangIntegrator(setup, cfg, model_of_node=state.model_of_node, device=device)
@@ -817,10 +883,10 @@ def run_simulation(state: NodeStateArray, setup: SimulationSetup, cfg: SchemeCon
                                np.empty_like(state.last_dvdt), state.model_of_node.copy())
     t, v = integ.traces()
     if integ.world > 1:  # one global SimulationResult on every rank (splitting.cpp:286-293)
-        lat, apd = integ.gather(final)
+        lat, apd = integ.gather(final, maps_out)
     else:
         integ.download(final)
-        lat, apd = integ.maps()
+        lat, apd = integ.maps(maps_out)
     traces = [Trace(pr.node, pr.name, t.copy(), v[q].copy()) for q, pr in enumerate(setup.probes)]
     tb = TimingBreakdown(total_ms=(time.perf_counter() - t0) * 1e3)
     return SimulationResult(traces, lat, apd, tb, integ.k_histogram(), integ.dt_effective(), setup.op.dt_s,

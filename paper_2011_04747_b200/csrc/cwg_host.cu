@@ -478,10 +478,21 @@ void ctx_free(cwg_ctx* c) {
   delete c;
 }
 
+// Host -> device copy that has LANDED on return. cudaMemcpy from pageable
+// memory returns once the data sits in the driver's staging buffer, with the
+// DMA still queued on the legacy stream; the contexts' streams are
+// non-blocking, so a kernel on them could otherwise read the old contents
+// (seen: a 13 MB stimulus-pointer upload racing the kernel that rebases it).
+void h2d(void* d, const void* h, size_t bytes) {
+  if (!bytes) return;
+  CUDA_TRY(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaStreamSynchronize(nullptr));
+}
+
 template <class T>
 T* upload(const T* h, size_t count) {
   T* d = dev_alloc<T>(count);
-  if (count) CUDA_TRY(cudaMemcpy(d, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  h2d(d, h, count * sizeof(T));
   return d;
 }
 
@@ -499,6 +510,89 @@ struct DevScope {
       if (p) dev_pool().put(p);
   }
 };
+
+// ------------------------------------------------- device sheet assembly
+// A regular sheet's operator assembled on the device (assemble.cu): the full
+// [9][n] stencil table, lumped mass and dt_s. Validation failures are
+// reported like the reference's loops throw them: the first degenerate
+// element (fem.cpp:84-86), then the first node failing the structural checks
+// in the reference's order (mass, symmetry per entry, row sum; fem.cpp:154-172),
+// then the first non-diffusive row (fem.cpp:184-187).
+struct SheetAsm {
+  double* coef = nullptr;  // [9][n] (pool memory; owner frees)
+  double* mass = nullptr;  // [n]
+  unsigned char* nnz_row = nullptr;
+  long long n = 0, w = 0;
+  double dt_s = 0.0;
+  void release() {
+    dev_free(coef);
+    dev_free(mass);
+    dev_free(nnz_row);
+  }
+};
+
+SheetAsm assemble_sheet2d(const cwg_sheet2d* g, cudaStream_t st) {
+  validation(g != nullptr, "operator: CWG_OP_SHEET2D needs cwg_problem.sheet2d");
+  validation(g->h > 0.0 && std::isfinite(g->h), "mesh: spacing h must be positive and finite");
+  validation(g->nx >= 1 && g->ny >= 1, "mesh: the sheet needs at least one element per axis");
+  validation(g->d0_myocyte > 0.0 && g->d0_fibrotic > 0.0, "diffusion: coefficients must be positive");
+  validation(g->rho > 0.0 && g->rho <= 1.0, "diffusion: rho must lie in (0, 1]");
+  SheetAsm a;
+  a.w = g->nx + 1;
+  a.n = a.w * (g->ny + 1);
+  validation(a.n < (1ll << 40), "mesh: at most 2^40 nodes");
+  DevScope tmp;
+  const int32_t* dtags = g->node_tags ? tmp.keep(upload(g->node_tags, static_cast<size_t>(a.n))) : nullptr;
+  const double* desc = g->elem_scale ? tmp.keep(upload(g->elem_scale, static_cast<size_t>(g->nx * g->ny))) : nullptr;
+  unsigned long long* dkeys = tmp.keep(dev_alloc<unsigned long long>(5));
+  a.coef = dev_alloc<double>(static_cast<size_t>(9 * a.n));
+  a.mass = dev_alloc<double>(static_cast<size_t>(a.n));
+  a.nnz_row = dev_alloc<unsigned char>(static_cast<size_t>(a.n));
+  try {
+    const Sheet2DDev d{g->nx, g->ny, g->h, std::cos(g->fiber_angle), std::sin(g->fiber_angle), g->d0_myocyte,
+                       g->d0_fibrotic, g->rho, dtags, desc};
+    CUDA_TRY(launch_sheet2d_assemble(d, AsmOut{a.coef, a.mass, a.nnz_row, dkeys}, st));
+    unsigned long long keys[5];
+    CUDA_TRY(cudaMemcpyAsync(keys, dkeys, sizeof(keys), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    const auto s = [](long long x) { return std::to_string(x); };
+    if (keys[0] != ~0ull)
+      throw Fail{CWG_EVALIDATION, "assemble: element " + s(static_cast<long long>(keys[0])) +
+                                      " has non-positive Jacobian (degenerate or clockwise)"};
+    if (keys[1] != ~0ull) {
+      const long long i = static_cast<long long>(keys[1] / 16);
+      const int what = static_cast<int>(keys[1] % 16);
+      if (what == 0) throw Fail{CWG_EVALIDATION, "assemble: non-positive lumped mass at node " + s(i)};
+      // the row's present entries, ascending column (= slot) order
+      double row[9];
+      CUDA_TRY(cudaMemcpy2D(row, sizeof(double), a.coef + i, static_cast<size_t>(a.n) * sizeof(double),
+                            sizeof(double), 9, cudaMemcpyDeviceToHost));
+      const long long iy = i / a.w, ix = i % a.w;
+      double row_sum = 0.0;
+      int p = 0;
+      for (int q = 0; q < 9; ++q) {
+        const long long jy = iy + q / 3 - 1, jx = ix + q % 3 - 1;
+        if (jy < 0 || jy > g->ny || jx < 0 || jx > g->nx) continue;
+        if (what == 1 + p)
+          throw Fail{CWG_EVALIDATION, "assemble: stiffness not symmetric at (" + s(i) + ", " + s(jy * a.w + jx) + ")"};
+        row_sum += row[q];
+        ++p;
+      }
+      throw Fail{CWG_EVALIDATION, "assemble: row " + s(i) + " sum " + std::to_string(row_sum) + " not zero"};
+    }
+    if (keys[2] != ~0ull)
+      throw Fail{CWG_EVALIDATION, "gershgorin: row " + s(static_cast<long long>(keys[2])) +
+                                      " has non-positive k_ii + sum|k_ij|; operator is not diffusive"};
+    double min_ratio;
+    std::memcpy(&min_ratio, &keys[4], sizeof(min_ratio));
+    validation(std::isfinite(min_ratio), "gershgorin: no diffusive row");
+    a.dt_s = 0.9 * min_ratio;
+  } catch (...) {
+    a.release();
+    throw;
+  }
+  return a;
+}
 
 // ---------------------------------------------------------------- step pieces
 // Exchange `rows` halo rows (planes) with both neighbours: my first / last
@@ -1159,7 +1253,7 @@ void setup_p2p_nccl(cwg_ctx* c) {
   DevScope scope;
   char* d_all = scope.keep(dev_alloc<char>(sizeof(P2PInfo) * c->world));
   char* d_mine = scope.keep(dev_alloc<char>(sizeof(P2PInfo)));
-  CUDA_TRY(cudaMemcpy(d_mine, &mine, sizeof(P2PInfo), cudaMemcpyHostToDevice));
+  h2d(d_mine, &mine, sizeof(P2PInfo));
   NCCL_TRY(g_nccl.allgather(d_mine, d_all, sizeof(P2PInfo), ncclChar, c->comm, c->stream));
   std::vector<P2PInfo> all(static_cast<size_t>(c->world));
   CUDA_TRY(cudaMemcpyAsync(all.data(), d_all, sizeof(P2PInfo) * c->world, cudaMemcpyDeviceToHost, c->stream));
@@ -1192,7 +1286,7 @@ void setup_p2p_nccl(cwg_ctx* c) {
   if (ok && c->rank + 1 < c->world) open(all[static_cast<size_t>(c->rank + 1)], hi_v, &hi_f);
   // every rank must take the same transport
   int* d_ok = scope.keep(dev_alloc<int>(1));
-  CUDA_TRY(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  h2d(d_ok, &ok, sizeof(int));
   NCCL_TRY(g_nccl.allreduce(d_ok, d_ok, 1, ncclInt, ncclMin, c->comm, c->stream));
   CUDA_TRY(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -1226,11 +1320,13 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   cwg_problem pc = *p_in;
   if (pc.op_kind == CWG_OP_AUTO) infer_grid(&pc);
   const cwg_problem* p = &pc;
+  const bool dev_sheet = pc.op_kind == CWG_OP_SHEET2D;  // operator assembled on the device below
   validation(p->n > 0, "integrator: empty problem");
-  validation(p->lumped_mass != nullptr || p->op_kind == CWG_OP_STRUCT3D, "integrator: missing assembled operator");
+  validation(p->lumped_mass != nullptr || p->op_kind == CWG_OP_STRUCT3D || dev_sheet,
+             "integrator: missing assembled operator");
   validation(p->n_models > 0 && p->model_kind, "integrator: no cell models");
   validation(p->record_interval_ms > 0.0, "scheme: record interval must be positive");
-  validation(p->dt_s > 0.0, "diffusion sub-steps: dt and dt_s must be positive");
+  validation(dev_sheet || p->dt_s > 0.0, "diffusion sub-steps: dt and dt_s must be positive");
   validation(p->world >= 1 && p->rank >= 0 && p->rank < p->world, "placement: bad rank/world");
   validation(p->n < (1ll << 40), "integrator: at most 2^40 nodes");
 
@@ -1244,6 +1340,23 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
   for (auto& e : c->ev) CUDA_TRY(cudaEventCreate(&e));
+
+  // ---- device-assembled sheet: stencil tables and dt_s from assemble.cu; from
+  // here on the context is a stencil-2D one (no CSR crosses PCIe)
+  SheetAsm sheet;
+  struct SheetRelease {
+    SheetAsm& a;
+    ~SheetRelease() { a.release(); }
+  } sheet_release{sheet};
+  if (dev_sheet) {
+    sheet = assemble_sheet2d(p->sheet2d, c->stream);
+    validation(p->n == sheet.n, "operator: n does not match the sheet");
+    pc.dt_s = sheet.dt_s;
+    pc.grid_nx1 = p->sheet2d->nx + 1;
+    pc.grid_ny1 = p->sheet2d->ny + 1;
+    pc.op_kind = CWG_OP_STENCIL2D;
+  }
+  tr.mark("device assembly");
 
   // ---- scheme (StrangIntegrator ctor, splitting.cpp:74-93)
   c->dt_s = p->dt_s;
@@ -1277,7 +1390,8 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   int kind = p->op_kind;
   if (kind == CWG_OP_AUTO) kind = stencil_ok(p) ? CWG_OP_STENCIL2D : CWG_OP_CSR;
   validation(kind == CWG_OP_CSR || kind == CWG_OP_STENCIL2D || kind == CWG_OP_STRUCT3D, "operator: unknown op_kind");
-  if (kind == CWG_OP_STENCIL2D) validation(stencil_ok(p), "operator: CSR is not a regular-sheet 9-point operator");
+  if (kind == CWG_OP_STENCIL2D && !dev_sheet)
+    validation(stencil_ok(p), "operator: CSR is not a regular-sheet 9-point operator");
   c->op_kind = kind;
   c->rank = p->rank;
   c->world = p->world;
@@ -1347,6 +1461,20 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
     CUDA_TRY(launch_mass_factor(c->d_mass, c->n_mass, c->dt_ad, c->d_cm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->d_coef = upload(s3_coef.data(), s3_coef.size());
+  } else if (dev_sheet) {
+    // the coefficient rows of this rank (owned rows + hrows_c halo rows each side)
+    // sliced out of the device-assembled tables; rows beyond the sheet: 0 / mass 1
+    const long long rows_c = (c->row_end - c->row_begin) + 2ll * c->hrows_c;
+    c->n_coef = rows_c * c->w;
+    const long long g0 = (c->row_begin - c->hrows_c) * c->w;
+    c->d_coef = dev_alloc<double>(static_cast<size_t>(9 * c->n_coef));
+    c->d_mass = dev_alloc<double>(static_cast<size_t>(c->n_coef));
+    CUDA_TRY(launch_sheet2d_slice(sheet.coef, sheet.mass, sheet.n, c->w, g0, c->n_coef, c->d_coef, c->d_mass,
+                                  c->stream));
+    c->n_mass = c->n_coef;
+    c->d_cm = dev_alloc<double>(c->n_coef);
+    CUDA_TRY(launch_mass_factor(c->d_mass, c->n_coef, c->dt_ad, c->d_cm, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
   } else {
     validation(p->lumped_mass != nullptr, "integrator: missing assembled operator");
     // lumped mass of the coefficient rows (owned rows, plus hrows_c halo rows
@@ -1366,7 +1494,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   if (kind == CWG_OP_STRUCT3D) {
     // tables uploaded above
   } else if (kind == CWG_OP_STENCIL2D) {
-    build_stencil(c, p);
+    if (!dev_sheet) build_stencil(c, p);
     setup_tma(c);
   } else {
     validation(p->row_ptr && p->col && p->val, "operator: CSR arrays missing");
@@ -1390,11 +1518,28 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   validation(p->model_of_node != nullptr, "integrator: model_of_node missing");
   validation(c->n_alloc < (1ll << 31), "integrator: more than 2^31 local nodes per device (use more ranks)");
   std::vector<long long> per_model(static_cast<size_t>(p->n_models), 0);
-  for (long long o = 0; o < c->n_own; ++o) {
-    const int m = p->model_of_node[c->own_global0 + o];
-    if (m >= p->n_models)  // (message built only on failure: this loop runs over every node)
-      validation(false, "initial state: node " + std::to_string(c->own_global0 + o) + " has no model");
-    ++per_model[static_cast<size_t>(m)];
+  {
+    // byte histogram over the owned nodes, four interleaved tables (no store-to-load chain on a run of equal ids)
+    std::vector<long long> hist(4 * 256, 0);
+    const uint8_t* mo = p->model_of_node + c->own_global0;
+    long long o = 0;
+    for (; o + 4 <= c->n_own; o += 4) {
+      ++hist[mo[o]];
+      ++hist[256 + mo[o + 1]];
+      ++hist[512 + mo[o + 2]];
+      ++hist[768 + mo[o + 3]];
+    }
+    for (; o < c->n_own; ++o) ++hist[mo[o]];
+    for (int m = 0; m < 256; ++m) {
+      const long long cnt = hist[m] + hist[256 + m] + hist[512 + m] + hist[768 + m];
+      if (m < p->n_models) {
+        per_model[static_cast<size_t>(m)] = cnt;
+      } else if (cnt > 0) {  // the reference names the first node without a model
+        for (long long q = 0; q < c->n_own; ++q)
+          if (mo[q] >= p->n_models)
+            validation(false, "initial state: node " + std::to_string(c->own_global0 + q) + " has no model");
+      }
+    }
   }
   for (int m = 0; m < p->n_models; ++m) {
     Bin b;
@@ -1431,7 +1576,9 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
         b.d_counter_b = dev_alloc<unsigned>(4);
         CUDA_TRY(cudaMemset(b.d_counter_b, 0, 4 * sizeof(unsigned)));
         const long long e = c->split_rows * c->w;
-        b.variant_b = choose_ord_variant(e, c->num_sms);
+        // the interior's launch shape: ptxas contracts mul/add pairs per kernel instance, so
+        // only the same instance keeps the slab run bit-identical to the single-GPU one
+        b.variant_b = b.variant;
         const int threads = is_ord(b.kind) ? react_ord_threads(b.variant_b) : react_exact_threads(b.kind);
         const int occ = std::max(1, is_ord(b.kind) ? react_ord_occupancy(b.kind, b.variant_b)
                                                    : react_exact_occupancy(b.kind));
@@ -1459,17 +1606,17 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
       validation(p->stim_duration[e] > 0.0, "stimulus: duration must be positive");
       validation(std::isfinite(p->stim_amplitude[e]), "stimulus: amplitude must be finite");
     }
-    std::vector<int32_t> ptr(static_cast<size_t>(c->n_alloc + 1), 0), ids;
-    for (long long li = 0; li < c->n_alloc; ++li) {
-      const long long g = li + c->node_offset;
-      const bool owned = li >= c->halo && li < c->halo + c->n_own;
-      if (owned && g >= 0 && g < p->n)
-        for (int32_t q = p->stim_node_ptr[g]; q < p->stim_node_ptr[g + 1]; ++q) ids.push_back(p->stim_ids[q]);
-      ptr[static_cast<size_t>(li + 1)] = static_cast<int32_t>(ids.size());
-    }
-    if (!ids.empty()) {
-      c->d_stim_ptr = upload(ptr.data(), ptr.size());
-      c->d_stim_ids = upload(ids.data(), ids.size());
+    // the owned nodes' entry lists are one contiguous slice of stim_ids; the local
+    // per-node pointer array (0 over the lower halo, the total over the upper one)
+    // is rebased from the caller's on the device
+    const int32_t id0 = p->stim_node_ptr[c->own_global0], id1 = p->stim_node_ptr[c->own_global0 + c->n_own];
+    if (id1 > id0) {
+      DevScope tmp;
+      const int32_t* gptr = tmp.keep(upload(p->stim_node_ptr + c->own_global0, static_cast<size_t>(c->n_own + 1)));
+      c->d_stim_ptr = dev_alloc<int32_t>(static_cast<size_t>(c->n_alloc + 1));
+      CUDA_TRY(launch_stim_local_ptr(gptr, c->n_own, c->halo, c->n_alloc, c->d_stim_ptr, c->stream));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      c->d_stim_ids = upload(p->stim_ids + id0, static_cast<size_t>(id1 - id0));
       c->d_st0 = upload(p->stim_t_start, p->n_stim);
       c->d_sdur = upload(p->stim_duration, p->n_stim);
       c->d_samp = upload(p->stim_amplitude, p->n_stim);
@@ -1483,7 +1630,7 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->d_clock = dev_alloc<long long>(1);
   c->d_khist = dev_alloc<unsigned long long>(c->khist_len);
   ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
-  CUDA_TRY(cudaMemcpy(c->d_err, &none, sizeof(none), cudaMemcpyHostToDevice));
+  h2d(c->d_err, &none, sizeof(none));
   CUDA_TRY(cudaMemset(c->d_clock, 0, sizeof(long long)));
   c->clock_at = 0;
   CUDA_TRY(cudaMemset(c->d_khist, 0, c->khist_len * sizeof(unsigned long long)));
@@ -1575,12 +1722,12 @@ bool fetch_error(cwg_ctx* c, bool use_t, double t_fixed, cwg_error* out) {
   if (c->world > 1 && !c->loopback) {
     long long* tmp = dev_alloc<long long>(2);
     long long h[2] = {r.key == kNoError ? (1ll << 62) : r.seq, 0};
-    CUDA_TRY(cudaMemcpy(tmp, h, sizeof(long long), cudaMemcpyHostToDevice));
+    h2d(tmp, h, sizeof(long long));
     NCCL_TRY(g_nccl.allreduce(tmp, tmp, 1, ncclInt64, ncclMin, c->comm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemcpy(h, tmp, sizeof(long long), cudaMemcpyDeviceToHost));
     unsigned long long key = (r.key != kNoError && r.seq == h[0]) ? r.key : kNoError;
-    CUDA_TRY(cudaMemcpy(tmp, &key, sizeof(key), cudaMemcpyHostToDevice));
+    h2d(tmp, &key, sizeof(key));
     NCCL_TRY(g_nccl.allreduce(tmp, tmp, 1, ncclUint64, ncclMin, c->comm, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemcpy(&key, tmp, sizeof(key), cudaMemcpyDeviceToHost));
@@ -1726,6 +1873,49 @@ int cwg_slab_plan(int64_t ny1, int world, int rank, int64_t* row_begin, int64_t*
   *row_begin = rank * base + std::min<int64_t>(rank, extra);
   *row_end = *row_begin + base + (rank < extra ? 1 : 0);
   return CWG_OK;
+}
+
+int64_t cwg_sheet2d_nnz(const cwg_sheet2d* g) {
+  if (!g || g->nx < 1 || g->ny < 1) return 0;
+  return (3 * g->nx + 1) * (3 * g->ny + 1);  // rows with 2 (edge) or 3 neighbours per axis, incl. the node
+}
+
+int cwg_sheet2d_assemble(const cwg_sheet2d* g, int device, int64_t* row_ptr, int64_t* col, double* val,
+                         double* lumped_mass, double* dt_s, cwg_error* err) {
+  return guarded(err, [&] {
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = nullptr;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    struct StreamGuard {
+      cudaStream_t s;
+      ~StreamGuard() { cudaStreamDestroy(s); }
+    } sg{st};
+    SheetAsm a = assemble_sheet2d(g, st);
+    struct Release {
+      SheetAsm& a;
+      ~Release() { a.release(); }
+    } rel{a};
+    if (dt_s) *dt_s = a.dt_s;
+    if (lumped_mass)
+      CUDA_TRY(cudaMemcpy(lumped_mass, a.mass, static_cast<size_t>(a.n) * sizeof(double), cudaMemcpyDeviceToHost));
+    if (row_ptr || col || val) {  // the stencil table -> the reference's CSR (ascending columns)
+      std::vector<double> coef(static_cast<size_t>(9 * a.n));
+      CUDA_TRY(cudaMemcpy(coef.data(), a.coef, coef.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      int64_t q = 0;
+      for (long long i = 0; i < a.n; ++i) {
+        if (row_ptr) row_ptr[i] = q;
+        const long long iy = i / a.w, ix = i % a.w;
+        for (int sl = 0; sl < 9; ++sl) {
+          const long long jy = iy + sl / 3 - 1, jx = ix + sl % 3 - 1;
+          if (jy < 0 || jy > g->ny || jx < 0 || jx > g->nx) continue;
+          if (col) col[q] = jy * a.w + jx;
+          if (val) val[q] = coef[static_cast<size_t>(sl) * a.n + i];
+          ++q;
+        }
+      }
+      if (row_ptr) row_ptr[a.n] = q;
+    }
+  });
 }
 
 int cwg_create(const cwg_problem* prob, cwg_ctx** out, cwg_error* err) {
@@ -2200,29 +2390,23 @@ int cwg_get_maps(cwg_ctx* c, double* lat, uint8_t* lat_valid, double* apd, uint8
   return guarded(nullptr, [&] {
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    // straight into the caller's arrays (no host temporaries), then NaN where a map has no value
+    // straight into the caller's arrays (no host temporaries); NaN where a map has
+    // no value, filled on the device on the way out
     const size_t n = static_cast<size_t>(c->n_own);
-    std::vector<unsigned char> lv_tmp, av_tmp;
-    unsigned char* lv = lat_valid;
-    unsigned char* av = apd_valid;
-    if (!lv && lat) {
-      lv_tmp.resize(n);
-      lv = lv_tmp.data();
+    DevScope tmp;
+    if (lat) {
+      double* d = tmp.keep(dev_alloc<double>(n));
+      CUDA_TRY(launch_map_values(c->det.lat, c->det.has_lat, static_cast<long long>(n), d, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(lat, d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     }
-    if (!av && apd) {
-      av_tmp.resize(n);
-      av = av_tmp.data();
+    if (apd) {
+      double* d = tmp.keep(dev_alloc<double>(n));
+      CUDA_TRY(launch_map_values(c->det.apd, c->det.has_apd, static_cast<long long>(n), d, c->stream));
+      CUDA_TRY(cudaMemcpyAsync(apd, d, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     }
-    if (lat) CUDA_TRY(cudaMemcpyAsync(lat, c->det.lat, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (apd) CUDA_TRY(cudaMemcpyAsync(apd, c->det.apd, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (lv) CUDA_TRY(cudaMemcpyAsync(lv, c->det.has_lat, n, cudaMemcpyDeviceToHost, c->stream));
-    if (av) CUDA_TRY(cudaMemcpyAsync(av, c->det.has_apd, n, cudaMemcpyDeviceToHost, c->stream));
+    if (lat_valid) CUDA_TRY(cudaMemcpyAsync(lat_valid, c->det.has_lat, n, cudaMemcpyDeviceToHost, c->stream));
+    if (apd_valid) CUDA_TRY(cudaMemcpyAsync(apd_valid, c->det.has_apd, n, cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
-    const double nan = std::nan("");
-    for (size_t i = 0; i < n; ++i) {
-      if (lat && !lv[i]) lat[i] = nan;
-      if (apd && !av[i]) apd[i] = nan;
-    }
   });
 }
 
@@ -2614,7 +2798,7 @@ extern "C" int cwg_diastolic_threshold(const cwg_problem* prob, const double* co
     c->d_err_dummy = dev_alloc<ErrRec>(1);
     {
       const ErrRec none{kNoError, kNoSeq, 0, 0, nullptr, nullptr};
-      CUDA_TRY(cudaMemcpy(c->d_err_dummy, &none, sizeof(none), cudaMemcpyHostToDevice));
+      h2d(c->d_err_dummy, &none, sizeof(none));
     }
     c->d_cross = dev_alloc<long long>(1);
     c->probe_local = probe - c->node_offset;

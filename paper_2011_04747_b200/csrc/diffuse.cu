@@ -1580,6 +1580,40 @@ cudaError_t launch_init_rest(double* v, double* S, long long pitch, double* last
   return cudaGetLastError();
 }
 
+namespace {
+__global__ void map_values(const double* val, const unsigned char* has, long long n, double* out) {
+  const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (i < n) out[i] = has[i] ? val[i] : __longlong_as_double(0x7ff8000000000000ll);
+}
+
+// ProtocolIndex pointer array of a slab context from the caller's global one
+// (gptr = its owned slice, n_own + 1 entries): 0 over the lower halo, rebased
+// over the owned nodes, the total over the upper halo.
+__global__ void stim_local_ptr(const int32_t* gptr, long long n_own, long long halo, long long n_alloc,
+                               int32_t* ptr) {
+  const long long li = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  if (li > n_alloc) return;
+  const int32_t base = gptr[0];
+  int32_t v;
+  if (li <= halo) v = 0;
+  else if (li <= halo + n_own) v = gptr[li - halo] - base;
+  else v = gptr[n_own] - base;
+  ptr[li] = v;  // ptr[li] = entries of local nodes < li
+}
+}  // namespace
+
+cudaError_t launch_map_values(const double* val, const unsigned char* has, long long n, double* out, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  map_values<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(val, has, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stim_local_ptr(const int32_t* gptr, long long n_own, long long halo, long long n_alloc,
+                                  int32_t* ptr, cudaStream_t st) {
+  stim_local_ptr<<<blocks_for(n_alloc + 1, 256, 1 << 30), 256, 0, st>>>(gptr, n_own, halo, n_alloc, ptr);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st) {
   if (n == 0) return cudaSuccess;
   mass_factor<<<blocks_for(n, 256, 1 << 30), 256, 0, st>>>(mass, n, dt_sub, cm);

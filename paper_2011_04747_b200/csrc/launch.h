@@ -71,6 +71,26 @@ cudaError_t launch_fp64_peak(double* out, int blocks, int iters, cudaStream_t st
 cudaError_t launch_init_rest(double* v, double* S, long long pitch, double* last, const int32_t* list,
                               long long first, long long count, const double* rest, int ns, int stride,
                               cudaStream_t st);
+// device assembly of a regular sheet (assemble.cu)
+struct Sheet2DDev {
+  long long nx, ny;                 // element counts
+  double h, fx, fy;                 // spacing, fibre direction (cos, sin: computed by the host's libm)
+  double d0m, d0f, rho;
+  const int32_t* tags;              // [n] device, 1 = fibroblast; null = none
+  const double* escale;             // [nx*ny] device; null = 1
+};
+struct AsmOut {
+  double* coef;                     // [9][n] stencil coefficients (slot order = ascending column)
+  double* mass;                     // [n] lumped mass
+  unsigned char* nnz_row;           // [n] entries per row
+  unsigned long long* keys;         // [5] element / structural / Gershgorin failure, max|k| bits, min m/den bits
+};
+cudaError_t launch_sheet2d_assemble(const Sheet2DDev& g, const AsmOut& o, cudaStream_t st);
+cudaError_t launch_sheet2d_slice(const double* coef, const double* mass, long long n, long long w, long long g0,
+                                 long long cnt, double* coef_out, double* mass_out, cudaStream_t st);
 cudaError_t launch_mass_factor(const double* mass, long long n, double dt_sub, double* cm, cudaStream_t st);
+cudaError_t launch_map_values(const double* val, const unsigned char* has, long long n, double* out, cudaStream_t st);
+cudaError_t launch_stim_local_ptr(const int32_t* gptr, long long n_own, long long halo, long long n_alloc,
+                                  int32_t* ptr, cudaStream_t st);
 
 }  // namespace cwg

@@ -10,7 +10,10 @@
 //   * 1/(1 + a/x) style terms are rewritten as x/(x + a) (one reciprocal);
 //   * e^x, e^2x, expm1(2x) for the GHK terms derive from one expm1(x); the
 //     reciprocal-pair exponentials (tff, tfcaf) share one exp;
-//   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one fexp(log).
+//   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one fexp(log);
+//   * Nernst potentials log(c_o / c_i) = log(c_o) - log(c_i) (no reciprocal);
+//   * every reciprocal is the MUFU seed + one cubic Newton step (3 DFMA,
+//     faithful, fastmath.cuh rcp_nc / rcp_g) instead of __drcp_rn's 5.
 // It therefore agrees with the reference to rounding, not bitwise; the parity
 // contract for ORd is max|dV| <= 1e-6 mV (tests/test_gpu_parity.py), which
 // the survey's +-1-ulp experiment shows is met with ~8 orders of margin.
@@ -39,7 +42,7 @@ constexpr double AGEO = 2.0 * 3.14 * 0.0011 * 0.0011 + 2.0 * 3.14 * 0.0011 * 0.0
 constexpr double ACAP = 2.0 * AGEO;
 constexpr double VMYO = 0.68 * VCELL, VNSR = 0.0552 * VCELL, VJSR = 0.0048 * VCELL, VSS = 0.02 * VCELL;
 
-__device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+__device__ __forceinline__ double rcp(double x) { return rcp_g(x); }  // fastmath.cuh
 
 // FP = true ("fast" evaluation, taken when |V| <= 130 mV): every exponent
 // argument that depends on V alone is then provably < 708 in magnitude and
@@ -47,10 +50,14 @@ __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
 // use the branch-free fexp_nc / rcp_nc. Concentration-dependent reciprocals
 // and exponentials always use the checked forms (they can reach 0 / Inf /
 // NaN while a node blows up, where IEEE semantics decide the abort step).
+// s (v + a) / b written as fma(v, s / b, s a / b) with both constants folded:
+// one FP64 instruction per exponent argument instead of an add and a multiply
+// (absolute error ~ulp(a / b), i.e. a few ulp of the exponential near x = 0)
+__device__ __forceinline__ double lin(double v, double slope, double offset) { return fma(v, slope, offset); }
 template <bool FP>
 __device__ __forceinline__ double vexp(double x) { return FP ? fexp_nc(x) : fexp(x); }
 template <bool FP>
-__device__ __forceinline__ double vrcp(double x) { return FP ? rcp_nc(x) : __drcp_rn(x); }
+__device__ __forceinline__ double vrcp(double x) { return FP ? rcp_nc(x) : rcp_g(x); }
 template <bool FP>
 __device__ __forceinline__ double sigm(double u) { return vrcp<FP>(1.0 + vexp<FP>(u)); }  // 1/(1+e^u)
 template <bool FP, int N>
@@ -68,7 +75,7 @@ __device__ __forceinline__ void vrcp_n(double (&x)[N]) {
     rcp_nc_n(x);
   } else {
 #pragma unroll
-    for (int i = 0; i < N; ++i) x[i] = __drcp_rn(x[i]);
+    for (int i = 0; i < N; ++i) x[i] = rcp_g(x[i]);
   }
 }
 
@@ -92,7 +99,9 @@ struct Var {
 // x / expm1(x) given em = expm1(x) (ohara_rudy_2011.cpp:67-70)
 template <bool FP>
 __device__ __forceinline__ double xem1(double x, double em) {
-  return fabs(x) < 1e-8 ? vrcp<FP>(1.0 + 0.5 * x) : x * vrcp<FP>(em);
+  const bool small = fabs(x) < 1e-8;
+  const double r = vrcp<FP>(small ? 1.0 + 0.5 * x : em);  // one reciprocal for both branches
+  return small ? r : x * r;
 }
 
 struct NcxShared {
@@ -134,17 +143,26 @@ enum {
   D, FF, FS, FCAF, FCAS, JCA, NCA, FFP, FCAFP, XRF, XRS, XS1, XS2, XK1, JRELNP, JRELP, CAMKT, NSTATE
 };
 
-// gate FE update: x += h * (x_inf - x) * rate (SA: register array or shared-memory column)
-// Output policy: R = false integrates in place (x += h*dx, never contracted);
-// R = true only reports dx (CellModel::rates semantics, for cwg_rates).
+// State FE updates (SA: register array or shared-memory column).
+// Output policy: R = false integrates in place; R = true only reports dx
+// (CellModel::rates semantics, for cwg_rates).
+#ifndef CWG_ORD_FMA_UPDATE
+#define CWG_ORD_FMA_UPDATE 1
+#endif
+// x += h * dx. With CWG_ORD_FMA_UPDATE the update is one fused multiply-add
+// (the exact x + h dx rounded once, where the reference rounds h dx first):
+// one FP64 instruction and one dependent step fewer per state; the membrane
+// potential keeps the reference's two roundings (fe, react.cuh).
 template <bool R, class SA>
 __device__ __forceinline__ void put(SA s, double* ds, int i, double h, double d) {
   if (R) ds[i] = d;
-  else s[i] = fe(s[i], h, d);
+  else s[i] = CWG_ORD_FMA_UPDATE ? fma(h, d, s[i]) : fe(s[i], h, d);
 }
+// gate: x += h * (x_inf - x) * rate, as x + (x_inf - x) (h rate) in one FMA
 template <bool R, class SA>
 __device__ __forceinline__ void gate(SA s, double* ds, int i, double h, double xinf, double rate) {
-  put<R>(s, ds, i, h, (xinf - s[i]) * rate);
+  if (R || !CWG_ORD_FMA_UPDATE) put<R>(s, ds, i, h, (xinf - s[i]) * rate);
+  else s[i] = fma(xinf - s[i], h * rate, s[i]);
 }
 
 // The evaluation is split into composable pieces (prologue, group A: INa,
@@ -167,9 +185,10 @@ template <int CT, bool FP, class SA>
 __device__ __forceinline__ Pro prologue(double v, SA s) {
   Pro p;
   const double nai = s[NAI], ki = s[KI], cass = s[CASS];
-  p.ena = RTF * flog(NAO * rcp(nai));
-  p.ek = RTF * flog(KO * rcp(ki));
-  p.eks = RTF * flog((KO + 0.01833 * NAO) * rcp(ki + 0.01833 * nai));
+  // log(a / x) = log(a) - log(x): no reciprocal (log 140, log 5.4, log(5.4 + 0.01833 * 140))
+  p.ena = RTF * (4.941642422609304 - flog(nai));
+  p.ek = RTF * (1.6863989535702288 - flog(ki));
+  p.eks = RTF * (2.0752075911477745 - flog(ki + 0.01833 * nai));
   p.camkt = s[CAMKT];
   p.camk_b = 0.05 * (1.0 - p.camkt) * cass * rcp(cass + 0.0015);
   const double camk_a = p.camk_b + p.camkt;
@@ -199,14 +218,14 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- INa + INaL: the 14 V-dependent exponentials in one batch
   double i_na;
   {
-    double e[12] = {-(v + 39.57) * (1.0 / 9.871),   (v + 11.64) * (1.0 / 34.77),  -(v + 77.42) * (1.0 / 5.955),
-                    (v + 82.90) * (1.0 / 6.086),    -(v + 1.196) * (1.0 / 6.285), (v + 0.5096) * (1.0 / 20.27),
-                    -(v + 17.95) * (1.0 / 28.05),   (v + 5.730) * (1.0 / 56.66),  -(v + 100.6) * (1.0 / 8.281),
-                    (v + 0.9941) * (1.0 / 38.45),   -(v + 42.85) * (1.0 / 5.264), (v + 87.61) * (1.0 / 7.488)};
+    double e[12] = {lin(v, -1.0 / (9.871), -(39.57) / (9.871)),   lin(v, 1.0 / (34.77), (11.64) / (34.77)),  lin(v, -1.0 / (5.955), -(77.42) / (5.955)),
+                    lin(v, 1.0 / (6.086), (82.90) / (6.086)),    lin(v, -1.0 / (6.285), -(1.196) / (6.285)), lin(v, 1.0 / (20.27), (0.5096) / (20.27)),
+                    lin(v, -1.0 / (28.05), -(17.95) / (28.05)),   lin(v, 1.0 / (56.66), (5.730) / (56.66)),  lin(v, -1.0 / (8.281), -(100.6) / (8.281)),
+                    lin(v, 1.0 / (38.45), (0.9941) / (38.45)),   lin(v, -1.0 / (5.264), -(42.85) / (5.264)), lin(v, 1.0 / (7.488), (87.61) / (7.488))};
     vexp_n<FP>(e);
     // e^((v+89.1)/6.086) = e^((v+82.9)/6.086) e^(6.2/6.086), e^((v+93.81)/7.488) = e^((v+87.61)/7.488) e^(6.2/7.488)
-    const double e_hp = FP ? e[3] * 2.7696792380394113 : vexp<FP>((v + 89.1) * (1.0 / 6.086));
-    const double e_hlp = FP ? e[11] * 2.288717124596482 : vexp<FP>((v + 93.81) * (1.0 / 7.488));
+    const double e_hp = FP ? e[3] * 2.7696792380394113 : vexp<FP>(lin(v, 1.0 / (6.086), (89.1) / (6.086)));
+    const double e_hlp = FP ? e[11] * 2.288717124596482 : vexp<FP>(lin(v, 1.0 / (7.488), (93.81) / (7.488)));
     double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e_hp, 1.0 + e[10], 1.0 + e[11], 1.0 + e_hlp,
                    0.02136 * e[8] + 0.3052 * e[9]};
     vrcp_n<FP>(q);
@@ -236,14 +255,14 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- Ito
   double i_to;
   {
-    double e[13] = {-(v - 14.34) * (1.0 / 14.82),     -(v - 18.4099) * (1.0 / 29.3814), (v + 100.0) * (1.0 / 29.3814),
-                    (v + 43.94) * (1.0 / 5.711),      -(v + 100.0) * (1.0 / 100.0),     (v + 50.0) * (1.0 / 16.59),
-                    -(v + 96.52) * (1.0 / 59.05),     (v + 114.1) * (1.0 / 8.079),      (v + 70.0) * (1.0 / 5.0),
-                    (v - 213.6) * (1.0 / 151.2),      (v - 167.4) * (1.0 / 15.89),      -(v - 12.23) * (1.0 / 0.2154),
-                    (v + 70.0) * (1.0 / 20.0)};
+    double e[13] = {lin(v, -1.0 / (14.82), -(-14.34) / (14.82)),     lin(v, -1.0 / (29.3814), -(-18.4099) / (29.3814)), lin(v, 1.0 / (29.3814), (100.0) / (29.3814)),
+                    lin(v, 1.0 / (5.711), (43.94) / (5.711)),      lin(v, -1.0 / (100.0), -(100.0) / (100.0)),     lin(v, 1.0 / (16.59), (50.0) / (16.59)),
+                    lin(v, -1.0 / (59.05), -(96.52) / (59.05)),     lin(v, 1.0 / (8.079), (114.1) / (8.079)),      lin(v, 1.0 / (5.0), (70.0) / (5.0)),
+                    lin(v, 1.0 / (151.2), (-213.6) / (151.2)),      lin(v, 1.0 / (15.89), (-167.4) / (15.89)),      lin(v, -1.0 / (0.2154), -(-12.23) / (0.2154)),
+                    lin(v, 1.0 / (20.0), (70.0) / (20.0))};
     vexp_n<FP>(e);
     // e^(-(v-24.34)/14.82) = e^(-(v-14.34)/14.82) e^(10/14.82)
-    const double e_ap = FP ? e[0] * 1.9635691902911017 : vexp<FP>(-(v - 24.34) * (1.0 / 14.82));
+    const double e_ap = FP ? e[0] * 1.9635691902911017 : vexp<FP>(lin(v, -1.0 / (14.82), -(-24.34) / (14.82)));
     double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), 1.0 + e[2], 1.0 + e[3],
                     0.3933 * e[4] + 0.08004 * e[5], 0.001416 * e[6] + 1.780e-8 * e[7], 1.0 + e[8],
                     1.0 + e[9], 1.0 + e_ap, e[10] + e[11], 1.0 + e[12]};
@@ -280,14 +299,14 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
-    double e[10] = {-(v + 3.940) * (1.0 / 4.230), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
-                    (v + 19.58) * (1.0 / 3.696),  (v + 20.0) * (1.0 / 10.0),  -(v + 5.0) * (1.0 / 4.0),
-                    (v + 5.0) * (1.0 / 6.0),      (v - 4.0) * (1.0 / 7.0),    -v * (1.0 / 3.0),
+    double e[10] = {lin(v, -1.0 / (4.230), -(3.940) / (4.230)), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
+                    lin(v, 1.0 / (3.696), (19.58) / (3.696)),  lin(v, 1.0 / (10.0), (20.0) / (10.0)),  lin(v, -1.0 / (4.0), -(5.0) / (4.0)),
+                    lin(v, 1.0 / (6.0), (5.0) / (6.0)),      lin(v, 1.0 / (7.0), (-4.0) / (7.0)),    -v * (1.0 / 3.0),
                     v * (1.0 / 7.0)};
     vexp_n<FP>(e);
     const double eff = e[4], efc = e[7];
     // e^((v-10)/10) = e^((v+20)/10) e^-3
-    const double e_fca = FP ? e[4] * 0.049787068367863944 : vexp<FP>((v - 10.0) * (1.0 / 10.0));
+    const double e_fca = FP ? e[4] * 0.049787068367863944 : vexp<FP>(lin(v, 1.0 / (10.0), (-10.0) / (10.0)));
     double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, 0.000035 * e[5] + 0.000035 * e[6], efc,
                    0.00012 * e[8] + 0.00012 * e[9], 1.0 + e_fca};
     vrcp_n<FP>(q);
@@ -346,9 +365,9 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
   // ---------------- IKr, IKs, IK1
   double i_k;  // IKr + IKs + IK1
   {
-    double e[8] = {-(v + 8.337) * (1.0 / 6.789), (v - 31.66) * (1.0 / 3.869), -(v - 47.78) * (1.0 / 20.38),
-                   (v - 34.70) * (1.0 / 7.355),  -(v - 29.74) * (1.0 / 25.94), (v + 54.81) * (1.0 / 38.21),
-                   (v + 55.0) * (1.0 / 75.0),    (v - 10.0) * (1.0 / 30.0)};
+    double e[8] = {lin(v, -1.0 / (6.789), -(8.337) / (6.789)), lin(v, 1.0 / (3.869), (-31.66) / (3.869)), lin(v, -1.0 / (20.38), -(-47.78) / (20.38)),
+                   lin(v, 1.0 / (7.355), (-34.70) / (7.355)),  lin(v, -1.0 / (25.94), -(-29.74) / (25.94)), lin(v, 1.0 / (38.21), (54.81) / (38.21)),
+                   lin(v, 1.0 / (75.0), (55.0) / (75.0)),    lin(v, 1.0 / (30.0), (-10.0) / (30.0))};
     vexp_n<FP>(e);
     double q[5] = {1.0 + e[0], 0.3652 * e[1] + 4.123e-5 * e[2], 0.06629 * e[3] + 1.128e-5 * e[4], 1.0 + e[5],
                    (1.0 + e[6]) * (1.0 + e[7])};
@@ -361,10 +380,10 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
-    double f[9] = {-(v + 11.60) * (1.0 / 8.932),  (v + 48.28) * (1.0 / 17.80), -(v + 210.0) * (1.0 / 230.0),
-                   (v - 50.0) * (1.0 / 20.0),     -(v + 66.54) * (1.0 / 31.0),
+    double f[9] = {lin(v, -1.0 / (8.932), -(11.60) / (8.932)),  lin(v, 1.0 / (17.80), (48.28) / (17.80)), lin(v, -1.0 / (230.0), -(210.0) / (230.0)),
+                   lin(v, 1.0 / (20.0), (-50.0) / (20.0)),     lin(v, -1.0 / (31.0), -(66.54) / (31.0)),
                    -(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)),
-                   -(v + 127.2) * (1.0 / 20.36),  (v + 236.8) * (1.0 / 69.33),  (v + 105.8 - 2.6 * KO) * (1.0 / 9.493)};
+                   lin(v, -1.0 / (20.36), -(127.2) / (20.36)),  lin(v, 1.0 / (69.33), (236.8) / (69.33)),  lin(v, 1.0 / (9.493), (105.8 - 2.6 * KO) / (9.493))};
     vexp_n<FP>(f);
     double p[4] = {1.0 + f[0], 2.326e-4 * f[1] + 0.001292 * f[2], 1.0 + f[5], 1.0 + f[8]};
     vrcp_n<FP>(p);
@@ -427,7 +446,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
   }
 
   // ---------------- background currents
-  const double i_kb = P::gkb * sigm<FP>(-(v - 14.48) * (1.0 / 18.34)) * (v - ek);
+  const double i_kb = P::gkb * sigm<FP>(lin(v, -1.0 / (18.34), -(-14.48) / (18.34))) * (v - ek);
   const double i_nab = (3.75e-10 * F) * (nai * e1 - NAO) * xq1;
   const double i_cab = (2.5e-8 * 2.0 * F) * (cai * e2 - 0.341 * CAO) * xq2;
   const double i_pca = 0.0005 * cai * rcp(0.0005 + cai);

