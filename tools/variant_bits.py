@@ -8,7 +8,7 @@ from paper_2011_04747_b200 import problems
 p = problems.c4(t_end=float(sys.argv[1]) if len(sys.argv) > 1 else 3.0)
 setup = p.setup()
 res = {}
-for v in ("1", "0"):
+for v in sys.argv[2].split() if len(sys.argv) > 2 else ("1", "0"):
     os.environ["CWG_ORD_VARIANT"] = v
     r = cw.run_simulation(p.initial_state(), setup, p.cfg)
     res[v] = r.final_state
