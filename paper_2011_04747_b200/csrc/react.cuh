@@ -35,12 +35,6 @@ __host__ __device__ constexpr bool preclaim_of() {
 }
 
 template <class M>
-__host__ __device__ constexpr bool staged_of() {
-  if constexpr (requires { M::kStaged; }) return M::kStaged;
-  return false;
-}
-
-template <class M>
 __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -145,211 +139,6 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Staged refill (M::kStaged: the persistent lockstep shapes). Every lane refill
-// above waits ~1 us for its node's 43 columns from HBM, and in lockstep all
-// warps refill at the top of the same evaluation round, so that latency sits on
-// every round (ncu C4: long scoreboard 5% + barrier 11% of the stall samples).
-// Here the block claims nodes in chunks of kStageChunk consecutive positions
-// and every thread stages a share of a chunk's V, last_dvdt, states, stimulus
-// pointers and GKr scale into shared memory with cp.async while the block
-// evaluates; refills then read shared memory. Two chunk buffers: `cur` is being
-// taken from, the other is either ready (its copies waited for and published by
-// the round barrier) or being filled. A lane that finds both exhausted claims a
-// single position from the global counter and loads it directly (the unstaged
-// path; e.g. k = 1 everywhere drains chunks faster than one per round).
-// Bookkeeping is thread 0's, between the round barrier and a second barrier;
-// the chunk it will assign next is claimed one rotation ahead, so the global
-// atomic's latency never sits between the two barriers.
-// ---------------------------------------------------------------------------
-constexpr int kStageChunk = 256;
-
-template <int NS>
-struct StageBuf {
-  double col[NS + 2][kStageChunk];  // V, last_dvdt, states
-  int2 stim[kStageChunk];           // ProtocolIndex node_ptr[node], node_ptr[node + 1]
-  double gkr[kStageChunk];
-};
-struct StageMeta {
-  long long base[2];  // first position of the chunk in each buffer
-  int cnt[2];         // positions in the chunk
-  unsigned take[2];   // positions taken (may overshoot cnt)
-  int ready[2];       // copies complete and published
-  int cur;            // buffer refills take from first
-  int fill;           // buffer whose copies start this round (-1: none)
-  int global_done;    // the global counter is exhausted
-};
-
-template <class M>
-__device__ __forceinline__ void stage_copy(const ReactArgs& a, StageBuf<M::NS>& b, long long base, int cnt) {
-  constexpr int R = M::NS + 2;
-  for (int e = threadIdx.x; e < (R + 2) * kStageChunk; e += blockDim.x) {
-    const int q = e / kStageChunk, j = e % kStageChunk;
-    if (j >= cnt) continue;
-    const long long pos = base + j;
-    const long long node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
-    const void* src;
-    void* dst;
-    if (q < R) {
-      src = q == 0 ? a.v + node : (q == 1 ? a.last + node : a.S + (q - 2) * a.pitch + node);
-      dst = &b.col[q][j];
-    } else if (q == R) {
-      if (!a.stim.node_ptr) continue;
-      const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&b.stim[j]));
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(a.stim.node_ptr + node) : "memory");
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa + 4), "l"(a.stim.node_ptr + node + 1)
-                   : "memory");
-      continue;
-    } else {
-      if (!M::kUsesGkr || !a.gkr) continue;
-      src = a.gkr + node;
-      dst = &b.gkr[j];
-    }
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src) : "memory");
-  }
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-
-template <class M>
-__device__ __forceinline__ void react_body_staged(const ReactArgs& a, unsigned* shist, StageBuf<M::NS>* buf,
-                                                  StageMeta& meta) {
-  const int lane = threadIdx.x & 31;
-  const long long step = *a.clock + a.step_off;
-  const double t = a.use_t_fixed ? a.t_fixed : static_cast<double>(step) * a.dt;  // splitting.cpp:270
-  const long long seq = step * a.evs + a.ev;
-  const long long first_span = static_cast<long long>(gridDim.x) * kStageChunk;  // static first chunks
-  long long pending = -1;  // thread 0: base of the chunk claimed for the next rotation
-
-  if (threadIdx.x == 0) {
-    const long long b0 = static_cast<long long>(blockIdx.x) * kStageChunk;
-    const long long b1 = atomicAdd(a.counter, static_cast<unsigned>(kStageChunk)) + first_span;
-    pending = atomicAdd(a.counter, static_cast<unsigned>(kStageChunk)) + first_span;
-    const long long bs[2] = {b0, b1};
-    for (int i = 0; i < 2; ++i) {
-      const long long left = a.count - bs[i];
-      meta.base[i] = bs[i];
-      meta.cnt[i] = static_cast<int>(left <= 0 ? 0 : (left < kStageChunk ? left : kStageChunk));
-      meta.take[i] = 0u;
-      meta.ready[i] = 1;
-    }
-    meta.cur = 0;
-    meta.fill = -1;
-    meta.global_done = 0;
-  }
-  __syncthreads();
-  stage_copy<M>(a, buf[0], meta.base[0], meta.cnt[0]);
-  stage_copy<M>(a, buf[1], meta.base[1], meta.cnt[1]);
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
-
-  long long node = -1;
-  int k = 0, j = 0, p0 = 0, p1 = 0;
-  double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
-  double s[M::NS];
-  while (true) {
-    // ---- refill: the current buffer, then the other if ready, then one global position
-    if (node < 0) {
-      int b = meta.cur;
-      int idx = static_cast<int>(atomicAdd(&meta.take[b], 1u));
-      if (idx >= meta.cnt[b]) {
-        b ^= 1;
-        idx = -1;
-        if (meta.ready[b]) {
-          idx = static_cast<int>(atomicAdd(&meta.take[b], 1u));
-          if (idx >= meta.cnt[b]) idx = -1;
-        }
-      }
-      if (idx >= 0) {
-        const StageBuf<M::NS>& sb = buf[b];
-        const long long pos = meta.base[b] + idx;
-        node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
-        v = sb.col[0][idx];
-        k = substeps(sb.col[1][idx], a.scheme, a.k0_up, a.k0_down, a.kmax);
-#pragma unroll
-        for (int q = 0; q < M::NS; ++q) s[q] = sb.col[2 + q][idx];
-        if (a.stim.node_ptr) {
-          p0 = sb.stim[idx].x;
-          p1 = sb.stim[idx].y;
-        }
-        if (M::kUsesGkr) g = a.gkr ? sb.gkr[idx] : 1.0;
-      } else if (!meta.global_done) {
-        const long long pos = atomicAdd(a.counter, 1u) + first_span;
-        if (pos < a.count) {
-          node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
-          v = a.v[node];
-          k = substeps(a.last[node], a.scheme, a.k0_up, a.k0_down, a.kmax);
-#pragma unroll
-          for (int q = 0; q < M::NS; ++q) s[q] = a.S[q * a.pitch + node];
-          if (a.stim.node_ptr) {
-            p0 = __ldg(a.stim.node_ptr + node);
-            p1 = __ldg(a.stim.node_ptr + node + 1);
-          }
-          if (M::kUsesGkr) g = a.gkr ? __ldg(a.gkr + node) : 1.0;
-        } else {
-          meta.global_done = 1;  // benign race: every writer stores 1
-        }
-      }
-      if (node >= 0) {
-        h = a.dt / static_cast<double>(k);  // dt_ar (splitting.cpp:117)
-        j = 0;
-        dv = 0.0;
-        atomicAdd(shist + k, 1u);
-      }
-    }
-    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's share of the chunk being filled
-    bool pend = false;
-    if (threadIdx.x == 0)  // a chunk still holds positions (take only grows: a stale read errs towards "pending")
-      pend = meta.take[0] < static_cast<unsigned>(meta.cnt[0]) || meta.take[1] < static_cast<unsigned>(meta.cnt[1]);
-    if (!__syncthreads_or(node >= 0 || pend)) break;
-    // ---- bookkeeping (thread 0): publish a filled buffer, rotate an exhausted one
-    if (threadIdx.x == 0) {
-      if (meta.fill >= 0) meta.ready[meta.fill] = 1;
-      meta.fill = -1;
-      const int c = meta.cur;
-      if (meta.take[c] >= static_cast<unsigned>(meta.cnt[c]) && meta.ready[c ^ 1]) {
-        meta.cur = c ^ 1;
-        const long long left = a.count - pending;
-        meta.base[c] = pending;
-        meta.cnt[c] = static_cast<int>(left <= 0 ? 0 : (left < kStageChunk ? left : kStageChunk));
-        meta.take[c] = 0u;
-        meta.ready[c] = 0;
-        if (meta.cnt[c] > 0) {
-          meta.fill = c;
-          pending = atomicAdd(a.counter, static_cast<unsigned>(kStageChunk)) + first_span;  // next rotation's
-        } else {
-          meta.ready[c] = 1;  // empty: nothing to wait for
-        }
-      }
-    }
-    __syncthreads();
-    if (meta.fill >= 0) stage_copy<M>(a, buf[meta.fill], meta.base[meta.fill], meta.cnt[meta.fill]);
-    // ---- one rates() evaluation
-    if (node >= 0) {
-      const double ts = __dadd_rn(t, __dmul_rn(static_cast<double>(j), h));  // t + j*dt_ar, never contracted
-      const double ist = p1 > p0 ? stim_current(a.stim, p0, p1, ts) : 0.0;
-      M::advance(v, s, ist, g, h, dv);
-      ++j;
-      const bool bad = !isfinite(v);
-      if (bad) {
-        const unsigned long long key = (static_cast<unsigned long long>(node + a.node_offset) << 22) |
-                                       (static_cast<unsigned long long>(k) << 11) |
-                                       static_cast<unsigned long long>(j - 1);
-        record_failure(a.err, key, seq, 1, 1, a.v, a.v);
-      }
-      if (bad || j == k) {
-        a.v[node] = v;
-        a.last[node] = dv;  // dv at the start of the last sub-step (splitting.cpp:143)
-#pragma unroll
-        for (int q = 0; q < M::NS; ++q) a.S[q * a.pitch + node] = s[q];
-        node = -1;
-      }
-    }
-  }
-  (void)lane;
-  asm volatile("cp.async.wait_all;" ::: "memory");
-}
-
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -368,15 +157,7 @@ __global__ void __launch_bounds__(M::kThreads, M::kMinBlocks) react_kernel(React
     for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x) shist[i] = 0u;
     if constexpr (requires { M::block_init(); }) M::block_init();  // e.g. the exp table (fastmath.cuh)
     __syncthreads();
-    if constexpr (staged_of<M>()) {
-      // dynamic shared memory: [khist (rounded to 16 B)] [StageMeta] [2 x StageBuf]
-      const int hist_bytes = ((a.khist_len + 3) & ~3) * static_cast<int>(sizeof(unsigned));
-      StageMeta* meta = reinterpret_cast<StageMeta*>(reinterpret_cast<char*>(shist) + hist_bytes);
-      auto* bufs = reinterpret_cast<StageBuf<M::NS>*>(reinterpret_cast<char*>(meta) + ((sizeof(StageMeta) + 15) & ~15));
-      react_body_staged<M>(a, shist, bufs, *meta);
-    } else {
-      react_body<M>(a, shist);
-    }
+    react_body<M>(a, shist);
     __syncthreads();
     for (int i = threadIdx.x; i < a.khist_len; i += blockDim.x)
       if (shist[i]) atomicAdd(a.khist + i, static_cast<unsigned long long>(shist[i]));

@@ -556,10 +556,9 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = (V == 1 || V == 4) ? 384 : (V == 2 ? 256 : (V == 7 ? 288 : 128));
+  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 7 ? 288 : 128));
   static constexpr int kMinBlocks = V == 0 ? 2 : 1;
   static constexpr bool kBlockSync = V != 0;
-  static constexpr bool kStaged = V == 4;  // react.cuh react_body_staged: refills from shared memory
   static constexpr bool kPreclaim = V == 0;  // react.cuh: claim the next node one trip ahead
   static constexpr bool kUsesGkr = true;
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
@@ -589,10 +588,6 @@ __global__ void ord_rates_kernel(long long n, const double* v, const double* s, 
 
 template <class M>
 static size_t smem_bytes(int khist_len) {
-  if constexpr (staged_of<M>()) {  // react_kernel: [khist] [StageMeta] [2 x StageBuf]
-    const size_t hist = static_cast<size_t>((khist_len + 3) & ~3) * sizeof(unsigned);
-    return hist + ((sizeof(StageMeta) + 15) & ~static_cast<size_t>(15)) + 2 * sizeof(StageBuf<M::NS>);
-  }
   const size_t hist = static_cast<size_t>((khist_len + 1) & ~1) * sizeof(unsigned);
   return hist;
 }
@@ -620,7 +615,7 @@ static int occupancy_t() {
 
 // Launch-shape variants (see ModelOrd). The host picks one per model bin
 // (cwg_host.cu: choose_ord_variant); CWG_ORD_VARIANT overrides for experiments.
-#define CWG_ORD_VARIANTS(X) X(0) X(1) X(2) X(4) X(7)
+#define CWG_ORD_VARIANTS(X) X(0) X(1) X(2) X(7)
 
 bool react_ord_variant_valid(int v) {
   switch (v) {
