@@ -50,10 +50,10 @@ FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<epi>>
 # (2*DFMA + DMUL + DADD predicated-on lane ops / evaluations), counted by ncu
 # over every reaction launch of a 40-step C4 run (tools/flops_per_eval.py c4 40;
-# profiles/r02b_flops_per_eval_c4.txt): 910.1 DFMA + 354.3 DMUL + 222.4 DADD
-# (was 2,735.9 before the short reciprocal and the fused updates,
-# profiles/r02_flops_per_eval_c4.txt). Updated when the kernel changes.
-ORD_FP64_FLOPS_PER_EVAL = 2396.9
+# profiles/r02c_flops_per_eval_c4.txt): 794.1 DFMA + 354.3 DMUL + 222.4 DADD
+# (C2: 2,153.6; 2,735.9 before this session's reciprocal / fused-update / exp
+# changes, profiles/r02_flops_per_eval_c4.txt). Updated when the kernel changes.
+ORD_FP64_FLOPS_PER_EVAL = 2164.9
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 

@@ -327,6 +327,15 @@ class DeviceSheetOperator:
     def rows(self):
         return self.n
 
+    def __getattr__(self, name):
+        # the CSR views (row_ptr, col, val, lumped_mass, entry) for the entry points that take an
+        # AssembledOperator (diffusion_substep, diastolic_threshold, ...): assembled once on demand
+        if name in ("row_ptr", "col", "val", "lumped_mass", "entry"):
+            if "_csr" not in self.__dict__:
+                self.__dict__["_csr"] = self.csr()
+            return getattr(self.__dict__["_csr"], name)
+        raise AttributeError(name)
+
     def csr(self) -> AssembledOperator:
         nnz = L.lib().cwg_sheet2d_nnz(C.byref(self.desc))
         rp, col = np.zeros(self.n + 1, np.int64), np.zeros(nnz, np.int64)

@@ -175,3 +175,15 @@ def test_device_operator_slabs(world):
         else:
             os.environ["CWG_LOOPBACK"] = old
     assert np.array_equal(out.v, ref.final_state.v)
+
+
+def test_device_operator_serves_csr_entry_points():
+    """The CSR-taking entry points (diffusion_substep, fem.cpp:194-207) accept a device-assembled operator: its
+    CSR views are assembled once on demand, and the sub-step equals the one on .csr()."""
+    import paper_2011_04747_b200 as cw
+    dev = cw.Sheet(1.0, 1.0, 0.02, 0.3, d0_myocyte=0.0012, rho=0.25, assembly="device")
+    v = np.random.default_rng(5).uniform(-90.0, 40.0, dev.n)
+    a = cw.diffusion_substep(dev.op, v, dev.op.dt_s)
+    b = cw.diffusion_substep(dev.op.csr(), v, dev.op.dt_s)
+    assert np.array_equal(a, b)
+    assert dev.op.entry(0, 0) == dev.op.csr().entry(0, 0)
