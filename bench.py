@@ -54,6 +54,9 @@ FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # (C2: 2,153.6; 2,735.9 before this session's reciprocal / fused-update / exp
 # changes, profiles/r02_flops_per_eval_c4.txt). Updated when the kernel changes.
 ORD_FP64_FLOPS_PER_EVAL = 2164.9
+# the same count in FP64 pipe issue slots (DFMA + DMUL + DADD warp-lane instructions per evaluation): a DMUL or
+# DADD takes the slot a DFMA does, so the pipe-slot fraction reads higher than the flop fraction
+ORD_FP64_INSTR_PER_EVAL = 1370.8
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 
@@ -478,14 +481,17 @@ def main():
                          "traffic": traffic, "peak_source": "in-run DFMA microbenchmark (MEASURED_PEAKS.json has no "
                                                              "FP64 entry)",
                          "flops_per_eval": ORD_FP64_FLOPS_PER_EVAL,
+                         "fp64_instr_per_eval": ORD_FP64_INSTR_PER_EVAL,
+                         "fp64_pipe_slot_frac": (ORD_FP64_INSTR_PER_EVAL * local_evals / (react_tot_ms / 1e3) / 1e12)
+                                                / (fp64_peak / 2.0) if fp64_peak > 0 else None,
                          "fp64_pipe_active_ncu": pipe_ncu / 100.0 if pipe_ncu is not None else None,
                          "note": ("latency regime: ~1 node per lane (8 warps/SM at >168 registers), each node's k "
                                   "sub-steps sequential, so the step's largest k sets the critical path; the "
                                   "event-timed phase includes ~10 us of launch/completion latency around a ~42 us "
                                   "kernel span (tools/react_trace.py, DESIGN.md 3.5)" if args.config in ("c1", "c2") else
-                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 55% of "
+                                  "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 50% of "
                                   "active cycles on C4, 8-cycle FP64 latency with 3 warps per sub-partition "
-                                  "(profiles/r02_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
+                                  "(profiles/r02c_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
                                   "read+write per launch (algorithmic 677 B x 3.2M nodes = 2.18 GB)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
