@@ -1,3 +1,4 @@
+"""Loopback (CWG_LOOPBACK=1) run of C4 split into y-slab contexts on one device: usage loopback_probe.py <t_end_ms> <world>; prints the cwg_loopback_steps status."""
 import os, sys, ctypes as C
 sys.path.insert(0, os.getcwd())
 os.environ["CWG_LOOPBACK"] = "1"
