@@ -476,11 +476,12 @@ __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& p
   // ---------------- SR release / uptake, buffers
   const double jrel = nfk * s[JRELNP] + fk * s[JRELP];
   {
-    const double rr = 1.5 * rcp(cajsr);
+    const double rc = rcp(cajsr);
+    const double rr = 1.5 * rc;
     const double rr2 = rr * rr, rr4 = rr2 * rr2;
     const double gate_rel = rcp(1.0 + rr4 * rr4);
     const double jrel_inf = (0.5 * 4.75 * P::jrel) * (-i_cal) * gate_rel;
-    double r_rel = (cajsr + 0.0123) * rcp(4.75 * cajsr);  // 1/tau_rel
+    double r_rel = (cajsr + 0.0123) * (rc * (1.0 / 4.75));  // 1/tau_rel (one reciprocal of cajsr for both)
     double r_relp = r_rel * (1.0 / 1.25);
     r_rel = r_rel > 200.0 ? 200.0 : r_rel;  // tau_rel >= 0.005 (NaN passes through, like the reference)
     r_relp = r_relp > 200.0 ? 200.0 : r_relp;
