@@ -12,7 +12,8 @@ reaction pass + 2l diffusion sub-steps + the record cadence). Default run:
 the whole 500 ms simulation (W warm-up steps, then K = 5000 - W timed).
 N > 1 (torchrun): strong scaling of the same C4 grid -- rank r owns a
 contiguous y-slab, halo exchange of the fused diffusion launches over NCCL
-(--scaling weak stacks one C4 per rank instead). --config c1/c2/c3/c5 pick
+(--scaling weak stacks one C4 per rank instead; --config c5 likewise splits the
+201M-node slab). --config c1/c2/c3/c5 pick
 the other BASELINE configurations.
 
 metric: node-updates/s = (reaction rates evaluations + diffusion node
@@ -166,6 +167,8 @@ def build_problem(config, world, rank, scaling="strong"):
     from paper_2011_04747_b200 import problems
     if config == "c4" and (world == 1 or scaling == "strong"):
         return problems.c4()  # N > 1: every rank gets the full grid and keeps its own y-slab (cwg_slab_plan)
+    if config == "c5" and (world == 1 or scaling == "strong"):
+        return problems.c5()  # BASELINE configs[4]: the 201M-node slab partitioned across the ranks' y-slabs
     if config == "c2":
         if world == 1:
             return problems.c2()
@@ -186,8 +189,6 @@ def build_problem(config, world, rank, scaling="strong"):
         # weak scaling: the slab grows in y with the number of ranks (same y extent per GPU)
         if config == "c4":
             return problems.slab(5.0, 5.0 * world, 1.0, 0.02, t_end=500.0)
-        if world == 1:
-            return problems.c5()
         return problems.slab(10.0, 10.0 * world, 2.0, 0.01, t_end=5.0, stim="sites", n_sites=16 * world,
                              amplitude=problems.C5_AMPLITUDE, site_radius=problems.C5_SITE_RADIUS)
     raise SystemExit(f"unknown config {config}")
@@ -200,8 +201,8 @@ def config_block(config, prob, world, l):
              "c3": "BASELINE configs[2] (extension): 1001x1001 scar/border-zone sheet",
              "c4": "BASELINE configs[3] (extension): 3D slab 5x5x1 cm, 251x251x51 nodes (3,213,051), fibres +60..-60 "
                    "deg, endocardial face stimulus, ORd-epi, DAETI dt 0.1 ms, 500 ms",
-             "c5": "BASELINE configs[4] (extension): 3D slab 10x10x2 cm, 1001x1001x201 nodes per GPU, 16 random "
-                   "endocardial sites, ORd-epi"}
+             "c5": "BASELINE configs[4] (extension): 3D slab 10x10x2 cm, 1001x1001x201 nodes (201M; y-slabs "
+                   "across the ranks), 16 random endocardial sites, ORd-epi"}
     return {"workload": names[config], "nodes": int(prob.n), "nodes_per_gpu": int(prob.n // max(world, 1)),
             "cell_model": prob.models[0], "scheme": "DAETI", "dt_ms": prob.cfg.dt_ms, "k0_up": prob.cfg.k0_up,
             "k0_down": prob.cfg.k0_down, "diffusion_substeps_per_step": 2 * l,
@@ -468,7 +469,8 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": t_dev_ms / K, "higher_is_better": True,
-            "scaling": "strong" if (args.config == "c4" and args.scaling == "strong") else "weak", "vs_baseline": None,
+            "scaling": "strong" if (args.config in ("c4", "c5") and args.scaling == "strong") else "weak",
+            "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "config": config_block(args.config, prob, world, info.l),
             "sim_ms_per_s": K * prob.cfg.dt_ms / (t_dev_ms / 1e3),
             "reaction_node_updates_per_s": reaction_evals / (t_dev_ms / 1e3),
