@@ -651,15 +651,19 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
+// Rows of the padded coefficient tensor: the coefficient rows of the context (owned rows plus hrows_c
+// halo rows each side on a multi-rank slab, so fused launches advance the neighbours' edge rows too)
+long long tma_rows(const cwg_ctx* c) { return (c->row_end - c->row_begin) + 2ll * c->hrows_c; }
+
 void refresh_padded_cm(cwg_ctx* c) {
   if (!c->d_coefp) return;
-  CUDA_TRY(launch_pad_planes(c->d_cm, 0, 1, c->w, c->row_end - c->row_begin, c->d_coefp, c->w_pad, 9, c->stream));
+  CUDA_TRY(launch_pad_planes(c->d_cm, 0, 1, c->w, tma_rows(c), c->d_coefp, c->w_pad, 9, c->stream));
 }
 
 void setup_tma(cwg_ctx* c) {
   const char* e = getenv("CWG_TB_TMA");
   if (e && e[0] == '0') return;
-  if (c->op_kind != CWG_OP_STENCIL2D || c->world > 1 || !c->d_coef) return;
+  if (c->op_kind != CWG_OP_STENCIL2D || !c->d_coef) return;
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q{};
   if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
@@ -667,14 +671,14 @@ void setup_tma(cwg_ctx* c) {
     cudaGetLastError();
     return;
   }
-  const long long rows = c->row_end - c->row_begin;
+  const long long rows = tma_rows(c);
   unsigned bx0 = 0, by0 = 0;
   int margin = 0;
   tbm_box(4, &bx0, &by0, &margin);
   c->w_pad = (c->w + margin + 1) / 2 * 2;  // zeroed left margin; 16-byte row pitch
   c->d_coefp = dev_alloc<double>(static_cast<size_t>(10 * rows * c->w_pad));
   CUDA_TRY(cudaMemsetAsync(c->d_coefp, 0, static_cast<size_t>(10 * rows * c->w_pad) * sizeof(double), c->stream));
-  CUDA_TRY(launch_pad_planes(c->d_coef, c->n_own, 9, c->w, rows, c->d_coefp, c->w_pad, 0, c->stream));
+  CUDA_TRY(launch_pad_planes(c->d_coef, c->n_coef, 9, c->w, rows, c->d_coefp, c->w_pad, 0, c->stream));
   refresh_padded_cm(c);
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(c->w + margin), static_cast<cuuint64_t>(rows), 10};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(c->w_pad) * 8, static_cast<cuuint64_t>(rows * c->w_pad) * 8};
@@ -693,9 +697,11 @@ void setup_tma(cwg_ctx* c) {
   c->tma_ok = ok;
 }
 
-// Large one-GPU sheets take the TMA-fed persistent kernel (enqueue_diffusion).
+// Large sheets (and y-slabs) take the TMA-fed persistent kernels (enqueue_diffusion). They do not store
+// the neighbours' halo rows themselves, so a slab linked by the peer-memory transport keeps the
+// register-loading kernel (which does); NCCL / loopback slabs exchange between launches.
 bool tma_path(const cwg_ctx* c) {
-  return c->tma_ok && ((c->w + 63) / 64) * ((c->row_end - c->row_begin + 15) / 16) >= 2ll * c->num_sms;
+  return c->tma_ok && !c->pl.on && ((c->w + 63) / 64) * ((c->row_end - c->row_begin + 15) / 16) >= 2ll * c->num_sms;
 }
 
 // sub-steps fused per launch by the temporal-blocking stencil (1 = off; CWG_DIFF_TB overrides): up to

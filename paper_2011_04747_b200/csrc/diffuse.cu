@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
             "r"(smem_u32(cfs)),
-        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(ly0 - (T - 1)), "r"(0), "r"(bar_a)
+        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(static_cast<int>(ly0 + s.hrows_c) - (T - 1)), "r"(0), "r"(bar_a)
         : "memory");
   };
   auto fetch_v = [&](int tile, double* vdst) {
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
             "r"(smem_u32(cfs)),
-        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(ly0 - (T - 1)), "r"(0), "r"(bar_a)
+        "l"(&tmap), "r"(gx0 - SX + kTmaMargin), "r"(static_cast<int>(ly0 + s.hrows_c) - (T - 1)), "r"(0), "r"(bar_a)
         : "memory");
   };
   // V rows ly0-T-1 .. ly0+TBY+T, columns gx0-VOFF .. gx0-VOFF+VX-1 (zero outside the sheet / local rows);
@@ -702,8 +702,10 @@ void tbm_box(int T, unsigned* cx, unsigned* cy, int* margin) {
 
 cudaError_t launch_diffuse_stencil2d_tbm(int T, const DiffArgs& a, const Stencil2D& s, const CUtensorMap& tm,
                                          int num_sms, cudaStream_t st) {
-  const char* e = getenv("CWG_TBQ");  // register-quad kernel by default; CWG_TBQ=0: the slot kernel (A/B)
-  if (!(e && e[0] == '0')) {
+  // register-quad kernel by default; CWG_TBQ=0: the slot kernel (A/B, one GPU only: it does not advance
+  // a slab's halo rows)
+  const char* e = getenv("CWG_TBQ");
+  if (!(e && e[0] == '0') || s.hrows_c > 0) {
     switch (T) {
       case 2: return launch_tbq_t<2>(a, s, tm, num_sms, st);
       case 3: return launch_tbq_t<3>(a, s, tm, num_sms, st);

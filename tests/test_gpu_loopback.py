@@ -223,3 +223,17 @@ def test_peer_memory_transport_2d(world):
     out, kh = _loopback(q, world, link=True)
     ref = _single(q)
     assert np.array_equal(out.v, ref.final_state.v) and np.array_equal(kh, ref.k_histogram)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_loopback_c3_tma_slabs(world):
+    """BASELINE configs[2] (C3, 1001 x 1001, 22 diffusion sub-steps per step) in y-slabs: the TMA-fed register-quad
+    diffusion kernel runs on the slabs too (coefficient tensor with the halo rows, fused depth <= the halo depth,
+    exchanges between launches) -- bit-identical to the single context, which fuses up to 6 sub-steps."""
+    from paper_2011_04747_b200 import problems
+    p = problems.c3(t_end=2.0)
+    out, kh = _loopback(p, world)
+    ref = _single(p)
+    assert np.array_equal(out.v, ref.final_state.v)
+    assert np.array_equal(out.s, ref.final_state.s)
+    assert np.array_equal(kh, ref.k_histogram)
