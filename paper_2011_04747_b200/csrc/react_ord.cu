@@ -42,7 +42,15 @@ constexpr double AGEO = 2.0 * 3.14 * 0.0011 * 0.0011 + 2.0 * 3.14 * 0.0011 * 0.0
 constexpr double ACAP = 2.0 * AGEO;
 constexpr double VMYO = 0.68 * VCELL, VNSR = 0.0552 * VCELL, VJSR = 0.0048 * VCELL, VSS = 0.02 * VCELL;
 
-__device__ __forceinline__ double rcp(double x) { return rcp_g(x); }  // fastmath.cuh
+// Concentration-dependent reciprocals and logs: on the fast path (FP: |V| <= 130
+// mV AND every concentration in the range conc_ok() checks) each argument is
+// provably a normal, finite, positive number, so the unchecked forms give the
+// same bits as the checked ones without a branch per call; otherwise the
+// checked forms keep IEEE special values (the abort step depends on them).
+template <bool FP>
+__device__ __forceinline__ double crcp(double x) { return FP ? rcp_nc(x) : rcp_g(x); }
+template <bool FP>
+__device__ __forceinline__ double clog(double x) { return FP ? flog_nc(x) : flog(x); }
 
 // FP = true ("fast" evaluation, taken when |V| <= 130 mV): every exponent
 // argument that depends on V alone is then provably < 708 in magnitude and
@@ -109,14 +117,15 @@ struct NcxShared {
 };
 
 // Na/Ca exchanger flux for one compartment (ohara_rudy_2011.cpp:264-300)
+template <bool FP>
 __device__ __forceinline__ double ncx(double na, double ca, const NcxShared& c) {
   constexpr double h10 = 12.5 + 1.0 + NAO / 15.0 * (1.0 + NAO / 5.0);
   constexpr double h11 = NAO * NAO / (h10 * 15.0 * 5.0);
   constexpr double k1 = 1.0 / h10 * CAO * 1.5e6;
   constexpr double k2 = 5.0e3, k5 = 5.0e3;
-  const double r1 = rcp(1.0 + na * (1.0 / 88.12) * (1.0 + c.hna));
+  const double r1 = crcp<FP>(1.0 + na * (1.0 / 88.12) * (1.0 + c.hna));
   const double h2 = na * c.hna * (1.0 / 88.12) * r1;
-  const double r4 = rcp(1.0 + na * (1.0 / 15.0) * (1.0 + na * (1.0 / 5.0)));
+  const double r4 = crcp<FP>(1.0 + na * (1.0 / 15.0) * (1.0 + na * (1.0 / 5.0)));
   const double h5 = na * na * (1.0 / 75.0) * r4;
   const double k3pp = c.h8 * 5.0e3;
   const double k3 = c.h9 * 6.0e4 + k3pp;
@@ -129,9 +138,9 @@ __device__ __forceinline__ double ncx(double na, double ca, const NcxShared& c) 
   const double x2 = k1 * k7 * (k4 + k5) + k4 * k6 * (k1 + k8);
   const double x3 = k1 * k3 * (k7 + k6) + k8 * k6 * (k2 + k3);
   const double x4 = k2 * k8 * (k4 + k5) + k3 * k5 * (k1 + k8);
-  const double rt = rcp(x1 + x2 + x3 + x4);
+  const double rt = crcp<FP>(x1 + x2 + x3 + x4);
   const double ca2 = ca * ca;
-  const double allo = ca2 * rcp(ca2 + 150.0e-6 * 150.0e-6);
+  const double allo = ca2 * crcp<FP>(ca2 + 150.0e-6 * 150.0e-6);
   const double j_na = 3.0 * (x4 * k7 - x1 * k8) + x3 * k4pp - x2 * k3pp;
   const double j_ca = x2 * k2 - x1 * k1;
   return allo * rt * (j_na + 2.0 * j_ca);
@@ -186,13 +195,13 @@ __device__ __forceinline__ Pro prologue(double v, SA s) {
   Pro p;
   const double nai = s[NAI], ki = s[KI], cass = s[CASS];
   // log(a / x) = log(a) - log(x): no reciprocal (log 140, log 5.4, log(5.4 + 0.01833 * 140))
-  p.ena = RTF * (4.941642422609304 - flog(nai));
-  p.ek = RTF * (1.6863989535702288 - flog(ki));
-  p.eks = RTF * (2.0752075911477745 - flog(ki + 0.01833 * nai));
+  p.ena = RTF * (4.941642422609304 - clog<FP>(nai));
+  p.ek = RTF * (1.6863989535702288 - clog<FP>(ki));
+  p.eks = RTF * (2.0752075911477745 - clog<FP>(ki + 0.01833 * nai));
   p.camkt = s[CAMKT];
-  p.camk_b = 0.05 * (1.0 - p.camkt) * cass * rcp(cass + 0.0015);
+  p.camk_b = 0.05 * (1.0 - p.camkt) * cass * crcp<FP>(cass + 0.0015);
   const double camk_a = p.camk_b + p.camkt;
-  p.fk = camk_a * rcp(camk_a + 0.15);
+  p.fk = camk_a * crcp<FP>(camk_a + 0.15);
   p.nfk = 1.0 - p.fk;
   p.vfrt = v * FRT;
   const double vfrt = p.vfrt;
@@ -323,9 +332,9 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     const double fpmix = 0.6 * s[FFP] + (1.0 - 0.6) * s[FS];
     const double fcapmix = a_fcaf * s[FCAFP] + a_fcas * s[FCAS];
     const double jca = s[JCA], nca = s[NCA];
-    const double cn = (cass + 0.002) * rcp(cass);
+    const double cn = (cass + 0.002) * crcp<FP>(cass);
     const double cn2 = cn * cn;
-    const double anca = jca * rcp(1000.0 + jca * (cn2 * cn2));
+    const double anca = jca * crcp<FP>(1000.0 + jca * (cn2 * cn2));
     const double phi_cal = 2.0 * F * (cass * e2 - 0.341 * CAO) * xq2;
     const double phi_cana = F * (0.75 * nass * e1 - 0.75 * NAO) * xq1;
     const double phi_cak = F * (0.75 * kss * e1 - 0.75 * KO) * xq1;
@@ -390,7 +399,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     const double xs_inf = p[0];
     const double r_xs1 = vrcp<FP>(817.3 + p[1]);
     const double r_xs2 = 0.01 * f[3] + 0.0193 * f[4];
-    const double ksca = 1.0 + 0.6 * rcp(1.0 + fexp(1.4 * (-10.177924398237888 - flog(cai))) /* log(3.8e-5) */);
+    const double ksca = 1.0 + 0.6 * crcp<FP>(1.0 + vexp<FP>(1.4 * (-10.177924398237888 - clog<FP>(cai))) /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
@@ -413,8 +422,8 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     const double r7 = vrcp<FP>(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
     c.h9 = r7;
     c.h8 = NAO * (1.0 / 88.12) * hna_r * r7;
-    inaca_i = (0.8 * P::gncx) * ncx(nai, cai, c);
-    inaca_ss = (0.2 * P::gncx) * ncx(nass, cass, c);
+    inaca_i = (0.8 * P::gncx) * ncx<FP>(nai, cai, c);
+    inaca_ss = (0.2 * P::gncx) * ncx<FP>(nass, cass, c);
   }
 
   // ---------------- INaK
@@ -425,13 +434,13 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     constexpr double b1 = 182.4 * 0.05, a2 = 687.2;
     constexpr double a4 = 639.0 * 9.8 / 1.698e-7 / (1.0 + 9.8 / 1.698e-7);
     constexpr double b3c = 79300.0 * 1.0e-7 / (1.0 + 9.8 / 1.698e-7);
-    const double p_hp = 4.2 * rcp(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
+    const double p_hp = 4.2 * crcp<FP>(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
     const double ri = nai * (1.0 / 9.073) * vexp<FP>((0.1550 / 3.0) * vfrt);     // nai / Knai
     const double ro = NAO * (1.0 / 27.78) * vexp<FP>(-(1.1550 / 3.0) * vfrt);   // nao / Knao
     const double rk = ki * 2.0;                                            // ki / 0.5
     const double ci = (1.0 + ri) * (1.0 + ri) * (1.0 + ri), qi = (1.0 + rk) * (1.0 + rk);
     const double co = (1.0 + ro) * (1.0 + ro) * (1.0 + ro);
-    const double di = rcp(ci + qi - 1.0), dco = rcp(co + qo - 1.0);
+    const double di = crcp<FP>(ci + qi - 1.0), dco = crcp<FP>(co + qo - 1.0);
     const double a1 = 949.5 * (ri * ri * ri) * di;
     const double b2 = 39.4 * (ro * ro * ro) * dco;
     const double a3 = 1899.0 * (rko * rko) * dco;
@@ -441,7 +450,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     const double y2 = b2 * b1 * b4 + a1 * a2 * a3 + a3 * b1 * b4 + a2 * a3 * b4;
     const double y3 = a2 * a3 * a4 + b3 * b2 * b1 + b2 * b1 * a4 + a3 * a4 * b1;
     const double y4 = b4 * b3 * b2 + a3 * a4 * a1 + b2 * a4 * a1 + b3 * b2 * a1;
-    const double ry = rcp(y1 + y2 + y3 + y4);
+    const double ry = crcp<FP>(y1 + y2 + y3 + y4);
     i_nak = P::pnak * ry * (3.0 * (y1 * a3 - y2 * b3) + 2.0 * (y4 * b1 - y3 * a1));
   }
 
@@ -449,7 +458,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
   const double i_kb = P::gkb * sigm<FP>(lin(v, -1.0 / (18.34), -(-14.48) / (18.34))) * (v - ek);
   const double i_nab = (3.75e-10 * F) * (nai * e1 - NAO) * xq1;
   const double i_cab = (2.5e-8 * 2.0 * F) * (cai * e2 - 0.341 * CAO) * xq2;
-  const double i_pca = 0.0005 * cai * rcp(0.0005 + cai);
+  const double i_pca = 0.0005 * cai * crcp<FP>(0.0005 + cai);
 
   o.i_k = i_k;
   o.inaca_i = inaca_i;
@@ -463,7 +472,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
 }
 
 // SR fluxes (Jrel gates need ICaL), CaMKt, buffers, concentrations, dV
-template <int CT, bool R, class SA>
+template <int CT, bool R, bool FP, class SA>
 __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& pr, const CurA& A, const CurB& B,
                                        double ist, double h, double& dv) {
   using P = Var<CT>;
@@ -476,10 +485,10 @@ __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& p
   // ---------------- SR release / uptake, buffers
   const double jrel = nfk * s[JRELNP] + fk * s[JRELP];
   {
-    const double rc = rcp(cajsr);
+    const double rc = crcp<FP>(cajsr);
     const double rr = 1.5 * rc;
     const double rr2 = rr * rr, rr4 = rr2 * rr2;
-    const double gate_rel = rcp(1.0 + rr4 * rr4);
+    const double gate_rel = crcp<FP>(1.0 + rr4 * rr4);
     const double jrel_inf = (0.5 * 4.75 * P::jrel) * (-i_cal) * gate_rel;
     double r_rel = (cajsr + 0.0123) * (rc * (1.0 / 4.75));  // 1/tau_rel (one reciprocal of cajsr for both)
     double r_relp = r_rel * (1.0 / 1.25);
@@ -489,8 +498,8 @@ __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& p
     gate<R>(s, ds, JRELP, h, jrel_inf * 1.25, r_relp);
     put<R>(s, ds, CAMKT, h, 0.05 * camk_b * (camk_b + camkt) - 0.00068 * camkt);
   }
-  const double jup_np = (0.004375 * P::jup) * cai * rcp(cai + 0.00092);
-  const double jup_p = (2.75 * 0.004375 * P::jup) * cai * rcp(cai + 0.00092 - 0.00017);
+  const double jup_np = (0.004375 * P::jup) * cai * crcp<FP>(cai + 0.00092);
+  const double jup_p = (2.75 * 0.004375 * P::jup) * cai * crcp<FP>(cai + 0.00092 - 0.00017);
   const double j_up = nfk * jup_np + fk * jup_p - (0.0039375 / 15.0) * cansr;
   const double j_tr = (cansr - cajsr) * (1.0 / 100.0);
   const double jd_na = (nass - nai) * 0.5;
@@ -501,14 +510,14 @@ __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& p
     const double kc = 0.00238 + cai, kt = 0.0005 + cai;
     const double kc2 = kc * kc, kt2 = kt * kt;
     const double pc = kc2 * kt2;
-    b_cai = pc * rcp(pc + (P::cmdn * 0.00238) * kt2 + (0.07 * 0.0005) * kc2);
+    b_cai = pc * crcp<FP>(pc + (P::cmdn * 0.00238) * kt2 + (0.07 * 0.0005) * kc2);
     const double kb = 0.00087 + cass, kl = 0.0087 + cass;
     const double kb2 = kb * kb, kl2 = kl * kl;
     const double pb = kb2 * kl2;
-    b_cass = pb * rcp(pb + (0.047 * 0.00087) * kl2 + (1.124 * 0.0087) * kb2);
+    b_cass = pb * crcp<FP>(pb + (0.047 * 0.00087) * kl2 + (1.124 * 0.0087) * kb2);
     const double kq = 0.8 + cajsr;
     const double kq2 = kq * kq;
-    b_cajsr = kq2 * rcp(kq2 + 10.0 * 0.8);
+    b_cajsr = kq2 * crcp<FP>(kq2 + 10.0 * 0.8);
   }
 
   // ---------------- concentrations (last: every current above read the old values)
@@ -526,13 +535,29 @@ __device__ __forceinline__ void finish(double& v, SA s, double* ds, const Pro& p
   if (!R) v = fe(v, h, dv);
 }
 
+// The fast path's precondition on the state (besides |V| <= 130 mV): the eight
+// concentrations in [1e-10, 1e10] mM, CaMKt in [0, 1e10] and the jca gate in
+// [0, 1e10]. Then every concentration-dependent denominator and log argument
+// of the model is a sum or product of bounded positive terms -- normal, finite,
+// positive (e.g. 1000 + jca cn^4 >= 1000 with cn <= 2e7; 1 + (1.5/cajsr)^8 <=
+// 3e80; the NCX cycle total and the INaK y-sum are positive sums of positive
+// rate products) -- so the unchecked reciprocals / logs return exactly the
+// checked ones' bits. Physiological values sit orders of magnitude inside.
+template <class SA>
+__device__ __forceinline__ bool conc_ok(SA s) {
+  bool ok = true;
+#pragma unroll
+  for (int q = NAI; q <= CAJSR; ++q) ok = ok && s[q] >= 1e-10 && s[q] <= 1e10;
+  return ok && s[CAMKT] >= 0.0 && s[CAMKT] <= 1e10 && s[JCA] >= 0.0 && s[JCA] <= 1e10;
+}
+
 template <int CT, bool R, bool FP, class SA>
 __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, double gkr_scale, double h,
                                      double& dv) {
   const Pro pr = prologue<CT, FP>(v, s);
   const CurA ca = group_a<CT, R, FP>(v, s, ds, pr, h);
   const CurB cb = group_b<CT, R, FP>(v, s, ds, pr, h, gkr_scale);
-  finish<CT, R>(v, s, ds, pr, ca, cb, ist, h, dv);
+  finish<CT, R, FP>(v, s, ds, pr, ca, cb, ist, h, dv);
 }
 
 // CellModel::rates (no update), for the batched rates entry point / tests
@@ -565,7 +590,7 @@ struct ModelOrd {
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
   __device__ __forceinline__ static void advance(double& v, SA s, double ist, double g, double h, double& dv) {
-    if (fabs(v) <= 130.0)
+    if (fabs(v) <= 130.0 && ord::conc_ok(s))
       ord::step<CT, false, true>(v, s, nullptr, ist, g, h, dv);
     else
       ord::step<CT, false, false>(v, s, nullptr, ist, g, h, dv);

@@ -13,3 +13,4 @@ lines.append("// clang-format on")
 out = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2011_04747_b200", "csrc",
                    "exp2tab2048.inc")
 open(out, "w").write("\n".join(lines) + "\n")
+
