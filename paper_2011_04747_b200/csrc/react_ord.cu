@@ -184,6 +184,7 @@ struct Pro {
 };
 struct CurA {
   double i_na, i_to, i_cal, i_cana, i_cak;  // i_na includes INaL
+  double e70;                                // e^((v+70)/20), reused by IKs (group B) on the fast path
 };
 struct CurB {
   double i_k, inaca_i, inaca_ss, i_nak, i_kb, i_nab, i_cab, i_pca;
@@ -263,19 +264,27 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
 
   // ---------------- Ito
   double i_to;
+  double e70, e70sq;  // e^((v+70)/20) and its square: ICaL and IKs reuse them on the fast path
   {
-    double e[13] = {lin(v, -1.0 / (14.82), -(-14.34) / (14.82)),     lin(v, -1.0 / (29.3814), -(-18.4099) / (29.3814)), lin(v, 1.0 / (29.3814), (100.0) / (29.3814)),
+    // 11 exponentials; on the fast path two more follow from them: e^((v+100)/29.3814) = K / e[1]
+    // (folded into its sigmoid: 1 / (1 + K / e) = e / (e + K)) and e^((v+70)/5) = (e^((v+70)/20))^4
+    double e[11] = {lin(v, -1.0 / (14.82), -(-14.34) / (14.82)),     lin(v, -1.0 / (29.3814), -(-18.4099) / (29.3814)),
                     lin(v, 1.0 / (5.711), (43.94) / (5.711)),      lin(v, -1.0 / (100.0), -(100.0) / (100.0)),     lin(v, 1.0 / (16.59), (50.0) / (16.59)),
-                    lin(v, -1.0 / (59.05), -(96.52) / (59.05)),     lin(v, 1.0 / (8.079), (114.1) / (8.079)),      lin(v, 1.0 / (5.0), (70.0) / (5.0)),
+                    lin(v, -1.0 / (59.05), -(96.52) / (59.05)),     lin(v, 1.0 / (8.079), (114.1) / (8.079)),
                     lin(v, 1.0 / (151.2), (-213.6) / (151.2)),      lin(v, 1.0 / (15.89), (-167.4) / (15.89)),      lin(v, -1.0 / (0.2154), -(-12.23) / (0.2154)),
                     lin(v, 1.0 / (20.0), (70.0) / (20.0))};
     vexp_n<FP>(e);
     // e^(-(v-24.34)/14.82) = e^(-(v-14.34)/14.82) e^(10/14.82)
     const double e_ap = FP ? e[0] * 1.9635691902911017 : vexp<FP>(lin(v, -1.0 / (14.82), -(-24.34) / (14.82)));
-    double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), 1.0 + e[2], 1.0 + e[3],
-                    0.3933 * e[4] + 0.08004 * e[5], 0.001416 * e[6] + 1.780e-8 * e[7], 1.0 + e[8],
-                    1.0 + e[9], 1.0 + e_ap, e[10] + e[11], 1.0 + e[12]};
+    e70sq = e[10] * e[10];  // e^((v+70)/10), also feeds ICaL below
+    const double e_d5 = FP ? e70sq * e70sq : vexp<FP>(lin(v, 1.0 / (5.0), (70.0) / (5.0)));
+    e70 = e[10];
+    double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]),
+                    FP ? e[1] + 56.266384148520984 : 1.0 + vexp<FP>(lin(v, 1.0 / (29.3814), (100.0) / (29.3814))), 1.0 + e[2],
+                    0.3933 * e[3] + 0.08004 * e[4], 0.001416 * e[5] + 1.780e-8 * e[6], 1.0 + e_d5,
+                    1.0 + e[7], 1.0 + e_ap, e[8] + e[9], 1.0 + e[10]};
     vrcp_n<FP>(q);
+    if (FP) q[2] *= e[1];
     const double a_inf = q[0];
     const double r_a = (1.0 / 1.0515) * (q[1] + 3.5 * q[2]);
     const double i_inf = q[3];
@@ -308,16 +317,25 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- ICaL, ICaNa, ICaK
   double i_cal, i_cana, i_cak;
   {
-    double e[10] = {lin(v, -1.0 / (4.230), -(3.940) / (4.230)), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
-                    lin(v, 1.0 / (3.696), (19.58) / (3.696)),  lin(v, 1.0 / (10.0), (20.0) / (10.0)),  lin(v, -1.0 / (4.0), -(5.0) / (4.0)),
-                    lin(v, 1.0 / (6.0), (5.0) / (6.0)),      lin(v, 1.0 / (7.0), (-4.0) / (7.0)),    -v * (1.0 / 3.0),
-                    v * (1.0 / 7.0)};
+    // 7 exponentials; on the fast path e^((v+20)/10) = e^((v+70)/10) e^-5 (Ito's), e^((v-4)/7) = e^(v/7) e^(-4/7)
+    // and e^(-(v+5)/4) = (e^(-(v+6)/20))^5 e^(1/4)
+    double e[7] = {lin(v, -1.0 / (4.230), -(3.940) / (4.230)), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
+                   lin(v, 1.0 / (3.696), (19.58) / (3.696)),  lin(v, 1.0 / (6.0), (5.0) / (6.0)),      -v * (1.0 / 3.0),
+                   v * (1.0 / 7.0)};
     vexp_n<FP>(e);
-    const double eff = e[4], efc = e[7];
+    const double eff = FP ? e70sq * 0.006737946999085467 : vexp<FP>(lin(v, 1.0 / (10.0), (20.0) / (10.0)));
+    const double efc = FP ? e[6] * 0.5647181220077593 : vexp<FP>(lin(v, 1.0 / (7.0), (-4.0) / (7.0)));
     // e^((v-10)/10) = e^((v+20)/10) e^-3
-    const double e_fca = FP ? e[4] * 0.049787068367863944 : vexp<FP>(lin(v, 1.0 / (10.0), (-10.0) / (10.0)));
-    double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, 0.000035 * e[5] + 0.000035 * e[6], efc,
-                   0.00012 * e[8] + 0.00012 * e[9], 1.0 + e_fca};
+    const double e_fca = FP ? e70sq * 0.00033546262790251185 : vexp<FP>(lin(v, 1.0 / (10.0), (-10.0) / (10.0)));
+    double t_fs;  // 0.000035 e^(-(v+5)/4) + 0.000035 e^((v+5)/6)
+    if (FP) {
+      const double x2 = e[1] * e[1];
+      t_fs = fma((x2 * x2) * e[1], 4.4940889584070944e-05, 0.000035 * e[4]);
+    } else {
+      t_fs = 0.000035 * vexp<FP>(lin(v, -1.0 / (4.0), -(5.0) / (4.0))) + 0.000035 * e[4];
+    }
+    double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, t_fs, efc,
+                   0.00012 * e[5] + 0.00012 * e[6], 1.0 + e_fca};
     vrcp_n<FP>(q);
     double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
     vrcp_n<FP>(q2);
@@ -360,12 +378,14 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   o.i_cal = i_cal;
   o.i_cana = i_cana;
   o.i_cak = i_cak;
+  o.e70 = e70;
   return o;
 }
 
 // group B: IKr, IKs, IK1 (5 gates), INaCa, INaK, background currents
 template <int CT, bool R, bool FP, class SA>
-__device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& pr, double h, double gkr_scale) {
+__device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& pr, double h, double gkr_scale,
+                                         double e70) {
   using P = Var<CT>;
   const double ek = pr.ek, eks = pr.eks, vfrt = pr.vfrt;
   const double e1 = pr.e1, e2 = pr.e2, xq1 = pr.xq1, xq2 = pr.xq2;
@@ -389,23 +409,25 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
-    double f[9] = {lin(v, -1.0 / (8.932), -(11.60) / (8.932)),  lin(v, 1.0 / (17.80), (48.28) / (17.80)), lin(v, -1.0 / (230.0), -(210.0) / (230.0)),
-                   lin(v, 1.0 / (20.0), (-50.0) / (20.0)),     lin(v, -1.0 / (31.0), -(66.54) / (31.0)),
+    // on the fast path e^((v-50)/20) = e^((v+70)/20) e^-6 (Ito's exponential, passed in as e70)
+    double f[8] = {lin(v, -1.0 / (8.932), -(11.60) / (8.932)),  lin(v, 1.0 / (17.80), (48.28) / (17.80)), lin(v, -1.0 / (230.0), -(210.0) / (230.0)),
+                   lin(v, -1.0 / (31.0), -(66.54) / (31.0)),
                    -(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)),
                    lin(v, -1.0 / (20.36), -(127.2) / (20.36)),  lin(v, 1.0 / (69.33), (236.8) / (69.33)),  lin(v, 1.0 / (9.493), (105.8 - 2.6 * KO) / (9.493))};
     vexp_n<FP>(f);
-    double p[4] = {1.0 + f[0], 2.326e-4 * f[1] + 0.001292 * f[2], 1.0 + f[5], 1.0 + f[8]};
+    double p[4] = {1.0 + f[0], 2.326e-4 * f[1] + 0.001292 * f[2], 1.0 + f[4], 1.0 + f[7]};
     vrcp_n<FP>(p);
     const double xs_inf = p[0];
     const double r_xs1 = vrcp<FP>(817.3 + p[1]);
-    const double r_xs2 = 0.01 * f[3] + 0.0193 * f[4];
+    const double r_xs2 = FP ? fma(e70, 2.4787521766663585e-05, 0.0193 * f[3])
+                            : 0.01 * vexp<FP>(lin(v, 1.0 / (20.0), (-50.0) / (20.0))) + 0.0193 * f[3];
     const double ksca = 1.0 + 0.6 * crcp<FP>(1.0 + vexp<FP>(1.4 * (-10.177924398237888 - clog<FP>(cai))) /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
 
     const double xk1_inf = p[2];
-    const double r_xk1 = (f[6] + f[7]) * (1.0 / 122.2);
+    const double r_xk1 = (f[5] + f[6]) * (1.0 / 122.2);
     const double rk1 = p[3];
     const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
     gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
@@ -556,7 +578,7 @@ __device__ __forceinline__ void step(double& v, SA s, double* ds, double ist, do
                                      double& dv) {
   const Pro pr = prologue<CT, FP>(v, s);
   const CurA ca = group_a<CT, R, FP>(v, s, ds, pr, h);
-  const CurB cb = group_b<CT, R, FP>(v, s, ds, pr, h, gkr_scale);
+  const CurB cb = group_b<CT, R, FP>(v, s, ds, pr, h, gkr_scale, ca.e70);
   finish<CT, R, FP>(v, s, ds, pr, ca, cb, ist, h, dv);
 }
 
