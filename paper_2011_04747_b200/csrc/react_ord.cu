@@ -138,11 +138,13 @@ __device__ __forceinline__ double ncx(double na, double ca, const NcxShared& c) 
   const double x2 = k1 * k7 * (k4 + k5) + k4 * k6 * (k1 + k8);
   const double x3 = k1 * k3 * (k7 + k6) + k8 * k6 * (k2 + k3);
   const double x4 = k2 * k8 * (k4 + k5) + k3 * k5 * (k1 + k8);
-  const double rt = crcp<FP>(x1 + x2 + x3 + x4);
   const double ca2 = ca * ca;
-  const double allo = ca2 * crcp<FP>(ca2 + 150.0e-6 * 150.0e-6);
   const double j_na = 3.0 * (x4 * k7 - x1 * k8) + x3 * k4pp - x2 * k3pp;
   const double j_ca = x2 * k2 - x1 * k1;
+  if (FP)  // allo / (x1 + .. + x4) with one reciprocal of the product (ca2 <= 1e20, the sum <= ~1e25 on the fast path)
+    return ca2 * crcp<FP>((ca2 + 150.0e-6 * 150.0e-6) * (x1 + x2 + x3 + x4)) * (j_na + 2.0 * j_ca);
+  const double rt = crcp<FP>(x1 + x2 + x3 + x4);
+  const double allo = ca2 * crcp<FP>(ca2 + 150.0e-6 * 150.0e-6);
   return allo * rt * (j_na + 2.0 * j_ca);
 }
 
@@ -236,14 +238,16 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     // e^((v+89.1)/6.086) = e^((v+82.9)/6.086) e^(6.2/6.086), e^((v+93.81)/7.488) = e^((v+87.61)/7.488) e^(6.2/7.488)
     const double e_hp = FP ? e[3] * 2.7696792380394113 : vexp<FP>(lin(v, 1.0 / (6.086), (89.1) / (6.086)));
     const double e_hlp = FP ? e[11] * 2.288717124596482 : vexp<FP>(lin(v, 1.0 / (7.488), (93.81) / (7.488)));
+    // 1 / (2.038 + 1 / s) = s / (2.038 s + 1): one reciprocal instead of two on the fast path
+    const double s_j = 0.02136 * e[8] + 0.3052 * e[9];
     double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e_hp, 1.0 + e[10], 1.0 + e[11], 1.0 + e_hlp,
-                   0.02136 * e[8] + 0.3052 * e[9]};
+                   FP ? fma(2.038, s_j, 1.0) : s_j};
     vrcp_n<FP>(q);
     const double m_inf = q[0], h_inf = q[1], hp_inf = q[2];
     const double r_m = 6.765 * e[1] + 8.552 * e[2];
     const double r_hf = 1.432e-5 * e[4] + 6.149 * e[5];
     const double r_hs = 0.009794 * e[6] + 0.3343 * e[7];
-    const double r_j = vrcp<FP>(2.038 + q[6]);
+    const double r_j = FP ? s_j * q[6] : vrcp<FP>(2.038 + q[6]);
     const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
     const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
     const double m = s[M];
@@ -279,30 +283,58 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     e70sq = e[10] * e[10];  // e^((v+70)/10), also feeds ICaL below
     const double e_d5 = FP ? e70sq * e70sq : vexp<FP>(lin(v, 1.0 / (5.0), (70.0) / (5.0)));
     e70 = e[10];
-    double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]),
-                    FP ? e[1] + 56.266384148520984 : 1.0 + vexp<FP>(lin(v, 1.0 / (29.3814), (100.0) / (29.3814))), 1.0 + e[2],
-                    0.3933 * e[3] + 0.08004 * e[4], 0.001416 * e[5] + 1.780e-8 * e[6], 1.0 + e_d5,
-                    1.0 + e[7], 1.0 + e_ap, e[8] + e[9], 1.0 + e[10]};
-    vrcp_n<FP>(q);
-    if (FP) q[2] *= e[1];
-    const double a_inf = q[0];
-    const double r_a = (1.0 / 1.0515) * (q[1] + 3.5 * q[2]);
-    const double i_inf = q[3];
-    double t_if = 4.562 + q[4];
-    double t_is = 23.62 + q[5];
-    if (P::epi) {
-      const double d_epi = 1.0 - 0.95 * q[6];
-      t_if *= d_epi;
-      t_is *= d_epi;
+    double a_inf, r_a, i_inf, a_if, ap_inf, r_if, r_is, r_dr;
+    if (FP) {
+      // every 1 / (c + 1 / s) is s / (c s + 1) and the epi / development / recovery factors
+      // (a + e) / (1 + e) go into the same denominators: one batch of 9 reciprocals
+      const double s_if = 0.3933 * e[3] + 0.08004 * e[4], s_is = 0.001416 * e[5] + 1.780e-8 * e[6];
+      const double s_dv = e[8] + e[9], g10 = 1.0 + e[10];
+      double d_if = fma(4.562, s_if, 1.0), d_is = fma(23.62, s_is, 1.0);
+      double n_if = s_if, n_is = s_is;
+      if (P::epi) {  // delta_epi = 1 - 0.95 / (1 + e) = (0.05 + e) / (1 + e)
+        const double ge = 1.0 + e_d5, he = 0.05 + e_d5;
+        d_if *= he;
+        d_is *= he;
+        n_if *= ge;
+        n_is *= ge;
+      }
+      // 1 / (dev rec), dev = 1.354 + 1e-4 / s_dv, rec = 1 - 0.5 / (1 + e10) = (0.5 + e10) / (1 + e10)
+      double q[9] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), e[1] + 56.266384148520984, 1.0 + e[2], d_if, d_is,
+                     1.0 + e[7], 1.0 + e_ap, fma(1.354, s_dv, 1.0e-4) * (0.5 + e[10])};
+      vrcp_n<FP>(q);
+      a_inf = q[0];
+      r_a = (1.0 / 1.0515) * (q[1] + 3.5 * (q[2] * e[1]));
+      i_inf = q[3];
+      r_if = n_if * q[4];
+      r_is = n_is * q[5];
+      a_if = q[6];
+      ap_inf = q[7];
+      r_dr = (s_dv * g10) * q[8];
+    } else {
+      double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]),
+                      1.0 + vexp<FP>(lin(v, 1.0 / (29.3814), (100.0) / (29.3814))), 1.0 + e[2],
+                      0.3933 * e[3] + 0.08004 * e[4], 0.001416 * e[5] + 1.780e-8 * e[6], 1.0 + e_d5,
+                      1.0 + e[7], 1.0 + e_ap, e[8] + e[9], 1.0 + e[10]};
+      vrcp_n<FP>(q);
+      a_inf = q[0];
+      r_a = (1.0 / 1.0515) * (q[1] + 3.5 * q[2]);
+      i_inf = q[3];
+      double t_if = 4.562 + q[4];
+      double t_is = 23.62 + q[5];
+      if (P::epi) {
+        const double d_epi = 1.0 - 0.95 * q[6];
+        t_if *= d_epi;
+        t_is *= d_epi;
+      }
+      a_if = q[7];
+      ap_inf = q[8];
+      const double dev = 1.354 + 1.0e-4 * q[9];
+      const double rec = 1.0 - 0.5 * q[10];
+      double r3[3] = {t_if, t_is, dev * rec};
+      vrcp_n<FP>(r3);
+      r_if = r3[0], r_is = r3[1], r_dr = r3[2];
     }
-    const double a_if = q[7];
     const double a_is = 1.0 - a_if;
-    const double ap_inf = q[8];
-    const double dev = 1.354 + 1.0e-4 * q[9];
-    const double rec = 1.0 - 0.5 * q[10];
-    double r3[3] = {t_if, t_is, dev * rec};
-    vrcp_n<FP>(r3);
-    const double r_if = r3[0], r_is = r3[1], r_dr = r3[2];
     const double imix = a_if * s[IF] + a_is * s[IS];
     const double ipmix = a_if * s[IFP] + a_is * s[ISP];
     i_to = P::gto * (v - ek) * (nfk * s[A] * imix + fk * s[AP] * ipmix);
@@ -334,16 +366,33 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     } else {
       t_fs = 0.000035 * vexp<FP>(lin(v, -1.0 / (4.0), -(5.0) / (4.0))) + 0.000035 * e[4];
     }
-    double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, t_fs, efc,
-                   0.00012 * e[5] + 0.00012 * e[6], 1.0 + e_fca};
-    vrcp_n<FP>(q);
-    double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
-    vrcp_n<FP>(q2);
-    double q3[2] = {7.0 + q2[1], 7.0 + q2[3]};
-    vrcp_n<FP>(q3);
-    const double d_inf = q[0], f_inf = q[2];
-    const double r_d = q2[0], r_fs = q2[2], r_fcas = q2[4], r_ff = q3[0], r_fcaf = q3[1];
-    const double a_fcaf = 0.3 + 0.6 * q[7];
+    double d_inf, f_inf, r_d, r_fs, r_fcas, r_ff, r_fcaf, q_fca;
+    if (FP) {
+      // 1 / (c + 1 / s) = s / (c s + 1); 1 / (7 + 1 / (a (e + 1 / e))) = a (e^2 + 1) / (7 a (e^2 + 1) + e):
+      // one batch of 8 reciprocals instead of 8 + 5 + 2
+      const double s_d = e[1] + e[2], s_ca = 0.00012 * e[5] + 0.00012 * e[6];
+      const double w_ff = fma(eff, eff, 1.0), w_fc = fma(efc, efc, 1.0);
+      double q[8] = {1.0 + e[0], fma(0.6, s_d, 1.0), 1.0 + e[3], fma(7.0 * 0.0045, w_ff, eff), fma(1000.0, t_fs, 1.0),
+                     fma(7.0 * 0.04, w_fc, efc), fma(100.0, s_ca, 1.0), 1.0 + e_fca};
+      vrcp_n<FP>(q);
+      d_inf = q[0], f_inf = q[2], q_fca = q[7];
+      r_d = s_d * q[1];
+      r_ff = (0.0045 * w_ff) * q[3];
+      r_fs = t_fs * q[4];
+      r_fcaf = (0.04 * w_fc) * q[5];
+      r_fcas = s_ca * q[6];
+    } else {
+      double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, t_fs, efc,
+                     0.00012 * e[5] + 0.00012 * e[6], 1.0 + e_fca};
+      vrcp_n<FP>(q);
+      double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
+      vrcp_n<FP>(q2);
+      double q3[2] = {7.0 + q2[1], 7.0 + q2[3]};
+      vrcp_n<FP>(q3);
+      d_inf = q[0], f_inf = q[2], q_fca = q[7];
+      r_d = q2[0], r_fs = q2[2], r_fcas = q2[4], r_ff = q3[0], r_fcaf = q3[1];
+    }
+    const double a_fcaf = 0.3 + 0.6 * q_fca;
     const double a_fcas = 1.0 - a_fcaf;
     const double fmix = 0.6 * s[FF] + (1.0 - 0.6) * s[FS];
     const double fcamix = a_fcaf * s[FCAF] + a_fcas * s[FCAS];
@@ -398,12 +447,20 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
                    lin(v, 1.0 / (7.355), (-34.70) / (7.355)),  lin(v, -1.0 / (25.94), -(-29.74) / (25.94)), lin(v, 1.0 / (38.21), (54.81) / (38.21)),
                    lin(v, 1.0 / (75.0), (55.0) / (75.0)),    lin(v, 1.0 / (30.0), (-10.0) / (30.0))};
     vexp_n<FP>(e);
-    double q[5] = {1.0 + e[0], 0.3652 * e[1] + 4.123e-5 * e[2], 0.06629 * e[3] + 1.128e-5 * e[4], 1.0 + e[5],
+    const double s_xrf = 0.3652 * e[1] + 4.123e-5 * e[2], s_xrs = 0.06629 * e[3] + 1.128e-5 * e[4];
+    double q[5] = {1.0 + e[0], FP ? fma(12.98, s_xrf, 1.0) : s_xrf, FP ? fma(1.865, s_xrs, 1.0) : s_xrs, 1.0 + e[5],
                    (1.0 + e[6]) * (1.0 + e[7])};
     vrcp_n<FP>(q);
-    double q2[2] = {12.98 + q[1], 1.865 + q[2]};
-    vrcp_n<FP>(q2);
-    const double xr_inf = q[0], r_xrf = q2[0], r_xrs = q2[1], a_xrf = q[3], rkr = q[4];
+    double r_xrf, r_xrs;
+    if (FP) {  // 1 / (c + 1 / s) = s / (c s + 1)
+      r_xrf = s_xrf * q[1];
+      r_xrs = s_xrs * q[2];
+    } else {
+      double q2[2] = {12.98 + q[1], 1.865 + q[2]};
+      vrcp_n<FP>(q2);
+      r_xrf = q2[0], r_xrs = q2[1];
+    }
+    const double xr_inf = q[0], a_xrf = q[3], rkr = q[4];
     const double xrmix = a_xrf * s[XRF] + (1.0 - a_xrf) * s[XRS];
     const double i_kr = (P::gkr * gkr_scale) * xrmix * rkr * (v - ek);  // sqrt(ko/5.4) == 1
     gate<R>(s, ds, XRF, h, xr_inf, r_xrf);
@@ -415,10 +472,11 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
                    -(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)),
                    lin(v, -1.0 / (20.36), -(127.2) / (20.36)),  lin(v, 1.0 / (69.33), (236.8) / (69.33)),  lin(v, 1.0 / (9.493), (105.8 - 2.6 * KO) / (9.493))};
     vexp_n<FP>(f);
-    double p[4] = {1.0 + f[0], 2.326e-4 * f[1] + 0.001292 * f[2], 1.0 + f[4], 1.0 + f[7]};
+    const double s_xs1 = 2.326e-4 * f[1] + 0.001292 * f[2];
+    double p[4] = {1.0 + f[0], FP ? fma(817.3, s_xs1, 1.0) : s_xs1, 1.0 + f[4], 1.0 + f[7]};
     vrcp_n<FP>(p);
     const double xs_inf = p[0];
-    const double r_xs1 = vrcp<FP>(817.3 + p[1]);
+    const double r_xs1 = FP ? s_xs1 * p[1] : vrcp<FP>(817.3 + p[1]);
     const double r_xs2 = FP ? fma(e70, 2.4787521766663585e-05, 0.0193 * f[3])
                             : 0.01 * vexp<FP>(lin(v, 1.0 / (20.0), (-50.0) / (20.0))) + 0.0193 * f[3];
     const double ksca = 1.0 + 0.6 * crcp<FP>(1.0 + vexp<FP>(1.4 * (-10.177924398237888 - clog<FP>(cai))) /* log(3.8e-5) */);
@@ -440,10 +498,16 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     NcxShared c;
     c.hna = vexp<FP>(0.5224 * vfrt);
     c.hca_r = vexp<FP>(-0.1670 * vfrt);  // 1/hca
-    const double hna_r = vrcp<FP>(c.hna);
-    const double r7 = vrcp<FP>(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
-    c.h9 = r7;
-    c.h8 = NAO * (1.0 / 88.12) * hna_r * r7;
+    if (FP) {  // h9 = 1 / (1 + c (1 + 1 / hna)) = hna / (hna + c (hna + 1)), h8 = c / (same)
+      const double r = vrcp<FP>(fma(NAO * (1.0 / 88.12), c.hna + 1.0, c.hna));
+      c.h9 = c.hna * r;
+      c.h8 = NAO * (1.0 / 88.12) * r;
+    } else {
+      const double hna_r = vrcp<FP>(c.hna);
+      const double r7 = vrcp<FP>(1.0 + NAO * (1.0 / 88.12) * (1.0 + hna_r));
+      c.h9 = r7;
+      c.h8 = NAO * (1.0 / 88.12) * hna_r * r7;
+    }
     inaca_i = (0.8 * P::gncx) * ncx<FP>(nai, cai, c);
     inaca_ss = (0.2 * P::gncx) * ncx<FP>(nass, cass, c);
   }
