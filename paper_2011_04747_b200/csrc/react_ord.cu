@@ -230,23 +230,27 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
   // ---------------- INa + INaL: the 14 V-dependent exponentials in one batch
   double i_na;
   {
-    double e[12] = {lin(v, -1.0 / (9.871), -(39.57) / (9.871)),   lin(v, 1.0 / (34.77), (11.64) / (34.77)),  lin(v, -1.0 / (5.955), -(77.42) / (5.955)),
-                    lin(v, 1.0 / (6.086), (82.90) / (6.086)),    lin(v, -1.0 / (6.285), -(1.196) / (6.285)), lin(v, 1.0 / (20.27), (0.5096) / (20.27)),
-                    lin(v, -1.0 / (28.05), -(17.95) / (28.05)),   lin(v, 1.0 / (56.66), (5.730) / (56.66)),  lin(v, -1.0 / (8.281), -(100.6) / (8.281)),
-                    lin(v, 1.0 / (38.45), (0.9941) / (38.45)),   lin(v, -1.0 / (5.264), -(42.85) / (5.264)), lin(v, 1.0 / (7.488), (87.61) / (7.488))};
+    // a e^u = e^(u + log a): the rate coefficients ride in the exponents' offsets (LN_x = log x)
+    constexpr double LN_6_765 = 1.9117622616227514, LN_8_552 = 2.146165173722744, LN_1_432em5 = -11.153853396431774;
+    constexpr double LN_6_149 = 1.8162894669713328, LN_0_009794 = -4.625985325702011, LN_0_3343 = -1.0957164855560841;
+    constexpr double LN_0_02136 = -3.846235264890143, LN_0_3052 = -1.186787979571835;
+    double e[12] = {lin(v, -1.0 / (9.871), -(39.57) / (9.871)),   lin(v, 1.0 / (34.77), (11.64) / (34.77) + LN_6_765),  lin(v, -1.0 / (5.955), -(77.42) / (5.955) + LN_8_552),
+                    lin(v, 1.0 / (6.086), (82.90) / (6.086)),    lin(v, -1.0 / (6.285), -(1.196) / (6.285) + LN_1_432em5), lin(v, 1.0 / (20.27), (0.5096) / (20.27) + LN_6_149),
+                    lin(v, -1.0 / (28.05), -(17.95) / (28.05) + LN_0_009794),   lin(v, 1.0 / (56.66), (5.730) / (56.66) + LN_0_3343),  lin(v, -1.0 / (8.281), -(100.6) / (8.281) + LN_0_02136),
+                    lin(v, 1.0 / (38.45), (0.9941) / (38.45) + LN_0_3052),   lin(v, -1.0 / (5.264), -(42.85) / (5.264)), lin(v, 1.0 / (7.488), (87.61) / (7.488))};
     vexp_n<FP>(e);
     // e^((v+89.1)/6.086) = e^((v+82.9)/6.086) e^(6.2/6.086), e^((v+93.81)/7.488) = e^((v+87.61)/7.488) e^(6.2/7.488)
     const double e_hp = FP ? e[3] * 2.7696792380394113 : vexp<FP>(lin(v, 1.0 / (6.086), (89.1) / (6.086)));
     const double e_hlp = FP ? e[11] * 2.288717124596482 : vexp<FP>(lin(v, 1.0 / (7.488), (93.81) / (7.488)));
     // 1 / (2.038 + 1 / s) = s / (2.038 s + 1): one reciprocal instead of two on the fast path
-    const double s_j = 0.02136 * e[8] + 0.3052 * e[9];
+    const double s_j = e[8] + e[9];
     double q[7] = {1.0 + e[0], 1.0 + e[3], 1.0 + e_hp, 1.0 + e[10], 1.0 + e[11], 1.0 + e_hlp,
                    FP ? fma(2.038, s_j, 1.0) : s_j};
     vrcp_n<FP>(q);
     const double m_inf = q[0], h_inf = q[1], hp_inf = q[2];
-    const double r_m = 6.765 * e[1] + 8.552 * e[2];
-    const double r_hf = 1.432e-5 * e[4] + 6.149 * e[5];
-    const double r_hs = 0.009794 * e[6] + 0.3343 * e[7];
+    const double r_m = e[1] + e[2];
+    const double r_hf = e[4] + e[5];
+    const double r_hs = e[6] + e[7];
     const double r_j = FP ? s_j * q[6] : vrcp<FP>(2.038 + q[6]);
     const double hmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HS];
     const double hpmix = 0.99 * s[HF] + (1.0 - 0.99) * s[HSP];
@@ -273,8 +277,8 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     // 11 exponentials; on the fast path two more follow from them: e^((v+100)/29.3814) = K / e[1]
     // (folded into its sigmoid: 1 / (1 + K / e) = e / (e + K)) and e^((v+70)/5) = (e^((v+70)/20))^4
     double e[11] = {lin(v, -1.0 / (14.82), -(-14.34) / (14.82)),     lin(v, -1.0 / (29.3814), -(-18.4099) / (29.3814)),
-                    lin(v, 1.0 / (5.711), (43.94) / (5.711)),      lin(v, -1.0 / (100.0), -(100.0) / (100.0)),     lin(v, 1.0 / (16.59), (50.0) / (16.59)),
-                    lin(v, -1.0 / (59.05), -(96.52) / (59.05)),     lin(v, 1.0 / (8.079), (114.1) / (8.079)),
+                    lin(v, 1.0 / (5.711), (43.94) / (5.711)),      lin(v, -1.0 / (100.0), -(100.0) / (100.0) - 0.9331825995443732 /* log 0.3933 */),     lin(v, 1.0 / (16.59), (50.0) / (16.59) - 2.5252287692666044 /* log 0.08004 */),
+                    lin(v, -1.0 / (59.05), -(96.52) / (59.05) - 6.5599192837106095 /* log 0.001416 */),     lin(v, 1.0 / (8.079), (114.1) / (8.079) - 17.844067379648372 /* log 1.780e-8 */),
                     lin(v, 1.0 / (151.2), (-213.6) / (151.2)),      lin(v, 1.0 / (15.89), (-167.4) / (15.89)),      lin(v, -1.0 / (0.2154), -(-12.23) / (0.2154)),
                     lin(v, 1.0 / (20.0), (70.0) / (20.0))};
     vexp_n<FP>(e);
@@ -287,7 +291,7 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     if (FP) {
       // every 1 / (c + 1 / s) is s / (c s + 1) and the epi / development / recovery factors
       // (a + e) / (1 + e) go into the same denominators: one batch of 9 reciprocals
-      const double s_if = 0.3933 * e[3] + 0.08004 * e[4], s_is = 0.001416 * e[5] + 1.780e-8 * e[6];
+      const double s_if = e[3] + e[4], s_is = e[5] + e[6];
       const double s_dv = e[8] + e[9], g10 = 1.0 + e[10];
       double d_if = fma(4.562, s_if, 1.0), d_is = fma(23.62, s_is, 1.0);
       double n_if = s_if, n_is = s_is;
@@ -299,7 +303,7 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
         n_is *= ge;
       }
       // 1 / (dev rec), dev = 1.354 + 1e-4 / s_dv, rec = 1 - 0.5 / (1 + e10) = (0.5 + e10) / (1 + e10)
-      double q[9] = {1.0 + e[0], 1.2089 * (1.0 + e[1]), e[1] + 56.266384148520984, 1.0 + e[2], d_if, d_is,
+      double q[9] = {1.0 + e[0], fma(e[1], 1.2089, 1.2089), e[1] + 56.266384148520984, 1.0 + e[2], d_if, d_is,
                      1.0 + e[7], 1.0 + e_ap, fma(1.354, s_dv, 1.0e-4) * (0.5 + e[10])};
       vrcp_n<FP>(q);
       a_inf = q[0];
@@ -313,7 +317,7 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     } else {
       double q[11] = {1.0 + e[0], 1.2089 * (1.0 + e[1]),
                       1.0 + vexp<FP>(lin(v, 1.0 / (29.3814), (100.0) / (29.3814))), 1.0 + e[2],
-                      0.3933 * e[3] + 0.08004 * e[4], 0.001416 * e[5] + 1.780e-8 * e[6], 1.0 + e_d5,
+                      e[3] + e[4], e[5] + e[6], 1.0 + e_d5,
                       1.0 + e[7], 1.0 + e_ap, e[8] + e[9], 1.0 + e[10]};
       vrcp_n<FP>(q);
       a_inf = q[0];
@@ -352,11 +356,11 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     // 7 exponentials; on the fast path e^((v+20)/10) = e^((v+70)/10) e^-5 (Ito's), e^((v-4)/7) = e^(v/7) e^(-4/7)
     // and e^(-(v+5)/4) = (e^(-(v+6)/20))^5 e^(1/4)
     double e[7] = {lin(v, -1.0 / (4.230), -(3.940) / (4.230)), -0.05 * (v + 6.0),          0.09 * (v + 14.0),
-                   lin(v, 1.0 / (3.696), (19.58) / (3.696)),  lin(v, 1.0 / (6.0), (5.0) / (6.0)),      -v * (1.0 / 3.0),
-                   v * (1.0 / 7.0)};
+                   lin(v, 1.0 / (3.696), (19.58) / (3.696)),  lin(v, 1.0 / (6.0), (5.0) / (6.0)),      lin(v, -1.0 / 3.0, -9.028018815182229 /* log 0.00012 */),
+                   lin(v, 1.0 / 7.0, -9.028018815182229)};
     vexp_n<FP>(e);
     const double eff = FP ? e70sq * 0.006737946999085467 : vexp<FP>(lin(v, 1.0 / (10.0), (20.0) / (10.0)));
-    const double efc = FP ? e[6] * 0.5647181220077593 : vexp<FP>(lin(v, 1.0 / (7.0), (-4.0) / (7.0)));
+    const double efc = FP ? e[6] * (0.5647181220077593 / 0.00012) : vexp<FP>(lin(v, 1.0 / (7.0), (-4.0) / (7.0)));
     // e^((v-10)/10) = e^((v+20)/10) e^-3
     const double e_fca = FP ? e70sq * 0.00033546262790251185 : vexp<FP>(lin(v, 1.0 / (10.0), (-10.0) / (10.0)));
     double t_fs;  // 0.000035 e^(-(v+5)/4) + 0.000035 e^((v+5)/6)
@@ -370,7 +374,7 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
     if (FP) {
       // 1 / (c + 1 / s) = s / (c s + 1); 1 / (7 + 1 / (a (e + 1 / e))) = a (e^2 + 1) / (7 a (e^2 + 1) + e):
       // one batch of 8 reciprocals instead of 8 + 5 + 2
-      const double s_d = e[1] + e[2], s_ca = 0.00012 * e[5] + 0.00012 * e[6];
+      const double s_d = e[1] + e[2], s_ca = e[5] + e[6];
       const double w_ff = fma(eff, eff, 1.0), w_fc = fma(efc, efc, 1.0);
       double q[8] = {1.0 + e[0], fma(0.6, s_d, 1.0), 1.0 + e[3], fma(7.0 * 0.0045, w_ff, eff), fma(1000.0, t_fs, 1.0),
                      fma(7.0 * 0.04, w_fc, efc), fma(100.0, s_ca, 1.0), 1.0 + e_fca};
@@ -383,7 +387,7 @@ __device__ __forceinline__ CurA group_a(double v, SA s, double* ds, const Pro& p
       r_fcas = s_ca * q[6];
     } else {
       double q[8] = {1.0 + e[0], e[1] + e[2], 1.0 + e[3], eff, t_fs, efc,
-                     0.00012 * e[5] + 0.00012 * e[6], 1.0 + e_fca};
+                     e[5] + e[6], 1.0 + e_fca};
       vrcp_n<FP>(q);
       double q2[5] = {0.6 + q[1], 0.0045 * (q[3] + eff), 1000.0 + q[4], 0.04 * (q[5] + efc), 100.0 + q[6]};
       vrcp_n<FP>(q2);
@@ -443,11 +447,11 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
   // ---------------- IKr, IKs, IK1
   double i_k;  // IKr + IKs + IK1
   {
-    double e[8] = {lin(v, -1.0 / (6.789), -(8.337) / (6.789)), lin(v, 1.0 / (3.869), (-31.66) / (3.869)), lin(v, -1.0 / (20.38), -(-47.78) / (20.38)),
-                   lin(v, 1.0 / (7.355), (-34.70) / (7.355)),  lin(v, -1.0 / (25.94), -(-29.74) / (25.94)), lin(v, 1.0 / (38.21), (54.81) / (38.21)),
+    double e[8] = {lin(v, -1.0 / (6.789), -(8.337) / (6.789)), lin(v, 1.0 / (3.869), (-31.66) / (3.869) - 1.0073101302613237 /* log 0.3652 */), lin(v, -1.0 / (20.38), -(-47.78) / (20.38) - 10.096344411245465 /* log 4.123e-5 */),
+                   lin(v, 1.0 / (7.355), (-34.70) / (7.355) - 2.713716222728837 /* log 0.06629 */),  lin(v, -1.0 / (25.94), -(-29.74) / (25.94) - 11.39247931189436 /* log 1.128e-5 */), lin(v, 1.0 / (38.21), (54.81) / (38.21)),
                    lin(v, 1.0 / (75.0), (55.0) / (75.0)),    lin(v, 1.0 / (30.0), (-10.0) / (30.0))};
     vexp_n<FP>(e);
-    const double s_xrf = 0.3652 * e[1] + 4.123e-5 * e[2], s_xrs = 0.06629 * e[3] + 1.128e-5 * e[4];
+    const double s_xrf = e[1] + e[2], s_xrs = e[3] + e[4];
     double q[5] = {1.0 + e[0], FP ? fma(12.98, s_xrf, 1.0) : s_xrf, FP ? fma(1.865, s_xrs, 1.0) : s_xrs, 1.0 + e[5],
                    (1.0 + e[6]) * (1.0 + e[7])};
     vrcp_n<FP>(q);
@@ -467,25 +471,25 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     gate<R>(s, ds, XRS, h, xr_inf, r_xrs);
 
     // on the fast path e^((v-50)/20) = e^((v+70)/20) e^-6 (Ito's exponential, passed in as e70)
-    double f[8] = {lin(v, -1.0 / (8.932), -(11.60) / (8.932)),  lin(v, 1.0 / (17.80), (48.28) / (17.80)), lin(v, -1.0 / (230.0), -(210.0) / (230.0)),
-                   lin(v, -1.0 / (31.0), -(66.54) / (31.0)),
+    double f[8] = {lin(v, -1.0 / (8.932), -(11.60) / (8.932)),  lin(v, 1.0 / (17.80), (48.28) / (17.80) - 8.36619031787971 /* log 2.326e-4 */), lin(v, -1.0 / (230.0), -(210.0) / (230.0) - 6.651563873621727 /* log 0.001292 */),
+                   lin(v, -1.0 / (31.0), -(66.54) / (31.0) - 3.947650183071297 /* log 0.0193 */),
                    -(v + 2.5538 * KO + 144.59) * (1.0 / (1.5692 * KO + 3.8115)),
-                   lin(v, -1.0 / (20.36), -(127.2) / (20.36)),  lin(v, 1.0 / (69.33), (236.8) / (69.33)),  lin(v, 1.0 / (9.493), (105.8 - 2.6 * KO) / (9.493))};
+                   lin(v, -1.0 / (20.36), -(127.2) / (20.36) - 4.805659046737495 /* log(1/122.2) */),  lin(v, 1.0 / (69.33), (236.8) / (69.33) - 4.805659046737495),  lin(v, 1.0 / (9.493), (105.8 - 2.6 * KO) / (9.493))};
     vexp_n<FP>(f);
-    const double s_xs1 = 2.326e-4 * f[1] + 0.001292 * f[2];
+    const double s_xs1 = f[1] + f[2];
     double p[4] = {1.0 + f[0], FP ? fma(817.3, s_xs1, 1.0) : s_xs1, 1.0 + f[4], 1.0 + f[7]};
     vrcp_n<FP>(p);
     const double xs_inf = p[0];
     const double r_xs1 = FP ? s_xs1 * p[1] : vrcp<FP>(817.3 + p[1]);
-    const double r_xs2 = FP ? fma(e70, 2.4787521766663585e-05, 0.0193 * f[3])
-                            : 0.01 * vexp<FP>(lin(v, 1.0 / (20.0), (-50.0) / (20.0))) + 0.0193 * f[3];
+    const double r_xs2 = FP ? fma(e70, 2.4787521766663585e-05, f[3])
+                            : 0.01 * vexp<FP>(lin(v, 1.0 / (20.0), (-50.0) / (20.0))) + f[3];
     const double ksca = 1.0 + 0.6 * crcp<FP>(1.0 + vexp<FP>(1.4 * (-10.177924398237888 - clog<FP>(cai))) /* log(3.8e-5) */);
     const double i_ks = P::gks * ksca * s[XS1] * s[XS2] * (v - eks);
     gate<R>(s, ds, XS1, h, xs_inf, r_xs1);
     gate<R>(s, ds, XS2, h, xs_inf, r_xs2);
 
     const double xk1_inf = p[2];
-    const double r_xk1 = (f[5] + f[6]) * (1.0 / 122.2);
+    const double r_xk1 = f[5] + f[6];
     const double rk1 = p[3];
     const double i_k1 = (P::gk1 * 2.3237900077244502) * rk1 * s[XK1] * (v - ek);  // sqrt(5.4)
     gate<R>(s, ds, XK1, h, xk1_inf, r_xk1);
@@ -521,8 +525,8 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     constexpr double a4 = 639.0 * 9.8 / 1.698e-7 / (1.0 + 9.8 / 1.698e-7);
     constexpr double b3c = 79300.0 * 1.0e-7 / (1.0 + 9.8 / 1.698e-7);
     const double p_hp = 4.2 * crcp<FP>(1.0 + 1.0e-7 / 1.698e-7 + nai * (1.0 / 224.0) + ki * (1.0 / 292.0));
-    const double ri = nai * (1.0 / 9.073) * vexp<FP>((0.1550 / 3.0) * vfrt);     // nai / Knai
-    const double ro = NAO * (1.0 / 27.78) * vexp<FP>(-(1.1550 / 3.0) * vfrt);   // nao / Knao
+    const double ri = nai * vexp<FP>(fma(vfrt, 0.1550 / 3.0, -2.2053029701874918 /* log(1/9.073) */));   // nai / Knai
+    const double ro = vexp<FP>(fma(vfrt, -(1.1550 / 3.0), 1.6173260852831066 /* log(140/27.78) */));  // nao / Knao
     const double rk = ki * 2.0;                                            // ki / 0.5
     const double ci = (1.0 + ri) * (1.0 + ri) * (1.0 + ri), qi = (1.0 + rk) * (1.0 + rk);
     const double co = (1.0 + ro) * (1.0 + ro) * (1.0 + ro);
@@ -532,10 +536,13 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
     const double a3 = 1899.0 * (rko * rko) * dco;
     const double b3 = b3c * p_hp;
     const double b4 = 40.0 * (rk * rk) * di;
-    const double y1 = a4 * a1 * a2 + b2 * b4 * b3 + a2 * b4 * b3 + b3 * a1 * a2;
-    const double y2 = b2 * b1 * b4 + a1 * a2 * a3 + a3 * b1 * b4 + a2 * a3 * b4;
-    const double y3 = a2 * a3 * a4 + b3 * b2 * b1 + b2 * b1 * a4 + a3 * a4 * b1;
-    const double y4 = b4 * b3 * b2 + a3 * a4 * a1 + b2 * a4 * a1 + b3 * b2 * a1;
+    // the cycle's state occupancies, each four triple products factored into two
+    const double a1a2 = a1 * a2, b3b4 = b3 * b4, b1b4 = b1 * b4, a2a3 = a2 * a3;
+    const double a3a4 = a3 * a4, b1b2 = b1 * b2, b2b3 = b2 * b3, a1a4 = a1 * a4;
+    const double y1 = a1a2 * (a4 + b3) + b3b4 * (b2 + a2);
+    const double y2 = b1b4 * (b2 + a3) + a2a3 * (a1 + b4);
+    const double y3 = a3a4 * (a2 + b1) + b1b2 * (b3 + a4);
+    const double y4 = b2b3 * (b4 + a1) + a1a4 * (a3 + b2);
     const double ry = crcp<FP>(y1 + y2 + y3 + y4);
     i_nak = P::pnak * ry * (3.0 * (y1 * a3 - y2 * b3) + 2.0 * (y4 * b1 - y3 * a1));
   }
