@@ -113,7 +113,7 @@ __device__ __forceinline__ double xem1(double x, double em) {
 }
 
 struct NcxShared {
-  double hna, hca_r, h8, h9;
+  double hna, hca6, h8, h9;  // hca6 = 6e4 / hca
 };
 
 // Na/Ca exchanger flux for one compartment (ohara_rudy_2011.cpp:264-300)
@@ -124,15 +124,13 @@ __device__ __forceinline__ double ncx(double na, double ca, const NcxShared& c) 
   constexpr double k1 = 1.0 / h10 * CAO * 1.5e6;
   constexpr double k2 = 5.0e3, k5 = 5.0e3;
   const double r1 = crcp<FP>(1.0 + na * (1.0 / 88.12) * (1.0 + c.hna));
-  const double h2 = na * c.hna * (1.0 / 88.12) * r1;
   const double r4 = crcp<FP>(1.0 + na * (1.0 / 15.0) * (1.0 + na * (1.0 / 5.0)));
-  const double h5 = na * na * (1.0 / 75.0) * r4;
   const double k3pp = c.h8 * 5.0e3;
   const double k3 = c.h9 * 6.0e4 + k3pp;
-  const double k4pp = h2 * 5.0e3;
-  const double k4 = r1 * 6.0e4 * c.hca_r + k4pp;
-  const double k6 = r4 * ca * 1.5e6;
-  const double k7 = h5 * h2 * 6.0e4;
+  const double k4pp = (na * (5.0e3 / 88.12)) * c.hna * r1;  // h2 k4pp_rate, h2 = na hna / 88.12 r1
+  const double k4 = r1 * c.hca6 + k4pp;                     // h3 wca = r1 / hca, times 6e4
+  const double k6 = r4 * (ca * 1.5e6);
+  const double k7 = (na * na) * (6.0e4 / (75.0 * 5.0e3)) * r4 * k4pp;  // h5 h2 wna, h5 = na^2 / 75 r4
   const double k8 = c.h8 * h11 * 6.0e4;
   const double x1 = k2 * k4 * (k7 + k6) + k5 * k7 * (k2 + k3);
   const double x2 = k1 * k7 * (k4 + k5) + k4 * k6 * (k1 + k8);
@@ -501,7 +499,7 @@ __device__ __forceinline__ CurB group_b(double v, SA s, double* ds, const Pro& p
   {
     NcxShared c;
     c.hna = vexp<FP>(0.5224 * vfrt);
-    c.hca_r = vexp<FP>(-0.1670 * vfrt);  // 1/hca
+    c.hca6 = vexp<FP>(fma(vfrt, -0.1670, 11.002099841204238 /* log 6e4 */));  // 6e4 / hca
     if (FP) {  // h9 = 1 / (1 + c (1 + 1 / hna)) = hna / (hna + c (hna + 1)), h8 = c / (same)
       const double r = vrcp<FP>(fma(NAO * (1.0 / 88.12), c.hna + 1.0, c.hna));
       c.h9 = c.hna * r;
