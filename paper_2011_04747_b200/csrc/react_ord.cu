@@ -13,7 +13,13 @@
 //   * pow(x, 2|3|8) are products, pow(3.8e-5/cai, 1.4) is one fexp(log);
 //   * Nernst potentials log(c_o / c_i) = log(c_o) - log(c_i) (no reciprocal);
 //   * every reciprocal is the MUFU seed + one cubic Newton step (3 DFMA,
-//     faithful, fastmath.cuh rcp_nc / rcp_g) instead of __drcp_rn's 5.
+//     faithful, fastmath.cuh rcp_nc / rcp_g) instead of __drcp_rn's 5;
+//   * on the fast path: exponentials whose slopes are commensurate come from
+//     one another (e^((v+70)/20) gives the (v+70)/5, (v+20)/10, (v-10)/10 and
+//     (v-50)/20 terms by products), rates 1 / (c + 1 / s) are s / (c s + 1),
+//     coefficients a e^u ride in the exponent as e^(u + log a), and the NCX /
+//     INaK cycle algebra is factored (tools/refill_cost_probe.py, DESIGN.md
+//     3.1: ~100 FP64 instructions fewer per evaluation).
 // It therefore agrees with the reference to rounding, not bitwise; the parity
 // contract for ORd is max|dV| <= 1e-6 mV (tests/test_gpu_parity.py), which
 // the survey's +-1-ulp experiment shows is met with ~8 orders of margin.
