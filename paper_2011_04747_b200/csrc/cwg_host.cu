@@ -1113,7 +1113,7 @@ void build_stencil(cwg_ctx* c, const cwg_problem* p) {
 // ORd launch shape. Throughput regime (many nodes per lane): one persistent
 // 384-thread block per SM (<= 168 registers) whose warps advance in lockstep
 // -- free-running warps drift apart and thrash the 32 KB L1.5 instruction
-// cache with the ~40 KB body (C3: 0.65 ms lockstep vs 1.12 ms free-running).
+// cache with the ~54 KB fast-path body (C3: 0.65 ms lockstep vs 1.12 ms free-running).
 // Latency regime (the bin fits into <= 10 warps per SM, e.g. C2's 40k nodes:
 // about one node per lane): two free-running 128-thread blocks per SM with up
 // to 255 registers -- there the per-evaluation barrier only adds waiting (C2

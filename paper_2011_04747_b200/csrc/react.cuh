@@ -21,7 +21,7 @@ namespace cwg {
 
 // kSync (M::kBlockSync): the warps of the (single, persistent) block on an SM
 // advance one rates() evaluation per loop trip in lockstep (one
-// __syncthreads_or per trip). The ORd body is ~40 KB of SASS, larger than the
+// __syncthreads_or per trip). The ORd fast-path body is ~54 KB of SASS, larger than the
 // 32 KB L1.5 instruction cache; warps that drift to different PCs thrash it
 // (ncu: ~35% of stall cycles were instruction fetch). In lockstep every
 // fetched line serves all warps.
