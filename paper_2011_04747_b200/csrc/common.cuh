@@ -74,9 +74,16 @@ __device__ __forceinline__ double fe(double x, double h, double d) {
   return __dadd_rn(x, __dmul_rn(h, d));
 }
 
+// State layout: columns in pairs, S[(q / 2) * 2 * pitch + 2 * i + (q & 1)] -- node i's states q, q + 1 (q even)
+// sit side by side, so a lane moves them with one 16-byte access and a warp's 32 consecutive nodes with one
+// 512-byte one (half the load/store instructions of one column per state).
+__host__ __device__ __forceinline__ long long sidx(int q, long long i, long long pitch) {
+  return static_cast<long long>(q >> 1) * 2 * pitch + 2 * i + (q & 1);
+}
+
 struct ReactArgs {
   double* v;            // local V (current buffer)
-  double* S;            // SoA states, S[q*pitch + i]
+  double* S;            // paired-column states, S[sidx(q, i, pitch)]
   long long pitch;
   double* last;         // last_dvdt
   const int32_t* list;  // position -> local node (nullptr: dense range)

@@ -1398,14 +1398,14 @@ __global__ void aos_to_soa(const double* aos, int stride, int ns, long long coun
                            long long dst0) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= count) return;
-  for (int q = 0; q < ns; ++q) soa[q * pitch + dst0 + i] = aos[i * stride + q];
+  for (int q = 0; q < ns; ++q) soa[sidx(q, dst0 + i, pitch)] = aos[i * stride + q];
 }
 
 __global__ void soa_to_aos(const double* soa, long long pitch, long long src0, int ns, long long count, double* aos,
                            int stride) {
   const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
   if (i >= count) return;
-  for (int q = 0; q < ns; ++q) aos[i * stride + q] = soa[q * pitch + src0 + i];
+  for (int q = 0; q < ns; ++q) aos[i * stride + q] = soa[sidx(q, src0 + i, pitch)];
   for (int q = ns; q < stride; ++q) aos[i * stride + q] = 0.0;
 }
 
@@ -1418,7 +1418,7 @@ __global__ void init_rest(double* v, double* S, long long pitch, double* last, c
   const long long i = list ? static_cast<long long>(list[p]) : first + p;
   v[i] = rest[0];
   last[i] = 0.0;
-  for (int q = 0; q < stride; ++q) S[q * pitch + i] = q < ns ? rest[q + 1] : 0.0;
+  for (int q = 0; q < stride; ++q) S[sidx(q, i, pitch)] = q < ns ? rest[q + 1] : 0.0;
 }
 
 // standalone diffusion_substep for cwg_diffusion_substep (no halo, no error record)

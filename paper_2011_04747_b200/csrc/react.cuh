@@ -11,8 +11,8 @@
 // reference's per-node k, splitting.cpp:116, makes the order of nodes
 // irrelevant to the results, so the dynamic schedule stays bit-deterministic).
 //
-// State is SoA (S[q*pitch + i]); the needy lanes of one refill get
-// consecutive node positions, so their 41 state loads coalesce.
+// State columns are stored in pairs (common.cuh sidx); the needy lanes of one
+// refill get consecutive node positions, so their 16-byte accesses coalesce.
 #pragma once
 
 #include "common.cuh"
@@ -87,8 +87,16 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
           h = a.dt / static_cast<double>(k);  // dt_ar (splitting.cpp:117)
           j = 0;
           dv = 0.0;
+          {
+            const double* sp = a.S + 2 * node;  // column pair q / 2 at sp + q * pitch (sidx)
 #pragma unroll
-          for (int q = 0; q < M::NS; ++q) s[q] = a.S[q * a.pitch + node];
+            for (int q = 0; q + 1 < M::NS; q += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(sp + q * a.pitch);
+              s[q] = t2.x;
+              s[q + 1] = t2.y;
+            }
+            if (M::NS & 1) s[M::NS > 0 ? M::NS - 1 : 0] = sp[(M::NS - 1) * a.pitch];
+          }
           if (a.stim.node_ptr) {
             p0 = __ldg(a.stim.node_ptr + node);
             p1 = __ldg(a.stim.node_ptr + node + 1);
@@ -131,8 +139,12 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
       if (bad || j == k) {
         a.v[node] = v;
         a.last[node] = dv;  // dv at the start of the last sub-step (splitting.cpp:143)
+        {
+          double* sp = a.S + 2 * node;
 #pragma unroll
-        for (int q = 0; q < M::NS; ++q) a.S[q * a.pitch + node] = s[q];
+          for (int q = 0; q + 1 < M::NS; q += 2) *reinterpret_cast<double2*>(sp + q * a.pitch) = make_double2(s[q], s[q + 1]);
+          if (M::NS & 1) sp[(M::NS - 1) * a.pitch] = s[M::NS > 0 ? M::NS - 1 : 0];
+        }
         node = -1;
       }
     }
