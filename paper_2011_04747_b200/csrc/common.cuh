@@ -74,16 +74,24 @@ __device__ __forceinline__ double fe(double x, double h, double d) {
   return __dadd_rn(x, __dmul_rn(h, d));
 }
 
-// State layout: columns in pairs, S[(q / 2) * 2 * pitch + 2 * i + (q & 1)] -- node i's states q, q + 1 (q even)
-// sit side by side, so a lane moves them with one 16-byte access and a warp's 32 consecutive nodes with one
-// 512-byte one (half the load/store instructions of one column per state).
+// State layout: columns in groups of four, S[(q / 4) * 4 * pitch + 4 * i + (q & 3)] -- node i's states
+// q .. q + 3 (q a multiple of 4) sit side by side, so a lane moves them with one 32-byte access (sm_100's
+// LDG/STG.256) and a warp's 32 consecutive nodes with one contiguous 1 KB one: a quarter of the load/store
+// instructions of one column per state.
+constexpr int kStateGroup = 4;
 __host__ __device__ __forceinline__ long long sidx(int q, long long i, long long pitch) {
-  return static_cast<long long>(q >> 1) * 2 * pitch + 2 * i + (q & 1);
+  return static_cast<long long>(q >> 2) * 4 * pitch + 4 * i + (q & 3);
+}
+__device__ __forceinline__ void ld_state4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+__device__ __forceinline__ void st_state4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
 
 struct ReactArgs {
   double* v;            // local V (current buffer)
-  double* S;            // paired-column states, S[sidx(q, i, pitch)]
+  double* S;            // grouped-column states, S[sidx(q, i, pitch)]
   long long pitch;
   double* last;         // last_dvdt
   const int32_t* list;  // position -> local node (nullptr: dense range)

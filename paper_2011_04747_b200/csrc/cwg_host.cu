@@ -1453,9 +1453,9 @@ void create_impl(const cwg_problem* p_in, cwg_ctx* c) {
   c->d_v[1] = dev_alloc<double>(c->n_alloc + kVPad);
   CUDA_TRY(cudaMemset(c->d_v[0], 0, (c->n_alloc + kVPad) * sizeof(double)));
   CUDA_TRY(cudaMemset(c->d_v[1], 0, (c->n_alloc + kVPad) * sizeof(double)));
-  c->d_S = dev_alloc<double>(static_cast<size_t>(c->pitch) * ((c->stride + 1) & ~1));  // columns in pairs (sidx)
+  c->d_S = dev_alloc<double>(static_cast<size_t>(c->pitch) * ((c->stride + 3) & ~3));  // columns in groups of 4 (sidx)
   c->d_last = dev_alloc<double>(c->n_alloc);
-  CUDA_TRY(cudaMemset(c->d_S, 0, static_cast<size_t>(c->pitch) * ((c->stride + 1) & ~1) * sizeof(double)));
+  CUDA_TRY(cudaMemset(c->d_S, 0, static_cast<size_t>(c->pitch) * ((c->stride + 3) & ~3) * sizeof(double)));
   CUDA_TRY(cudaMemset(c->d_last, 0, c->n_alloc * sizeof(double)));
   tr.mark("state alloc");
 

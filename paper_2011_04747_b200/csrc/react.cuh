@@ -11,8 +11,9 @@
 // reference's per-node k, splitting.cpp:116, makes the order of nodes
 // irrelevant to the results, so the dynamic schedule stays bit-deterministic).
 //
-// State columns are stored in pairs (common.cuh sidx); the needy lanes of one
-// refill get consecutive node positions, so their 16-byte accesses coalesce.
+// State columns are stored in groups of four (common.cuh sidx); the needy
+// lanes of one refill get consecutive node positions, so their 32-byte
+// accesses coalesce.
 #pragma once
 
 #include "common.cuh"
@@ -88,14 +89,11 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
           j = 0;
           dv = 0.0;
           {
-            const double* sp = a.S + 2 * node;  // column pair q / 2 at sp + q * pitch (sidx)
+            const double* sp = a.S + 4 * node;  // column group q / 4 at sp + (q & ~3) * pitch (sidx)
 #pragma unroll
-            for (int q = 0; q + 1 < M::NS; q += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(sp + q * a.pitch);
-              s[q] = t2.x;
-              s[q + 1] = t2.y;
-            }
-            if (M::NS & 1) s[M::NS > 0 ? M::NS - 1 : 0] = sp[(M::NS - 1) * a.pitch];
+            for (int q = 0; q + 3 < M::NS; q += 4) ld_state4(sp + q * a.pitch, s[q], s[q + 1], s[q + 2], s[q + 3]);
+#pragma unroll
+            for (int q = M::NS & ~3; q < M::NS; ++q) s[q] = sp[(q & ~3) * a.pitch + (q & 3)];
           }
           if (a.stim.node_ptr) {
             p0 = __ldg(a.stim.node_ptr + node);
@@ -140,10 +138,11 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         a.v[node] = v;
         a.last[node] = dv;  // dv at the start of the last sub-step (splitting.cpp:143)
         {
-          double* sp = a.S + 2 * node;
+          double* sp = a.S + 4 * node;
 #pragma unroll
-          for (int q = 0; q + 1 < M::NS; q += 2) *reinterpret_cast<double2*>(sp + q * a.pitch) = make_double2(s[q], s[q + 1]);
-          if (M::NS & 1) sp[(M::NS - 1) * a.pitch] = s[M::NS > 0 ? M::NS - 1 : 0];
+          for (int q = 0; q + 3 < M::NS; q += 4) st_state4(sp + q * a.pitch, s[q], s[q + 1], s[q + 2], s[q + 3]);
+#pragma unroll
+          for (int q = M::NS & ~3; q < M::NS; ++q) sp[(q & ~3) * a.pitch + (q & 3)] = s[q];
         }
         node = -1;
       }
