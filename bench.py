@@ -494,7 +494,7 @@ def main():
                                   "kernel span (tools/react_trace.py, DESIGN.md 3.5)" if args.config in ("c1", "c2") else
                                   "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 52% of "
                                   "active cycles on C4, 8-cycle FP64 latency with 3 warps per sub-partition "
-                                  "(profiles/r02e_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
+                                  "(profiles/r02f_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
                                   "read+write per launch (algorithmic 677 B x 3.2M nodes = 2.18 GB)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (

@@ -167,7 +167,8 @@ int cwg_set_stream(cwg_ctx* ctx, void* cuda_stream);
 void* cwg_stream(cwg_ctx* ctx);
 
 /* make_initial_state (splitting.cpp:183-217) result upload / final_state
- * download. AoS host layout s[i*stride+q] (NodeStateArray::s); device is SoA.
+ * download. AoS host layout s[i*stride+q] (NodeStateArray::s); the device keeps
+ * the states column-wise in groups of four (csrc/common.cuh sidx).
  * For world > 1 the arrays are the GLOBAL arrays; each rank copies its slab. */
 int cwg_upload_state(cwg_ctx* ctx, const double* v, const double* s_aos, int stride,
                      const double* last_dvdt);
