@@ -140,3 +140,35 @@ def test_3d_kernels_agree():
     assert np.array_equal(a.final_state.v, b.final_state.v)
     assert np.array_equal(a.final_state.s, b.final_state.s)
     assert np.array_equal(a.k_histogram, b.k_histogram)
+
+
+@pytest.mark.parametrize("models,extra", [(["ohara2011-epi"], 0), (["aliev-panfilov"], 0), (["maccannell2007"], 3),
+                                          (["ohara2011-endo", "maccannell2007"], 5), (["aliev-panfilov"], 2)])
+def test_state_upload_download_round_trip(cw, models, extra):
+    """The device keeps the states column-wise in groups of four (common.cuh sidx, 32-byte refill accesses);
+    whatever the model's state count (40, 2, 1: full groups and ragged tails) and the caller's stride (>= the
+    largest state count, e.g. a checkpoint of a wider model list), upload then download returns the caller's
+    NodeStateArray bit for bit in the columns the models own and zeros beyond (ionic.hpp:39-55)."""
+    from paper_2011_04747_b200 import api, problems
+    sh = cw.Sheet(0.21, 0.13, 0.01, 0.3, d0_myocyte=0.0012, rho=0.25)
+    rng = np.random.default_rng(7)
+    mon = (np.arange(sh.n) % len(models)).astype(np.uint8)
+    p = problems.Problem("layout", sh, models, mon, [], api.SchemeConfig(dt_ms=0.1, t_end_ms=1.0, k0_down=3), [])
+    integ = cw.StrangIntegrator(p.setup(), p.cfg, model_of_node=mon)
+    try:
+        st0 = p.initial_state()
+        stride = st0.stride + extra
+        counts = np.array([cw.make_model(m).state_count() for m in models])[mon]
+        s = rng.standard_normal((sh.n, stride))
+        s[np.arange(stride)[None, :] >= counts[:, None]] = 0.0
+        st = api.NodeStateArray(sh.n, stride, rng.standard_normal(sh.n), s.reshape(-1).copy(),
+                                rng.standard_normal(sh.n), mon)
+        integ.upload(st)
+        back = api.NodeStateArray(sh.n, stride, np.full(sh.n, np.nan), np.full(sh.n * stride, np.nan),
+                                  np.full(sh.n, np.nan), mon)
+        integ.download(back)
+        assert np.array_equal(back.v, st.v)
+        assert np.array_equal(back.last_dvdt, st.last_dvdt)
+        assert np.array_equal(back.s, st.s)
+    finally:
+        integ.close()
