@@ -43,7 +43,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
   const double t = a.use_t_fixed ? a.t_fixed : static_cast<double>(step) * a.dt;  // splitting.cpp:270
   const long long seq = step * a.evs + a.ev;
 
-  long long node = -1;
+  int node = -1;  // local node index (< 2^31: a rank holds at most ~2.7e8 ORd nodes in 180 GB)
   bool open = true;  // may still receive work
   int k = 0, j = 0, p0 = 0, p1 = 0;
   double h = 0.0, v = 0.0, dv = 0.0, g = 1.0;
@@ -81,7 +81,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
       nxt = -1;
       {
         if (pos < a.count) {
-          node = a.list ? static_cast<long long>(__ldg(a.list + pos)) : a.first + pos;
+          node = a.list ? __ldg(a.list + pos) : static_cast<int>(a.first + pos);
           v = a.v[node];
           const double last = a.last[node];
           k = substeps(last, a.scheme, a.k0_up, a.k0_down, a.kmax);
@@ -89,7 +89,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
           j = 0;
           dv = 0.0;
           {
-            const double* sp = a.S + 4 * node;  // column group q / 4 at sp + (q & ~3) * pitch (sidx)
+            const double* sp = a.S + 4ll * node;  // column group q / 4 at sp + (q & ~3) * pitch (sidx)
 #pragma unroll
             for (int q = 0; q + 3 < M::NS; q += 4) ld_state4(sp + q * a.pitch, s[q], s[q + 1], s[q + 2], s[q + 3]);
 #pragma unroll
@@ -138,7 +138,7 @@ __device__ __forceinline__ void react_body(const ReactArgs& a, unsigned* shist) 
         a.v[node] = v;
         a.last[node] = dv;  // dv at the start of the last sub-step (splitting.cpp:143)
         {
-          double* sp = a.S + 4 * node;
+          double* sp = a.S + 4ll * node;
 #pragma unroll
           for (int q = 0; q + 3 < M::NS; q += 4) st_state4(sp + q * a.pitch, s[q], s[q + 1], s[q + 2], s[q + 3]);
 #pragma unroll
