@@ -679,11 +679,14 @@ __device__ void rates(double v, const double* s, double ist, double& dv, double*
 template <int CT, int V = 0>
 struct ModelOrd {
   static constexpr int NS = ord::NSTATE;
-  static constexpr int kThreads = V == 1 ? 384 : (V == 2 ? 256 : (V == 7 ? 288 : 128));
-  static constexpr int kMinBlocks = V == 0 ? 2 : 1;
-  static constexpr bool kBlockSync = V != 0;
-  static constexpr bool kPreclaim = V == 0;  // react.cuh: claim the next node one trip ahead
-  static constexpr bool kUsesGkr = true;
+  // V = 10 / 11: shapes 0 / 1 for runs without a per-node GKr scale (launch_ct picks them when a.gkr is null):
+  // the scale is the constant 1 there, two registers fewer in the lane-refill loop
+  static constexpr int S = V == 10 ? 0 : (V == 11 ? 1 : V);  // the launch shape
+  static constexpr int kThreads = S == 1 ? 384 : (S == 2 ? 256 : (S == 7 ? 288 : 128));
+  static constexpr int kMinBlocks = S == 0 ? 2 : 1;
+  static constexpr bool kBlockSync = S != 0;
+  static constexpr bool kPreclaim = S == 0;  // react.cuh: claim the next node one trip ahead
+  static constexpr bool kUsesGkr = V < 10;
   __device__ __forceinline__ static void block_init() { exp_table_init(); }
   template <class SA>
   __device__ __forceinline__ static void advance(double& v, SA s, double ist, double g, double h, double& dv) {
@@ -751,6 +754,10 @@ bool react_ord_variant_valid(int v) {
 
 template <int CT>
 static cudaError_t launch_ct(int variant, const ReactArgs& a, int grid, cudaStream_t st) {
+  if (!a.gkr) {  // no per-node GKr scale: the twins with the scale folded to 1
+    if (variant == 0) return launch_react_t<ModelOrd<CT, 10>>(a, grid, st);
+    if (variant == 1) return launch_react_t<ModelOrd<CT, 11>>(a, grid, st);
+  }
   switch (variant) {
 #define CWG_CASE(n) case n: return launch_react_t<ModelOrd<CT, n>>(a, grid, st);
     CWG_ORD_VARIANTS(CWG_CASE)
