@@ -51,14 +51,14 @@ FLUSH_BYTES = 256 << 20  # > 126 MB L2
 # Executed FP64 flops per ORd rates evaluation of react_kernel<ModelOrd<epi>>
 # (2*DFMA + DMUL + DADD predicated-on lane ops / evaluations), counted by ncu
 # over every reaction launch of a 40-step C4 run (tools/flops_per_eval.py c4 40;
-# profiles/r02e_flops_per_eval_c4.txt): 704.1 DFMA + 334.3 DMUL + 205.4 DADD
-# on the final build (C2: 1,948.6; 2,152.9 before the fast path's algebraic cuts,
+# profiles/r02g_flops_per_eval_c4.txt): 704.1 DFMA + 333.3 DMUL + 205.4 DADD
+# on the final build (C2: 1,947.6; 2,152.9 before the fast path's algebraic cuts,
 # 2,735.9 at the start of round 2's second session,
 # profiles/r02_flops_per_eval_c4.txt). Updated when the kernel changes.
-ORD_FP64_FLOPS_PER_EVAL = 1947.9
+ORD_FP64_FLOPS_PER_EVAL = 1946.9
 # the same count in FP64 pipe issue slots (DFMA + DMUL + DADD warp-lane instructions per evaluation): a DMUL or
 # DADD takes the slot a DFMA does, so the pipe-slot fraction reads higher than the flop fraction
-ORD_FP64_INSTR_PER_EVAL = 1243.8
+ORD_FP64_INSTR_PER_EVAL = 1242.8
 DIFF_BYTES_PER_NODE_SUBSTEP = 96.0  # 2D stencil: V in + out, 9 coefficients, dt/m
 
 
@@ -494,7 +494,7 @@ def main():
                                   "kernel span (tools/react_trace.py, DESIGN.md 3.5)" if args.config in ("c1", "c2") else
                                   "throughput regime: one 384-thread lockstep block per SM; FP64 pipe 52% of "
                                   "active cycles on C4, 8-cycle FP64 latency with 3 warps per sub-partition "
-                                  "(profiles/r02f_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
+                                  "(profiles/r02g_react_c4_digest.txt, r02_fp64_latency.txt); traffic = ncu DRAM "
                                   "read+write per launch (algorithmic 677 B x 3.2M nodes = 2.18 GB)")},
             "roofline_diffusion": {"bound": "hbm",
                                    "kernel": "diffuse_struct3d" if is3d else (
