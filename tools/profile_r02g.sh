@@ -1,5 +1,5 @@
 #!/bin/bash
-# Round-2 last-session evidence (after the algebraic FP64 cuts of the ORd fast path) on one B200: GPU test suite, bench lines for every BASELINE config, the C4
+# Round-2 final-build evidence (the r02e / r02f / r02g passes of the last session ran this script) on one B200: GPU test suite, bench lines for every BASELINE config, the C4
 # reference arm, executed FP64 flops per evaluation (C4, C2), the ncu launch list of the default bench and one
 # full ncu capture of the reaction kernel. Outputs -> gpurun_out/r02g/.
 set -u
